@@ -1,0 +1,319 @@
+/*
+ * nglod_b200 -- C ABI of the B200 (sm_100a) NGLOD render hot path.
+ *
+ * The reference (arxiv/paper_2101_10994, package `octfield`) is pure Python
+ * and exposes no FFI: its boundary is the Python module API
+ * (octfield/__init__.py:11-164). These entry points are what a ctypes / cffi
+ * binding of that API needs; each names the reference function it replaces.
+ * The Python host package `paper_2101_10994_b200` binds them with ctypes
+ * (INTEGRATION.md shows the binding a maintainer would add to octfield).
+ *
+ * Conventions
+ *  - Plain C types only. Every pointer argument is DEVICE memory owned by
+ *    the caller (PyTorch allocates it); nothing here frees caller memory.
+ *  - `stream` is a cudaStream_t passed as void*. Calls are asynchronous on
+ *    that stream unless documented otherwise.
+ *  - Every function returns an int status (NG_OK = 0). NG_ERR_* map 1:1 to
+ *    the reference exception classes (octfield/errors.py:4-29); the message
+ *    of the last failure on the calling thread is ng_last_error().
+ *  - Variable-length outputs use two-phase sizing: counts are written to
+ *    device memory; when a count exceeds the capacity the caller passed,
+ *    the data is not written and the caller retries with larger buffers.
+ */
+#ifndef NGLOD_B200_H
+#define NGLOD_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NG_OK 0
+#define NG_ERR_STRUCTURAL 1  /* octfield.errors.StructuralError */
+#define NG_ERR_CONFIG 2      /* octfield.errors.ConfigError */
+#define NG_ERR_CAPACITY 3    /* internal: grow buffers and retry */
+#define NG_ERR_CUDA 4        /* CUDA runtime failure */
+#define NG_ERR_OCTFIELD 5    /* octfield.errors.OctfieldError (e.g. non-finite decoder input) */
+
+#define NG_MAX_TLEVELS 16    /* virtual + stored traversal levels */
+#define NG_FEAT_PAD 32       /* feature rows are padded to 32 fp32 channels (128 B) */
+#define NG_W1_STRIDE 36      /* packed decoder row: 3 x-weights, 32 feature weights, b1 */
+
+/* Device-resident sparse voxel octree (octree.py:100-131).
+ * Traversal level t = level + n_virtual; levels -n_virtual..-1 are the
+ * virtual coarse grids above the stored root (octree.py:1-8, 208-212). */
+typedef struct ng_octree {
+  int32_t r0;
+  int32_t max_level;
+  int32_t n_virtual;            /* log2(r0) */
+  int32_t n_tlevels;            /* n_virtual + max_level + 1 */
+  int64_t count[NG_MAX_TLEVELS];              /* voxels per traversal level */
+  const uint64_t* codes[NG_MAX_TLEVELS];      /* strictly ascending Morton codes */
+  const int32_t* child_start[NG_MAX_TLEVELS]; /* index of first child in level t+1 */
+  const uint8_t* child_mask[NG_MAX_TLEVELS];  /* occupied-octant bits (bit = code & 7) */
+  const uint64_t* bitmap[NG_MAX_TLEVELS];     /* occupancy bit per Morton code (res^3 bits) */
+  const uint32_t* rank[NG_MAX_TLEVELS];       /* exclusive popcount per 64-bit bitmap word */
+  const int32_t* corners[NG_MAX_TLEVELS];     /* feature levels: (count, 8) global corner ids */
+  double region_lo[3];          /* occupied finest-level AABB (octree.py:204-206) */
+  double region_hi[3];
+  double half_diag_finest;      /* 0.5*sqrt(3)*edge(max_level) (octree.py:123-124) */
+} ng_octree;
+
+/* Neural field parameters (field.py:30-48, 242-269), packed for the device.
+ *  Z:        (corner_count, 32) fp32, channels >= m zero.
+ *  decoders: n_decoders blocks of dec_stride floats; block L-1 holds
+ *            W1b[h][36] (x weights, feature weights padded to 32, b1),
+ *            W2[h], b2, zero padding. */
+typedef struct ng_field {
+  const float* Z;
+  const float* decoders;
+  int32_t m;
+  int32_t h;
+  int32_t n_decoders;
+  int32_t dec_stride;
+  int64_t corner_count;
+} ng_field;
+
+/* EvalCounter (field.py:79-90) plus a non-finite-input tally; device int64. */
+typedef struct ng_counters {
+  int64_t decoder_evals;
+  int64_t evals_missing_level;
+  int64_t empty_fallbacks;
+  int64_t nonfinite_inputs;
+} ng_counters;
+
+/* One batched SDF query. Modes:
+ *  - predict / forward (field.py:194-218, 337-357): out_levels selects the
+ *    decoder levels L to output (bit L-1), one fp64 column per set bit in
+ *    ascending L; each column equals predict(x, L).
+ *  - blend (field.py:226-239): blend_base >= 1 and blend_alpha in (0,1)
+ *    outputs one column (1-a)*predict(base) + a*predict(base+1).
+ *  - query_field (render.py:155-171): inside_level >= 0 answers points that
+ *    are not inside that level's voxels with empty_space_value. */
+typedef struct ng_query_args {
+  int32_t out_levels;
+  int32_t inside_level;
+  int32_t blend_base;
+  int32_t pad;
+  double blend_alpha;
+} ng_query_args;
+
+/* Ray record (traversal.py:40-56): origin, unit direction, 1/direction,
+ * flags bits 0-2 = (d<0) per axis (traversal.py:147-154), bits 3-5 = (d==0). */
+typedef struct ng_ray {
+  double o[3];
+  double d[3];
+  double inv[3];
+  int32_t flags;
+  int32_t pad;
+} ng_ray;
+
+/* (ray, voxel) pair at one traversal level (traversal.py:59-70). */
+typedef struct ng_pair {
+  int32_t ray;
+  int32_t voxel;
+} ng_pair;
+
+/* Final-level hit with its entry/exit distances (traversal.py:233-246). */
+typedef struct ng_hit_pair {
+  int32_t ray;
+  int32_t voxel;
+  double t_enter;
+  double t_exit;
+} ng_hit_pair;
+
+/* Pinhole camera (render.py:43-88); basis precomputed on the host in fp64. */
+typedef struct ng_camera {
+  double position[3];
+  double fwd[3];
+  double right[3];
+  double up[3];
+  double tan_half;
+  double aspect;
+  int32_t width;
+  int32_t height;
+} ng_camera;
+
+/* RenderConfig (render.py:91-114), resolved on the host. */
+typedef struct ng_render_cfg {
+  double delta;
+  double far_plane;
+  double skip_eps;
+  double osc_tol;         /* osc_factor * delta */
+  double lod;             /* resolved detail level, >= 1 */
+  double normal_eps;
+  double light[3];        /* normalised */
+  double albedo[3];
+  double ambient;
+  double background[3];
+  int32_t max_iters;
+  int32_t trace_level;    /* min(ceil(lod), max_level) */
+} ng_render_cfg;
+
+/* Per-pixel frame outputs (render.py:117-128), device arrays of n pixels. */
+typedef struct ng_frame {
+  uint8_t* hit;           /* (n,) */
+  double* t;              /* (n,) nan on miss */
+  double* normal;         /* (n, 3), zero where invalid */
+  uint8_t* normal_ok;     /* (n,) */
+  int32_t* iterations;    /* (n,) */
+  int32_t* evals;         /* (n,) */
+  uint8_t* color;         /* (n, 3) */
+} ng_frame;
+
+/* Scratch for traversal and tracing; sized by ng_render_workspace_bytes. */
+typedef struct ng_workspace {
+  void* base;
+  size_t bytes;
+  int64_t pair_capacity;  /* per ping-pong pair buffer */
+  int64_t hit_capacity;   /* final hit-pair list */
+  void* ev_trace_done;    /* optional cudaEvent_t recorded between march and normals */
+} ng_workspace;
+
+/* Device-side frame statistics (FrameReport, render.py:131-137). */
+typedef struct ng_frame_stats {
+  int64_t pairs[NG_MAX_TLEVELS + 1]; /* list length entering each level; [target+1] = hits */
+  int64_t visible;
+  int64_t active_rays;
+  ng_counters counters;
+  int64_t overflow;              /* nonzero: a pair list exceeded its capacity */
+} ng_frame_stats;
+
+/* ---- library ----------------------------------------------------------- */
+int ng_abi_version(void);
+const char* ng_last_error(void);
+int ng_sm_count(int device);
+
+/* ---- Morton / binning / locate (octree.py:35-85, 134-143, 259-282) ----- */
+int ng_morton_encode(const int64_t* ijk, int64_t n, uint64_t* codes, void* stream);
+int ng_morton_decode(const uint64_t* codes, int64_t n, int64_t* ijk, void* stream);
+int ng_locate(const ng_octree* tree, const double* pts, int64_t n, int32_t level,
+              int64_t* out_index, void* stream);
+/* ray_aabb_batch (octree.py:311-333): rows matched; t_enter/t_exit fp64, hit u8. */
+int ng_ray_aabb(const double* o, const double* d, const double* lo, const double* hi,
+                int64_t n, double* t_enter, double* t_exit, uint8_t* hit, void* stream);
+
+/* ---- octree build (octree.py:146-256) ----------------------------------- */
+/* Set the finest-level bit of every sample's cell (octree.py:170-175). */
+int ng_build_mark_samples(const double* pts, int64_t n, int32_t res, uint64_t* bitmap,
+                          void* stream);
+/* Corner test (octree.py:225-246) from an fp32 |d| lattice of (res+1)^3 in
+ * (i,j,k) C order: set cells whose min corner |d| <= tol (fp64 compare). */
+int ng_build_mark_lattice(const float* absd, int32_t res, double tol, uint64_t* bitmap,
+                          void* stream);
+/* |d| of a built-in analytic SDF on the corner lattice, as fp32.
+ * kind 1 sphere (r), 2 torus (R, r), 3 closed polyline tube (params =
+ * [tube, x0,y0,z0, x1,...], nverts = (n_params-1)/3, params in device memory). */
+int ng_sdf_lattice(int32_t kind, const double* params, int32_t n_params, int32_t res,
+                   float* absd, void* stream);
+int ng_sdf_eval(int32_t kind, const double* params, int32_t n_params, const double* pts,
+                int64_t n, double* out, void* stream);
+/* Parent closure: parent bit p = OR of child bits 8p..8p+7 (octree.py:183-187). */
+int ng_bitmap_parent(const uint64_t* child_bitmap, int64_t child_words, uint64_t* parent_bitmap,
+                     int64_t parent_words, void* stream);
+/* Exclusive popcount prefix per word; total written to *d_total (device). */
+int ng_bitmap_rank(const uint64_t* bitmap, int64_t n_words, uint32_t* rank, int64_t* d_total,
+                   void* scratch, size_t scratch_bytes, void* stream);
+/* Sorted set-bit positions -> codes (np.unique order). */
+int ng_bitmap_extract(const uint64_t* bitmap, const uint32_t* rank, int64_t n_words,
+                      uint64_t* codes, void* stream);
+/* parents (octree.py:197) from the parent level's bitmap/rank. */
+int ng_level_parents(const uint64_t* codes, int64_t n, const uint64_t* parent_bitmap,
+                     const uint32_t* parent_rank, int32_t* parents, void* stream);
+/* child_start / child_mask for traversal (children_ranges, octree.py:303-308). */
+int ng_level_children(const uint64_t* codes, int64_t n, const uint64_t* child_bitmap,
+                      const uint32_t* child_rank, int32_t* child_start, uint8_t* child_mask,
+                      void* stream);
+/* Corner keys of every voxel into a (2*res)^3-bit corner bitmap (octree.py:249-253). */
+int ng_corner_mark(const uint64_t* codes, int64_t n, uint64_t* corner_bitmap, void* stream);
+/* Corner table: offset + rank of each corner key (octree.py:254-256). */
+int ng_corner_table(const uint64_t* codes, int64_t n, const uint64_t* corner_bitmap,
+                    const uint32_t* corner_rank, int32_t offset, int32_t* corners, void* stream);
+/* Min / max cell coordinate of a level (for the region AABB, octree.py:204-206). */
+int ng_cell_extent(const uint64_t* codes, int64_t n, int32_t* d_minmax6, void* stream);
+
+/* ---- scans (traversal.py:113-144) --------------------------------------- */
+size_t ng_scan_scratch_bytes(int64_t n);
+int ng_exclusive_sum_i64(const int64_t* in, int64_t n, int64_t* out, void* scratch,
+                         size_t scratch_bytes, void* stream);
+
+/* ---- field (field.py:104-239, 337-357; render.py:155-171) -------------- */
+int ng_query(const ng_octree* tree, const ng_field* fld, const ng_query_args* args,
+             const double* pts, int64_t n, double* out, ng_counters* d_counters, void* stream);
+/* sum_features / trilinear: z = sum of levels [level_lo, level_hi] as fp64
+ * (n, m) and per-level presence mask (n, level_hi-level_lo+1). */
+int ng_interp(const ng_octree* tree, const ng_field* fld, const double* pts, int64_t n,
+              int32_t level_lo, int32_t level_hi, double* z, uint8_t* mask, void* stream);
+/* empty_space_value (field.py:185-191). */
+int ng_empty_value(const ng_octree* tree, const double* pts, int64_t n, double* out,
+                   void* stream);
+
+/* ---- traversal (traversal.py:95-255) ------------------------------------ */
+/* Build ray records from origins/directions (n,3) fp64. */
+int ng_rays_from_arrays(const double* o, const double* d, int64_t n, ng_ray* rays,
+                        void* stream);
+/* One BFS pass at traversal level t: decide + exclusive scan + subdivide
+ * (or, when final != 0, decide + compactify + entry/exit distances).
+ * in == NULL means the implicit root list (i, 0) of d_count_in rays.
+ * Counts live in device memory; writes past the capacity are dropped and
+ * the full count is still reported. */
+size_t ng_level_scratch_bytes(int64_t max_pairs);
+int ng_traverse_level(const ng_octree* tree, const ng_ray* rays, int32_t t, int32_t final,
+                      const ng_pair* in, const int64_t* d_count_in, int64_t in_capacity,
+                      ng_pair* out_pairs, ng_hit_pair* out_hits, int64_t* d_count_out,
+                      int64_t out_capacity, void* scratch, size_t scratch_bytes, void* stream);
+/* ray_segments (traversal.py:250-255) over a final hit list (device count). */
+int ng_segments(const ng_hit_pair* hits, const int64_t* d_count, int64_t capacity,
+                int64_t n_rays, int64_t* seg_start, int64_t* seg_end, void* stream);
+
+/* ---- rendering (render.py:43-448) --------------------------------------- */
+int ng_camera_rays(const ng_camera* cam, ng_ray* rays, void* stream);
+size_t ng_render_workspace_bytes(int64_t n_rays, int64_t pair_capacity, int64_t hit_capacity);
+/* sphere_trace (render.py:174-274) over an existing final list. */
+int ng_sphere_trace(const ng_octree* tree, const ng_field* fld, const ng_render_cfg* cfg,
+                    const ng_ray* rays, int64_t n_rays, const ng_hit_pair* hits,
+                    const int64_t* d_hit_count, const int64_t* seg_start,
+                    const int64_t* seg_end, uint8_t* hit, double* t_hit, int32_t* iters,
+                    int32_t* evals, ng_counters* d_counters, void* stream);
+/* normals (render.py:277-300) at hit points p (k,3) fp64 -> normal fp64, ok u8. */
+int ng_normals(const ng_octree* tree, const ng_field* fld, const ng_render_cfg* cfg,
+               const double* pts, int64_t k, double* normal, uint8_t* ok,
+               ng_counters* d_counters, void* stream);
+/* shade (render.py:303-314). */
+int ng_shade(const uint8_t* hit, const double* normal, int64_t n, const ng_render_cfg* cfg,
+             uint8_t* color, void* stream);
+/* Whole frame: rays -> traversal -> march -> normals -> shade, with no host
+ * synchronisation (capturable in a CUDA graph). Statistics are written to
+ * *d_stats (device); stats.overflow != 0 means retry with more capacity. */
+int ng_render_frame(const ng_octree* tree, const ng_field* fld, const ng_render_cfg* cfg,
+                    const ng_camera* cam, const ng_frame* frame, const ng_workspace* ws,
+                    ng_frame_stats* d_stats, void* stream);
+/* Same, for arbitrary rays (metrics.trace_field_rays, metrics.py:135-142). */
+int ng_render_rays(const ng_octree* tree, const ng_field* fld, const ng_render_cfg* cfg,
+                   const ng_ray* rays, int64_t n_rays, const ng_frame* frame,
+                   const ng_workspace* ws, ng_frame_stats* d_stats, int32_t do_normals,
+                   void* stream);
+/* Standalone decoder (decode, field.py:172-182) on given inputs: x (n,3),
+ * z (n,m) fp64 -> out (n,) fp64; decoder is one packed block. Non-finite
+ * inputs are counted in *d_nonfinite (device int64). */
+int ng_decode(const float* decoder, int32_t h, int32_t m, const double* x, const double* z, int64_t n,
+              double* out, int64_t* d_nonfinite, void* stream);
+/* decide (traversal.py:95-110) for an explicit pair list at traversal level t. */
+int ng_decide(const ng_octree* tree, const ng_ray* rays, int32_t t, int32_t final, const ng_pair* pairs,
+              int64_t n, int64_t* decisions, void* stream);
+/* subdivide (traversal.py:165-191) from decisions D and their exclusive sum S. */
+int ng_subdivide(const ng_octree* tree, const ng_ray* rays, int32_t t, const ng_pair* pairs, int64_t n,
+                 const int64_t* D, const int64_t* S, ng_pair* out, void* stream);
+/* compactify (traversal.py:194-204). */
+int ng_compactify(const ng_pair* pairs, int64_t n, const int64_t* D, const int64_t* S, ng_pair* out,
+                  void* stream);
+/* Hit positions o + t*d for hit rays (FrameBuffer.points, render.py:395-396). */
+int ng_hit_points(const ng_ray* rays, const uint8_t* hit, const double* t, int64_t n,
+                  double* points, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NGLOD_B200_H */

@@ -1,0 +1,224 @@
+// Shared device helpers for the nglod_b200 kernels (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <math.h>
+
+#include "../../include/nglod_b200.h"
+
+namespace ng {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+// ---------------------------------------------------------------- errors
+void set_error(const char* fmt, ...);
+int cuda_status(cudaError_t e, const char* where);
+int launch_status(const char* where);
+int sm_count();
+
+#define NG_CHECK_LAUNCH(name)                         \
+  do {                                                \
+    int _s = ::ng::launch_status(name);               \
+    if (_s != NG_OK) return _s;                       \
+  } while (0)
+
+// ---------------------------------------------------------------- morton
+// 21-bit coordinate spread, x in bit 0 of each triad (octree.py:35-60).
+__host__ __device__ __forceinline__ uint64_t spread3(uint64_t v) {
+  v &= 0x1FFFFFull;
+  v = (v | (v << 32)) & 0x1F00000000FFFFull;
+  v = (v | (v << 16)) & 0x1F0000FF0000FFull;
+  v = (v | (v << 8)) & 0x100F00F00F00F00Full;
+  v = (v | (v << 4)) & 0x10C30C30C30C30C3ull;
+  v = (v | (v << 2)) & 0x1249249249249249ull;
+  return v;
+}
+
+__host__ __device__ __forceinline__ uint32_t compact3(uint64_t v) {
+  v &= 0x1249249249249249ull;
+  v = (v ^ (v >> 2)) & 0x10C30C30C30C30C3ull;
+  v = (v ^ (v >> 4)) & 0x100F00F00F00F00Full;
+  v = (v ^ (v >> 8)) & 0x1F0000FF0000FFull;
+  v = (v ^ (v >> 16)) & 0x1F00000000FFFFull;
+  v = (v ^ (v >> 32)) & 0x1FFFFFull;
+  return (uint32_t)v;
+}
+
+__host__ __device__ __forceinline__ uint64_t morton(uint32_t i, uint32_t j, uint32_t k) {
+  return spread3(i) | (spread3(j) << 1) | (spread3(k) << 2);
+}
+
+// ---------------------------------------------------------------- exact fp64
+// The reference computes in float64 with numpy's operation order; these
+// helpers pin each rounding step so nvcc never contracts into an FMA.
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+
+// numpy minimum/maximum propagate NaN.
+__device__ __forceinline__ double np_min(double a, double b) {
+  return (a != a) ? a : ((b != b) ? b : (a < b ? a : b));
+}
+__device__ __forceinline__ double np_max(double a, double b) {
+  return (a != a) ? a : ((b != b) ? b : (a > b ? a : b));
+}
+
+// Half-open binning: floor((x - (-1)) * (res / 2)) clipped to [0, res-1]
+// (octree.py:134-139). res/2 is a power of two, so the product is exact.
+__device__ __forceinline__ int bin_axis(double x, int res) {
+  double f = dmul(dadd(x, 1.0), 0.5 * (double)res);
+  double c = floor(f);
+  int i = (c < 0.0) ? 0 : (c > (double)(res - 1) ? res - 1 : (int)c);
+  return i;
+}
+
+// cell_origin (octree.py:142-143): -1 + ijk * (2/res); exact for our sizes.
+__device__ __forceinline__ double cell_lo(int ijk, int res) {
+  return dadd(-1.0, dmul((double)ijk, 2.0 / (double)res));
+}
+
+// ---------------------------------------------------------------- octree
+__device__ __forceinline__ int level_res(const ng_octree& t, int level) {
+  return level >= 0 ? (t.r0 << level) : (t.r0 >> (-level));
+}
+
+// Index of the voxel holding Morton code `code` at traversal level tl, or -1.
+__device__ __forceinline__ int64_t rank_lookup(const uint64_t* __restrict__ bm,
+                                               const uint32_t* __restrict__ rk, uint64_t code) {
+  uint64_t w = __ldg(bm + (code >> 6));
+  uint32_t b = (uint32_t)(code & 63);
+  if (!((w >> b) & 1ull)) return -1;
+  return (int64_t)__ldg(rk + (code >> 6)) + __popcll(w & ((1ull << b) - 1ull));
+}
+
+// ---------------------------------------------------------------- slab test
+// ray_aabb_batch (octree.py:311-333) for one ray / one box, bit-exact.
+__device__ __forceinline__ bool slab_test(const ng_ray& r, const double lo[3], const double hi[3],
+                                          double& t_enter, double& t_exit) {
+  double near = -INFINITY, far = INFINITY;
+  bool nan_seen = false;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    double an, af;
+    if ((r.flags >> (3 + a)) & 1) {
+      bool inside = (r.o[a] >= lo[a]) && (r.o[a] <= hi[a]);
+      an = inside ? -INFINITY : INFINITY;
+      af = inside ? INFINITY : -INFINITY;
+    } else {
+      double t1 = dmul(dsub(lo[a], r.o[a]), r.inv[a]);
+      double t2 = dmul(dsub(hi[a], r.o[a]), r.inv[a]);
+      an = np_min(t1, t2);
+      af = np_max(t1, t2);
+    }
+    if (a == 0) {
+      near = an;
+      far = af;
+    } else {
+      near = np_max(near, an);
+      far = np_min(far, af);
+    }
+  }
+  nan_seen = (near != near) || (far != far);
+  t_enter = np_max(near, 0.0);
+  t_exit = far;
+  return !nan_seen && (near <= far) && (far >= 0.0);
+}
+
+__device__ __forceinline__ void load_ray(const ng_ray* __restrict__ rays, int64_t i, ng_ray& r) {
+  const double2* p = reinterpret_cast<const double2*>(rays + i);
+  double2 a = __ldg(p + 0), b = __ldg(p + 1), c = __ldg(p + 2), d = __ldg(p + 3), e = __ldg(p + 4);
+  r.o[0] = a.x; r.o[1] = a.y; r.o[2] = b.x;
+  r.d[0] = b.y; r.d[1] = c.x; r.d[2] = c.y;
+  r.inv[0] = d.x; r.inv[1] = d.y; r.inv[2] = e.x;
+  r.flags = __double_as_longlong(e.y) & 0xffffffff;
+  r.pad = 0;
+}
+
+__device__ __forceinline__ void make_ray(double ox, double oy, double oz, double dx, double dy,
+                                         double dz, ng_ray& r) {
+  r.o[0] = ox; r.o[1] = oy; r.o[2] = oz;
+  r.d[0] = dx; r.d[1] = dy; r.d[2] = dz;
+  int flags = 0;
+  double d3[3] = {dx, dy, dz};
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    r.inv[a] = 1.0 / d3[a];
+    if (d3[a] < 0.0) flags |= 1 << a;
+    if (d3[a] == 0.0) flags |= 1 << (3 + a);
+  }
+  r.flags = flags;
+  r.pad = 0;
+}
+
+// ---------------------------------------------------------------- warp utils
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31; }
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_incl_scan(T v) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    T n = __shfl_up_sync(FULL, v, o);
+    if ((int)lane_id() >= o) v += n;
+  }
+  return v;
+}
+
+// ---------------------------------------------------------------- look-back scan
+// Single-pass decoupled look-back tile states: value in the low 62 bits,
+// status in the top 2 (0 = not ready, 1 = aggregate, 2 = inclusive prefix).
+constexpr uint64_t TS_AGG = 1ull << 62;
+constexpr uint64_t TS_PREFIX = 2ull << 62;
+constexpr uint64_t TS_VALUE = (1ull << 62) - 1;
+
+// Called by one thread: publish this tile's aggregate and return the
+// exclusive prefix of all earlier tiles.
+__device__ __forceinline__ int64_t tile_lookback(unsigned long long* states, int64_t tile,
+                                                 int64_t aggregate) {
+  if (tile == 0) {
+    __threadfence();
+    atomicExch(states, (unsigned long long)(TS_PREFIX | (uint64_t)aggregate));
+    return 0;
+  }
+  __threadfence();
+  atomicExch(states + tile, (unsigned long long)(TS_AGG | (uint64_t)aggregate));
+  int64_t excl = 0;
+  int64_t p = tile - 1;
+  while (true) {
+    uint64_t s = *((volatile unsigned long long*)(states + p));
+    uint64_t st = s & ~TS_VALUE;
+    if (st == 0) continue;
+    excl += (int64_t)(s & TS_VALUE);
+    if (st == TS_PREFIX) break;
+    --p;
+  }
+  __threadfence();
+  atomicExch(states + tile, (unsigned long long)(TS_PREFIX | (uint64_t)(excl + aggregate)));
+  return excl;
+}
+
+// Block-wide exclusive scan of one int64 per thread; returns the block total.
+template <int NT>
+__device__ __forceinline__ int64_t block_excl_scan(int64_t v, int64_t& excl, int64_t* sm_warp) {
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  int64_t inc = warp_incl_scan<int64_t>(v);
+  if (l == 31) sm_warp[w] = inc;
+  __syncthreads();
+  if (w == 0) {
+    int64_t x = (l < NT / 32) ? sm_warp[l] : 0;
+    int64_t xi = warp_incl_scan<int64_t>(x);
+    if (l < NT / 32) sm_warp[l] = xi - x;
+    if (l == NT / 32 - 1) sm_warp[NT / 32] = xi;
+  }
+  __syncthreads();
+  excl = sm_warp[w] + inc - v;
+  int64_t total = sm_warp[NT / 32];
+  return total;
+}
+
+}  // namespace ng

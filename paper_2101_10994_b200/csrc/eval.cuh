@@ -1,0 +1,247 @@
+// Warp-cooperative SDF evaluation: the per-LOD trilinear feature gather and
+// the per-LOD decoder (field.py:104-218, render.py:155-171).
+//
+// A warp evaluates 32 points at once, one per lane.
+//  1. Lane = point: fp64 binning of x at the finest gathered level, then per
+//     level a bitmap rank lookup (locate, octree.py:259-282), the voxel's 8
+//     corner ids and the 8 trilinear weights (field.py:104-135), staged in
+//     shared memory.
+//  2. Lane = feature channel: for every point with the level present, the 8
+//     corner rows Z[id, 0:32] are read as coalesced 128-byte loads (one
+//     feature per lane), weighted and added into the shared z tile, so the
+//     running level sum (sum_features, field.py:154-169) never leaves SMEM.
+//  3. Lane = point again: at each requested decoder level L the lane reads
+//     its z_L row and runs the 35 -> h -> 1 MLP (decode, field.py:172-182)
+//     in fp32 with the decoder weights broadcast from shared memory.
+#pragma once
+
+#include "common.cuh"
+
+namespace ng {
+
+struct WarpScratch {
+  int4 ids[32][2];      // corner ids of each lane's point at the current level
+  float4 w[32][2];      // trilinear weights
+  float zt[32][33];     // running feature sum, row = point, col = channel (+1 pad)
+};
+
+struct EvalCtx {
+  const float* __restrict__ Z;       // (C, 32)
+  const float* dec;                  // shared-memory decoders, level dec_first first
+  int dec_first;                     // decoder level of the first staged block
+  int dec_stride;                    // floats per decoder block
+  int h;
+  int gather_level;                  // G: highest level interpolated
+  int inside_level;                  // -1 or query_field level
+  int out_mask;                      // decoder levels evaluated (bit L-1)
+};
+
+// empty_space_value (field.py:185-191) in float64, numpy operation order.
+__device__ __forceinline__ double empty_value(const ng_octree& t, const double x[3]) {
+  double g[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    double lo = np_max(dsub(t.region_lo[a], x[a]), 0.0);
+    double hi = np_max(dsub(x[a], t.region_hi[a]), 0.0);
+    g[a] = dadd(lo, hi);
+  }
+  double s = dadd(dadd(dmul(g[0], g[0]), dmul(g[1], g[1])), dmul(g[2], g[2]));
+  return dadd(__dsqrt_rn(s), t.half_diag_finest);
+}
+
+__device__ __forceinline__ int64_t locate_point(const ng_octree& t, const double x[3], int level) {
+  const int res = t.r0 << level;
+  const int tl = level + t.n_virtual;
+  uint64_t code = morton(bin_axis(x[0], res), bin_axis(x[1], res), bin_axis(x[2], res));
+  return rank_lookup(t.bitmap[tl], t.rank[tl], code);
+}
+
+// 35 -> h -> 1 decoder in fp32; weights broadcast from shared memory.
+__device__ __forceinline__ float mlp_eval(const float* __restrict__ dec, int h, const float xin[3],
+                                          const float* zrow, bool& nonfinite) {
+  float in[35];
+  in[0] = xin[0];
+  in[1] = xin[1];
+  in[2] = xin[2];
+#pragma unroll
+  for (int k = 0; k < 32; ++k) in[3 + k] = zrow[k];
+  float chk = 0.f;
+#pragma unroll
+  for (int k = 0; k < 35; ++k) chk += in[k] - in[k];
+  nonfinite = !(chk == 0.f);
+  const float* W2 = dec + h * NG_W1_STRIDE;
+  float out = W2[h];  // b2
+#pragma unroll 2
+  for (int j = 0; j < h; ++j) {
+    const float4* row = reinterpret_cast<const float4*>(dec + j * NG_W1_STRIDE);
+    float4 r0 = row[0], r1 = row[1], r2 = row[2], r3 = row[3], r4 = row[4];
+    float4 r5 = row[5], r6 = row[6], r7 = row[7], r8 = row[8];
+    float a0 = r8.w;  // b1
+    float a1 = 0.f, a2 = 0.f, a3 = 0.f;
+    a0 = fmaf(r0.x, in[0], a0); a1 = fmaf(r0.y, in[1], a1); a2 = fmaf(r0.z, in[2], a2); a3 = fmaf(r0.w, in[3], a3);
+    a0 = fmaf(r1.x, in[4], a0); a1 = fmaf(r1.y, in[5], a1); a2 = fmaf(r1.z, in[6], a2); a3 = fmaf(r1.w, in[7], a3);
+    a0 = fmaf(r2.x, in[8], a0); a1 = fmaf(r2.y, in[9], a1); a2 = fmaf(r2.z, in[10], a2); a3 = fmaf(r2.w, in[11], a3);
+    a0 = fmaf(r3.x, in[12], a0); a1 = fmaf(r3.y, in[13], a1); a2 = fmaf(r3.z, in[14], a2); a3 = fmaf(r3.w, in[15], a3);
+    a0 = fmaf(r4.x, in[16], a0); a1 = fmaf(r4.y, in[17], a1); a2 = fmaf(r4.z, in[18], a2); a3 = fmaf(r4.w, in[19], a3);
+    a0 = fmaf(r5.x, in[20], a0); a1 = fmaf(r5.y, in[21], a1); a2 = fmaf(r5.z, in[22], a2); a3 = fmaf(r5.w, in[23], a3);
+    a0 = fmaf(r6.x, in[24], a0); a1 = fmaf(r6.y, in[25], a1); a2 = fmaf(r6.z, in[26], a2); a3 = fmaf(r6.w, in[27], a3);
+    a0 = fmaf(r7.x, in[28], a0); a1 = fmaf(r7.y, in[29], a1); a2 = fmaf(r7.z, in[30], a2); a3 = fmaf(r7.w, in[31], a3);
+    a0 = fmaf(r8.x, in[32], a0); a1 = fmaf(r8.y, in[33], a1); a2 = fmaf(r8.z, in[34], a2);
+    float pre = (a0 + a1) + (a2 + a3);
+    out = fmaf(W2[j], fmaxf(pre, 0.f), out);
+  }
+  return out;
+}
+
+// Per-lane outcome of one evaluation.
+struct EvalLane {
+  unsigned present;   // bit l-1: voxel exists at level l
+  bool inside;        // inside the query_field level (true when not tested)
+};
+
+// Evaluate the warp's 32 points. `emit(L, value_f32, nonfinite, lane)` is called
+// warp-uniformly for every decoder level L in ctx.out_mask, in ascending L,
+// after the lane's z_L is complete; lanes decide what to do with it.
+template <class Emit>
+__device__ __forceinline__ EvalLane warp_eval(const ng_octree& tree, const EvalCtx& c, WarpScratch& ws,
+                                              bool act, const double x[3], Emit&& emit) {
+  const int lane = (int)lane_id();
+  EvalLane res;
+  res.present = 0;
+  res.inside = true;
+  bool dec = act;
+  if (act && c.inside_level >= 0) {
+    res.inside = locate_point(tree, x, c.inside_level) >= 0;
+    dec = res.inside;
+  }
+  const int G = c.gather_level;
+  const int resG = tree.r0 << G;
+  int cell[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) cell[a] = bin_axis(x[a], resG);
+  const float xf[3] = {(float)x[0], (float)x[1], (float)x[2]};
+#pragma unroll
+  for (int p = 0; p < 32; ++p) ws.zt[p][lane] = 0.f;
+
+  for (int l = 1; l <= G; ++l) {
+    const int sh = G - l;
+    const int resl = resG >> sh;
+    const int tl = l + tree.n_virtual;
+    const int ci = cell[0] >> sh, cj = cell[1] >> sh, ck = cell[2] >> sh;
+    int64_t idx = -1;
+    if (dec) idx = rank_lookup(tree.bitmap[tl], tree.rank[tl], morton(ci, cj, ck));
+    const bool pres = idx >= 0;
+    int4 ia = make_int4(0, 0, 0, 0), ib = ia;
+    float4 wa = make_float4(0.f, 0.f, 0.f, 0.f), wb = wa;
+    if (pres) {
+      res.present |= 1u << (l - 1);
+      const int4* cr = reinterpret_cast<const int4*>(tree.corners[tl] + 8 * idx);
+      ia = __ldg(cr);
+      ib = __ldg(cr + 1);
+      // u = clip(f - cell, 0, 1) with f = (x + 1) * (res / 2)  (field.py:115-116)
+      const double half = 0.5 * (double)resl;
+      float u[3];
+      const int cc[3] = {ci, cj, ck};
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        double f = dsub(dmul(dadd(x[a], 1.0), half), (double)cc[a]);
+        f = f < 0.0 ? 0.0 : (f > 1.0 ? 1.0 : f);
+        u[a] = (float)f;
+      }
+      const float wx0 = 1.f - u[0], wy0 = 1.f - u[1], wz0 = 1.f - u[2];
+      // corner j weight = wx[j&1] * wy[j>>1&1] * wz[j>>2&1]  (field.py:122-135)
+      wa = make_float4(wx0 * wy0 * wz0, u[0] * wy0 * wz0, wx0 * u[1] * wz0, u[0] * u[1] * wz0);
+      wb = make_float4(wx0 * wy0 * u[2], u[0] * wy0 * u[2], wx0 * u[1] * u[2], u[0] * u[1] * u[2]);
+    }
+    ws.ids[lane][0] = ia;
+    ws.ids[lane][1] = ib;
+    ws.w[lane][0] = wa;
+    ws.w[lane][1] = wb;
+    unsigned pm = __ballot_sync(FULL, pres);
+    __syncwarp();
+    // lane = channel: coalesced 128-byte corner rows
+    const float* __restrict__ Zc = c.Z + lane;
+    while (pm) {
+      const int p0 = __ffs(pm) - 1;
+      pm &= pm - 1;
+      const int p1 = pm ? __ffs(pm) - 1 : -1;
+      if (p1 >= 0) pm &= pm - 1;
+      const int4 a0 = ws.ids[p0][0], b0 = ws.ids[p0][1];
+      const float4 u0 = ws.w[p0][0], v0 = ws.w[p0][1];
+      float s0 = u0.x * __ldg(Zc + 32 * (int64_t)a0.x);
+      s0 = fmaf(u0.y, __ldg(Zc + 32 * (int64_t)a0.y), s0);
+      s0 = fmaf(u0.z, __ldg(Zc + 32 * (int64_t)a0.z), s0);
+      s0 = fmaf(u0.w, __ldg(Zc + 32 * (int64_t)a0.w), s0);
+      s0 = fmaf(v0.x, __ldg(Zc + 32 * (int64_t)b0.x), s0);
+      s0 = fmaf(v0.y, __ldg(Zc + 32 * (int64_t)b0.y), s0);
+      s0 = fmaf(v0.z, __ldg(Zc + 32 * (int64_t)b0.z), s0);
+      s0 = fmaf(v0.w, __ldg(Zc + 32 * (int64_t)b0.w), s0);
+      if (p1 >= 0) {
+        const int4 a1 = ws.ids[p1][0], b1 = ws.ids[p1][1];
+        const float4 u1 = ws.w[p1][0], v1 = ws.w[p1][1];
+        float s1 = u1.x * __ldg(Zc + 32 * (int64_t)a1.x);
+        s1 = fmaf(u1.y, __ldg(Zc + 32 * (int64_t)a1.y), s1);
+        s1 = fmaf(u1.z, __ldg(Zc + 32 * (int64_t)a1.z), s1);
+        s1 = fmaf(u1.w, __ldg(Zc + 32 * (int64_t)a1.w), s1);
+        s1 = fmaf(v1.x, __ldg(Zc + 32 * (int64_t)b1.x), s1);
+        s1 = fmaf(v1.y, __ldg(Zc + 32 * (int64_t)b1.y), s1);
+        s1 = fmaf(v1.z, __ldg(Zc + 32 * (int64_t)b1.z), s1);
+        s1 = fmaf(v1.w, __ldg(Zc + 32 * (int64_t)b1.w), s1);
+        ws.zt[p1][lane] += s1;
+      }
+      ws.zt[p0][lane] += s0;
+    }
+    __syncwarp();
+    if ((c.out_mask >> (l - 1)) & 1) {
+      const bool any = __any_sync(FULL, dec && (res.present != 0));
+      float d = 0.f;
+      bool bad = false;
+      if (any) {
+        const float* decw = c.dec + (l - c.dec_first) * c.dec_stride;
+        d = mlp_eval(decw, c.h, xf, &ws.zt[lane][0], bad);
+      }
+      emit(l, d, bad && dec && res.present != 0, res);
+    }
+  }
+  __syncwarp();
+  return res;
+}
+
+// Stage decoder blocks [first, last] into shared memory (whole CTA).
+__device__ __forceinline__ void stage_decoders(float* dst, const float* __restrict__ src, int first,
+                                               int last, int stride) {
+  const int n = (last - first + 1) * stride;
+  const float4* s4 = reinterpret_cast<const float4*>(src + (first - 1) * stride);
+  float4* d4 = reinterpret_cast<float4*>(dst);
+  for (int i = threadIdx.x; i < n / 4; i += blockDim.x) d4[i] = __ldg(s4 + i);
+  __syncthreads();
+}
+
+// Counters accumulated per lane and flushed once per warp.
+struct LaneCounters {
+  long long evals = 0, missing = 0, empty = 0, nonfinite = 0;
+  __device__ __forceinline__ void flush(ng_counters* d) {
+    long long v[4] = {evals, missing, empty, nonfinite};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+#pragma unroll
+      for (int o = 16; o; o >>= 1) v[k] += __shfl_xor_sync(FULL, v[k], o);
+    }
+    if (lane_id() == 0 && d != nullptr) {
+      if (v[0]) atomicAdd((unsigned long long*)&d->decoder_evals, (unsigned long long)v[0]);
+      if (v[1]) atomicAdd((unsigned long long*)&d->evals_missing_level, (unsigned long long)v[1]);
+      if (v[2]) atomicAdd((unsigned long long*)&d->empty_fallbacks, (unsigned long long)v[2]);
+      if (v[3]) atomicAdd((unsigned long long*)&d->nonfinite_inputs, (unsigned long long)v[3]);
+    }
+  }
+};
+
+// Full query_field / blend / predict semantics for one lane: combines the
+// emitted decoder outputs into the value the reference returns.
+struct BlendAcc {
+  int base;        // decoder level for predict / lower blend level
+  double alpha;    // 0 -> plain predict(base)
+  double lo = 0.0, hi = 0.0;
+};
+
+}  // namespace ng

@@ -1,0 +1,802 @@
+// Frame rendering: camera rays, sparse sphere tracing with persistent-lane
+// ray compaction, central-difference normals and Lambert shading
+// (render.py:43-448).
+//
+// The march is a persistent kernel: every lane owns one ray and, the moment
+// that ray terminates, pulls the next one from a global work counter, so a
+// warp keeps 32 live rays until the work runs out despite per-ray iteration
+// counts ranging from 1 to ~100. Each iteration is one warp-cooperative
+// evaluation (eval.cuh). All control-flow arithmetic (t, clamp, stop rules)
+// is fp64 in the reference's operation order; only features and the MLP are
+// fp32.
+#include "eval.cuh"
+
+#include <algorithm>
+
+namespace ng {
+
+int grid_for(int64_t n, int nt);
+size_t level_scratch_bytes(int64_t max_pairs);
+int traverse_level(const ng_octree& tree, const ng_ray* rays, int t, bool final, const ng_pair* in,
+                   const int64_t* d_count_in, int64_t in_cap, ng_pair* out_pairs, ng_hit_pair* out_hits,
+                   int64_t* d_count_out, int64_t out_cap, void* scratch, size_t scratch_bytes,
+                   cudaStream_t s);
+
+constexpr int R_NW = 8;  // warps per CTA for march / normals
+
+// Pixel-centre rays, bit-exact with Camera.rays (render.py:74-88), fused with
+// the per-pixel output defaults and the background colour.
+__global__ void k_camera_rays(ng_camera cam, ng_ray* __restrict__ rays, ng_frame fr, uint8_t bg0, uint8_t bg1,
+                              uint8_t bg2, int64_t* d_root_count) {
+  const int64_t n = (int64_t)cam.width * cam.height;
+  if (blockIdx.x == 0 && threadIdx.x == 0 && d_root_count) *d_root_count = n;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (rays) {
+      const int px_i = (int)(i % cam.width), py_i = (int)(i / cam.width);
+      double px = dmul(dmul(dsub(dmul(2.0, dadd((double)px_i, 0.5)) / (double)cam.width, 1.0), cam.tan_half),
+                       cam.aspect);
+      double py = dmul(dsub(1.0, dmul(2.0, dadd((double)py_i, 0.5)) / (double)cam.height), cam.tan_half);
+      double d[3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) d[a] = dadd(dadd(cam.fwd[a], dmul(px, cam.right[a])), dmul(py, cam.up[a]));
+      double nrm = __dsqrt_rn(dadd(dadd(dmul(d[0], d[0]), dmul(d[1], d[1])), dmul(d[2], d[2])));
+      ng_ray r;
+      make_ray(cam.position[0], cam.position[1], cam.position[2], d[0] / nrm, d[1] / nrm, d[2] / nrm, r);
+      rays[i] = r;
+    }
+    if (fr.hit) {
+      fr.hit[i] = 0;
+      fr.t[i] = __longlong_as_double(0x7ff8000000000000ll);
+      fr.normal[3 * i] = 0.0;
+      fr.normal[3 * i + 1] = 0.0;
+      fr.normal[3 * i + 2] = 0.0;
+      fr.normal_ok[i] = 0;
+      fr.iterations[i] = 0;
+      fr.evals[i] = 0;
+      fr.color[3 * i] = bg0;
+      fr.color[3 * i + 1] = bg1;
+      fr.color[3 * i + 2] = bg2;
+    }
+  }
+}
+
+__global__ void k_set_count(int64_t* p, int64_t v) { *p = v; }
+
+__global__ void k_frame_defaults(ng_frame fr, int64_t n, uint8_t bg0, uint8_t bg1, uint8_t bg2) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    fr.hit[i] = 0;
+    fr.t[i] = __longlong_as_double(0x7ff8000000000000ll);
+    fr.normal[3 * i] = 0.0;
+    fr.normal[3 * i + 1] = 0.0;
+    fr.normal[3 * i + 2] = 0.0;
+    fr.normal_ok[i] = 0;
+    fr.iterations[i] = 0;
+    fr.evals[i] = 0;
+    fr.color[3 * i] = bg0;
+    fr.color[3 * i + 1] = bg1;
+    fr.color[3 * i + 2] = bg2;
+  }
+}
+
+// ray_segments over the final list plus the list of rays that have one.
+__global__ void k_segments_active(const ng_hit_pair* __restrict__ hits, const int64_t* __restrict__ d_count,
+                                  int64_t cap, int64_t* __restrict__ seg_start, int64_t* __restrict__ seg_end,
+                                  int32_t* __restrict__ active, unsigned long long* d_active) {
+  int64_t n = *d_count;
+  if (n > cap) n = cap;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < n; base += stride) {
+    const int64_t i = base + threadIdx.x;
+    bool first = false;
+    int32_t r = -1;
+    if (i < n) {
+      r = hits[i].ray;
+      first = (i == 0 || hits[i - 1].ray != r);
+      if (first) seg_start[r] = i;
+      if (i == n - 1 || hits[i + 1].ray != r) seg_end[r] = i + 1;
+    }
+    const unsigned m = __ballot_sync(FULL, first);
+    if (m) {
+      unsigned long long b = 0;
+      const int leader = __ffs(m) - 1;
+      if ((int)lane_id() == leader) b = atomicAdd(d_active, (unsigned long long)__popc(m));
+      b = __shfl_sync(FULL, b, leader);
+      if (first) active[b + __popc(m & lanemask_lt())] = r;
+    }
+  }
+}
+
+struct MarchArgs {
+  ng_render_cfg cfg;
+  int G, out_mask, dec_first, dec_last, passes;
+  int blend_base;
+  double blend_alpha;
+  const ng_ray* rays;
+  const int32_t* work;           // ray ids to trace, or null for 0..n_work-1
+  const unsigned long long* d_n_work;
+  int64_t n_work;
+  const ng_hit_pair* hits;
+  const int64_t* seg_start;
+  const int64_t* seg_end;
+  uint8_t* hit;
+  double* t;
+  int32_t* iters;
+  int32_t* evals;
+  int32_t* hit_list;             // optional: ids of hit rays
+  unsigned long long* d_hit_count;
+  unsigned long long* work_counter;
+  ng_counters* counters;
+};
+
+// One lane's query_field (render.py:155-171) result assembled from the
+// decoder outputs emitted by warp_eval (blend of predict(base), predict(base+1)).
+struct FieldValue {
+  double lo = 0.0, hi = 0.0;
+};
+
+template <int NW>
+__global__ void __launch_bounds__(NW * 32) k_march(const __grid_constant__ ng_octree tree, ng_field f,
+                                                  const __grid_constant__ MarchArgs A) {
+  extern __shared__ float4 smem4[];
+  float* dec = reinterpret_cast<float*>(smem4);
+  WarpScratch* wsa = reinterpret_cast<WarpScratch*>(dec + (A.dec_last - A.dec_first + 1) * f.dec_stride);
+  stage_decoders(dec, f.decoders, A.dec_first, A.dec_last, f.dec_stride);
+  WarpScratch& ws = wsa[threadIdx.x >> 5];
+  EvalCtx c;
+  c.Z = f.Z;
+  c.dec = dec;
+  c.dec_first = A.dec_first;
+  c.dec_stride = f.dec_stride;
+  c.h = f.h;
+  c.gather_level = A.G;
+  c.inside_level = A.cfg.trace_level;
+  c.out_mask = A.out_mask;
+  const int lane = (int)lane_id();
+  const int64_t n_work = A.d_n_work ? (int64_t)*A.d_n_work : A.n_work;
+  const int tl = A.cfg.trace_level + tree.n_virtual;
+  const int res = tree.r0 << A.cfg.trace_level;
+  const double edge = 2.0 / (double)res;
+  const uint64_t* __restrict__ codes = tree.codes[tl];
+  const double NaN = __longlong_as_double(0x7ff8000000000000ll);
+  LaneCounters lc;
+
+  int ray = -1;
+  bool drained = false, ready = false;
+  int64_t cur = 0, end = 0;
+  double t = 0.0, prev = NaN;
+  int it = 0, ev = 0;
+  double o[3] = {0, 0, 0}, d[3] = {0, 0, 0};
+
+  auto finish = [&](bool is_hit, double th) {
+    A.hit[ray] = is_hit ? 1 : 0;
+    A.t[ray] = is_hit ? th : NaN;
+    A.iters[ray] = it;
+    A.evals[ray] = ev;
+    ray = -1;
+  };
+
+  while (true) {
+    // ---- acquire rays and advance each to its next query point (render.py:200-238)
+    while (true) {
+      const bool want = (ray < 0) && !drained;
+      const unsigned wm = __ballot_sync(FULL, want);
+      if (wm) {
+        const int leader = __ffs(wm) - 1;
+        unsigned long long b = 0;
+        if (lane == leader) b = atomicAdd(A.work_counter, (unsigned long long)__popc(wm));
+        b = __shfl_sync(FULL, b, leader);
+        if (want) {
+          const int64_t k = (int64_t)b + __popc(wm & lanemask_lt());
+          if (k >= n_work) {
+            drained = true;
+          } else {
+            ray = A.work ? A.work[k] : (int)k;
+            cur = A.seg_start[ray];
+            end = A.seg_end[ray];
+            t = 0.0;
+            prev = NaN;
+            it = 0;
+            ev = 0;
+            ready = false;
+            const ng_ray* rp = A.rays + ray;
+            o[0] = rp->o[0]; o[1] = rp->o[1]; o[2] = rp->o[2];
+            d[0] = rp->d[0]; d[1] = rp->d[1]; d[2] = rp->d[2];
+          }
+        }
+      }
+      if (ray >= 0 && !ready) {
+        bool dead = false;
+        while (true) {
+          if (cur >= end || t > A.cfg.far_plane) {
+            dead = true;
+            break;
+          }
+          const ng_hit_pair h = A.hits[cur];
+          if (t >= h.t_exit) {
+            ++cur;
+            prev = NaN;
+            continue;
+          }
+          if (t < h.t_enter) {
+            const double t_in = dadd(h.t_enter, A.cfg.skip_eps);
+            if (t_in >= h.t_exit) {  // grazing sliver thinner than the nudge
+              ++cur;
+              continue;
+            }
+            t = t_in;
+          }
+          break;
+        }
+        if (dead) finish(false, 0.0);
+        else ready = true;
+      }
+      if (!__any_sync(FULL, ray < 0 && !drained)) break;
+    }
+    const bool act = ray >= 0;
+    if (!__any_sync(FULL, act)) break;
+
+    // ---- query point: x = o + t d clamped into the current voxel (render.py:244-245)
+    double x[3] = {0.0, 0.0, 0.0};
+    if (act) {
+      const uint64_t code = __ldg(codes + A.hits[cur].voxel);
+      const int cc[3] = {(int)compact3(code), (int)compact3(code >> 1), (int)compact3(code >> 2)};
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        const double lo = cell_lo(cc[a], res);
+        const double hi = dadd(lo, edge);
+        const double top = dsub(hi, dmul(dsub(hi, lo), 1e-9));  // clamp_into, octree.py:293-300
+        double v = dadd(o[a], dmul(t, d[a]));
+        v = np_max(v, lo);
+        v = np_min(v, top);
+        x[a] = v;
+      }
+    }
+    FieldValue fv;
+    const EvalLane er = warp_eval(tree, c, ws, act, x, [&](int L, float dv, bool bad, const EvalLane& e) {
+      if (!act || !e.inside) return;
+      double v;
+      if (e.present & ((1u << L) - 1u)) {
+        v = (double)dv;
+        lc.evals += 1;
+        if (!((e.present >> (L - 1)) & 1u)) lc.missing += 1;
+        if (bad) lc.nonfinite += 1;
+      } else {
+        v = empty_value(tree, x);
+        lc.empty += 1;
+      }
+      if (L == A.blend_base) fv.lo = v; else fv.hi = v;
+    });
+
+    // ---- stop rules (render.py:247-272)
+    if (act) {
+      double dval;
+      if (!er.inside) {
+        dval = empty_value(tree, x);
+        lc.empty += 1;
+      } else if (A.blend_alpha != 0.0) {
+        dval = dadd(dmul(dsub(1.0, A.blend_alpha), fv.lo), dmul(A.blend_alpha, fv.hi));
+      } else {
+        dval = fv.lo;
+      }
+      ev += A.passes;
+      it += 1;
+      const bool is_hit = dval < A.cfg.delta;
+      const bool stalled = !is_hit && (dval >= prev) && (fabs(dsub(dval, prev)) < A.cfg.osc_tol);
+      if (is_hit) {
+        if (A.hit_list) {
+          const unsigned long long slot = atomicAdd(A.d_hit_count, 1ull);
+          A.hit_list[slot] = ray;
+        }
+        finish(true, dadd(t, dval));
+      } else if (stalled || it >= A.cfg.max_iters) {
+        finish(false, 0.0);
+      } else {
+        prev = dval;
+        t = dadd(t, dval);
+        ready = false;
+      }
+    }
+  }
+  lc.flush(A.counters);
+}
+
+struct NormalArgs {
+  ng_render_cfg cfg;
+  int G, out_mask, dec_first, dec_last;
+  int blend_base;
+  double blend_alpha;
+  const double* pts;                 // explicit points, or null: hit rays below
+  int64_t n_pts;
+  const ng_ray* rays;
+  const int32_t* hit_list;
+  const unsigned long long* d_hit_count;
+  const double* t_hit;
+  double* normal;                    // per point (explicit) or per ray
+  uint8_t* ok;
+  uint8_t* color;                    // per ray when shading in place, else null
+  ng_counters* counters;
+};
+
+// normals (render.py:277-300) + shade (render.py:303-314) for hit pixels.
+template <int NW>
+__global__ void __launch_bounds__(NW * 32) k_normals(const __grid_constant__ ng_octree tree, ng_field f,
+                                                    const __grid_constant__ NormalArgs A) {
+  extern __shared__ float4 smem4[];
+  float* dec = reinterpret_cast<float*>(smem4);
+  WarpScratch* wsa = reinterpret_cast<WarpScratch*>(dec + (A.dec_last - A.dec_first + 1) * f.dec_stride);
+  stage_decoders(dec, f.decoders, A.dec_first, A.dec_last, f.dec_stride);
+  WarpScratch& ws = wsa[threadIdx.x >> 5];
+  EvalCtx c;
+  c.Z = f.Z;
+  c.dec = dec;
+  c.dec_first = A.dec_first;
+  c.dec_stride = f.dec_stride;
+  c.h = f.h;
+  c.gather_level = A.G;
+  c.inside_level = A.cfg.trace_level;
+  c.out_mask = A.out_mask;
+  const int64_t n = A.pts ? A.n_pts : (int64_t)*A.d_hit_count;
+  const double eps = A.cfg.normal_eps;
+  LaneCounters lc;
+  const int64_t n_chunks = (n + 31) / 32;
+  for (int64_t chunk = (int64_t)blockIdx.x * NW + (threadIdx.x >> 5); chunk < n_chunks;
+       chunk += (int64_t)gridDim.x * NW) {
+    const int64_t i = chunk * 32 + lane_id();
+    const bool act = i < n;
+    int64_t dst = i;
+    double p[3] = {0.0, 0.0, 0.0};
+    if (act) {
+      if (A.pts) {
+        p[0] = A.pts[3 * i];
+        p[1] = A.pts[3 * i + 1];
+        p[2] = A.pts[3 * i + 2];
+      } else {
+        dst = A.hit_list[i];
+        const ng_ray* rp = A.rays + dst;
+        const double th = A.t_hit[dst];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) p[a] = dadd(rp->o[a], dmul(th, rp->d[a]));  // render.py:396
+      }
+    }
+    double vals[6];
+#pragma unroll 1
+    for (int j = 0; j < 6; ++j) {
+      const int axis = j % 3;
+      double x[3] = {p[0], p[1], p[2]};
+      x[axis] = (j < 3) ? dadd(x[axis], eps) : dsub(x[axis], eps);
+#pragma unroll
+      for (int a = 0; a < 3; ++a) x[a] = np_min(np_max(x[a], -1.0), 1.0);
+      FieldValue fv;
+      const EvalLane er = warp_eval(tree, c, ws, act, x, [&](int L, float dv, bool bad, const EvalLane& e) {
+        if (!act || !e.inside) return;
+        double v;
+        if (e.present & ((1u << L) - 1u)) {
+          v = (double)dv;
+          lc.evals += 1;
+          if (!((e.present >> (L - 1)) & 1u)) lc.missing += 1;
+          if (bad) lc.nonfinite += 1;
+        } else {
+          v = empty_value(tree, x);
+          lc.empty += 1;
+        }
+        if (L == A.blend_base) fv.lo = v; else fv.hi = v;
+      });
+      double v = 0.0;
+      if (act) {
+        if (!er.inside) {
+          v = empty_value(tree, x);
+          lc.empty += 1;
+        } else if (A.blend_alpha != 0.0) {
+          v = dadd(dmul(dsub(1.0, A.blend_alpha), fv.lo), dmul(A.blend_alpha, fv.hi));
+        } else {
+          v = fv.lo;
+        }
+      }
+      vals[j] = v;
+    }
+    if (act) {
+      const double two_eps = 2.0 * eps;
+      double g[3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) g[a] = dsub(vals[a], vals[3 + a]) / two_eps;
+      const double nrm = __dsqrt_rn(dadd(dadd(dmul(g[0], g[0]), dmul(g[1], g[1])), dmul(g[2], g[2])));
+      const bool ok = isfinite(nrm) && nrm > 1e-12;
+      double nv[3] = {0.0, 0.0, 0.0};
+      if (ok) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) nv[a] = g[a] / nrm;
+      }
+#pragma unroll
+      for (int a = 0; a < 3; ++a) A.normal[3 * dst + a] = nv[a];
+      A.ok[dst] = ok ? 1 : 0;
+      if (A.color) {
+        // shade (render.py:303-314) with the fp64 normal
+        double lam = dadd(dadd(dmul(nv[0], A.cfg.light[0]), dmul(nv[1], A.cfg.light[1])),
+                          dmul(nv[2], A.cfg.light[2]));
+        lam = lam < 0.0 ? 0.0 : (lam > 1.0 ? 1.0 : lam);
+        const double amb = A.cfg.ambient;
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) {
+          double rgb = dmul(A.cfg.albedo[ch], dadd(amb, dmul(dsub(1.0, amb), lam)));
+          rgb = rgb < 0.0 ? 0.0 : (rgb > 1.0 ? 1.0 : rgb);
+          A.color[3 * dst + ch] = (uint8_t)dadd(dmul(rgb, 255.0), 0.5);
+        }
+      }
+    }
+  }
+  lc.flush(A.counters);
+}
+
+__global__ void k_shade(const uint8_t* __restrict__ hit, const double* __restrict__ normal, int64_t n,
+                        ng_render_cfg cfg, uint8_t* __restrict__ color) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double rgb[3];
+    if (hit[i]) {
+      double lam = dadd(dadd(dmul(normal[3 * i], cfg.light[0]), dmul(normal[3 * i + 1], cfg.light[1])),
+                        dmul(normal[3 * i + 2], cfg.light[2]));
+      lam = lam < 0.0 ? 0.0 : (lam > 1.0 ? 1.0 : lam);
+      for (int ch = 0; ch < 3; ++ch)
+        rgb[ch] = dmul(cfg.albedo[ch], dadd(cfg.ambient, dmul(dsub(1.0, cfg.ambient), lam)));
+    } else {
+      for (int ch = 0; ch < 3; ++ch) rgb[ch] = cfg.background[ch];
+    }
+    for (int ch = 0; ch < 3; ++ch) {
+      double v = rgb[ch] < 0.0 ? 0.0 : (rgb[ch] > 1.0 ? 1.0 : rgb[ch]);
+      color[3 * i + ch] = (uint8_t)dadd(dmul(v, 255.0), 0.5);
+    }
+  }
+}
+
+__global__ void k_hit_points(const ng_ray* __restrict__ rays, const uint8_t* __restrict__ hit,
+                             const double* __restrict__ t, int64_t n, double* __restrict__ pts) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    for (int a = 0; a < 3; ++a) pts[3 * i + a] = hit[i] ? dadd(rays[i].o[a], dmul(t[i], rays[i].d[a])) : 0.0;
+  }
+}
+
+__global__ void k_finish_stats(ng_frame_stats* st, int n_levels, int64_t pair_cap, int64_t hit_cap,
+                               const unsigned long long* d_hits, const unsigned long long* d_active) {
+  int64_t over = 0;
+  for (int t = 1; t < n_levels; ++t) over |= (st->pairs[t] > pair_cap);
+  over |= (st->pairs[n_levels] > hit_cap);
+  st->overflow = over;
+  st->visible = (int64_t)*d_hits;
+  st->active_rays = (int64_t)*d_active;
+}
+
+// ------------------------------------------------------------------ host side
+
+struct LodPlan {
+  int G, out_mask, dec_first, dec_last, passes, blend_base;
+  double alpha;
+};
+
+static LodPlan plan_lod(const ng_render_cfg& cfg) {
+  // blend (field.py:226-239) / query_field (render.py:159) for the resolved lod
+  LodPlan p;
+  const double lod = cfg.lod < 1.0 ? 1.0 : cfg.lod;
+  const int base = (int)floor(lod);
+  const double alpha = lod - (double)base;
+  p.blend_base = base;
+  p.alpha = alpha;
+  if (alpha == 0.0) {
+    p.out_mask = 1 << (base - 1);
+    p.G = std::max(base, cfg.trace_level);
+    p.dec_first = p.dec_last = base;
+    p.passes = 1;
+  } else {
+    p.out_mask = (1 << (base - 1)) | (1 << base);
+    p.G = std::max(base + 1, cfg.trace_level);
+    p.dec_first = base;
+    p.dec_last = base + 1;
+    p.passes = 2;
+  }
+  return p;
+}
+
+template <class K>
+static int prep_kernel(K kernel, size_t smem, int nt, int& per_sm) {
+  static size_t configured = 0;
+  if (smem > configured) {
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)std::max<size_t>(smem, 48 * 1024));
+    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute");
+    configured = smem;
+  }
+  per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, nt, smem);
+  if (per_sm < 1) per_sm = 1;
+  return NG_OK;
+}
+
+static int launch_march(const ng_octree& tree, const ng_field& f, MarchArgs& A, cudaStream_t s) {
+  const size_t smem = (size_t)(A.dec_last - A.dec_first + 1) * f.dec_stride * 4 + R_NW * sizeof(WarpScratch);
+  int per_sm;
+  int r = prep_kernel(k_march<R_NW>, smem, R_NW * 32, per_sm);
+  if (r) return r;
+  k_march<R_NW><<<sm_count() * per_sm, R_NW * 32, smem, s>>>(tree, f, A);
+  NG_CHECK_LAUNCH("k_march");
+  return NG_OK;
+}
+
+static int launch_normals(const ng_octree& tree, const ng_field& f, NormalArgs& A, int64_t max_n,
+                          cudaStream_t s) {
+  const size_t smem = (size_t)(A.dec_last - A.dec_first + 1) * f.dec_stride * 4 + R_NW * sizeof(WarpScratch);
+  int per_sm;
+  int r = prep_kernel(k_normals<R_NW>, smem, R_NW * 32, per_sm);
+  if (r) return r;
+  int64_t want = (max_n + 32 * R_NW - 1) / (32 * R_NW);
+  int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sm_count() * per_sm));
+  k_normals<R_NW><<<grid, R_NW * 32, smem, s>>>(tree, f, A);
+  NG_CHECK_LAUNCH("k_normals");
+  return NG_OK;
+}
+
+static void background_u8(const ng_render_cfg& cfg, uint8_t bg[3]) {
+  for (int c = 0; c < 3; ++c) {
+    double v = cfg.background[c] < 0.0 ? 0.0 : (cfg.background[c] > 1.0 ? 1.0 : cfg.background[c]);
+    bg[c] = (uint8_t)(v * 255.0 + 0.5);
+  }
+}
+
+// Workspace layout (all offsets 256-byte aligned).
+struct WsLayout {
+  size_t rays, pairs_a, pairs_b, hits, seg_start, seg_end, active, hit_list, scratch, ctr, total;
+  size_t scratch_bytes;
+};
+
+static size_t al(size_t x) { return (x + 255) & ~size_t(255); }
+
+static WsLayout layout(int64_t n, int64_t pair_cap, int64_t hit_cap) {
+  WsLayout L;
+  size_t o = 0;
+  L.rays = o; o = al(o + (size_t)n * sizeof(ng_ray));
+  L.pairs_a = o; o = al(o + (size_t)pair_cap * sizeof(ng_pair));
+  L.pairs_b = o; o = al(o + (size_t)pair_cap * sizeof(ng_pair));
+  L.hits = o; o = al(o + (size_t)hit_cap * sizeof(ng_hit_pair));
+  L.seg_start = o; o = al(o + (size_t)n * 8);
+  L.seg_end = o; o = al(o + (size_t)n * 8);
+  L.active = o; o = al(o + (size_t)n * 4);
+  L.hit_list = o; o = al(o + (size_t)n * 4);
+  L.scratch_bytes = level_scratch_bytes(std::max<int64_t>(std::max<int64_t>(pair_cap, n), 1));
+  L.scratch = o; o = al(o + L.scratch_bytes);
+  L.ctr = o; o = al(o + 64);
+  L.total = o;
+  return L;
+}
+
+static int render_common(const ng_octree& tree, const ng_field& f, const ng_render_cfg& cfg,
+                         const ng_camera* cam, const ng_ray* user_rays, int64_t n, const ng_frame& fr,
+                         const ng_workspace& ws, ng_frame_stats* st, bool do_normals, cudaStream_t s) {
+  if (cfg.trace_level < 0 || cfg.trace_level > tree.max_level) {
+    set_error("trace level %d outside 0..%d", cfg.trace_level, tree.max_level);
+    return NG_ERR_CONFIG;
+  }
+  if (cfg.lod > (double)f.n_decoders) {
+    set_error("lod %g above max level %d", cfg.lod, f.n_decoders);
+    return NG_ERR_CONFIG;
+  }
+  const WsLayout L = layout(n, ws.pair_capacity, ws.hit_capacity);
+  if (ws.bytes < L.total) {
+    set_error("render workspace %zu < %zu bytes", ws.bytes, L.total);
+    return NG_ERR_CAPACITY;
+  }
+  char* b = (char*)ws.base;
+  ng_ray* rays = user_rays ? (ng_ray*)user_rays : (ng_ray*)(b + L.rays);
+  ng_pair* pa = (ng_pair*)(b + L.pairs_a);
+  ng_pair* pb = (ng_pair*)(b + L.pairs_b);
+  ng_hit_pair* hits = (ng_hit_pair*)(b + L.hits);
+  int64_t* seg_start = (int64_t*)(b + L.seg_start);
+  int64_t* seg_end = (int64_t*)(b + L.seg_end);
+  int32_t* active = (int32_t*)(b + L.active);
+  int32_t* hit_list = (int32_t*)(b + L.hit_list);
+  void* scratch = b + L.scratch;
+  unsigned long long* ctr = (unsigned long long*)(b + L.ctr);  // [0] active, [1] hits, [2] work
+  int r;
+  if ((r = cuda_status(cudaMemsetAsync(st, 0, sizeof(ng_frame_stats), s), "stats memset"))) return r;
+  if ((r = cuda_status(cudaMemsetAsync(ctr, 0, 64, s), "ctr memset"))) return r;
+  uint8_t bg[3];
+  background_u8(cfg, bg);
+  if (cam) {
+    k_camera_rays<<<grid_for(n, 256), 256, 0, s>>>(*cam, rays, fr, bg[0], bg[1], bg[2], &st->pairs[0]);
+    NG_CHECK_LAUNCH("k_camera_rays");
+  } else {
+    k_frame_defaults<<<grid_for(n, 256), 256, 0, s>>>(fr, n, bg[0], bg[1], bg[2]);
+    NG_CHECK_LAUNCH("k_frame_defaults");
+    k_set_count<<<1, 1, 0, s>>>(&st->pairs[0], n);  // root list (i, 0) of n rays
+    NG_CHECK_LAUNCH("k_set_count");
+  }
+  // ---- traversal (traversal.py:207-247)
+  const int target = cfg.trace_level + tree.n_virtual;
+  const ng_pair* in = nullptr;
+  int64_t in_cap = n;
+  for (int t = 0; t < target; ++t) {
+    ng_pair* out = (t % 2 == 0) ? pa : pb;
+    r = traverse_level(tree, rays, t, false, in, &st->pairs[t], in_cap, out, nullptr, &st->pairs[t + 1],
+                       ws.pair_capacity, scratch, L.scratch_bytes, s);
+    if (r) return r;
+    in = out;
+    in_cap = ws.pair_capacity;
+  }
+  r = traverse_level(tree, rays, target, true, in, &st->pairs[target], in_cap, nullptr, hits,
+                     &st->pairs[target + 1], ws.hit_capacity, scratch, L.scratch_bytes, s);
+  if (r) return r;
+  // ---- segments + active rays
+  if ((r = cuda_status(cudaMemsetAsync(seg_start, 0, n * 8, s), "seg memset"))) return r;
+  if ((r = cuda_status(cudaMemsetAsync(seg_end, 0, n * 8, s), "seg memset"))) return r;
+  k_segments_active<<<grid_for(std::max<int64_t>(ws.hit_capacity, 1), 256), 256, 0, s>>>(
+      hits, &st->pairs[target + 1], ws.hit_capacity, seg_start, seg_end, active, ctr + 0);
+  NG_CHECK_LAUNCH("k_segments_active");
+  // ---- sphere trace (render.py:174-274)
+  const LodPlan P = plan_lod(cfg);
+  MarchArgs A;
+  A.cfg = cfg;
+  A.G = P.G;
+  A.out_mask = P.out_mask;
+  A.dec_first = P.dec_first;
+  A.dec_last = P.dec_last;
+  A.passes = P.passes;
+  A.blend_base = P.blend_base;
+  A.blend_alpha = P.alpha;
+  A.rays = rays;
+  A.work = active;
+  A.d_n_work = ctr + 0;
+  A.n_work = 0;
+  A.hits = hits;
+  A.seg_start = seg_start;
+  A.seg_end = seg_end;
+  A.hit = fr.hit;
+  A.t = fr.t;
+  A.iters = fr.iterations;
+  A.evals = fr.evals;
+  A.hit_list = hit_list;
+  A.d_hit_count = ctr + 1;
+  A.work_counter = ctr + 2;
+  A.counters = &st->counters;
+  if ((r = launch_march(tree, f, A, s))) return r;
+  if (ws.ev_trace_done && (r = cuda_status(cudaEventRecord((cudaEvent_t)ws.ev_trace_done, s), "event record")))
+    return r;
+  // ---- normals + shading (render.py:399-414, 440)
+  if (do_normals) {
+    NormalArgs B;
+    B.cfg = cfg;
+    B.G = P.G;
+    B.out_mask = P.out_mask;
+    B.dec_first = P.dec_first;
+    B.dec_last = P.dec_last;
+    B.blend_base = P.blend_base;
+    B.blend_alpha = P.alpha;
+    B.pts = nullptr;
+    B.n_pts = 0;
+    B.rays = rays;
+    B.hit_list = hit_list;
+    B.d_hit_count = ctr + 1;
+    B.t_hit = fr.t;
+    B.normal = fr.normal;
+    B.ok = fr.normal_ok;
+    B.color = fr.color;
+    B.counters = &st->counters;
+    if ((r = launch_normals(tree, f, B, n, s))) return r;
+  }
+  k_finish_stats<<<1, 1, 0, s>>>(st, target + 1, ws.pair_capacity, ws.hit_capacity, ctr + 1, ctr + 0);
+  NG_CHECK_LAUNCH("k_finish_stats");
+  return NG_OK;
+}
+
+}  // namespace ng
+
+using namespace ng;
+
+extern "C" {
+
+int ng_camera_rays(const ng_camera* cam, ng_ray* rays, void* stream) {
+  int64_t n = (int64_t)cam->width * cam->height;
+  k_camera_rays<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(*cam, rays, ng_frame{}, 0, 0, 0, nullptr);
+  NG_CHECK_LAUNCH("ng_camera_rays");
+  return NG_OK;
+}
+
+size_t ng_render_workspace_bytes(int64_t n_rays, int64_t pair_capacity, int64_t hit_capacity) {
+  return layout(n_rays, pair_capacity, hit_capacity).total;
+}
+
+int ng_render_frame(const ng_octree* tree, const ng_field* fld, const ng_render_cfg* cfg, const ng_camera* cam,
+                    const ng_frame* frame, const ng_workspace* ws, ng_frame_stats* d_stats, void* stream) {
+  const int64_t n = (int64_t)cam->width * cam->height;
+  return render_common(*tree, *fld, *cfg, cam, nullptr, n, *frame, *ws, d_stats, true, (cudaStream_t)stream);
+}
+
+int ng_render_rays(const ng_octree* tree, const ng_field* fld, const ng_render_cfg* cfg, const ng_ray* rays,
+                   int64_t n_rays, const ng_frame* frame, const ng_workspace* ws, ng_frame_stats* d_stats,
+                   int32_t do_normals, void* stream) {
+  return render_common(*tree, *fld, *cfg, nullptr, rays, n_rays, *frame, *ws, d_stats, do_normals != 0,
+                       (cudaStream_t)stream);
+}
+
+int ng_sphere_trace(const ng_octree* tree, const ng_field* fld, const ng_render_cfg* cfg, const ng_ray* rays,
+                    int64_t n_rays, const ng_hit_pair* hits, const int64_t* d_hit_count,
+                    const int64_t* seg_start, const int64_t* seg_end, uint8_t* hit, double* t_hit,
+                    int32_t* iters, int32_t* evals, ng_counters* d_counters, void* stream) {
+  if (n_rays <= 0) return NG_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  unsigned long long* work = nullptr;
+  int r = cuda_status(cudaMallocAsync((void**)&work, 8, s), "ng_sphere_trace alloc");
+  if (r) return r;
+  if ((r = cuda_status(cudaMemsetAsync(work, 0, 8, s), "ng_sphere_trace memset"))) return r;
+  const LodPlan P = plan_lod(*cfg);
+  MarchArgs A;
+  A.cfg = *cfg;
+  A.G = P.G;
+  A.out_mask = P.out_mask;
+  A.dec_first = P.dec_first;
+  A.dec_last = P.dec_last;
+  A.passes = P.passes;
+  A.blend_base = P.blend_base;
+  A.blend_alpha = P.alpha;
+  A.rays = rays;
+  A.work = nullptr;
+  A.d_n_work = nullptr;
+  A.n_work = n_rays;
+  A.hits = hits;
+  A.seg_start = seg_start;
+  A.seg_end = seg_end;
+  A.hit = hit;
+  A.t = t_hit;
+  A.iters = iters;
+  A.evals = evals;
+  A.hit_list = nullptr;
+  A.d_hit_count = nullptr;
+  A.work_counter = work;
+  A.counters = d_counters;
+  (void)d_hit_count;
+  r = launch_march(*tree, *fld, A, s);
+  cudaFreeAsync(work, s);
+  return r;
+}
+
+int ng_normals(const ng_octree* tree, const ng_field* fld, const ng_render_cfg* cfg, const double* pts, int64_t k,
+               double* normal, uint8_t* ok, ng_counters* d_counters, void* stream) {
+  if (k <= 0) return NG_OK;
+  const LodPlan P = plan_lod(*cfg);
+  NormalArgs B;
+  B.cfg = *cfg;
+  B.G = P.G;
+  B.out_mask = P.out_mask;
+  B.dec_first = P.dec_first;
+  B.dec_last = P.dec_last;
+  B.blend_base = P.blend_base;
+  B.blend_alpha = P.alpha;
+  B.pts = pts;
+  B.n_pts = k;
+  B.rays = nullptr;
+  B.hit_list = nullptr;
+  B.d_hit_count = nullptr;
+  B.t_hit = nullptr;
+  B.normal = normal;
+  B.ok = ok;
+  B.color = nullptr;
+  B.counters = d_counters;
+  return launch_normals(*tree, *fld, B, k, (cudaStream_t)stream);
+}
+
+int ng_shade(const uint8_t* hit, const double* normal, int64_t n, const ng_render_cfg* cfg, uint8_t* color,
+             void* stream) {
+  if (n <= 0) return NG_OK;
+  k_shade<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(hit, normal, n, *cfg, color);
+  NG_CHECK_LAUNCH("ng_shade");
+  return NG_OK;
+}
+
+int ng_hit_points(const ng_ray* rays, const uint8_t* hit, const double* t, int64_t n, double* points,
+                  void* stream) {
+  if (n <= 0) return NG_OK;
+  k_hit_points<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(rays, hit, t, n, points);
+  NG_CHECK_LAUNCH("ng_hit_points");
+  return NG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,388 @@
+"""The neural distance field, evaluated on the GPU.
+
+Drop-in for octfield.field (field.py:1-413, forward path). A flat feature
+volume Z holds one m-vector per unique voxel corner; a query at level L
+trilinearly interpolates the containing voxel's corners at every feature
+level 1..L, sums them and decodes [x, z] with level L's MLP. Parameters are
+fp32 (as the reference stores them); the device computes the gather and the
+MLP in fp32 and the geometry (binning, weights' local coordinates, empty-
+space values, blends) in fp64, which keeps SDF values within 1e-4 of the
+reference's all-fp64 path.
+
+Device layout: Z is padded to 32 channels (128-byte rows, one coalesced
+line per corner); decoders are packed per level as W1b[h][36] = (x weights,
+feature weights, b1), W2[h], b2 (include/nglod_b200.h, ng_field).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import call, ptr, stream_ptr
+from .errors import OctfieldError, StructuralError
+from .octree import DOMAIN_MAX, DOMAIN_MIN, SparseVoxelOctree
+
+FEATURE_DIM = 32
+HIDDEN_DIM = 128
+FEATURE_INIT_SIGMA = 0.01
+
+
+@dataclass
+class Decoder:
+    """Single-hidden-layer MLP weights for one detail level (field.py:30-48)."""
+
+    W1: np.ndarray  # (h, 3 + m)
+    b1: np.ndarray  # (h,)
+    W2: np.ndarray  # (1, h)
+    b2: np.ndarray  # (1,)
+
+    def param_count(self) -> int:
+        return self.W1.size + self.b1.size + self.W2.size + self.b2.size
+
+    def astype(self, dtype) -> "Decoder":
+        return Decoder(self.W1.astype(dtype), self.b1.astype(dtype), self.W2.astype(dtype), self.b2.astype(dtype))
+
+
+def init_features(svo: SparseVoxelOctree, m: int = FEATURE_DIM, seed: int = 0) -> np.ndarray:
+    """Gaussian features, one row per unique corner (field.py:51-56)."""
+    rng = np.random.default_rng(seed)
+    return (FEATURE_INIT_SIGMA * rng.standard_normal((svo.corner_count, m))).astype(np.float32)
+
+
+def init_decoders(max_level: int, m: int = FEATURE_DIM, h: int = HIDDEN_DIM, seed: int = 0) -> list:
+    """Uniform fan-in init, one decoder per level (field.py:59-76)."""
+    rng = np.random.default_rng(seed)
+    out = []
+    for _ in range(max_level):
+        k1 = 1.0 / np.sqrt(3 + m)
+        k2 = 1.0 / np.sqrt(h)
+        out.append(Decoder(
+            rng.uniform(-k1, k1, size=(h, 3 + m)).astype(np.float32),
+            rng.uniform(-k1, k1, size=h).astype(np.float32),
+            rng.uniform(-k2, k2, size=(1, h)).astype(np.float32),
+            rng.uniform(-k2, k2, size=1).astype(np.float32),
+        ))
+    return out
+
+
+class EvalCounter:
+    """Tallies decoder work (field.py:79-90)."""
+
+    def __init__(self):
+        self.decoder_evals = 0
+        self.evals_missing_level = 0
+        self.empty_fallbacks = 0
+
+    def reset(self):
+        self.decoder_evals = 0
+        self.evals_missing_level = 0
+        self.empty_fallbacks = 0
+
+    def add(self, c) -> None:
+        self.decoder_evals += int(c[0])
+        self.evals_missing_level += int(c[1])
+        self.empty_fallbacks += int(c[2])
+
+
+def decoder_stride(h: int) -> int:
+    return h * _lib.W1_STRIDE + ((h + 1 + 3) // 4) * 4
+
+
+def pack_decoders(decoders: list, m: int) -> np.ndarray:
+    """Pack per-level decoders into the device layout (ng_field)."""
+    if m > _lib.FEAT_PAD:
+        raise StructuralError(f"feature dim {m} above the device limit {_lib.FEAT_PAD}")
+    h = decoders[0].W1.shape[0]
+    stride = decoder_stride(h)
+    buf = np.zeros((len(decoders), stride), dtype=np.float32)
+    for i, d in enumerate(decoders):
+        W1 = np.asarray(d.W1, dtype=np.float32)
+        if W1.shape != (h, 3 + m):
+            raise StructuralError("decoders must share (h, 3 + m) shapes")
+        blk = buf[i, :h * _lib.W1_STRIDE].reshape(h, _lib.W1_STRIDE)
+        blk[:, 0:3 + m] = W1
+        blk[:, 35] = np.asarray(d.b1, dtype=np.float32).ravel()
+        buf[i, h * _lib.W1_STRIDE:h * _lib.W1_STRIDE + h] = np.asarray(d.W2, dtype=np.float32).ravel()
+        buf[i, h * _lib.W1_STRIDE + h] = np.float32(np.asarray(d.b2).ravel()[0])
+    return buf
+
+
+class DeviceField:
+    """Device copies of Z (padded to 32 channels) and the packed decoders."""
+
+    def __init__(self, Z, decoders: list):
+        dev = _lib.device()
+        if isinstance(Z, torch.Tensor):
+            m = Z.shape[1]
+            z = Z.to(device=dev, dtype=torch.float32)
+        else:
+            Zn = np.asarray(Z)
+            m = Zn.shape[1]
+            z = torch.from_numpy(np.ascontiguousarray(Zn, dtype=np.float32)).to(dev)
+        if m > _lib.FEAT_PAD:
+            raise StructuralError(f"feature dim {m} above the device limit {_lib.FEAT_PAD}")
+        if m < _lib.FEAT_PAD:
+            zp = torch.zeros((z.shape[0], _lib.FEAT_PAD), dtype=torch.float32, device=dev)
+            zp[:, :m] = z
+            z = zp
+        self.Z = z.contiguous()
+        self.m = m
+        self.h = decoders[0].W1.shape[0]
+        self.n_decoders = len(decoders)
+        self.dec = torch.from_numpy(pack_decoders(decoders, m)).to(dev)
+        s = _lib.NgField()
+        s.Z = ptr(self.Z)
+        s.decoders = ptr(self.dec)
+        s.m, s.h, s.n_decoders = m, self.h, self.n_decoders
+        s.dec_stride = decoder_stride(self.h)
+        s.corner_count = self.Z.shape[0]
+        self.struct = s
+
+    def ref(self):
+        return ctypes.byref(self.struct)
+
+
+def _as_points(x):
+    pts = np.asarray(x, dtype=np.float64)
+    single = pts.ndim == 1
+    return np.atleast_2d(pts), single
+
+
+def _check_level(L, max_level):
+    if not 1 <= L <= max_level:
+        raise StructuralError(f"level {L} outside 1..{max_level}")
+
+
+class _Counters:
+    def __init__(self):
+        self.t = torch.zeros(4, dtype=torch.int64, device=_lib.device())
+
+    def ptr(self):
+        return ptr(self.t)
+
+    def host(self):
+        return self.t.cpu().numpy()
+
+
+def _run_query(svo, dfield: DeviceField, pts_dev: torch.Tensor, out_levels=0, inside_level=-1,
+               blend_base=0, blend_alpha=0.0, ncols=1, counter: EvalCounter | None = None) -> torch.Tensor:
+    n = pts_dev.shape[0]
+    out = torch.empty((n, ncols), dtype=torch.float64, device=pts_dev.device)
+    args = _lib.NgQueryArgs(out_levels, inside_level, blend_base, 0, blend_alpha)
+    cnt = _Counters()
+    call("ng_query", svo.device.ref(), dfield.ref(), ctypes.byref(args), ptr(pts_dev), n, ptr(out), cnt.ptr(),
+         stream_ptr())
+    c = cnt.host()
+    if c[3]:
+        raise OctfieldError("non-finite decoder input")
+    if counter is not None:
+        counter.add(c)
+    return out
+
+
+def _dev_points(pts: np.ndarray) -> torch.Tensor:
+    if len(pts) and (np.any(pts < DOMAIN_MIN) or np.any(pts > DOMAIN_MAX)):
+        raise StructuralError("point outside the domain box")
+    return torch.from_numpy(np.ascontiguousarray(pts)).to(_lib.device())
+
+
+# ---------------------------------------------------------------- interpolation
+
+def trilinear_weights(u: np.ndarray) -> np.ndarray:
+    """(k, 8) corner weights from local coordinates (field.py:122-135);
+    corner j at offset (j & 1, j >> 1 & 1, j >> 2 & 1). Host helper."""
+    u = np.asarray(u, dtype=np.float64)
+    cx = np.stack([1.0 - u[:, 0], u[:, 0]], axis=1)
+    cy = np.stack([1.0 - u[:, 1], u[:, 1]], axis=1)
+    cz = np.stack([1.0 - u[:, 2], u[:, 2]], axis=1)
+    j = np.arange(8)
+    return cx[:, j & 1] * cy[:, (j >> 1) & 1] * cz[:, (j >> 2) & 1]
+
+
+def _interp(svo, Z, pts, lo, hi, dfield=None):
+    df = dfield if dfield is not None else DeviceField(Z, [Decoder(np.zeros((1, 3 + np.shape(Z)[1]), np.float32),
+                                                                   np.zeros(1, np.float32), np.zeros((1, 1), np.float32),
+                                                                   np.zeros(1, np.float32))])
+    n = len(pts)
+    z = torch.zeros((n, df.m), dtype=torch.float64, device=_lib.device())
+    mask = torch.zeros((n, hi - lo + 1), dtype=torch.uint8, device=_lib.device())
+    if n:
+        d = _dev_points(pts)
+        call("ng_interp", svo.device.ref(), df.ref(), ptr(d), n, lo, hi, ptr(z), ptr(mask), stream_ptr())
+    return z.cpu().numpy(), mask.cpu().numpy().astype(bool)
+
+
+def trilinear(svo, Z, x, level: int):
+    """Interpolated features at one level (field.py:138-146): (values, mask)."""
+    pts, _ = _as_points(x)
+    if not 1 <= level <= svo.max_level:
+        raise StructuralError(f"level {level} outside 1..{svo.max_level}")
+    z, mask = _interp(svo, Z, pts, level, level)
+    return z, mask[:, 0]
+
+
+def sum_features(svo, Z, x, L: int):
+    """z(x) = sum of levels 1..L and the (n, L) presence mask (field.py:154-169)."""
+    if L < 1:
+        raise StructuralError("L must be >= 1")
+    pts, _ = _as_points(x)
+    return _interp(svo, Z, pts, 1, L)
+
+
+def decode(decoder: Decoder, x, z):
+    """d = W2 relu(W1 [x, z] + b1) + b2 (field.py:172-182), fp32 on device."""
+    pts = np.atleast_2d(np.asarray(x, dtype=np.float64))
+    z = np.atleast_2d(np.asarray(z, dtype=np.float64))
+    inp = np.concatenate([pts, z], axis=1)
+    if not np.all(np.isfinite(inp)):
+        raise OctfieldError("non-finite decoder input")
+    m = z.shape[1]
+    h = decoder.W1.shape[0]
+    dev = _lib.device()
+    blk = torch.from_numpy(pack_decoders([decoder], m)[0]).to(dev)
+    n = len(pts)
+    out = torch.empty(n, dtype=torch.float64, device=dev)
+    bad = torch.zeros(1, dtype=torch.int64, device=dev)
+    if n:
+        dx = torch.from_numpy(np.ascontiguousarray(pts)).to(dev)
+        dz = torch.from_numpy(np.ascontiguousarray(z)).to(dev)
+        call("ng_decode", ptr(blk), h, m, ptr(dx), ptr(dz), n, ptr(out), ptr(bad), stream_ptr())
+    if int(bad.item()):
+        raise OctfieldError("non-finite decoder input")
+    return out.cpu().numpy()
+
+
+def empty_space_value(svo: SparseVoxelOctree, x) -> np.ndarray:
+    """Distance to the occupied region's AABB + finest half diagonal (field.py:185-191)."""
+    pts, _ = _as_points(x)
+    n = len(pts)
+    out = torch.empty(n, dtype=torch.float64, device=_lib.device())
+    if n:
+        d = torch.from_numpy(np.ascontiguousarray(pts)).to(_lib.device())
+        call("ng_empty_value", svo.device.ref(), ptr(d), n, ptr(out), stream_ptr())
+    return out.cpu().numpy()
+
+
+# ---------------------------------------------------------------- prediction
+
+def predict(svo, Z, decoders, x, L: int, counter: EvalCounter | None = None, _dfield=None):
+    """Distance at integer level L (field.py:194-218)."""
+    pts, single = _as_points(x)
+    _check_level(L, len(decoders))
+    df = _dfield if _dfield is not None else DeviceField(Z, decoders)
+    out = _run_query(svo, df, _dev_points(pts), out_levels=1 << (L - 1), counter=counter)[:, 0].cpu().numpy()
+    return float(out[0]) if single else out
+
+
+def blend(svo, Z, decoders, x, L_tilde: float, counter: EvalCounter | None = None, _dfield=None):
+    """Continuous-level prediction (field.py:226-239)."""
+    if L_tilde > len(decoders):
+        raise StructuralError(f"blend level {L_tilde} above max {len(decoders)}")
+    L_tilde = max(float(L_tilde), 1.0)
+    base = int(np.floor(L_tilde))
+    alpha = L_tilde - base
+    if alpha == 0.0:
+        return predict(svo, Z, decoders, x, base, counter, _dfield)
+    pts, single = _as_points(x)
+    df = _dfield if _dfield is not None else DeviceField(Z, decoders)
+    out = _run_query(svo, df, _dev_points(pts), blend_base=base, blend_alpha=alpha, counter=counter)
+    out = out[:, 0].cpu().numpy()
+    return float(out[0]) if single else out
+
+
+@dataclass
+class ForwardCache:
+    """What a forward pass hands its caller (field.py:321-334). The backward
+    pass is outside this package's scope, so only the inputs
+    and outputs are kept."""
+
+    svo: SparseVoxelOctree
+    Z: np.ndarray
+    decoder: Decoder
+    L: int
+    pts: np.ndarray
+    out: np.ndarray
+
+
+def forward(svo, Z, decoders, x, L: int, _dfield=None) -> tuple:
+    """predict plus a cache (field.py:337-357)."""
+    pts = np.atleast_2d(np.asarray(x, dtype=np.float64))
+    _check_level(L, len(decoders))
+    df = _dfield if _dfield is not None else DeviceField(Z, decoders)
+    out = _run_query(svo, df, _dev_points(pts), out_levels=1 << (L - 1))[:, 0].cpu().numpy()
+    return out, ForwardCache(svo, Z, decoders[L - 1], L, pts, out)
+
+
+def forward_levels_device(svo, dfield: DeviceField, pts: torch.Tensor, levels, counter=None) -> torch.Tensor:
+    """Batched SDF query on device points: one fp64 column per level in
+    `levels` (ascending), each equal to forward(x, L)[0]. All levels share one
+    gather pass: z_L is the running prefix sum (the training-forward caller
+    trainer.loss_batch, trainer.py:132-142, recomputes 1..L per L)."""
+    levels = sorted(set(int(v) for v in levels))
+    for L in levels:
+        _check_level(L, dfield.n_decoders)
+    mask = 0
+    for L in levels:
+        mask |= 1 << (L - 1)
+    return _run_query(svo, dfield, pts, out_levels=mask, ncols=len(levels), counter=counter)
+
+
+def forward_levels(svo, Z, decoders, x, levels) -> np.ndarray:
+    pts = np.atleast_2d(np.asarray(x, dtype=np.float64))
+    return forward_levels_device(svo, DeviceField(Z, decoders), _dev_points(pts), levels).cpu().numpy()
+
+
+@dataclass
+class NeuralField:
+    """Octree plus parameters (field.py:242-269). The device copy of the
+    parameters is made on first use; call `invalidate()` after editing Z or
+    the decoders in place."""
+
+    svo: SparseVoxelOctree
+    Z: np.ndarray
+    decoders: list
+    _device: DeviceField | None = field(default=None, repr=False, compare=False)
+
+    @property
+    def max_level(self) -> int:
+        return self.svo.max_level
+
+    @property
+    def feature_dim(self) -> int:
+        return int(np.shape(self.Z)[1])
+
+    @property
+    def hidden_dim(self) -> int:
+        return self.decoders[0].W1.shape[0]
+
+    @property
+    def device(self) -> DeviceField:
+        if self._device is None:
+            self._device = DeviceField(self.Z, self.decoders)
+        return self._device
+
+    def invalidate(self) -> None:
+        self._device = None
+
+    def predict(self, x, L: int, counter: EvalCounter | None = None):
+        return predict(self.svo, self.Z, self.decoders, x, L, counter, self.device)
+
+    def blend(self, x, L_tilde: float, counter: EvalCounter | None = None):
+        return blend(self.svo, self.Z, self.decoders, x, L_tilde, counter, self.device)
+
+    def forward(self, x, L: int):
+        return forward(self.svo, self.Z, self.decoders, x, L, self.device)
+
+    def forward_levels(self, x, levels):
+        pts = np.atleast_2d(np.asarray(x, dtype=np.float64))
+        return forward_levels_device(self.svo, self.device, _dev_points(pts), levels).cpu().numpy()
+
+
+def new_field(svo: SparseVoxelOctree, m: int = FEATURE_DIM, h: int = HIDDEN_DIM, seed: int = 0) -> NeuralField:
+    """Freshly initialised field (field.py:272-283)."""
+    return NeuralField(svo, init_features(svo, m, seed), init_decoders(svo.max_level, m, h, seed + 1))

@@ -1,0 +1,521 @@
+"""Sphere tracing of the octree field on the GPU, and image output.
+
+Drop-in for octfield.render (render.py:1-448). A frame is one C-ABI call
+(`ng_render_frame`): device ray generation (bit-exact with Camera.rays),
+the breadth-first traversal, the persistent-lane sphere-trace march, the
+central-difference normals with Lambert shading fused in, and frame
+statistics -- no host synchronisation until the caller reads a result.
+`FrameBuffer` fields are device tensors materialised as numpy on access.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import call, ptr, stream_ptr
+from .errors import ConfigError, OctfieldError, StructuralError
+from .field import EvalCounter, NeuralField, _Counters, _dev_points, _run_query
+from .octree import DOMAIN_MAX, DOMAIN_MIN
+from .traversal import RayBundle, RayVoxelPairList, device_rays, ray_segments
+
+_RAY_SHARD = 8192  # kept for API parity; the device path has no shards
+
+
+@dataclass
+class Camera:
+    """Pinhole camera (render.py:43-88)."""
+
+    position: np.ndarray
+    look_at: np.ndarray
+    up: np.ndarray
+    fov_y_deg: float
+    width: int
+    height: int
+
+    def __post_init__(self):
+        self.position = np.asarray(self.position, dtype=np.float64)
+        self.look_at = np.asarray(self.look_at, dtype=np.float64)
+        self.up = np.asarray(self.up, dtype=np.float64)
+        if not 0.0 < self.fov_y_deg < 180.0:
+            raise ConfigError("vertical FOV must be in (0, 180) degrees")
+        if self.width < 1 or self.height < 1:
+            raise ConfigError("image dimensions must be positive")
+        fwd = self.look_at - self.position
+        if np.linalg.norm(fwd) < 1e-12:
+            raise ConfigError("camera position and look_at coincide")
+        if np.linalg.norm(np.cross(fwd, self.up)) < 1e-12:
+            raise ConfigError("up vector is parallel to the view direction")
+
+    def basis(self):
+        fwd = self.look_at - self.position
+        fwd = fwd / np.linalg.norm(fwd)
+        right = np.cross(fwd, self.up)
+        right = right / np.linalg.norm(right)
+        true_up = np.cross(right, fwd)
+        return fwd, right, true_up
+
+    def struct(self) -> _lib.NgCamera:
+        fwd, right, up = self.basis()
+        c = _lib.NgCamera()
+        for a in range(3):
+            c.position[a] = float(self.position[a])
+            c.fwd[a] = float(fwd[a])
+            c.right[a] = float(right[a])
+            c.up[a] = float(up[a])
+        c.tan_half = math.tan(math.radians(self.fov_y_deg) / 2.0)
+        c.aspect = self.width / self.height
+        c.width = int(self.width)
+        c.height = int(self.height)
+        return c
+
+    def device_rays(self) -> torch.Tensor:
+        n = self.width * self.height
+        buf = torch.empty(n * _lib.RAY_BYTES, dtype=torch.uint8, device=_lib.device())
+        call("ng_camera_rays", ctypes.byref(self.struct()), ptr(buf), stream_ptr())
+        return buf
+
+    def rays(self) -> RayBundle:
+        """Primary rays through pixel centres, row-major, row 0 at the top
+        (render.py:74-88); generated on the device."""
+        raw = self.device_rays().cpu().numpy()
+        rec = raw.view(np.float64).reshape(-1, 10)
+        return RayBundle(rec[:, 0:3].copy(), rec[:, 3:6].copy())
+
+
+@dataclass
+class RenderConfig:
+    """render.py:91-114."""
+
+    delta: float = 0.0003
+    max_iters: int = 200
+    far_plane: float = 5.0
+    lod: float | None = None
+    lod_thresholds: list | None = None
+    normal_eps: float | None = None
+    skip_eps: float = 1e-5
+    osc_factor: float = 6.0
+    workers: int = 1
+    light_dir: tuple = (-0.45, 0.8, -0.55)
+    albedo: tuple = (0.82, 0.84, 0.88)
+    ambient: float = 0.12
+    background: tuple = (0.09, 0.10, 0.13)
+
+    def __post_init__(self):
+        for name in ("delta", "far_plane", "skip_eps", "osc_factor"):
+            if getattr(self, name) <= 0.0:
+                raise ConfigError(f"{name} must be positive")
+        if self.max_iters < 1 or self.workers < 1:
+            raise ConfigError("max_iters and workers must be positive")
+        if self.normal_eps is not None and self.normal_eps <= 0.0:
+            raise ConfigError("normal_eps must be positive")
+
+
+class FrameBuffer:
+    """Per-pixel outputs (render.py:117-128). Backed by device tensors; each
+    field is copied to the host on first access."""
+
+    _FIELDS = ("hit", "t", "points", "normal", "normal_ok", "iterations", "evals", "color")
+
+    def __init__(self, width, height, dev: dict, camera: Camera | None = None, rays: torch.Tensor | None = None):
+        self.width = width
+        self.height = height
+        self.device = dev
+        self._camera = camera
+        self._rays = rays
+        self._host = {}
+
+    def _shape(self, *tail):
+        return (self.height, self.width) + tail
+
+    def _get(self, name):
+        if name in self._host:
+            return self._host[name]
+        d = self.device
+        if name == "hit":
+            v = d["hit"].cpu().numpy().astype(bool).reshape(self._shape())
+        elif name == "t":
+            v = d["t"].cpu().numpy().reshape(self._shape())
+        elif name == "normal":
+            v = d["normal"].cpu().numpy().reshape(self._shape(3))
+        elif name == "normal_ok":
+            v = d["normal_ok"].cpu().numpy().astype(bool).reshape(self._shape())
+        elif name == "iterations":
+            v = d["iterations"].cpu().numpy().reshape(self._shape())
+        elif name == "evals":
+            v = d["evals"].cpu().numpy().astype(np.int64).reshape(self._shape())
+        elif name == "color":
+            v = d["color"].cpu().numpy().reshape(self._shape(3))
+        elif name == "points":
+            n = self.width * self.height
+            rays = self._rays if self._rays is not None else self._camera.device_rays()
+            out = torch.empty((n, 3), dtype=torch.float64, device=d["t"].device)
+            call("ng_hit_points", ptr(rays), ptr(d["hit"]), ptr(d["t"]), n, ptr(out), stream_ptr())
+            v = out.cpu().numpy().reshape(self._shape(3))
+        else:
+            raise AttributeError(name)
+        self._host[name] = v
+        return v
+
+    def __getattr__(self, name):
+        if name in FrameBuffer._FIELDS:
+            return self._get(name)
+        raise AttributeError(name)
+
+    def __setattr__(self, name, value):
+        if name in FrameBuffer._FIELDS:
+            self._host[name] = value
+        else:
+            object.__setattr__(self, name, value)
+
+
+@dataclass
+class FrameReport:
+    """render.py:131-137; times are CUDA-event device times."""
+
+    ms_trace: float
+    ms_normals: float
+    evals: int
+    visible: int
+    lod: float
+
+
+def select_lod(camera: Camera, svo, thresholds) -> float:
+    """Piecewise-linear detail level from the eye-to-region distance (render.py:140-152)."""
+    th = np.asarray(thresholds, dtype=np.float64)
+    if th.ndim != 1 or len(th) != svo.max_level:
+        raise ConfigError(f"need {svo.max_level} distance thresholds")
+    if np.any(np.diff(th) <= 0.0):
+        raise ConfigError("thresholds must be strictly increasing")
+    center = 0.5 * (svo.region.lo + svo.region.hi)
+    dist = float(np.linalg.norm(np.asarray(camera.position) - center))
+    levels = np.arange(svo.max_level, 0, -1, dtype=np.float64)
+    return float(np.interp(dist, th, levels))
+
+
+def _trace_level(fld: NeuralField, lod: float) -> int:
+    return min(int(math.ceil(max(lod, 1.0))), fld.max_level)
+
+
+def resolve_config(fld: NeuralField, config: RenderConfig, lod: float, eps: float | None = None) -> _lib.NgRenderCfg:
+    c = _lib.NgRenderCfg()
+    c.delta = float(config.delta)
+    c.far_plane = float(config.far_plane)
+    c.skip_eps = float(config.skip_eps)
+    c.osc_tol = float(config.osc_factor * config.delta)
+    c.lod = float(lod)
+    if eps is None:
+        eps = config.normal_eps if config.normal_eps is not None else 0.5 * fld.svo.voxel_edge(fld.max_level)
+    c.normal_eps = float(eps)
+    light = np.asarray(config.light_dir, dtype=np.float64)
+    light = light / np.linalg.norm(light)
+    for a in range(3):
+        c.light[a] = float(light[a])
+        c.albedo[a] = float(config.albedo[a])
+        c.background[a] = float(config.background[a])
+    c.ambient = float(config.ambient)
+    c.max_iters = int(config.max_iters)
+    c.trace_level = _trace_level(fld, lod)
+    return c
+
+
+def _lod_split(lod: float):
+    L = max(float(lod), 1.0)
+    base = int(np.floor(L))
+    return base, L - base
+
+
+def query_field(fld: NeuralField, pts: np.ndarray, lod: float, counter: EvalCounter | None = None) -> np.ndarray:
+    """Decode only inside trace-level voxels; elsewhere the empty-space
+    value (render.py:155-171)."""
+    p = np.atleast_2d(np.asarray(pts, dtype=np.float64))
+    lvl = _trace_level(fld, lod)
+    if lod > len(fld.decoders):
+        raise StructuralError(f"blend level {lod} above max {len(fld.decoders)}")
+    base, alpha = _lod_split(lod)
+    if alpha == 0.0:
+        out = _run_query(fld.svo, fld.device, _dev_points(p), out_levels=1 << (base - 1), inside_level=lvl,
+                         counter=counter)
+    else:
+        out = _run_query(fld.svo, fld.device, _dev_points(p), inside_level=lvl, blend_base=base, blend_alpha=alpha,
+                         counter=counter)
+    return out[:, 0].cpu().numpy()
+
+
+def _hit_records(final: RayVoxelPairList) -> torch.Tensor:
+    n = len(final)
+    rec = np.zeros(max(n, 1), dtype=np.dtype([("ray", "<i4"), ("voxel", "<i4"), ("t_enter", "<f8"),
+                                              ("t_exit", "<f8")]))
+    if n:
+        rec["ray"][:n] = final.rays
+        rec["voxel"][:n] = final.voxels
+        rec["t_enter"][:n] = final.t_enter
+        rec["t_exit"][:n] = final.t_exit
+    return torch.from_numpy(np.frombuffer(rec.tobytes(), dtype=np.uint8).copy()).to(_lib.device())
+
+
+def sphere_trace(fld: NeuralField, rays: RayBundle, final: RayVoxelPairList, lod: float, config: RenderConfig,
+                 counter: EvalCounter | None = None):
+    """March every ray through its voxel list (render.py:174-274).
+    Returns (hit, t_hit, iterations, evals)."""
+    n = rays.count
+    hit = np.zeros(n, dtype=bool)
+    t_hit = np.full(n, np.nan)
+    iters = np.zeros(n, dtype=np.int32)
+    evals = np.zeros(n, dtype=np.int64)
+    if len(final) == 0 or n == 0:
+        return hit, t_hit, iters, evals
+    dev = _lib.device()
+    d_rays = device_rays(rays)
+    d_hits = _hit_records(final)
+    cnt = torch.tensor([len(final)], dtype=torch.int64, device=dev)
+    s, e = ray_segments(final, n)
+    d_s = torch.from_numpy(s).to(dev)
+    d_e = torch.from_numpy(e).to(dev)
+    o_hit = torch.empty(n, dtype=torch.uint8, device=dev)
+    o_t = torch.empty(n, dtype=torch.float64, device=dev)
+    o_it = torch.empty(n, dtype=torch.int32, device=dev)
+    o_ev = torch.empty(n, dtype=torch.int32, device=dev)
+    cfg = resolve_config(fld, config, max(float(lod), 1.0))
+    cfg.trace_level = final.level
+    c = _Counters()
+    call("ng_sphere_trace", fld.svo.device.ref(), fld.device.ref(), ctypes.byref(cfg), ptr(d_rays), n, ptr(d_hits),
+         ptr(cnt), ptr(d_s), ptr(d_e), ptr(o_hit), ptr(o_t), ptr(o_it), ptr(o_ev), c.ptr(), stream_ptr())
+    ch = c.host()
+    if ch[3]:
+        raise OctfieldError("non-finite decoder input")
+    if counter is not None:
+        counter.add(ch)
+    return (o_hit.cpu().numpy().astype(bool), o_t.cpu().numpy(), o_it.cpu().numpy(),
+            o_ev.cpu().numpy().astype(np.int64))
+
+
+def normals(fld: NeuralField, points: np.ndarray, eps: float, lod: float, counter: EvalCounter | None = None):
+    """Central-difference gradients, normalised (render.py:277-300).
+    Returns (normals, ok)."""
+    pts = np.atleast_2d(np.asarray(points, dtype=np.float64))
+    k = len(pts)
+    if k == 0:
+        return np.zeros((0, 3)), np.zeros(0, dtype=bool)
+    dev = _lib.device()
+    cfg = resolve_config(fld, RenderConfig(), max(float(lod), 1.0), eps=eps)
+    out = torch.empty((k, 3), dtype=torch.float64, device=dev)
+    ok = torch.empty(k, dtype=torch.uint8, device=dev)
+    c = _Counters()
+    d_pts = torch.from_numpy(np.ascontiguousarray(pts)).to(dev)
+    call("ng_normals", fld.svo.device.ref(), fld.device.ref(), ctypes.byref(cfg), ptr(d_pts), k, ptr(out), ptr(ok),
+         c.ptr(), stream_ptr())
+    ch = c.host()
+    if ch[3]:
+        raise OctfieldError("non-finite decoder input")
+    if counter is not None:
+        counter.add(ch)
+    return out.cpu().numpy(), ok.cpu().numpy().astype(bool)
+
+
+def shade(hit, nrm, config: RenderConfig) -> np.ndarray:
+    """Lambert shading, 8-bit RGB (render.py:303-314)."""
+    hit = np.asarray(hit, dtype=bool)
+    nrm = np.asarray(nrm, dtype=np.float64)
+    shape = hit.shape
+    n = hit.size
+    dev = _lib.device()
+    c = _lib.NgRenderCfg()
+    light = np.asarray(config.light_dir, dtype=np.float64)
+    light = light / np.linalg.norm(light)
+    for a in range(3):
+        c.light[a] = float(light[a])
+        c.albedo[a] = float(config.albedo[a])
+        c.background[a] = float(config.background[a])
+    c.ambient = float(config.ambient)
+    out = torch.empty((max(n, 1), 3), dtype=torch.uint8, device=dev)
+    if n:
+        d_hit = torch.from_numpy(np.ascontiguousarray(hit.ravel()).astype(np.uint8)).to(dev)
+        d_n = torch.from_numpy(np.ascontiguousarray(nrm.reshape(-1, 3))).to(dev)
+        call("ng_shade", ptr(d_hit), ptr(d_n), n, ctypes.byref(c), ptr(out), stream_ptr())
+    return out[:n].cpu().numpy().reshape(shape + (3,))
+
+
+def write_ppm(path, image: np.ndarray) -> None:
+    """Binary P6, 8-bit (render.py:317-324)."""
+    if image.ndim != 3 or image.shape[2] != 3 or image.dtype != np.uint8:
+        raise StructuralError("write_ppm expects (h, w, 3) uint8")
+    h, w = image.shape[:2]
+    with open(path, "wb") as fh:
+        fh.write(f"P6\n{w} {h}\n255\n".encode("ascii"))
+        fh.write(image.tobytes())
+
+
+def normal_image(fb: FrameBuffer) -> np.ndarray:
+    rgb = np.where(fb.hit[..., None], 0.5 * (fb.normal + 1.0), 0.0)
+    return (np.clip(rgb, 0.0, 1.0) * 255.0 + 0.5).astype(np.uint8)
+
+
+def depth_image(fb: FrameBuffer, far: float) -> np.ndarray:
+    g = np.where(fb.hit, 1.0 - np.nan_to_num(fb.t) / far, 0.0)
+    g = (np.clip(g, 0.0, 1.0) * 255.0 + 0.5).astype(np.uint8)
+    return np.repeat(g[..., None], 3, axis=2)
+
+
+# ------------------------------------------------------------------ frames
+
+def resolve_lod(camera: Camera, fld: NeuralField, config: RenderConfig) -> float:
+    """render.py:345-353."""
+    if config.lod is not None:
+        lod = float(config.lod)
+        if lod > fld.max_level:
+            raise ConfigError(f"lod {lod} above max level {fld.max_level}")
+    elif config.lod_thresholds is not None:
+        lod = select_lod(camera, fld.svo, config.lod_thresholds)
+    else:
+        lod = float(fld.max_level)
+    return max(lod, 1.0)
+
+
+class RenderSession:
+    """Reusable device state for rendering frames of one size: workspace,
+    frame buffers, statistics. `enqueue` launches a frame with no host sync;
+    `finish` reads the statistics and applies the reference's per-frame
+    checks. Capacities grow (and the frame reruns) on overflow."""
+
+    def __init__(self, fld: NeuralField, width: int, height: int, n_rays: int | None = None):
+        self.fld = fld
+        self.width, self.height = width, height
+        self.n = n_rays if n_rays is not None else width * height
+        self.pair_cap = max(8 * self.n, 1 << 16)
+        self.hit_cap = max(4 * self.n, 1 << 16)
+        self.dev = _lib.device()
+        self._alloc_ws()
+        self.stats = torch.zeros(ctypes.sizeof(_lib.NgFrameStats) // 8, dtype=torch.int64, device=self.dev)
+        self.stats_host = torch.zeros_like(self.stats, device="cpu").pin_memory()
+        self.ev0 = torch.cuda.Event(enable_timing=True)
+        self.ev1 = torch.cuda.Event(enable_timing=True)
+        self.ev2 = torch.cuda.Event(enable_timing=True)
+
+    def _alloc_ws(self):
+        nbytes = _lib.lib().ng_render_workspace_bytes(self.n, self.pair_cap, self.hit_cap)
+        self.ws_buf = torch.empty(nbytes, dtype=torch.uint8, device=self.dev)
+        self.ws = _lib.NgWorkspace(ptr(self.ws_buf), nbytes, self.pair_cap, self.hit_cap, None)
+
+    def new_frame(self) -> dict:
+        n, dev = self.n, self.dev
+        return {
+            "hit": torch.empty(n, dtype=torch.uint8, device=dev),
+            "t": torch.empty(n, dtype=torch.float64, device=dev),
+            "normal": torch.empty((n, 3), dtype=torch.float64, device=dev),
+            "normal_ok": torch.empty(n, dtype=torch.uint8, device=dev),
+            "iterations": torch.empty(n, dtype=torch.int32, device=dev),
+            "evals": torch.empty(n, dtype=torch.int32, device=dev),
+            "color": torch.empty((n, 3), dtype=torch.uint8, device=dev),
+        }
+
+    @staticmethod
+    def frame_struct(fr: dict) -> _lib.NgFrame:
+        return _lib.NgFrame(ptr(fr["hit"]), ptr(fr["t"]), ptr(fr["normal"]), ptr(fr["normal_ok"]),
+                            ptr(fr["iterations"]), ptr(fr["evals"]), ptr(fr["color"]))
+
+    def enqueue(self, cfg: _lib.NgRenderCfg, frame: dict, camera: Camera | None = None, rays: torch.Tensor | None = None,
+                timed: bool = False, do_normals: bool = True) -> None:
+        """Launch one frame on the current stream. With `timed`, ev0 / ev1 /
+        ev2 bracket traversal+march and normals (ev1 is recorded by the C side)."""
+        fs = self.frame_struct(frame)
+        if timed:
+            self.ev1.record()  # materialise the handle; re-recorded mid-frame
+            self.ws.ev_trace_done = self.ev1.cuda_event
+            self.ev0.record()
+        else:
+            self.ws.ev_trace_done = None
+        if camera is not None:
+            call("ng_render_frame", self.fld.svo.device.ref(), self.fld.device.ref(), ctypes.byref(cfg),
+                 ctypes.byref(camera.struct()), ctypes.byref(fs), ctypes.byref(self.ws), ptr(self.stats),
+                 stream_ptr())
+        else:
+            call("ng_render_rays", self.fld.svo.device.ref(), self.fld.device.ref(), ctypes.byref(cfg), ptr(rays),
+                 self.n, ctypes.byref(fs), ctypes.byref(self.ws), ptr(self.stats), int(do_normals), stream_ptr())
+        if timed:
+            self.ev2.record()
+        self.ws.ev_trace_done = None
+
+    def read_stats(self) -> _lib.NgFrameStats:
+        self.stats_host.copy_(self.stats, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        raw = self.stats_host.numpy().tobytes()
+        return _lib.NgFrameStats.from_buffer_copy(raw[:ctypes.sizeof(_lib.NgFrameStats)])
+
+    def grow(self, st: _lib.NgFrameStats, n_levels: int) -> bool:
+        """Grow capacities after an overflow; True when a rerun is needed."""
+        if not st.overflow:
+            return False
+        need_pairs = max(st.pairs[t] for t in range(1, n_levels))
+        self.pair_cap = max(self.pair_cap, int(need_pairs) + 4096)
+        self.hit_cap = max(self.hit_cap, int(st.pairs[n_levels]) + 4096)
+        self._alloc_ws()
+        return True
+
+
+_SESSIONS: dict = {}
+
+
+def _session(fld: NeuralField, width: int, height: int) -> RenderSession:
+    key = (id(fld), width, height)
+    s = _SESSIONS.get(key)
+    if s is None or s.fld is not fld:
+        if len(_SESSIONS) > 8:
+            _SESSIONS.clear()
+        s = RenderSession(fld, width, height)
+        _SESSIONS[key] = s
+    return s
+
+
+def render(camera: Camera, fld: NeuralField, config: RenderConfig):
+    """Trace a frame (render.py:342-448). Returns (FrameBuffer, FrameReport);
+    the report times traversal + march and the normals separately with CUDA
+    events, matching the benchmark scope."""
+    lod = resolve_lod(camera, fld, config)
+    cfg = resolve_config(fld, config, lod)
+    sess = _session(fld, camera.width, camera.height)
+    n_levels = cfg.trace_level + fld.svo.device.n_virtual + 1
+    while True:
+        frame = sess.new_frame()
+        sess.enqueue(cfg, frame, camera=camera, timed=True)
+        st = sess.read_stats()
+        if not sess.grow(st, n_levels):
+            break
+    if st.counters.nonfinite_inputs:
+        raise OctfieldError("non-finite decoder input")
+    if st.counters.evals_missing_level != 0:
+        raise OctfieldError("internal: decoder ran outside the queried level's voxels")
+    ms_trace = sess.ev0.elapsed_time(sess.ev1)
+    ms_normals = sess.ev1.elapsed_time(sess.ev2)
+    fb = FrameBuffer(camera.width, camera.height, frame, camera=camera)
+    report = FrameReport(ms_trace=float(ms_trace), ms_normals=float(ms_normals),
+                         evals=int(st.counters.decoder_evals), visible=int(st.visible), lod=lod)
+    return fb, report
+
+
+def trace_rays(fld: NeuralField, rays: RayBundle, lod: float, config: RenderConfig | None = None):
+    """(hit, t_hit) for arbitrary rays with the renderer's rules; the
+    device version of metrics.trace_field_rays (metrics.py:135-142)."""
+    config = config or RenderConfig()
+    lod = max(float(lod), 1.0)
+    cfg = resolve_config(fld, config, lod)
+    n = rays.count
+    if n == 0:
+        return np.zeros(0, dtype=bool), np.zeros(0)
+    sess = RenderSession(fld, n, 1, n_rays=n)
+    d_rays = device_rays(rays)
+    n_levels = cfg.trace_level + fld.svo.device.n_virtual + 1
+    while True:
+        frame = sess.new_frame()
+        sess.enqueue(cfg, frame, rays=d_rays, do_normals=False)
+        st = sess.read_stats()
+        if not sess.grow(st, n_levels):
+            break
+    if st.counters.nonfinite_inputs:
+        raise OctfieldError("non-finite decoder input")
+    return frame["hit"].cpu().numpy().astype(bool), frame["t"].cpu().numpy()
