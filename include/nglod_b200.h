@@ -170,6 +170,7 @@ typedef struct ng_workspace {
   int64_t pair_capacity;  /* per ping-pong pair buffer */
   int64_t hit_capacity;   /* final hit-pair list */
   void* ev_trace_done;    /* optional cudaEvent_t recorded between march and normals */
+  void* ev_march_begin;   /* optional cudaEvent_t recorded just before the march kernel */
 } ng_workspace;
 
 /* Device-side frame statistics (FrameReport, render.py:131-137). */

@@ -96,7 +96,7 @@ class NgFrame(C.Structure):
 
 class NgWorkspace(C.Structure):
     _fields_ = [("base", P), ("bytes", C.c_size_t), ("pair_capacity", C.c_int64),
-                ("hit_capacity", C.c_int64), ("ev_trace_done", P)]
+                ("hit_capacity", C.c_int64), ("ev_trace_done", P), ("ev_march_begin", P)]
 
 
 class NgFrameStats(C.Structure):

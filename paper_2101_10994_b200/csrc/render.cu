@@ -657,6 +657,8 @@ static int render_common(const ng_octree& tree, const ng_field& f, const ng_rend
   A.d_hit_count = ctr + 1;
   A.work_counter = ctr + 2;
   A.counters = &st->counters;
+  if (ws.ev_march_begin && (r = cuda_status(cudaEventRecord((cudaEvent_t)ws.ev_march_begin, s), "event record")))
+    return r;
   if ((r = launch_march(tree, f, A, s))) return r;
   if (ws.ev_trace_done && (r = cuda_status(cudaEventRecord((cudaEvent_t)ws.ev_trace_done, s), "event record")))
     return r;

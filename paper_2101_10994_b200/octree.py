@@ -306,7 +306,7 @@ def build_octree(oracle, max_level: int, surface_samples: np.ndarray, r0: int = 
     codes = []
     for t in range(T):
         c = torch.empty(int(counts_host[t]), dtype=torch.int64, device=dev)
-        call("ng_bitmap_extract", ptr(bitmaps[t]), bitmaps[t].numel(), ptr(ranks[t]), ptr(c), st)
+        call("ng_bitmap_extract", ptr(bitmaps[t]), ptr(ranks[t]), bitmaps[t].numel(), ptr(c), st)
         codes.append(c)
     for lv in range(1, max_level + 1):
         t = lv + nv
@@ -403,7 +403,8 @@ def locate_device(svo: SparseVoxelOctree, pts: torch.Tensor, level: int) -> torc
     n = pts.shape[0]
     out = torch.empty(n, dtype=torch.int64, device=pts.device)
     if n:
-        call("ng_locate", svo.device.ref(), ptr(pts.contiguous()), n, int(level), ptr(out), stream_ptr())
+        pc = pts.contiguous()
+        call("ng_locate", svo.device.ref(), ptr(pc), n, int(level), ptr(out), stream_ptr())
     return out
 
 

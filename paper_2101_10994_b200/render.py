@@ -400,7 +400,7 @@ class RenderSession:
     def _alloc_ws(self):
         nbytes = _lib.lib().ng_render_workspace_bytes(self.n, self.pair_cap, self.hit_cap)
         self.ws_buf = torch.empty(nbytes, dtype=torch.uint8, device=self.dev)
-        self.ws = _lib.NgWorkspace(ptr(self.ws_buf), nbytes, self.pair_cap, self.hit_cap, None)
+        self.ws = _lib.NgWorkspace(ptr(self.ws_buf), nbytes, self.pair_cap, self.hit_cap, None, None)
 
     def new_frame(self) -> dict:
         n, dev = self.n, self.dev

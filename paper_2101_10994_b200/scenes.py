@@ -41,7 +41,8 @@ class Shape:
         prm = torch.from_numpy(params).to(_lib.device())
         out = torch.empty(pts.shape[0], dtype=torch.float64, device=pts.device)
         if pts.shape[0]:
-            call("ng_sdf_eval", int(kind), ptr(prm), int(prm.numel()), ptr(pts.contiguous()), pts.shape[0], ptr(out),
+            pc = pts.contiguous()
+            call("ng_sdf_eval", int(kind), ptr(prm), int(prm.numel()), ptr(pc), pts.shape[0], ptr(out),
                  stream_ptr())
         return out
 

@@ -113,8 +113,8 @@ def decide(rays: RayBundle, pairs: RayVoxelPairList, svo: SparseVoxelOctree, fin
         return np.zeros(0, dtype=np.int64)
     t = pairs.level + _n_virtual(svo)
     D = torch.empty(n, dtype=torch.int64, device=_lib.device())
-    call("ng_decide", svo.device.ref(), ptr(device_rays(rays)), t, int(bool(final)), ptr(_pairs_dev(pairs)), n,
-         ptr(D), stream_ptr())
+    d_rays, d_pairs = device_rays(rays), _pairs_dev(pairs)  # keep alive until the kernel is enqueued
+    call("ng_decide", svo.device.ref(), ptr(d_rays), t, int(bool(final)), ptr(d_pairs), n, ptr(D), stream_ptr())
     return D.cpu().numpy()
 
 
@@ -174,8 +174,9 @@ def subdivide(pairs: RayVoxelPairList, D: np.ndarray, S: np.ndarray, svo: Sparse
     out = torch.empty((total, 2), dtype=torch.int32, device=dev)
     dD = torch.from_numpy(np.ascontiguousarray(D)).to(dev)
     dS = torch.from_numpy(np.ascontiguousarray(S)).to(dev)
-    call("ng_subdivide", svo.device.ref(), ptr(device_rays(rays)), t, ptr(_pairs_dev(pairs)), len(pairs), ptr(dD),
-         ptr(dS), ptr(out), stream_ptr())
+    d_rays, d_pairs = device_rays(rays), _pairs_dev(pairs)
+    call("ng_subdivide", svo.device.ref(), ptr(d_rays), t, ptr(d_pairs), len(pairs), ptr(dD), ptr(dS), ptr(out),
+         stream_ptr())
     o = out.cpu().numpy().astype(np.int64)
     res = RayVoxelPairList(nxt, o[:, 0].copy(), o[:, 1].copy())
     if len(res) != total:
@@ -197,7 +198,8 @@ def compactify(pairs: RayVoxelPairList, D: np.ndarray, S: np.ndarray) -> RayVoxe
     out = torch.empty((total, 2), dtype=torch.int32, device=dev)
     dD = torch.from_numpy(np.ascontiguousarray(D)).to(dev)
     dS = torch.from_numpy(np.ascontiguousarray(S)).to(dev)
-    call("ng_compactify", ptr(_pairs_dev(pairs)), len(pairs), ptr(dD), ptr(dS), ptr(out), stream_ptr())
+    d_pairs = _pairs_dev(pairs)
+    call("ng_compactify", ptr(d_pairs), len(pairs), ptr(dD), ptr(dS), ptr(out), stream_ptr())
     o = out.cpu().numpy().astype(np.int64)
     return RayVoxelPairList(pairs.level, o[:, 0].copy(), o[:, 1].copy())
 
