@@ -718,11 +718,12 @@ class OracleFrame:
 
 
 def render(tree, Z, decoders, camera: dict, cfg: RenderParams, shard: int = 8192,
-           ray_slice: slice | None = None, workers: int = 1) -> OracleFrame:
+           ray_slice=None, workers: int = 1) -> OracleFrame:
     """render (render.py:342-448). `camera` holds position, look_at, up,
-    fov_y_deg, width, height. `ray_slice` restricts the frame to a
-    contiguous pixel range (bounded CPU samples for the bench); `workers`
-    shards the march over threads like the reference (render.py:389-414)."""
+    fov_y_deg, width, height. `ray_slice` (a slice or an index array)
+    restricts the frame to a subset of pixels (bounded CPU samples for the
+    bench); `workers` shards the march over threads like the reference
+    (render.py:389-414)."""
     L = tree.max_level
     lod = float(cfg.lod) if cfg.lod is not None else float(L)
     if lod > L:
