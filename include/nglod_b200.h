@@ -124,7 +124,10 @@ typedef struct ng_hit_pair {
   double t_exit;
 } ng_hit_pair;
 
-/* Pinhole camera (render.py:43-88); basis precomputed on the host in fp64. */
+/* Pinhole camera (render.py:43-88); basis precomputed on the host in fp64.
+ * Image tiling for multi-GPU frames: the image is cut into bands of
+ * band_rows rows; this camera generates the rays of bands b with
+ * b % band_stride == band_offset, in order (band_stride = 1: whole frame). */
 typedef struct ng_camera {
   double position[3];
   double fwd[3];
@@ -134,6 +137,10 @@ typedef struct ng_camera {
   double aspect;
   int32_t width;
   int32_t height;
+  int32_t band_rows;
+  int32_t band_stride;
+  int32_t band_offset;
+  int32_t local_rows;   /* rows this camera generates */
 } ng_camera;
 
 /* RenderConfig (render.py:91-114), resolved on the host. */

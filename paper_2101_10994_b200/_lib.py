@@ -79,7 +79,8 @@ class NgQueryArgs(C.Structure):
 class NgCamera(C.Structure):
     _fields_ = [("position", C.c_double * 3), ("fwd", C.c_double * 3), ("right", C.c_double * 3),
                 ("up", C.c_double * 3), ("tan_half", C.c_double), ("aspect", C.c_double),
-                ("width", C.c_int32), ("height", C.c_int32)]
+                ("width", C.c_int32), ("height", C.c_int32), ("band_rows", C.c_int32),
+                ("band_stride", C.c_int32), ("band_offset", C.c_int32), ("local_rows", C.c_int32)]
 
 
 class NgRenderCfg(C.Structure):

@@ -125,6 +125,55 @@ __device__ __forceinline__ bool slab_test(const ng_ray& r, const double lo[3], c
   return !nan_seen && (near <= far) && (far >= 0.0);
 }
 
+// Per-axis slab intervals of the two child halves of a parent cell. The
+// child planes lo/mid/hi are exact dyadic values, so t = (plane - o) * inv
+// per plane is bit-identical to ray_aabb_batch on each child box; a parent
+// computes 9 plane distances once instead of 8 x 6.
+struct ChildSlabs {
+  double an[3][2];  // per axis, per half: min(t_lo, t_hi)
+  double af[3][2];  // max(t_lo, t_hi)
+};
+
+__device__ __forceinline__ void child_slabs(const ng_ray& r, int px, int py, int pz, int cres, ChildSlabs& cs) {
+  const int pc[3] = {px, py, pz};
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const double p0 = cell_lo(2 * pc[a], cres), p1 = cell_lo(2 * pc[a] + 1, cres),
+                 p2 = cell_lo(2 * pc[a] + 2, cres);
+    if ((r.flags >> (3 + a)) & 1) {
+      const bool in0 = (r.o[a] >= p0) && (r.o[a] <= p1);
+      const bool in1 = (r.o[a] >= p1) && (r.o[a] <= p2);
+      cs.an[a][0] = in0 ? -INFINITY : INFINITY;
+      cs.af[a][0] = in0 ? INFINITY : -INFINITY;
+      cs.an[a][1] = in1 ? -INFINITY : INFINITY;
+      cs.af[a][1] = in1 ? INFINITY : -INFINITY;
+    } else {
+      const double t0 = dmul(dsub(p0, r.o[a]), r.inv[a]);
+      const double t1 = dmul(dsub(p1, r.o[a]), r.inv[a]);
+      const double t2 = dmul(dsub(p2, r.o[a]), r.inv[a]);
+      cs.an[a][0] = np_min(t0, t1);
+      cs.af[a][0] = np_max(t0, t1);
+      cs.an[a][1] = np_min(t1, t2);
+      cs.af[a][1] = np_max(t1, t2);
+    }
+  }
+}
+
+// Slab test of child octant `oct` from precomputed halves (same reduction
+// order as slab_test / ray_aabb_batch).
+__device__ __forceinline__ bool child_hit(const ChildSlabs& cs, int oct, double& t_enter, double& t_exit) {
+  // selects, not indexing: keeps ChildSlabs in registers
+  const bool b0 = oct & 1, b1 = (oct >> 1) & 1, b2 = (oct >> 2) & 1;
+  double near = b0 ? cs.an[0][1] : cs.an[0][0], far = b0 ? cs.af[0][1] : cs.af[0][0];
+  near = np_max(near, b1 ? cs.an[1][1] : cs.an[1][0]);
+  far = np_min(far, b1 ? cs.af[1][1] : cs.af[1][0]);
+  near = np_max(near, b2 ? cs.an[2][1] : cs.an[2][0]);
+  far = np_min(far, b2 ? cs.af[2][1] : cs.af[2][0]);
+  t_enter = np_max(near, 0.0);
+  t_exit = far;
+  return (near <= far) && (far >= 0.0);
+}
+
 __device__ __forceinline__ void load_ray(const ng_ray* __restrict__ rays, int64_t i, ng_ray& r) {
   const double2* p = reinterpret_cast<const double2*>(rays + i);
   double2 a = __ldg(p + 0), b = __ldg(p + 1), c = __ldg(p + 2), d = __ldg(p + 3), e = __ldg(p + 4);

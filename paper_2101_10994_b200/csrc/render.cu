@@ -12,15 +12,15 @@
 #include "eval.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace ng {
 
 int grid_for(int64_t n, int nt);
 size_t level_scratch_bytes(int64_t max_pairs);
-int traverse_level(const ng_octree& tree, const ng_ray* rays, int t, bool final, const ng_pair* in,
-                   const int64_t* d_count_in, int64_t in_cap, ng_pair* out_pairs, ng_hit_pair* out_hits,
-                   int64_t* d_count_out, int64_t out_cap, void* scratch, size_t scratch_bytes,
-                   cudaStream_t s);
+int traverse_hits(const ng_octree& tree, const ng_ray* rays, int t, bool next_final, const ng_pair* in,
+                  const int64_t* d_count_in, int64_t in_cap, ng_pair* out_pairs, ng_hit_pair* out_hits,
+                  int64_t* d_count_out, int64_t out_cap, void* scratch, size_t scratch_bytes, cudaStream_t s);
 
 constexpr int R_NW = 8;  // warps per CTA for march / normals
 
@@ -28,12 +28,15 @@ constexpr int R_NW = 8;  // warps per CTA for march / normals
 // the per-pixel output defaults and the background colour.
 __global__ void k_camera_rays(ng_camera cam, ng_ray* __restrict__ rays, ng_frame fr, uint8_t bg0, uint8_t bg1,
                               uint8_t bg2, int64_t* d_root_count) {
-  const int64_t n = (int64_t)cam.width * cam.height;
+  const int64_t n = (int64_t)cam.width * cam.local_rows;
   if (blockIdx.x == 0 && threadIdx.x == 0 && d_root_count) *d_root_count = n;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     if (rays) {
-      const int px_i = (int)(i % cam.width), py_i = (int)(i / cam.width);
+      const int px_i = (int)(i % cam.width);
+      const int lrow = (int)(i / cam.width);
+      const int band = lrow / cam.band_rows;
+      const int py_i = (band * cam.band_stride + cam.band_offset) * cam.band_rows + lrow % cam.band_rows;
       double px = dmul(dmul(dsub(dmul(2.0, dadd((double)px_i, 0.5)) / (double)cam.width, 1.0), cam.tan_half),
                        cam.aspect);
       double py = dmul(dsub(1.0, dmul(2.0, dadd((double)py_i, 0.5)) / (double)cam.height), cam.tan_half);
@@ -518,6 +521,12 @@ static int launch_march(const ng_octree& tree, const ng_field& f, MarchArgs& A, 
   int per_sm;
   int r = prep_kernel(k_march<R_NW>, smem, R_NW * 32, per_sm);
   if (r) return r;
+  static int cap = -1;  // NG_MARCH_CTAS_PER_SM: experiment knob for the persistent grid
+  if (cap < 0) {
+    const char* e = getenv("NG_MARCH_CTAS_PER_SM");
+    cap = e ? atoi(e) : 0;
+  }
+  if (cap > 0 && cap < per_sm) per_sm = cap;
   k_march<R_NW><<<sm_count() * per_sm, R_NW * 32, smem, s>>>(tree, f, A);
   NG_CHECK_LAUNCH("k_march");
   return NG_OK;
@@ -529,6 +538,8 @@ static int launch_normals(const ng_octree& tree, const ng_field& f, NormalArgs& 
   int per_sm;
   int r = prep_kernel(k_normals<R_NW>, smem, R_NW * 32, per_sm);
   if (r) return r;
+  // persistent: the work count may live on the device, so size for the SMs
+  // (decoders are staged once per CTA)
   int64_t want = (max_n + 32 * R_NW - 1) / (32 * R_NW);
   int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sm_count() * per_sm));
   k_normals<R_NW><<<grid, R_NW * 32, smem, s>>>(tree, f, A);
@@ -610,26 +621,26 @@ static int render_common(const ng_octree& tree, const ng_field& f, const ng_rend
     k_set_count<<<1, 1, 0, s>>>(&st->pairs[0], n);  // root list (i, 0) of n rays
     NG_CHECK_LAUNCH("k_set_count");
   }
-  // ---- traversal (traversal.py:207-247)
+  // ---- traversal (traversal.py:207-247), hit-filtered: pass t expands the
+  // hits at level t into the hit children at level t+1; the last pass
+  // writes the final (ray, voxel, t_enter, t_exit) list
   const int target = cfg.trace_level + tree.n_virtual;
   const ng_pair* in = nullptr;
   int64_t in_cap = n;
   for (int t = 0; t < target; ++t) {
+    const bool last = (t + 1 == target);
     ng_pair* out = (t % 2 == 0) ? pa : pb;
-    r = traverse_level(tree, rays, t, false, in, &st->pairs[t], in_cap, out, nullptr, &st->pairs[t + 1],
-                       ws.pair_capacity, scratch, L.scratch_bytes, s);
+    r = traverse_hits(tree, rays, t, last, in, &st->pairs[t], in_cap, last ? nullptr : out, last ? hits : nullptr,
+                      &st->pairs[t + 1], last ? ws.hit_capacity : ws.pair_capacity, scratch, L.scratch_bytes, s);
     if (r) return r;
     in = out;
     in_cap = ws.pair_capacity;
   }
-  r = traverse_level(tree, rays, target, true, in, &st->pairs[target], in_cap, nullptr, hits,
-                     &st->pairs[target + 1], ws.hit_capacity, scratch, L.scratch_bytes, s);
-  if (r) return r;
   // ---- segments + active rays
   if ((r = cuda_status(cudaMemsetAsync(seg_start, 0, n * 8, s), "seg memset"))) return r;
   if ((r = cuda_status(cudaMemsetAsync(seg_end, 0, n * 8, s), "seg memset"))) return r;
   k_segments_active<<<grid_for(std::max<int64_t>(ws.hit_capacity, 1), 256), 256, 0, s>>>(
-      hits, &st->pairs[target + 1], ws.hit_capacity, seg_start, seg_end, active, ctr + 0);
+      hits, &st->pairs[target], ws.hit_capacity, seg_start, seg_end, active, ctr + 0);
   NG_CHECK_LAUNCH("k_segments_active");
   // ---- sphere trace (render.py:174-274)
   const LodPlan P = plan_lod(cfg);
@@ -684,7 +695,7 @@ static int render_common(const ng_octree& tree, const ng_field& f, const ng_rend
     B.counters = &st->counters;
     if ((r = launch_normals(tree, f, B, n, s))) return r;
   }
-  k_finish_stats<<<1, 1, 0, s>>>(st, target + 1, ws.pair_capacity, ws.hit_capacity, ctr + 1, ctr + 0);
+  k_finish_stats<<<1, 1, 0, s>>>(st, target, ws.pair_capacity, ws.hit_capacity, ctr + 1, ctr + 0);
   NG_CHECK_LAUNCH("k_finish_stats");
   return NG_OK;
 }
@@ -696,7 +707,7 @@ using namespace ng;
 extern "C" {
 
 int ng_camera_rays(const ng_camera* cam, ng_ray* rays, void* stream) {
-  int64_t n = (int64_t)cam->width * cam->height;
+  int64_t n = (int64_t)cam->width * cam->local_rows;
   k_camera_rays<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(*cam, rays, ng_frame{}, 0, 0, 0, nullptr);
   NG_CHECK_LAUNCH("ng_camera_rays");
   return NG_OK;
@@ -708,7 +719,11 @@ size_t ng_render_workspace_bytes(int64_t n_rays, int64_t pair_capacity, int64_t 
 
 int ng_render_frame(const ng_octree* tree, const ng_field* fld, const ng_render_cfg* cfg, const ng_camera* cam,
                     const ng_frame* frame, const ng_workspace* ws, ng_frame_stats* d_stats, void* stream) {
-  const int64_t n = (int64_t)cam->width * cam->height;
+  if (cam->band_rows < 1 || cam->band_stride < 1 || cam->band_offset < 0 || cam->band_offset >= cam->band_stride) {
+    set_error("bad camera band layout");
+    return NG_ERR_CONFIG;
+  }
+  const int64_t n = (int64_t)cam->width * cam->local_rows;
   return render_common(*tree, *fld, *cfg, cam, nullptr, n, *frame, *ws, d_stats, true, (cudaStream_t)stream);
 }
 

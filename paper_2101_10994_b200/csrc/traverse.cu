@@ -133,6 +133,123 @@ __global__ void __launch_bounds__(TR_NT) k_traverse_level(
 // ray_segments (traversal.py:250-255): per-ray lower / upper bound of the ray
 // id in the (ray-sorted) final list, so rays without pairs get the same
 // insertion position numpy's searchsorted reports.
+// Render-path variant of one BFS pass: the input pairs at level t are
+// already known hits (or the implicit root list, tested here); each pair's
+// occupied children are slab-tested in the parent's thread, front to back,
+// and only hit children are written. The final hit list is therefore the
+// same sequence the reference produces (its candidate lists filtered in
+// order), with a fraction of the pair traffic: the ray record is read once
+// per hit parent instead of once per candidate child.
+template <bool NEXT_FINAL>
+__global__ void __launch_bounds__(TR_NT) k_traverse_hits(
+    const __grid_constant__ ng_octree tree, const ng_ray* __restrict__ rays, int t,
+    const ng_pair* __restrict__ in, const int64_t* __restrict__ d_count_in, int64_t in_cap,
+    ng_pair* __restrict__ out_pairs, ng_hit_pair* __restrict__ out_hits,
+    int64_t* __restrict__ d_count_out, int64_t out_cap, unsigned long long* states,
+    unsigned int* tile_counter) {
+  __shared__ int64_t sm_warp[TR_NT / 32 + 1];
+  __shared__ int64_t sm_tile, sm_excl;
+  int64_t n = *d_count_in;
+  if (in != nullptr && n > in_cap) n = in_cap;
+  const int level = t - tree.n_virtual;
+  const int cres = level_res(tree, level + 1);
+  const double cedge = 2.0 / (double)cres;
+  const uint64_t* __restrict__ codes = tree.codes[t];
+  const int32_t* __restrict__ cstart = tree.child_start[t];
+  const uint8_t* __restrict__ cmask = tree.child_mask[t];
+  const int64_t tile_elems = (int64_t)TR_NT * TR_ITEMS;
+  const int64_t n_tiles = (n + tile_elems - 1) / tile_elems;
+  if (n_tiles == 0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) *d_count_out = 0;
+    return;
+  }
+  while (true) {
+    if (threadIdx.x == 0) sm_tile = atomicAdd(tile_counter, 1u);
+    __syncthreads();
+    const int64_t tile = sm_tile;
+    if (tile >= n_tiles) break;
+    const int64_t base = tile * tile_elems + (int64_t)threadIdx.x * TR_ITEMS;
+    int32_t pr[TR_ITEMS], pv[TR_ITEMS];
+    unsigned hm[TR_ITEMS];  // bit k: k-th front-to-back child is hit
+    int64_t sum = 0;
+#pragma unroll
+    for (int q = 0; q < TR_ITEMS; ++q) {
+      const int64_t i = base + q;
+      hm[q] = 0;
+      pr[q] = 0;
+      pv[q] = 0;
+      if (i < n) {
+        ng_ray r;
+        bool parent_hit = true;
+        if (in != nullptr) {
+          const ng_pair p = in[i];
+          pr[q] = p.ray;
+          pv[q] = p.voxel;
+          load_ray(rays, pr[q], r);
+        } else {  // implicit root list: the root box itself must be hit
+          pr[q] = (int32_t)i;
+          load_ray(rays, pr[q], r);
+          const double lo[3] = {-1.0, -1.0, -1.0}, hi[3] = {1.0, 1.0, 1.0};
+          double a, b;
+          parent_hit = slab_test(r, lo, hi, a, b);
+        }
+        if (parent_hit) {
+          const unsigned m = __ldg(cmask + pv[q]);
+          const uint64_t c = __ldg(codes + pv[q]);
+          const int px = (int)compact3(c), py = (int)compact3(c >> 1), pz = (int)compact3(c >> 2);
+          const int dm = r.flags & 7;
+          ChildSlabs cs;
+          child_slabs(r, px, py, pz, cres, cs);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const int oct = k ^ dm;
+            double a0, b0;
+            if (((m >> oct) & 1u) && child_hit(cs, oct, a0, b0)) hm[q] |= 1u << k;
+          }
+        }
+      }
+      sum += __popc(hm[q]);
+    }
+    int64_t excl;
+    const int64_t agg = block_excl_scan<TR_NT>(sum, excl, sm_warp);
+    if (threadIdx.x == 0) sm_excl = tile_lookback(states, tile, agg);
+    __syncthreads();
+    int64_t o = sm_excl + excl;
+#pragma unroll
+    for (int q = 0; q < TR_ITEMS; ++q) {
+      if (!hm[q]) continue;
+      ng_ray r;
+      load_ray(rays, pr[q], r);
+      const int dm = r.flags & 7;
+      const unsigned m = __ldg(cmask + pv[q]);
+      const int32_t first = __ldg(cstart + pv[q]);
+      const uint64_t c = __ldg(codes + pv[q]);
+      const int px = (int)compact3(c), py = (int)compact3(c >> 1), pz = (int)compact3(c >> 2);
+      ChildSlabs cs;
+      if (NEXT_FINAL) child_slabs(r, px, py, pz, cres, cs);
+      for (unsigned bits = hm[q]; bits; bits &= bits - 1) {
+        const int k = __ffs(bits) - 1;
+        const int oct = k ^ dm;
+        const int32_t child = first + __popc(m & ((1u << oct) - 1u));
+        if (o < out_cap) {
+          if (NEXT_FINAL) {
+            ng_hit_pair h;
+            h.ray = pr[q];
+            h.voxel = child;
+            child_hit(cs, oct, h.t_enter, h.t_exit);
+            out_hits[o] = h;
+          } else {
+            out_pairs[o] = ng_pair{pr[q], child};
+          }
+        }
+        ++o;
+      }
+    }
+    if (tile == n_tiles - 1 && threadIdx.x == TR_NT - 1) *d_count_out = o;
+    __syncthreads();
+  }
+}
+
 __global__ void k_segments(const ng_hit_pair* __restrict__ hits, const int64_t* __restrict__ d_count,
                            int64_t cap, int64_t n_rays, int64_t* __restrict__ seg_start,
                            int64_t* __restrict__ seg_end) {
@@ -260,6 +377,31 @@ int traverse_level(const ng_octree& tree, const ng_ray* rays, int t, bool final,
     k_traverse_level<false><<<grid, TR_NT, 0, s>>>(tree, rays, t, in, d_count_in, in_cap, out_pairs,
                                                    out_hits, d_count_out, out_cap, states, counter);
   NG_CHECK_LAUNCH("ng_traverse_level");
+  return NG_OK;
+}
+
+int traverse_hits(const ng_octree& tree, const ng_ray* rays, int t, bool next_final, const ng_pair* in,
+                  const int64_t* d_count_in, int64_t in_cap, ng_pair* out_pairs, ng_hit_pair* out_hits,
+                  int64_t* d_count_out, int64_t out_cap, void* scratch, size_t scratch_bytes, cudaStream_t s) {
+  size_t need = level_scratch_bytes(in_cap);
+  if (scratch_bytes < need) {
+    set_error("traverse_hits: scratch %zu < %zu bytes", scratch_bytes, need);
+    return NG_ERR_CAPACITY;
+  }
+  int r = cuda_status(cudaMemsetAsync(scratch, 0, need, s), "traverse_hits memset");
+  if (r) return r;
+  const int64_t tile = (int64_t)TR_NT * TR_ITEMS;
+  int64_t tiles = (in_cap + tile - 1) / tile;
+  int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)sm_count() * 6));
+  unsigned int* counter = (unsigned int*)scratch;
+  unsigned long long* states = (unsigned long long*)((char*)scratch + 16);
+  if (next_final)
+    k_traverse_hits<true><<<grid, TR_NT, 0, s>>>(tree, rays, t, in, d_count_in, in_cap, out_pairs, out_hits,
+                                                 d_count_out, out_cap, states, counter);
+  else
+    k_traverse_hits<false><<<grid, TR_NT, 0, s>>>(tree, rays, t, in, d_count_in, in_cap, out_pairs, out_hits,
+                                                  d_count_out, out_cap, states, counter);
+  NG_CHECK_LAUNCH("k_traverse_hits");
   return NG_OK;
 }
 

@@ -1,0 +1,110 @@
+"""Multi-GPU frames: image bands sharded across ranks, framebuffer gathered
+over NCCL (BASELINE.json configs[3] / [4]).
+
+One process per GPU. Rays are independent (render.py:389-394 already
+shards them), so each rank renders the bands b with b % world == rank
+(interleaved 8-row bands balance the costlier silhouette rows) with its own
+replica of the octree and field, then the colour (and optionally depth /
+hit) tiles are all-gathered with one NCCL collective and assembled. There
+is no other data-path exchange.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _lib
+from ._lib import call, ptr, stream_ptr
+from .errors import OctfieldError
+from .render import Camera, RenderConfig, RenderSession, band_rows_of, resolve_config, resolve_lod
+
+DEFAULT_BAND_ROWS = 8
+
+
+def band_layout(height: int, world: int, band_rows: int = DEFAULT_BAND_ROWS) -> list:
+    """Global rows owned by each rank, in local order."""
+    return [band_rows_of(height, band_rows, world, r) for r in range(world)]
+
+
+def assemble(gathered: torch.Tensor, layout: list, height: int) -> torch.Tensor:
+    """Scatter per-rank band tiles back into image order.
+
+    gathered: (world, max_rows, ...) as produced by all_gather_into_tensor of
+    row-padded local tiles; returns (height, ...)."""
+    world = gathered.shape[0]
+    out = gathered.new_empty((height,) + tuple(gathered.shape[2:]))
+    for r in range(world):
+        rows = layout[r]
+        if len(rows):
+            idx = torch.as_tensor(rows, dtype=torch.long, device=gathered.device)
+            out.index_copy_(0, idx, gathered[r, :len(rows)])
+    return out
+
+
+def gather_tiles(local: torch.Tensor, layout: list, height: int, group=None) -> torch.Tensor:
+    """All-gather row-padded local tiles (rows, ...) and assemble the image."""
+    world = dist.get_world_size(group)
+    max_rows = max(len(rows) for rows in layout)
+    padded = local.new_zeros((max_rows,) + tuple(local.shape[1:]))
+    padded[:local.shape[0]] = local
+    flat = local.new_empty((world * max_rows,) + tuple(local.shape[1:]))
+    dist.all_gather_into_tensor(flat, padded, group=group)
+    return assemble(flat.view((world, max_rows) + tuple(local.shape[1:])), layout, height)
+
+
+class TiledRenderer:
+    """Renders frames of one camera size cooperatively across the ranks of
+    the default process group (NCCL)."""
+
+    def __init__(self, fld, width: int, height: int, band_rows: int = DEFAULT_BAND_ROWS, group=None):
+        self.fld = fld
+        self.width, self.height = width, height
+        self.group = group
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.band_rows = band_rows
+        self.layout = band_layout(height, self.world, band_rows)
+        self.local_rows = len(self.layout[self.rank])
+        self.sess = RenderSession(fld, width, max(self.local_rows, 1), n_rays=max(self.local_rows * width, 1))
+        self.frame = self.sess.new_frame()
+
+    def enqueue(self, camera: Camera, cfg) -> None:
+        """Launch this rank's bands (no host sync)."""
+        cs = camera.band_struct(self.band_rows, self.world, self.rank)
+        fs = self.sess.frame_struct(self.frame)
+        if self.local_rows:
+            call("ng_render_frame", self.fld.svo.device.ref(), self.fld.device.ref(), ctypes.byref(cfg),
+                 ctypes.byref(cs), ctypes.byref(fs), ctypes.byref(self.sess.ws), ptr(self.sess.stats),
+                 stream_ptr())
+
+    def gather_color(self) -> torch.Tensor:
+        """(height, width, 3) uint8 image on every rank."""
+        local = self.frame["color"][:self.local_rows * self.width].view(self.local_rows, self.width, 3)
+        return gather_tiles(local, self.layout, self.height, self.group)
+
+    def render(self, camera: Camera, config: RenderConfig):
+        """One frame: returns (image (H, W, 3) uint8 device tensor, visible, evals)."""
+        lod = resolve_lod(camera, self.fld, config)
+        cfg = resolve_config(self.fld, config, lod)
+        n_levels = cfg.trace_level + self.fld.svo.device.n_virtual
+        while True:
+            self.enqueue(camera, cfg)
+            st = self.sess.read_stats()
+            again = torch.tensor([1 if st.overflow else 0], device=_lib.device())
+            if self.world > 1:
+                dist.all_reduce(again, group=self.group)
+            if st.overflow:
+                self.sess.grow(st, n_levels)
+            if int(again.item()) == 0:
+                break
+        if st.counters.evals_missing_level or st.counters.nonfinite_inputs:
+            raise OctfieldError("decoder ran outside the queried level's voxels or on non-finite input")
+        img = self.gather_color()
+        counts = torch.tensor([st.visible, st.counters.decoder_evals], dtype=torch.int64, device=_lib.device())
+        if self.world > 1:
+            dist.all_reduce(counts, group=self.group)
+        return img, int(counts[0].item()), int(counts[1].item())

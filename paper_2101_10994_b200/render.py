@@ -72,6 +72,15 @@ class Camera:
         c.aspect = self.width / self.height
         c.width = int(self.width)
         c.height = int(self.height)
+        c.band_rows, c.band_stride, c.band_offset, c.local_rows = int(self.height), 1, 0, int(self.height)
+        return c
+
+    def band_struct(self, band_rows: int, stride: int, offset: int) -> _lib.NgCamera:
+        """Camera restricted to the image bands owned by one of `stride`
+        ranks (bands of `band_rows` rows, band b to rank b % stride)."""
+        c = self.struct()
+        c.band_rows, c.band_stride, c.band_offset = int(band_rows), int(stride), int(offset)
+        c.local_rows = len(band_rows_of(self.height, band_rows, stride, offset))
         return c
 
     def device_rays(self) -> torch.Tensor:
@@ -86,6 +95,12 @@ class Camera:
         raw = self.device_rays().cpu().numpy()
         rec = raw.view(np.float64).reshape(-1, 10)
         return RayBundle(rec[:, 0:3].copy(), rec[:, 3:6].copy())
+
+
+def band_rows_of(height: int, band_rows: int, stride: int, offset: int) -> np.ndarray:
+    """Global image rows of the bands b = offset, offset + stride, ... in order."""
+    rows = np.arange(height)
+    return rows[(rows // band_rows) % stride == offset]
 
 
 @dataclass
@@ -479,7 +494,7 @@ def render(camera: Camera, fld: NeuralField, config: RenderConfig):
     lod = resolve_lod(camera, fld, config)
     cfg = resolve_config(fld, config, lod)
     sess = _session(fld, camera.width, camera.height)
-    n_levels = cfg.trace_level + fld.svo.device.n_virtual + 1
+    n_levels = cfg.trace_level + fld.svo.device.n_virtual  # index of the final hit count
     while True:
         frame = sess.new_frame()
         sess.enqueue(cfg, frame, camera=camera, timed=True)
@@ -509,7 +524,7 @@ def trace_rays(fld: NeuralField, rays: RayBundle, lod: float, config: RenderConf
         return np.zeros(0, dtype=bool), np.zeros(0)
     sess = RenderSession(fld, n, 1, n_rays=n)
     d_rays = device_rays(rays)
-    n_levels = cfg.trace_level + fld.svo.device.n_virtual + 1
+    n_levels = cfg.trace_level + fld.svo.device.n_virtual  # index of the final hit count
     while True:
         frame = sess.new_frame()
         sess.enqueue(cfg, frame, rays=d_rays, do_normals=False)

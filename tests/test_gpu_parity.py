@@ -360,3 +360,34 @@ def test_sphere_trace_and_normals_api_match_oracle(ng, golden, O):
         q = ng.query_field(fld, pts, lod)
         qo = O.query(tree, fld.Z, decs, pts, lod)
         assert np.abs(q - qo).max(initial=0.0) <= SDF_TOL
+
+
+def test_band_tiles_reassemble_to_full_frame(ng, golden, O):
+    """The multi-GPU tiling (parallel.py) on one device: each rank's bands
+    rendered separately and assembled equal the single full-frame render."""
+    import ctypes
+    import torch
+    from paper_2101_10994_b200 import scenes, parallel
+    from paper_2101_10994_b200.render import RenderSession, resolve_config, resolve_lod
+    from paper_2101_10994_b200 import _lib
+    go = golden("octree")
+    svo = ng.build_octree(O.sdf_torus(0.5, 0.2), 4, go["samples_b"])
+    fld = scenes.planted_field(svo, O.sdf_torus(0.5, 0.2), seed=0, device_sdf=False)
+    W, H, world = 96, 45, 3
+    cam = ng.Camera((0.0, 2.0, 3.5), (0.0, 0.0, 0.0), (0.0, 1.0, 0.0), 30.0, W, H)
+    full, _ = ng.render(cam, fld, ng.RenderConfig())
+    layout = parallel.band_layout(H, world, 8)
+    cfg = resolve_config(fld, ng.RenderConfig(), resolve_lod(cam, fld, ng.RenderConfig()))
+    max_rows = max(len(r) for r in layout)
+    gathered = torch.zeros((world, max_rows, W, 3), dtype=torch.uint8, device="cuda")
+    for r in range(world):
+        n = len(layout[r]) * W
+        sess = RenderSession(fld, W, len(layout[r]), n_rays=n)
+        fr = sess.new_frame()
+        cs = cam.band_struct(8, world, r)
+        _lib.call("ng_render_frame", svo.device.ref(), fld.device.ref(), ctypes.byref(cfg), ctypes.byref(cs),
+                  ctypes.byref(sess.frame_struct(fr)), ctypes.byref(sess.ws), _lib.ptr(sess.stats), _lib.stream_ptr())
+        assert not sess.read_stats().overflow
+        gathered[r, :len(layout[r])] = fr["color"].view(len(layout[r]), W, 3)
+    img = parallel.assemble(gathered, layout, H).cpu().numpy()
+    np.testing.assert_array_equal(img, full.color)
