@@ -157,6 +157,12 @@ typedef struct ng_render_cfg {
   double background[3];
   int32_t max_iters;
   int32_t trace_level;    /* min(ceil(lod), max_level) */
+  /* Secondary shadow rays (BASELINE.json configs[4]; not in the reference):
+   * from p + shadow_offset * n toward the light, traced with the same rules;
+   * a hit means the pixel is shaded with the ambient term only. */
+  double shadow_offset;
+  int32_t shadows;
+  int32_t pad;
 } ng_render_cfg;
 
 /* Per-pixel frame outputs (render.py:117-128), device arrays of n pixels. */
@@ -187,6 +193,8 @@ typedef struct ng_frame_stats {
   int64_t active_rays;
   ng_counters counters;
   int64_t overflow;              /* nonzero: a pair list exceeded its capacity */
+  int64_t shadow_pairs[NG_MAX_TLEVELS + 1]; /* shadow-ray traversal (when cfg.shadows) */
+  int64_t shadowed;              /* hit pixels whose shadow ray hit the surface */
 } ng_frame_stats;
 
 /* ---- library ----------------------------------------------------------- */

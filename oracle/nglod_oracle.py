@@ -561,6 +561,8 @@ class RenderParams:
     albedo: tuple = (0.82, 0.84, 0.88)
     ambient: float = 0.12
     background: tuple = (0.09, 0.10, 0.13)
+    shadows: bool = False           # extension (configs[4]); not in the reference
+    shadow_offset: float | None = None
 
 
 def camera_rays(position, look_at, up, fov_y_deg, width, height):
@@ -691,11 +693,14 @@ def normals(tree, Z, decoders, pts, eps: float, lod: float, counts: Counts | Non
     return out, ok
 
 
-def shade(hit, nrm, cfg: RenderParams) -> np.ndarray:
-    """shade (render.py:303-314): Lambert, 8-bit."""
+def shade(hit, nrm, cfg: RenderParams, shadowed=None) -> np.ndarray:
+    """shade (render.py:303-314): Lambert, 8-bit; shadowed pixels keep only
+    the ambient term (shadow extension)."""
     light = np.asarray(cfg.light_dir, dtype=np.float64)
     light = light / np.linalg.norm(light)
     lam = np.clip(nrm @ light, 0.0, 1.0)
+    if shadowed is not None:
+        lam = np.where(shadowed, 0.0, lam)
     rgb = np.where(hit[..., None],
                    np.asarray(cfg.albedo) * (cfg.ambient + (1.0 - cfg.ambient) * lam[..., None]),
                    np.asarray(cfg.background))
@@ -715,6 +720,7 @@ class OracleFrame:
     total_evals: int
     visible: int
     lod: float
+    shadowed: np.ndarray | None = None
 
 
 def render(tree, Z, decoders, camera: dict, cfg: RenderParams, shard: int = 8192,
@@ -772,6 +778,21 @@ def render(tree, Z, decoders, camera: dict, cfg: RenderParams, shard: int = 8192
         return c
 
     counts += run(do_normals, [slice(s, min(s + shard, len(hot))) for s in range(0, len(hot), shard)])
+    shadowed = None
+    if cfg.shadows and len(hot):
+        # secondary rays: the reference's composition for arbitrary rays
+        # (metrics.trace_field_rays, metrics.py:135-142) from p + off * n
+        off = cfg.shadow_offset if cfg.shadow_offset is not None else 2.0 * eps
+        light = np.asarray(cfg.light_dir, dtype=np.float64)
+        light = light / np.linalg.norm(light)
+        so = pts[hot] + off * nrm[hot]
+        sd = np.broadcast_to(light, so.shape).copy()
+        sfin = traverse(tree, so, sd, level)[-1]
+        c = Counts()
+        shit, _, _, _ = march(tree, Z, decoders, so, sd, sfin, lod, cfg, c)
+        counts.append(c)
+        shadowed = np.zeros(n, dtype=bool)
+        shadowed[hot] = shit
     total = sum(c.decoder_evals for c in counts)
     if sum(c.evals_missing_level for c in counts):
         raise OracleError("decoder ran outside the queried level's voxels")
@@ -780,10 +801,12 @@ def render(tree, Z, decoders, camera: dict, cfg: RenderParams, shard: int = 8192
         shp = (h, w)
     else:
         shp = (n,)
-    color = shade(hit.reshape(shp), nrm.reshape(shp + (3,)), cfg)
+    color = shade(hit.reshape(shp), nrm.reshape(shp + (3,)), cfg,
+                  None if shadowed is None else shadowed.reshape(shp))
     return OracleFrame(hit.reshape(shp), t_hit.reshape(shp), pts.reshape(shp + (3,)),
                        nrm.reshape(shp + (3,)), ok.reshape(shp), iters.reshape(shp),
-                       evals.reshape(shp), color, int(total), int(hit.sum()), lod)
+                       evals.reshape(shp), color, int(total), int(hit.sum()), lod,
+                       None if shadowed is None else shadowed.reshape(shp))
 
 
 # --------------------------------------------------------------------------

@@ -87,7 +87,8 @@ class NgRenderCfg(C.Structure):
     _fields_ = [("delta", C.c_double), ("far_plane", C.c_double), ("skip_eps", C.c_double),
                 ("osc_tol", C.c_double), ("lod", C.c_double), ("normal_eps", C.c_double),
                 ("light", C.c_double * 3), ("albedo", C.c_double * 3), ("ambient", C.c_double),
-                ("background", C.c_double * 3), ("max_iters", C.c_int32), ("trace_level", C.c_int32)]
+                ("background", C.c_double * 3), ("max_iters", C.c_int32), ("trace_level", C.c_int32),
+                ("shadow_offset", C.c_double), ("shadows", C.c_int32), ("pad", C.c_int32)]
 
 
 class NgFrame(C.Structure):
@@ -102,7 +103,8 @@ class NgWorkspace(C.Structure):
 
 class NgFrameStats(C.Structure):
     _fields_ = [("pairs", C.c_int64 * (MAX_TLEVELS + 1)), ("visible", C.c_int64),
-                ("active_rays", C.c_int64), ("counters", NgCounters), ("overflow", C.c_int64)]
+                ("active_rays", C.c_int64), ("counters", NgCounters), ("overflow", C.c_int64),
+                ("shadow_pairs", C.c_int64 * (MAX_TLEVELS + 1)), ("shadowed", C.c_int64)]
 
 
 RAY_BYTES = 80

@@ -471,6 +471,61 @@ __global__ void k_finish_stats(ng_frame_stats* st, int n_levels, int64_t pair_ca
   st->active_rays = (int64_t)*d_active;
 }
 
+// Shadow rays for the hit pixels: origin p + offset * n, direction = light.
+__global__ void k_shadow_rays(const ng_ray* __restrict__ rays, const int32_t* __restrict__ hit_list,
+                              const unsigned long long* __restrict__ d_hits, const double* __restrict__ t_hit,
+                              const double* __restrict__ normal, ng_render_cfg cfg, ng_ray* __restrict__ srays,
+                              int64_t* d_root) {
+  const int64_t n = (int64_t)*d_hits;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *d_root = n;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t px = hit_list[j];
+    const ng_ray& r = rays[px];
+    const double th = t_hit[px];
+    double o[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+      o[a] = dadd(dadd(r.o[a], dmul(th, r.d[a])), dmul(cfg.shadow_offset, normal[3 * px + a]));
+    ng_ray sr;
+    make_ray(o[0], o[1], o[2], cfg.light[0], cfg.light[1], cfg.light[2], sr);
+    srays[j] = sr;
+  }
+}
+
+// Lambert shading of hit pixels with the shadow term (ambient only in shadow).
+__global__ void k_shade_shadowed(const int32_t* __restrict__ hit_list, const unsigned long long* __restrict__ d_hits,
+                                 const double* __restrict__ normal, const uint8_t* __restrict__ s_hit,
+                                 ng_render_cfg cfg, uint8_t* __restrict__ color, int64_t* d_shadowed) {
+  const int64_t n = (int64_t)*d_hits;
+  int local = 0;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t px = hit_list[j];
+    double lam = 0.0;
+    if (!s_hit[j]) {
+      lam = dadd(dadd(dmul(normal[3 * px], cfg.light[0]), dmul(normal[3 * px + 1], cfg.light[1])),
+                 dmul(normal[3 * px + 2], cfg.light[2]));
+      lam = lam < 0.0 ? 0.0 : (lam > 1.0 ? 1.0 : lam);
+    } else {
+      ++local;
+    }
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) {
+      double rgb = dmul(cfg.albedo[ch], dadd(cfg.ambient, dmul(dsub(1.0, cfg.ambient), lam)));
+      rgb = rgb < 0.0 ? 0.0 : (rgb > 1.0 ? 1.0 : rgb);
+      color[3 * px + ch] = (uint8_t)dadd(dmul(rgb, 255.0), 0.5);
+    }
+  }
+  for (int o = 16; o; o >>= 1) local += __shfl_xor_sync(FULL, local, o);
+  if ((threadIdx.x & 31) == 0 && local) atomicAdd((unsigned long long*)d_shadowed, (unsigned long long)local);
+}
+
+__global__ void k_shadow_overflow(ng_frame_stats* st, int n_levels, int64_t pair_cap, int64_t hit_cap) {
+  int64_t over = 0;
+  for (int t = 1; t < n_levels; ++t) over |= (st->shadow_pairs[t] > pair_cap);
+  over |= (st->shadow_pairs[n_levels] > hit_cap);
+  if (over) st->overflow = 1;
+}
+
 // ------------------------------------------------------------------ host side
 
 struct LodPlan {
@@ -557,6 +612,7 @@ static void background_u8(const ng_render_cfg& cfg, uint8_t bg[3]) {
 // Workspace layout (all offsets 256-byte aligned).
 struct WsLayout {
   size_t rays, pairs_a, pairs_b, hits, seg_start, seg_end, active, hit_list, scratch, ctr, total;
+  size_t s_rays, s_hit, s_t, s_it, s_ev;  // shadow-ray pass
   size_t scratch_bytes;
 };
 
@@ -576,8 +632,66 @@ static WsLayout layout(int64_t n, int64_t pair_cap, int64_t hit_cap) {
   L.scratch_bytes = level_scratch_bytes(std::max<int64_t>(std::max<int64_t>(pair_cap, n), 1));
   L.scratch = o; o = al(o + L.scratch_bytes);
   L.ctr = o; o = al(o + 64);
+  L.s_rays = o; o = al(o + (size_t)n * sizeof(ng_ray));
+  L.s_hit = o; o = al(o + (size_t)n);
+  L.s_t = o; o = al(o + (size_t)n * 8);
+  L.s_it = o; o = al(o + (size_t)n * 4);
+  L.s_ev = o; o = al(o + (size_t)n * 4);
   L.total = o;
   return L;
+}
+
+// Hit-filtered traversal of `rays` (root count already in counts[0]),
+// per-ray segments and the list of rays with a segment, then the march
+// arguments (outputs left to the caller).
+static int trace_pass(const ng_octree& tree, const ng_render_cfg& cfg, const LodPlan& P, const ng_ray* rays,
+                      int64_t n, int64_t* counts, const WsLayout& L, const ng_workspace& ws, char* b,
+                      unsigned long long* d_active, unsigned long long* work_counter, cudaStream_t s,
+                      MarchArgs& A) {
+  ng_pair* pa = (ng_pair*)(b + L.pairs_a);
+  ng_pair* pb = (ng_pair*)(b + L.pairs_b);
+  ng_hit_pair* hits = (ng_hit_pair*)(b + L.hits);
+  int64_t* seg_start = (int64_t*)(b + L.seg_start);
+  int64_t* seg_end = (int64_t*)(b + L.seg_end);
+  int32_t* active = (int32_t*)(b + L.active);
+  void* scratch = b + L.scratch;
+  int r;
+  // pass t expands the hits at level t into the hit children at level t+1;
+  // the last pass writes the final (ray, voxel, t_enter, t_exit) list
+  const int target = cfg.trace_level + tree.n_virtual;
+  const ng_pair* in = nullptr;
+  int64_t in_cap = n;
+  for (int t = 0; t < target; ++t) {
+    const bool last = (t + 1 == target);
+    ng_pair* out = (t % 2 == 0) ? pa : pb;
+    r = traverse_hits(tree, rays, t, last, in, &counts[t], in_cap, last ? nullptr : out, last ? hits : nullptr,
+                      &counts[t + 1], last ? ws.hit_capacity : ws.pair_capacity, scratch, L.scratch_bytes, s);
+    if (r) return r;
+    in = out;
+    in_cap = ws.pair_capacity;
+  }
+  if ((r = cuda_status(cudaMemsetAsync(seg_start, 0, n * 8, s), "seg memset"))) return r;
+  if ((r = cuda_status(cudaMemsetAsync(seg_end, 0, n * 8, s), "seg memset"))) return r;
+  k_segments_active<<<grid_for(std::max<int64_t>(ws.hit_capacity, 1), 256), 256, 0, s>>>(
+      hits, &counts[target], ws.hit_capacity, seg_start, seg_end, active, d_active);
+  NG_CHECK_LAUNCH("k_segments_active");
+  A.cfg = cfg;
+  A.G = P.G;
+  A.out_mask = P.out_mask;
+  A.dec_first = P.dec_first;
+  A.dec_last = P.dec_last;
+  A.passes = P.passes;
+  A.blend_base = P.blend_base;
+  A.blend_alpha = P.alpha;
+  A.rays = rays;
+  A.work = active;
+  A.d_n_work = d_active;
+  A.n_work = 0;
+  A.hits = hits;
+  A.seg_start = seg_start;
+  A.seg_end = seg_end;
+  A.work_counter = work_counter;
+  return NG_OK;
 }
 
 static int render_common(const ng_octree& tree, const ng_field& f, const ng_render_cfg& cfg,
@@ -598,15 +712,9 @@ static int render_common(const ng_octree& tree, const ng_field& f, const ng_rend
   }
   char* b = (char*)ws.base;
   ng_ray* rays = user_rays ? (ng_ray*)user_rays : (ng_ray*)(b + L.rays);
-  ng_pair* pa = (ng_pair*)(b + L.pairs_a);
-  ng_pair* pb = (ng_pair*)(b + L.pairs_b);
-  ng_hit_pair* hits = (ng_hit_pair*)(b + L.hits);
-  int64_t* seg_start = (int64_t*)(b + L.seg_start);
-  int64_t* seg_end = (int64_t*)(b + L.seg_end);
-  int32_t* active = (int32_t*)(b + L.active);
   int32_t* hit_list = (int32_t*)(b + L.hit_list);
-  void* scratch = b + L.scratch;
-  unsigned long long* ctr = (unsigned long long*)(b + L.ctr);  // [0] active, [1] hits, [2] work
+  // [0] active rays, [1] hits, [2] march work, [3] shadow active, [4] shadow work
+  unsigned long long* ctr = (unsigned long long*)(b + L.ctr);
   int r;
   if ((r = cuda_status(cudaMemsetAsync(st, 0, sizeof(ng_frame_stats), s), "stats memset"))) return r;
   if ((r = cuda_status(cudaMemsetAsync(ctr, 0, 64, s), "ctr memset"))) return r;
@@ -621,52 +729,17 @@ static int render_common(const ng_octree& tree, const ng_field& f, const ng_rend
     k_set_count<<<1, 1, 0, s>>>(&st->pairs[0], n);  // root list (i, 0) of n rays
     NG_CHECK_LAUNCH("k_set_count");
   }
-  // ---- traversal (traversal.py:207-247), hit-filtered: pass t expands the
-  // hits at level t into the hit children at level t+1; the last pass
-  // writes the final (ray, voxel, t_enter, t_exit) list
+  // ---- traversal (traversal.py:207-247) + segments + march setup
   const int target = cfg.trace_level + tree.n_virtual;
-  const ng_pair* in = nullptr;
-  int64_t in_cap = n;
-  for (int t = 0; t < target; ++t) {
-    const bool last = (t + 1 == target);
-    ng_pair* out = (t % 2 == 0) ? pa : pb;
-    r = traverse_hits(tree, rays, t, last, in, &st->pairs[t], in_cap, last ? nullptr : out, last ? hits : nullptr,
-                      &st->pairs[t + 1], last ? ws.hit_capacity : ws.pair_capacity, scratch, L.scratch_bytes, s);
-    if (r) return r;
-    in = out;
-    in_cap = ws.pair_capacity;
-  }
-  // ---- segments + active rays
-  if ((r = cuda_status(cudaMemsetAsync(seg_start, 0, n * 8, s), "seg memset"))) return r;
-  if ((r = cuda_status(cudaMemsetAsync(seg_end, 0, n * 8, s), "seg memset"))) return r;
-  k_segments_active<<<grid_for(std::max<int64_t>(ws.hit_capacity, 1), 256), 256, 0, s>>>(
-      hits, &st->pairs[target], ws.hit_capacity, seg_start, seg_end, active, ctr + 0);
-  NG_CHECK_LAUNCH("k_segments_active");
-  // ---- sphere trace (render.py:174-274)
   const LodPlan P = plan_lod(cfg);
   MarchArgs A;
-  A.cfg = cfg;
-  A.G = P.G;
-  A.out_mask = P.out_mask;
-  A.dec_first = P.dec_first;
-  A.dec_last = P.dec_last;
-  A.passes = P.passes;
-  A.blend_base = P.blend_base;
-  A.blend_alpha = P.alpha;
-  A.rays = rays;
-  A.work = active;
-  A.d_n_work = ctr + 0;
-  A.n_work = 0;
-  A.hits = hits;
-  A.seg_start = seg_start;
-  A.seg_end = seg_end;
+  if ((r = trace_pass(tree, cfg, P, rays, n, st->pairs, L, ws, b, ctr + 0, ctr + 2, s, A))) return r;
   A.hit = fr.hit;
   A.t = fr.t;
   A.iters = fr.iterations;
   A.evals = fr.evals;
   A.hit_list = hit_list;
   A.d_hit_count = ctr + 1;
-  A.work_counter = ctr + 2;
   A.counters = &st->counters;
   if (ws.ev_march_begin && (r = cuda_status(cudaEventRecord((cudaEvent_t)ws.ev_march_begin, s), "event record")))
     return r;
@@ -691,12 +764,34 @@ static int render_common(const ng_octree& tree, const ng_field& f, const ng_rend
     B.t_hit = fr.t;
     B.normal = fr.normal;
     B.ok = fr.normal_ok;
-    B.color = fr.color;
+    B.color = cfg.shadows ? nullptr : fr.color;
     B.counters = &st->counters;
     if ((r = launch_normals(tree, f, B, n, s))) return r;
   }
   k_finish_stats<<<1, 1, 0, s>>>(st, target, ws.pair_capacity, ws.hit_capacity, ctr + 1, ctr + 0);
   NG_CHECK_LAUNCH("k_finish_stats");
+  // ---- shadow rays toward the light (configs[4]) with the same traversal + march
+  if (cfg.shadows && do_normals) {
+    ng_ray* srays = (ng_ray*)(b + L.s_rays);
+    k_shadow_rays<<<grid_for(n, 256), 256, 0, s>>>(rays, hit_list, ctr + 1, fr.t, fr.normal, cfg, srays,
+                                                  &st->shadow_pairs[0]);
+    NG_CHECK_LAUNCH("k_shadow_rays");
+    MarchArgs S;
+    if ((r = trace_pass(tree, cfg, P, srays, n, st->shadow_pairs, L, ws, b, ctr + 3, ctr + 4, s, S))) return r;
+    S.hit = (uint8_t*)(b + L.s_hit);
+    S.t = (double*)(b + L.s_t);
+    S.iters = (int32_t*)(b + L.s_it);
+    S.evals = (int32_t*)(b + L.s_ev);
+    S.hit_list = nullptr;
+    S.d_hit_count = nullptr;
+    S.counters = &st->counters;
+    if ((r = launch_march(tree, f, S, s))) return r;
+    k_shade_shadowed<<<grid_for(n, 256), 256, 0, s>>>(hit_list, ctr + 1, fr.normal, S.hit, cfg, fr.color,
+                                                     &st->shadowed);
+    NG_CHECK_LAUNCH("k_shade_shadowed");
+    k_shadow_overflow<<<1, 1, 0, s>>>(st, target, ws.pair_capacity, ws.hit_capacity);
+    NG_CHECK_LAUNCH("k_shadow_overflow");
+  }
   return NG_OK;
 }
 

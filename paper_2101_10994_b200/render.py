@@ -120,8 +120,15 @@ class RenderConfig:
     albedo: tuple = (0.82, 0.84, 0.88)
     ambient: float = 0.12
     background: tuple = (0.09, 0.10, 0.13)
+    # extension (BASELINE.json configs[4]; not in the reference): secondary
+    # shadow rays from p + shadow_offset * n toward the light (default offset
+    # 2 * normal_eps, one finest voxel edge); shadowed pixels get the ambient term
+    shadows: bool = False
+    shadow_offset: float | None = None
 
     def __post_init__(self):
+        if self.shadow_offset is not None and self.shadow_offset <= 0.0:
+            raise ConfigError("shadow_offset must be positive")
         for name in ("delta", "far_plane", "skip_eps", "osc_factor"):
             if getattr(self, name) <= 0.0:
                 raise ConfigError(f"{name} must be positive")
@@ -198,6 +205,7 @@ class FrameReport:
     evals: int
     visible: int
     lod: float
+    shadowed: int = 0
 
 
 def select_lod(camera: Camera, svo, thresholds) -> float:
@@ -236,6 +244,9 @@ def resolve_config(fld: NeuralField, config: RenderConfig, lod: float, eps: floa
     c.ambient = float(config.ambient)
     c.max_iters = int(config.max_iters)
     c.trace_level = _trace_level(fld, lod)
+    c.shadows = 1 if getattr(config, "shadows", False) else 0
+    off = getattr(config, "shadow_offset", None)
+    c.shadow_offset = float(off) if off is not None else 2.0 * c.normal_eps
     return c
 
 
@@ -509,7 +520,8 @@ def render(camera: Camera, fld: NeuralField, config: RenderConfig):
     ms_normals = sess.ev1.elapsed_time(sess.ev2)
     fb = FrameBuffer(camera.width, camera.height, frame, camera=camera)
     report = FrameReport(ms_trace=float(ms_trace), ms_normals=float(ms_normals),
-                         evals=int(st.counters.decoder_evals), visible=int(st.visible), lod=lod)
+                         evals=int(st.counters.decoder_evals), visible=int(st.visible), lod=lod,
+                         shadowed=int(st.shadowed))
     return fb, report
 
 

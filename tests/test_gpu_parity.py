@@ -391,3 +391,25 @@ def test_band_tiles_reassemble_to_full_frame(ng, golden, O):
         gathered[r, :len(layout[r])] = fr["color"].view(len(layout[r]), W, 3)
     img = parallel.assemble(gathered, layout, H).cpu().numpy()
     np.testing.assert_array_equal(img, full.color)
+
+
+@pytest.mark.parametrize("lod", [4.0, 3.5])
+def test_shadow_rays_match_oracle(ng, golden, O, lod):
+    """configs[4]: continuous LOD + secondary shadow rays (an extension; the
+    oracle composes its reference-equivalent traversal + march on the shadow
+    rays, as metrics.trace_field_rays does, metrics.py:135-142)."""
+    from paper_2101_10994_b200 import scenes
+    go = golden("octree")
+    svo = ng.build_octree(O.sdf_torus(0.5, 0.2), 4, go["samples_b"])
+    tree = oracle_tree_from_golden(go, "b_")
+    fld = scenes.planted_field(svo, O.sdf_torus(0.5, 0.2), seed=0, device_sdf=False)
+    decs = [O.OracleDecoder(d.W1, d.b1, d.W2, d.b2) for d in fld.decoders]
+    cam = dict(position=(0.0, 2.0, 3.5), look_at=(0.0, 0.0, 0.0), up=(0.0, 1.0, 0.0), fov_y_deg=30.0,
+               width=96, height=72)
+    fb, rep = ng.render(ng.Camera(**cam), fld, ng.RenderConfig(lod=lod, shadows=True))
+    fr = O.render(tree, fld.Z, decs, cam, O.RenderParams(lod=lod, shadows=True))
+    assert np.mean(fb.hit == fr.hit) >= 0.999
+    both = fb.hit & fr.hit
+    assert fr.shadowed[both].sum() > 0, "test scene should cast shadows"
+    assert abs(rep.shadowed - int(fr.shadowed.sum())) <= max(3, int(fr.shadowed.sum()) // 50)
+    assert np.mean(np.all(fb.color == fr.color, axis=-1)) >= 0.99
