@@ -84,6 +84,8 @@ class TiledRenderer:
     def gather_color(self) -> torch.Tensor:
         """(height, width, 3) uint8 image on every rank."""
         local = self.frame["color"][:self.local_rows * self.width].view(self.local_rows, self.width, 3)
+        if self.world == 1:
+            return local
         return gather_tiles(local, self.layout, self.height, self.group)
 
     def render(self, camera: Camera, config: RenderConfig):
