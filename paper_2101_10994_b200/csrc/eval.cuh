@@ -99,12 +99,25 @@ struct EvalLane {
   bool inside;        // inside the query_field level (true when not tested)
 };
 
-// Evaluate the warp's 32 points. `emit(L, value_f32, nonfinite, lane)` is called
-// warp-uniformly for every decoder level L in ctx.out_mask, in ascending L,
-// after the lane's z_L is complete; lanes decide what to do with it.
-template <class Emit>
+// SIMT decoder policy: each lane runs its point's MLP (skipped when no lane
+// of the warp needs a decode).
+struct SimtMlp {
+  const EvalCtx& c;
+  __device__ __forceinline__ float operator()(int l, const float xf[3], const float* zrow, bool any,
+                                              bool& bad) const {
+    bad = false;
+    if (!any) return 0.f;
+    return mlp_eval(c.dec + (l - c.dec_first) * c.dec_stride, c.h, xf, zrow, bad);
+  }
+};
+
+// Evaluate the warp's 32 points. At every decoder level L in ctx.out_mask
+// (ascending) the decoder policy `mlp` turns the lane's z_L into a value and
+// `emit(L, value_f32, nonfinite, lane)` is called warp-uniformly; lanes
+// decide what to do with it.
+template <class Mlp, class Emit>
 __device__ __forceinline__ EvalLane warp_eval(const ng_octree& tree, const EvalCtx& c, WarpScratch& ws,
-                                              bool act, const double x[3], Emit&& emit) {
+                                              bool act, const double x[3], const Mlp& mlp, Emit&& emit) {
   const int lane = (int)lane_id();
   EvalLane res;
   res.present = 0;
@@ -194,12 +207,8 @@ __device__ __forceinline__ EvalLane warp_eval(const ng_octree& tree, const EvalC
     __syncwarp();
     if ((c.out_mask >> (l - 1)) & 1) {
       const bool any = __any_sync(FULL, dec && (res.present != 0));
-      float d = 0.f;
       bool bad = false;
-      if (any) {
-        const float* decw = c.dec + (l - c.dec_first) * c.dec_stride;
-        d = mlp_eval(decw, c.h, xf, &ws.zt[lane][0], bad);
-      }
+      const float d = mlp(l, xf, &ws.zt[lane][0], any, bad);
       emit(l, d, bad && dec && res.present != 0, res);
     }
   }

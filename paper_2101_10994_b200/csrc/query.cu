@@ -4,10 +4,15 @@
 #include "eval.cuh"
 
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
 
 namespace ng {
 
 int grid_for(int64_t n, int nt);
+int run_query_tc(const ng_octree& tree, const ng_field& f, const ng_query_args& a, int G, int out_mask,
+                 int dec_first, int dec_last, int ncols, const double* pts, int64_t n, double* out,
+                 ng_counters* counters, cudaStream_t s);
 
 constexpr int Q_NW = 8;  // warps per CTA
 
@@ -52,7 +57,7 @@ __global__ void __launch_bounds__(NW * 32) k_query(const __grid_constant__ ng_oc
     }
     int col = 0;
     double lo_v = 0.0, hi_v = 0.0;
-    EvalLane r = warp_eval(tree, c, ws, act, x, [&](int L, float d, bool bad, const EvalLane& er) {
+    EvalLane r = warp_eval(tree, c, ws, act, x, SimtMlp{c}, [&](int L, float d, bool bad, const EvalLane& er) {
       if (act) {
         double v;
         if (!er.inside) {
@@ -181,6 +186,16 @@ int run_query(const ng_octree& tree, const ng_field& f, const ng_query_args& a, 
   if (n <= 0) return NG_OK;
   const int dec_first = __builtin_ctz((unsigned)out_mask) + 1;
   const int dec_last = G;
+  // tensor-core decoder (query_tc.cu) unless NG_DECODER=simt
+  static int use_tc = -1;
+  if (use_tc < 0) {
+    const char* e = getenv("NG_DECODER");
+    use_tc = (e && strcmp(e, "simt") == 0) ? 0 : 1;
+  }
+  if (use_tc) {
+    int r = run_query_tc(tree, f, a, G, out_mask, dec_first, dec_last, ncols, pts, n, out, counters, s);
+    if (r != NG_ERR_CAPACITY) return r;
+  }
   const size_t smem = query_smem_bytes(dec_last - dec_first + 1, f.dec_stride, Q_NW);
   static size_t configured = 0;
   if (smem > configured) {

@@ -257,7 +257,7 @@ __global__ void __launch_bounds__(NW * 32) k_march(const __grid_constant__ ng_oc
       }
     }
     FieldValue fv;
-    const EvalLane er = warp_eval(tree, c, ws, act, x, [&](int L, float dv, bool bad, const EvalLane& e) {
+    const EvalLane er = warp_eval(tree, c, ws, act, x, SimtMlp{c}, [&](int L, float dv, bool bad, const EvalLane& e) {
       if (!act || !e.inside) return;
       double v;
       if (e.present & ((1u << L) - 1u)) {
@@ -372,7 +372,7 @@ __global__ void __launch_bounds__(NW * 32) k_normals(const __grid_constant__ ng_
 #pragma unroll
       for (int a = 0; a < 3; ++a) x[a] = np_min(np_max(x[a], -1.0), 1.0);
       FieldValue fv;
-      const EvalLane er = warp_eval(tree, c, ws, act, x, [&](int L, float dv, bool bad, const EvalLane& e) {
+      const EvalLane er = warp_eval(tree, c, ws, act, x, SimtMlp{c}, [&](int L, float dv, bool bad, const EvalLane& e) {
         if (!act || !e.inside) return;
         double v;
         if (e.present & ((1u << L) - 1u)) {
