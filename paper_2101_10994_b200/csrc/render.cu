@@ -9,10 +9,11 @@
 // evaluation (eval.cuh). All control-flow arithmetic (t, clamp, stop rules)
 // is fp64 in the reference's operation order; only features and the MLP are
 // fp32.
-#include "eval.cuh"
+#include "tc_mlp.cuh"
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 
 namespace ng {
 
@@ -139,17 +140,43 @@ struct FieldValue {
   double lo = 0.0, hi = 0.0;
 };
 
-template <int NW>
-__global__ void __launch_bounds__(NW * 32) k_march(const __grid_constant__ ng_octree tree, ng_field f,
-                                                  const __grid_constant__ MarchArgs A) {
-  extern __shared__ float4 smem4[];
-  float* dec = reinterpret_cast<float*>(smem4);
-  WarpScratch* wsa = reinterpret_cast<WarpScratch*>(dec + (A.dec_last - A.dec_first + 1) * f.dec_stride);
-  stage_decoders(dec, f.decoders, A.dec_first, A.dec_last, f.dec_stride);
-  WarpScratch& ws = wsa[threadIdx.x >> 5];
+// Decoder policy setup shared by the march and normals kernels: SIMT stages
+// fp32 decoders; TC carves TMEM / A tiles / bf16 B tiles (tc_mlp.cuh).
+template <bool TC>
+struct DecoderSetup {
+  float* dec = nullptr;
+  WarpScratch* ws = nullptr;
+  TcSmem t;
+  uint32_t tmem_base = 0;
+  __device__ __forceinline__ DecoderSetup(uint8_t* smem, const ng_field& f, int first, int last, int groups) {
+    if constexpr (TC) {
+      t = tc_carve(smem, last - first + 1, groups);
+      tmem_base = tc_setup(t, f.decoders, first, last, f.dec_stride, groups);
+      ws = t.ws;
+    } else {
+      dec = reinterpret_cast<float*>(smem);
+      ws = reinterpret_cast<WarpScratch*>(dec + (last - first + 1) * f.dec_stride);
+      stage_decoders(dec, f.decoders, first, last, f.dec_stride);
+    }
+  }
+};
+
+template <int NW, bool TC>
+__global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_constant__ ng_octree tree, ng_field f,
+                                                              const __grid_constant__ MarchArgs A) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  __shared__ int gflag[NW];
+  constexpr int GROUPS = TC ? NW / 4 : 1;
+  DecoderSetup<TC> D(smem_raw, f, A.dec_first, A.dec_last, GROUPS);
+  const int w = threadIdx.x >> 5;
+  const int g = w / 4;
+  WarpScratch& ws = D.ws[w];
+  uint32_t phase = 0;
+  TcMlp tcm;
+  if constexpr (TC) tcm = tc_policy(D.t, D.tmem_base, A.dec_first, &phase);
   EvalCtx c;
   c.Z = f.Z;
-  c.dec = dec;
+  c.dec = D.dec;
   c.dec_first = A.dec_first;
   c.dec_stride = f.dec_stride;
   c.h = f.h;
@@ -238,7 +265,15 @@ __global__ void __launch_bounds__(NW * 32) k_march(const __grid_constant__ ng_oc
       if (!__any_sync(FULL, ray < 0 && !drained)) break;
     }
     const bool act = ray >= 0;
-    if (!__any_sync(FULL, act)) break;
+    if constexpr (TC) {
+      // the group's 4 warps step together (one 128-row GEMM per output level)
+      const int wf = __any_sync(FULL, act) ? 1 : 0;
+      if (lane == 0) gflag[w] = wf;
+      tc::named_sync(1 + g, 128);
+      if (!(gflag[4 * g] | gflag[4 * g + 1] | gflag[4 * g + 2] | gflag[4 * g + 3])) break;
+    } else {
+      if (!__any_sync(FULL, act)) break;
+    }
 
     // ---- query point: x = o + t d clamped into the current voxel (render.py:244-245)
     double x[3] = {0.0, 0.0, 0.0};
@@ -257,7 +292,7 @@ __global__ void __launch_bounds__(NW * 32) k_march(const __grid_constant__ ng_oc
       }
     }
     FieldValue fv;
-    const EvalLane er = warp_eval(tree, c, ws, act, x, SimtMlp{c}, [&](int L, float dv, bool bad, const EvalLane& e) {
+    auto emit = [&](int L, float dv, bool bad, const EvalLane& e) {
       if (!act || !e.inside) return;
       double v;
       if (e.present & ((1u << L) - 1u)) {
@@ -270,7 +305,10 @@ __global__ void __launch_bounds__(NW * 32) k_march(const __grid_constant__ ng_oc
         lc.empty += 1;
       }
       if (L == A.blend_base) fv.lo = v; else fv.hi = v;
-    });
+    };
+    EvalLane er;
+    if constexpr (TC) er = warp_eval(tree, c, ws, act, x, tcm, emit);
+    else er = warp_eval(tree, c, ws, act, x, SimtMlp{c}, emit);
 
     // ---- stop rules (render.py:247-272)
     if (act) {
@@ -303,6 +341,7 @@ __global__ void __launch_bounds__(NW * 32) k_march(const __grid_constant__ ng_oc
     }
   }
   lc.flush(A.counters);
+  if constexpr (TC) tc_teardown(D.tmem_base, GROUPS);
 }
 
 struct NormalArgs {
@@ -323,17 +362,20 @@ struct NormalArgs {
 };
 
 // normals (render.py:277-300) + shade (render.py:303-314) for hit pixels.
-template <int NW>
-__global__ void __launch_bounds__(NW * 32) k_normals(const __grid_constant__ ng_octree tree, ng_field f,
-                                                    const __grid_constant__ NormalArgs A) {
-  extern __shared__ float4 smem4[];
-  float* dec = reinterpret_cast<float*>(smem4);
-  WarpScratch* wsa = reinterpret_cast<WarpScratch*>(dec + (A.dec_last - A.dec_first + 1) * f.dec_stride);
-  stage_decoders(dec, f.decoders, A.dec_first, A.dec_last, f.dec_stride);
-  WarpScratch& ws = wsa[threadIdx.x >> 5];
+template <int NW, bool TC>
+__global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_normals(const __grid_constant__ ng_octree tree, ng_field f,
+                                                                const __grid_constant__ NormalArgs A) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  constexpr int GROUPS = TC ? NW / 4 : 1;
+  DecoderSetup<TC> D(smem_raw, f, A.dec_first, A.dec_last, GROUPS);
+  const int w = threadIdx.x >> 5;
+  WarpScratch& ws = D.ws[w];
+  uint32_t phase = 0;
+  TcMlp tcm;
+  if constexpr (TC) tcm = tc_policy(D.t, D.tmem_base, A.dec_first, &phase);
   EvalCtx c;
   c.Z = f.Z;
-  c.dec = dec;
+  c.dec = D.dec;
   c.dec_first = A.dec_first;
   c.dec_stride = f.dec_stride;
   c.h = f.h;
@@ -343,10 +385,13 @@ __global__ void __launch_bounds__(NW * 32) k_normals(const __grid_constant__ ng_
   const int64_t n = A.pts ? A.n_pts : (int64_t)*A.d_hit_count;
   const double eps = A.cfg.normal_eps;
   LaneCounters lc;
-  const int64_t n_chunks = (n + 31) / 32;
-  for (int64_t chunk = (int64_t)blockIdx.x * NW + (threadIdx.x >> 5); chunk < n_chunks;
-       chunk += (int64_t)gridDim.x * NW) {
-    const int64_t i = chunk * 32 + lane_id();
+  // work units: 32 points per warp (SIMT) or 128 per 4-warp group (TC)
+  constexpr int UNIT = TC ? 128 : 32;
+  constexpr int PER_CTA = TC ? NW / 4 : NW;
+  const int my = TC ? w / 4 : w;
+  const int64_t n_units = (n + UNIT - 1) / UNIT;
+  for (int64_t u = (int64_t)blockIdx.x * PER_CTA + my; u < n_units; u += (int64_t)gridDim.x * PER_CTA) {
+    const int64_t i = u * UNIT + (TC ? 32 * (w % 4) : 0) + lane_id();
     const bool act = i < n;
     int64_t dst = i;
     double p[3] = {0.0, 0.0, 0.0};
@@ -372,7 +417,7 @@ __global__ void __launch_bounds__(NW * 32) k_normals(const __grid_constant__ ng_
 #pragma unroll
       for (int a = 0; a < 3; ++a) x[a] = np_min(np_max(x[a], -1.0), 1.0);
       FieldValue fv;
-      const EvalLane er = warp_eval(tree, c, ws, act, x, SimtMlp{c}, [&](int L, float dv, bool bad, const EvalLane& e) {
+      auto emit = [&](int L, float dv, bool bad, const EvalLane& e) {
         if (!act || !e.inside) return;
         double v;
         if (e.present & ((1u << L) - 1u)) {
@@ -385,7 +430,10 @@ __global__ void __launch_bounds__(NW * 32) k_normals(const __grid_constant__ ng_
           lc.empty += 1;
         }
         if (L == A.blend_base) fv.lo = v; else fv.hi = v;
-      });
+      };
+      EvalLane er;
+      if constexpr (TC) er = warp_eval(tree, c, ws, act, x, tcm, emit);
+      else er = warp_eval(tree, c, ws, act, x, SimtMlp{c}, emit);
       double v = 0.0;
       if (act) {
         if (!er.inside) {
@@ -430,6 +478,7 @@ __global__ void __launch_bounds__(NW * 32) k_normals(const __grid_constant__ ng_
     }
   }
   lc.flush(A.counters);
+  if constexpr (TC) tc_teardown(D.tmem_base, GROUPS);
 }
 
 __global__ void k_shade(const uint8_t* __restrict__ hit, const double* __restrict__ normal, int64_t n,
@@ -571,35 +620,51 @@ static int prep_kernel(K kernel, size_t smem, int nt, int& per_sm) {
   return NG_OK;
 }
 
-static int launch_march(const ng_octree& tree, const ng_field& f, MarchArgs& A, cudaStream_t s) {
-  const size_t smem = (size_t)(A.dec_last - A.dec_first + 1) * f.dec_stride * 4 + R_NW * sizeof(WarpScratch);
-  int per_sm;
-  int r = prep_kernel(k_march<R_NW>, smem, R_NW * 32, per_sm);
-  if (r) return r;
-  static int cap = -1;  // NG_MARCH_CTAS_PER_SM: experiment knob for the persistent grid
-  if (cap < 0) {
-    const char* e = getenv("NG_MARCH_CTAS_PER_SM");
-    cap = e ? atoi(e) : 0;
+constexpr int R_NW_TC = 12;  // 3 tile groups of 4 warps
+
+static bool use_tc_decoder(const ng_field& f) {
+  static int env = -1;
+  if (env < 0) {
+    const char* e = getenv("NG_DECODER");
+    env = (e && strcmp(e, "simt") == 0) ? 0 : 1;
   }
-  if (cap > 0 && cap < per_sm) per_sm = cap;
-  k_march<R_NW><<<sm_count() * per_sm, R_NW * 32, smem, s>>>(tree, f, A);
-  NG_CHECK_LAUNCH("k_march");
+  return env && f.h == tc::N;
+}
+
+template <class KS, class KT, class Args>
+static int launch_eval_kernel(KS ksimt, KT ktc, const ng_field& f, const ng_octree& tree, const Args& A, int64_t max_units,
+                              bool cap_by_work, const char* name, cudaStream_t s) {
+  const int ndec = A.dec_last - A.dec_first + 1;
+  int per_sm, r;
+  if (use_tc_decoder(f) && tc_smem_bytes(ndec, R_NW_TC / 4) <= 227 * 1024) {
+    const size_t smem = tc_smem_bytes(ndec, R_NW_TC / 4);
+    if ((r = prep_kernel(ktc, smem, R_NW_TC * 32, per_sm))) return r;
+    int64_t grid = (int64_t)sm_count() * per_sm;
+    if (cap_by_work) grid = std::max<int64_t>(1, std::min<int64_t>(grid, (max_units + 127) / 128));
+    ktc<<<(int)grid, R_NW_TC * 32, smem, s>>>(tree, f, A);
+  } else {
+    const size_t smem = (size_t)ndec * f.dec_stride * 4 + R_NW * sizeof(WarpScratch);
+    if ((r = prep_kernel(ksimt, smem, R_NW * 32, per_sm))) return r;
+    static int cap = -1;  // NG_MARCH_CTAS_PER_SM: experiment knob for the persistent grid
+    if (cap < 0) {
+      const char* e = getenv("NG_MARCH_CTAS_PER_SM");
+      cap = e ? atoi(e) : 0;
+    }
+    if (cap > 0 && cap < per_sm) per_sm = cap;
+    int64_t grid = (int64_t)sm_count() * per_sm;
+    if (cap_by_work) grid = std::max<int64_t>(1, std::min<int64_t>(grid, (max_units + 32 * R_NW - 1) / (32 * R_NW)));
+    ksimt<<<(int)grid, R_NW * 32, smem, s>>>(tree, f, A);
+  }
+  NG_CHECK_LAUNCH(name);
   return NG_OK;
 }
 
-static int launch_normals(const ng_octree& tree, const ng_field& f, NormalArgs& A, int64_t max_n,
-                          cudaStream_t s) {
-  const size_t smem = (size_t)(A.dec_last - A.dec_first + 1) * f.dec_stride * 4 + R_NW * sizeof(WarpScratch);
-  int per_sm;
-  int r = prep_kernel(k_normals<R_NW>, smem, R_NW * 32, per_sm);
-  if (r) return r;
-  // persistent: the work count may live on the device, so size for the SMs
-  // (decoders are staged once per CTA)
-  int64_t want = (max_n + 32 * R_NW - 1) / (32 * R_NW);
-  int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sm_count() * per_sm));
-  k_normals<R_NW><<<grid, R_NW * 32, smem, s>>>(tree, f, A);
-  NG_CHECK_LAUNCH("k_normals");
-  return NG_OK;
+static int launch_march(const ng_octree& tree, const ng_field& f, MarchArgs& A, cudaStream_t s) {
+  return launch_eval_kernel(k_march<R_NW, false>, k_march<R_NW_TC, true>, f, tree, A, 0, false, "k_march", s);
+}
+
+static int launch_normals(const ng_octree& tree, const ng_field& f, NormalArgs& A, int64_t max_n, cudaStream_t s) {
+  return launch_eval_kernel(k_normals<R_NW, false>, k_normals<R_NW_TC, true>, f, tree, A, max_n, true, "k_normals", s);
 }
 
 static void background_u8(const ng_render_cfg& cfg, uint8_t bg[3]) {

@@ -1,0 +1,152 @@
+// Tensor-core decoder policy shared by the query, march and normals kernels.
+#pragma once
+
+#include "eval.cuh"
+#include "tc.cuh"
+
+namespace ng {
+
+constexpr int DEC_TC_BYTES = 2 * tc::TILE_BYTES + 128 * 4 + 128;  // B_hi, B_lo, W2[128], b2 (+pad)
+
+struct TcMlp {
+  uint8_t* a_hi;
+  uint8_t* a_lo;
+  const uint8_t* dec_tiles;  // DEC_TC_BYTES per decoder, level dec_first first
+  int dec_first;
+  uint32_t tmem;
+  uint64_t* mbar;
+  uint32_t* phase;
+  int wg;
+  int bar_id;
+
+  __device__ __forceinline__ float operator()(int l, const float xf[3], const float* zrow, bool /*any*/,
+                                              bool& bad) const {
+    const int lane = (int)lane_id();
+    const int row = 32 * wg + lane;
+    float v[36];
+    v[0] = xf[0];
+    v[1] = xf[1];
+    v[2] = xf[2];
+#pragma unroll
+    for (int k = 0; k < 32; ++k) v[3 + k] = zrow[k];
+    v[35] = 1.0f;  // bias input: B row 35 holds b1
+    float chk = 0.f;
+#pragma unroll
+    for (int k = 0; k < 35; ++k) chk += v[k] - v[k];
+    bad = !(chk == 0.f);
+    tc::write_row(a_hi, a_lo, row, v);
+    tc::fence_proxy_async();
+    tc::fence_before_sync();
+    tc::named_sync(bar_id, 128);
+    const uint8_t* dt = dec_tiles + (size_t)(l - dec_first) * DEC_TC_BYTES;
+    if (wg == 0 && lane == 0)
+      tc::issue_gemm(tmem, tc::smem_u32(a_hi), tc::smem_u32(a_lo), tc::smem_u32(dt), tc::smem_u32(dt + tc::TILE_BYTES),
+                     mbar);
+    tc::mbar_wait(mbar, *phase & 1u);
+    *phase += 1;
+    tc::fence_after_sync();
+    const float* W2 = reinterpret_cast<const float*>(dt + 2 * tc::TILE_BYTES);
+    float acc = W2[128];  // b2
+    const uint32_t taddr = tmem + ((uint32_t)(32 * wg) << 16);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      float h[32];
+      tc::tmem_ld32(taddr + 32 * c, h);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) acc = fmaf(W2[32 * c + i], fmaxf(h[i], 0.f), acc);
+    }
+    tc::fence_before_sync();
+    return acc;
+  }
+};
+
+// Convert packed fp32 decoders (ng_field layout) into bf16 hi/lo B tiles.
+__device__ __forceinline__ void stage_decoder_tiles(uint8_t* dst, const float* __restrict__ src, int first, int last, int stride) {
+  const int ndec = last - first + 1;
+  for (int idx = threadIdx.x; idx < ndec * 128 * tc::CHUNKS; idx += blockDim.x) {
+    const int d = idx / (128 * tc::CHUNKS);
+    const int j = (idx / tc::CHUNKS) % 128;
+    const int c = idx % tc::CHUNKS;
+    const float* row = src + (size_t)(first - 1 + d) * stride + (size_t)j * NG_W1_STRIDE;
+    __align__(16) __nv_bfloat16 h[8], lo[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int k = c * 8 + q;
+      tc::split_bf16(k < NG_W1_STRIDE ? __ldg(row + k) : 0.f, h[q], lo[q]);
+    }
+    uint8_t* t = dst + (size_t)d * DEC_TC_BYTES;
+    const int off = tc::tile_off(j, c * 8);
+    *reinterpret_cast<uint4*>(t + off) = *reinterpret_cast<const uint4*>(h);
+    *reinterpret_cast<uint4*>(t + tc::TILE_BYTES + off) = *reinterpret_cast<const uint4*>(lo);
+  }
+  for (int idx = threadIdx.x; idx < ndec * 129; idx += blockDim.x) {
+    const int d = idx / 129, j = idx % 129;
+    const float* w2 = src + (size_t)(first - 1 + d) * stride + 128 * NG_W1_STRIDE;
+    reinterpret_cast<float*>(dst + (size_t)d * DEC_TC_BYTES + 2 * tc::TILE_BYTES)[j] = __ldg(w2 + j);
+  }
+}
+
+
+// Shared-memory carve-up for a kernel with `groups` 4-warp tile groups.
+struct TcSmem {
+  uint8_t* dec_tiles;
+  uint8_t* a_tiles;
+  WarpScratch* ws;
+  uint64_t* mbar;
+  uint32_t* tmem_slot;
+};
+
+__host__ __device__ constexpr size_t tc_smem_bytes(int ndec, int groups) {
+  return (size_t)ndec * DEC_TC_BYTES + (size_t)groups * 2 * tc::TILE_BYTES + (size_t)groups * 4 * sizeof(WarpScratch) +
+         (size_t)groups * 8 + 16;
+}
+
+__device__ __forceinline__ TcSmem tc_carve(uint8_t* smem, int ndec, int groups) {
+  TcSmem t;
+  t.dec_tiles = smem;
+  t.a_tiles = t.dec_tiles + (size_t)ndec * DEC_TC_BYTES;
+  t.ws = reinterpret_cast<WarpScratch*>(t.a_tiles + (size_t)groups * 2 * tc::TILE_BYTES);
+  t.mbar = reinterpret_cast<uint64_t*>(t.ws + groups * 4);
+  t.tmem_slot = reinterpret_cast<uint32_t*>(t.mbar + groups);
+  return t;
+}
+
+// CTA prologue: TMEM (128 columns per group), mbarriers, decoder B tiles.
+__device__ __forceinline__ uint32_t tc_setup(const TcSmem& t, const float* decoders, int first, int last, int stride,
+                                             int groups) {
+  if ((threadIdx.x >> 5) == 0) tc::tmem_alloc(t.tmem_slot, 128 * groups);
+  if (threadIdx.x == 0)
+    for (int i = 0; i < groups; ++i) tc::mbar_init(t.mbar + i, 1);
+  stage_decoder_tiles(t.dec_tiles, decoders, first, last, stride);
+  tc::fence_proxy_async();
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  return *t.tmem_slot;
+}
+
+__device__ __forceinline__ void tc_teardown(uint32_t tmem_base, int groups) {
+  tc::fence_before_sync();
+  __syncthreads();
+  if ((threadIdx.x >> 5) == 0) {
+    tc::fence_after_sync();
+    tc::tmem_free(tmem_base, 128 * groups);
+  }
+}
+
+__device__ __forceinline__ TcMlp tc_policy(const TcSmem& t, uint32_t tmem_base, int dec_first, uint32_t* phase) {
+  const int w = threadIdx.x >> 5, g = w / 4;
+  TcMlp m;
+  m.a_hi = t.a_tiles + (size_t)g * 2 * tc::TILE_BYTES;
+  m.a_lo = m.a_hi + tc::TILE_BYTES;
+  m.dec_tiles = t.dec_tiles;
+  m.dec_first = dec_first;
+  m.tmem = tmem_base + 128 * g;
+  m.mbar = t.mbar + g;
+  m.phase = phase;
+  m.wg = w % 4;
+  m.bar_id = 1 + g;
+  return m;
+}
+
+}  // namespace ng
