@@ -111,10 +111,15 @@ __device__ __forceinline__ TcSmem tc_carve(uint8_t* smem, int ndec, int groups) 
   return t;
 }
 
+// TMEM allocations are powers of two >= 32 columns.
+__host__ __device__ constexpr uint32_t tmem_cols(int groups) {
+  return groups <= 1 ? 128u : (groups <= 2 ? 256u : 512u);
+}
+
 // CTA prologue: TMEM (128 columns per group), mbarriers, decoder B tiles.
 __device__ __forceinline__ uint32_t tc_setup(const TcSmem& t, const float* decoders, int first, int last, int stride,
                                              int groups) {
-  if ((threadIdx.x >> 5) == 0) tc::tmem_alloc(t.tmem_slot, 128 * groups);
+  if ((threadIdx.x >> 5) == 0) tc::tmem_alloc(t.tmem_slot, tmem_cols(groups));
   if (threadIdx.x == 0)
     for (int i = 0; i < groups; ++i) tc::mbar_init(t.mbar + i, 1);
   stage_decoder_tiles(t.dec_tiles, decoders, first, last, stride);
@@ -130,7 +135,7 @@ __device__ __forceinline__ void tc_teardown(uint32_t tmem_base, int groups) {
   __syncthreads();
   if ((threadIdx.x >> 5) == 0) {
     tc::fence_after_sync();
-    tc::tmem_free(tmem_base, 128 * groups);
+    tc::tmem_free(tmem_base, tmem_cols(groups));
   }
 }
 
