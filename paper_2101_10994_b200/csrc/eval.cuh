@@ -136,21 +136,55 @@ __device__ __forceinline__ EvalLane warp_eval(const ng_octree& tree, const EvalC
 #pragma unroll
   for (int p = 0; p < 32; ++p) ws.zt[p][lane] = 0.f;
 
+  // Per-lane lookups are software-pipelined across levels so their latency
+  // hides behind the gather: while level l is gathered, level l+1's corner
+  // ids and level l+2's bitmap / rank words are already in flight.
+  auto level_code = [&](int l) -> uint64_t {
+    const int sh = G - l;
+    return morton(cell[0] >> sh, cell[1] >> sh, cell[2] >> sh);
+  };
+  auto words = [&](int l, uint64_t& w, uint32_t& r) {
+    const int tl = l + tree.n_virtual;
+    const uint64_t code = level_code(l);
+    w = __ldg(tree.bitmap[tl] + (code >> 6));
+    r = __ldg(tree.rank[tl] + (code >> 6));
+  };
+  auto index_of = [&](int l, uint64_t w, uint32_t r) -> int64_t {
+    const uint32_t b = (uint32_t)(level_code(l) & 63);
+    return ((w >> b) & 1ull) ? (int64_t)r + __popcll(w & ((1ull << b) - 1ull)) : -1;
+  };
+  auto corners = [&](int l, int64_t idx, int4& a, int4& b) {
+    if (idx >= 0) {
+      const int4* cr = reinterpret_cast<const int4*>(tree.corners[l + tree.n_virtual] + 8 * idx);
+      a = __ldg(cr);
+      b = __ldg(cr + 1);
+    }
+  };
+  int64_t idx_cur = -1, idx_nxt = -1;
+  int4 ca = make_int4(0, 0, 0, 0), cb = ca, na = ca, nb = ca;
+  uint64_t w_nxt = 0;
+  uint32_t r_nxt = 0;
+  if (dec) {
+    uint64_t w1;
+    uint32_t r1;
+    words(1, w1, r1);
+    if (G >= 2) words(2, w_nxt, r_nxt);
+    idx_cur = index_of(1, w1, r1);
+    corners(1, idx_cur, ca, cb);
+  }
+
   for (int l = 1; l <= G; ++l) {
     const int sh = G - l;
     const int resl = resG >> sh;
-    const int tl = l + tree.n_virtual;
     const int ci = cell[0] >> sh, cj = cell[1] >> sh, ck = cell[2] >> sh;
-    int64_t idx = -1;
-    if (dec) idx = rank_lookup(tree.bitmap[tl], tree.rank[tl], morton(ci, cj, ck));
+    const int64_t idx = idx_cur;
     const bool pres = idx >= 0;
     int4 ia = make_int4(0, 0, 0, 0), ib = ia;
     float4 wa = make_float4(0.f, 0.f, 0.f, 0.f), wb = wa;
     if (pres) {
       res.present |= 1u << (l - 1);
-      const int4* cr = reinterpret_cast<const int4*>(tree.corners[tl] + 8 * idx);
-      ia = __ldg(cr);
-      ib = __ldg(cr + 1);
+      ia = ca;
+      ib = cb;
       // u = clip(f - cell, 0, 1) with f = (x + 1) * (res / 2)  (field.py:115-116)
       const double half = 0.5 * (double)resl;
       float u[3];
@@ -166,43 +200,57 @@ __device__ __forceinline__ EvalLane warp_eval(const ng_octree& tree, const EvalC
       wa = make_float4(wx0 * wy0 * wz0, u[0] * wy0 * wz0, wx0 * u[1] * wz0, u[0] * u[1] * wz0);
       wb = make_float4(wx0 * wy0 * u[2], u[0] * wy0 * u[2], wx0 * u[1] * u[2], u[0] * u[1] * u[2]);
     }
+    // prefetch: corners of level l+1, words of level l+2
+    if (dec && l < G) {
+      idx_nxt = index_of(l + 1, w_nxt, r_nxt);
+      corners(l + 1, idx_nxt, na, nb);
+      if (l + 2 <= G) words(l + 2, w_nxt, r_nxt);
+    }
     ws.ids[lane][0] = ia;
     ws.ids[lane][1] = ib;
     ws.w[lane][0] = wa;
     ws.w[lane][1] = wb;
     unsigned pm = __ballot_sync(FULL, pres);
     __syncwarp();
-    // lane = channel: coalesced 128-byte corner rows
+    // lane = channel: coalesced 128-byte corner rows, 4 points (32 loads) in
+    // flight per iteration; absent slots re-read a present point and are
+    // masked out of the accumulation
     const float* __restrict__ Zc = c.Z + lane;
     while (pm) {
-      const int p0 = __ffs(pm) - 1;
-      pm &= pm - 1;
-      const int p1 = pm ? __ffs(pm) - 1 : -1;
-      if (p1 >= 0) pm &= pm - 1;
-      const int4 a0 = ws.ids[p0][0], b0 = ws.ids[p0][1];
-      const float4 u0 = ws.w[p0][0], v0 = ws.w[p0][1];
-      float s0 = u0.x * __ldg(Zc + 32 * (int64_t)a0.x);
-      s0 = fmaf(u0.y, __ldg(Zc + 32 * (int64_t)a0.y), s0);
-      s0 = fmaf(u0.z, __ldg(Zc + 32 * (int64_t)a0.z), s0);
-      s0 = fmaf(u0.w, __ldg(Zc + 32 * (int64_t)a0.w), s0);
-      s0 = fmaf(v0.x, __ldg(Zc + 32 * (int64_t)b0.x), s0);
-      s0 = fmaf(v0.y, __ldg(Zc + 32 * (int64_t)b0.y), s0);
-      s0 = fmaf(v0.z, __ldg(Zc + 32 * (int64_t)b0.z), s0);
-      s0 = fmaf(v0.w, __ldg(Zc + 32 * (int64_t)b0.w), s0);
-      if (p1 >= 0) {
-        const int4 a1 = ws.ids[p1][0], b1 = ws.ids[p1][1];
-        const float4 u1 = ws.w[p1][0], v1 = ws.w[p1][1];
-        float s1 = u1.x * __ldg(Zc + 32 * (int64_t)a1.x);
-        s1 = fmaf(u1.y, __ldg(Zc + 32 * (int64_t)a1.y), s1);
-        s1 = fmaf(u1.z, __ldg(Zc + 32 * (int64_t)a1.z), s1);
-        s1 = fmaf(u1.w, __ldg(Zc + 32 * (int64_t)a1.w), s1);
-        s1 = fmaf(v1.x, __ldg(Zc + 32 * (int64_t)b1.x), s1);
-        s1 = fmaf(v1.y, __ldg(Zc + 32 * (int64_t)b1.y), s1);
-        s1 = fmaf(v1.z, __ldg(Zc + 32 * (int64_t)b1.z), s1);
-        s1 = fmaf(v1.w, __ldg(Zc + 32 * (int64_t)b1.w), s1);
-        ws.zt[p1][lane] += s1;
+      int pp[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        pp[q] = pm ? __ffs(pm) - 1 : -1;
+        pm &= pm ? pm - 1 : 0u;
       }
-      ws.zt[p0][lane] += s0;
+      float v[4][8];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int p = pp[q] >= 0 ? pp[q] : pp[0];
+        const int4 a = ws.ids[p][0], b = ws.ids[p][1];
+        v[q][0] = __ldg(Zc + 32 * (int64_t)a.x);
+        v[q][1] = __ldg(Zc + 32 * (int64_t)a.y);
+        v[q][2] = __ldg(Zc + 32 * (int64_t)a.z);
+        v[q][3] = __ldg(Zc + 32 * (int64_t)a.w);
+        v[q][4] = __ldg(Zc + 32 * (int64_t)b.x);
+        v[q][5] = __ldg(Zc + 32 * (int64_t)b.y);
+        v[q][6] = __ldg(Zc + 32 * (int64_t)b.z);
+        v[q][7] = __ldg(Zc + 32 * (int64_t)b.w);
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (pp[q] < 0) continue;
+        const float4 u0 = ws.w[pp[q]][0], u1 = ws.w[pp[q]][1];
+        float acc = u0.x * v[q][0];
+        acc = fmaf(u0.y, v[q][1], acc);
+        acc = fmaf(u0.z, v[q][2], acc);
+        acc = fmaf(u0.w, v[q][3], acc);
+        acc = fmaf(u1.x, v[q][4], acc);
+        acc = fmaf(u1.y, v[q][5], acc);
+        acc = fmaf(u1.z, v[q][6], acc);
+        acc = fmaf(u1.w, v[q][7], acc);
+        ws.zt[pp[q]][lane] += acc;
+      }
     }
     __syncwarp();
     if ((c.out_mask >> (l - 1)) & 1) {
@@ -211,6 +259,9 @@ __device__ __forceinline__ EvalLane warp_eval(const ng_octree& tree, const EvalC
       const float d = mlp(l, xf, &ws.zt[lane][0], any, bad);
       emit(l, d, bad && dec && res.present != 0, res);
     }
+    idx_cur = idx_nxt;
+    ca = na;
+    cb = nb;
   }
   __syncwarp();
   return res;
