@@ -181,7 +181,10 @@ __global__ void __launch_bounds__(RANK_NT) k_bitmap_rank(const uint64_t* __restr
     }
     int64_t excl;
     int64_t agg = block_excl_scan<RANK_NT>(sum, excl, sm_warp);
-    if (threadIdx.x == 0) sm_excl = tile_lookback(states, tile, agg);
+    if (threadIdx.x < 32) {
+      const int64_t e = tile_lookback_warp(states, tile, agg);
+      if (threadIdx.x == 0) sm_excl = e;
+    }
     __syncthreads();
     int64_t run = sm_excl + excl;
 #pragma unroll

@@ -251,6 +251,49 @@ __device__ __forceinline__ int64_t tile_lookback(unsigned long long* states, int
   return excl;
 }
 
+// Warp-parallel look-back (called by all 32 lanes of one warp): 32
+// predecessors are inspected per round, so a tile resolves its prefix in
+// about one L2 round trip instead of one per predecessor.
+__device__ __forceinline__ int64_t tile_lookback_warp(unsigned long long* states, int64_t tile,
+                                                      int64_t aggregate) {
+  const int lane = (int)(threadIdx.x & 31);
+  if (tile == 0) {
+    if (lane == 0) {
+      __threadfence();
+      atomicExch(states, (unsigned long long)(TS_PREFIX | (uint64_t)aggregate));
+    }
+    return 0;
+  }
+  if (lane == 0) {
+    __threadfence();
+    atomicExch(states + tile, (unsigned long long)(TS_AGG | (uint64_t)aggregate));
+  }
+  int64_t excl = 0;
+  int64_t base = tile - 1;
+  while (true) {
+    const int64_t p = base - lane;  // lane i looks at the i-th nearest predecessor
+    uint64_t s = TS_PREFIX;         // before tile 0: an empty prefix
+    if (p >= 0) {
+      do {
+        s = *((volatile unsigned long long*)(states + p));
+      } while ((s & ~TS_VALUE) == 0);
+    }
+    const unsigned pm = __ballot_sync(FULL, (s & ~TS_VALUE) == TS_PREFIX);
+    const int first = pm ? __ffs(pm) - 1 : 32;
+    int64_t v = (lane <= first) ? (int64_t)(s & TS_VALUE) : 0;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+    excl += v;
+    if (pm) break;
+    base -= 32;
+  }
+  if (lane == 0) {
+    __threadfence();
+    atomicExch(states + tile, (unsigned long long)(TS_PREFIX | (uint64_t)(excl + aggregate)));
+  }
+  return excl;
+}
+
 // Block-wide exclusive scan of one int64 per thread; returns the block total.
 template <int NT>
 __device__ __forceinline__ int64_t block_excl_scan(int64_t v, int64_t& excl, int64_t* sm_warp) {

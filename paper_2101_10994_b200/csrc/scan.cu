@@ -32,7 +32,10 @@ __global__ void __launch_bounds__(SCAN_NT) k_exclusive_sum(const int64_t* __rest
     }
     int64_t excl;
     int64_t agg = block_excl_scan<SCAN_NT>(sum, excl, sm_warp);
-    if (threadIdx.x == 0) sm_excl = tile_lookback(states, tile, agg);
+    if (threadIdx.x < 32) {
+      const int64_t e = tile_lookback_warp(states, tile, agg);
+      if (threadIdx.x == 0) sm_excl = e;
+    }
     __syncthreads();
     int64_t run = sm_excl + excl;
 #pragma unroll

@@ -15,7 +15,8 @@
 namespace ng {
 
 constexpr int TR_NT = 256;
-constexpr int TR_ITEMS = 4;
+constexpr int TR_ITEMS = 4;   // candidate passes (API path)
+constexpr int TH_ITEMS = 12;  // hit-filtered passes (render path)
 
 template <bool FINAL>
 __global__ void __launch_bounds__(TR_NT) k_traverse_level(
@@ -89,7 +90,10 @@ __global__ void __launch_bounds__(TR_NT) k_traverse_level(
     }
     int64_t excl;
     const int64_t agg = block_excl_scan<TR_NT>(sum, excl, sm_warp);
-    if (threadIdx.x == 0) sm_excl = tile_lookback(states, tile, agg);
+    if (threadIdx.x < 32) {
+      const int64_t e = tile_lookback_warp(states, tile, agg);
+      if (threadIdx.x == 0) sm_excl = e;
+    }
     __syncthreads();
     int64_t o = sm_excl + excl;
 #pragma unroll
@@ -157,7 +161,7 @@ __global__ void __launch_bounds__(TR_NT) k_traverse_hits(
   const uint64_t* __restrict__ codes = tree.codes[t];
   const int32_t* __restrict__ cstart = tree.child_start[t];
   const uint8_t* __restrict__ cmask = tree.child_mask[t];
-  const int64_t tile_elems = (int64_t)TR_NT * TR_ITEMS;
+  const int64_t tile_elems = (int64_t)TR_NT * TH_ITEMS;
   const int64_t n_tiles = (n + tile_elems - 1) / tile_elems;
   if (n_tiles == 0) {
     if (blockIdx.x == 0 && threadIdx.x == 0) *d_count_out = 0;
@@ -168,12 +172,12 @@ __global__ void __launch_bounds__(TR_NT) k_traverse_hits(
     __syncthreads();
     const int64_t tile = sm_tile;
     if (tile >= n_tiles) break;
-    const int64_t base = tile * tile_elems + (int64_t)threadIdx.x * TR_ITEMS;
-    int32_t pr[TR_ITEMS], pv[TR_ITEMS];
-    unsigned hm[TR_ITEMS];  // bit k: k-th front-to-back child is hit
+    const int64_t base = tile * tile_elems + (int64_t)threadIdx.x * TH_ITEMS;
+    int32_t pr[TH_ITEMS], pv[TH_ITEMS];
+    unsigned hm[TH_ITEMS];  // bit k: k-th front-to-back child is hit
     int64_t sum = 0;
 #pragma unroll
-    for (int q = 0; q < TR_ITEMS; ++q) {
+    for (int q = 0; q < TH_ITEMS; ++q) {
       const int64_t i = base + q;
       hm[q] = 0;
       pr[q] = 0;
@@ -212,11 +216,14 @@ __global__ void __launch_bounds__(TR_NT) k_traverse_hits(
     }
     int64_t excl;
     const int64_t agg = block_excl_scan<TR_NT>(sum, excl, sm_warp);
-    if (threadIdx.x == 0) sm_excl = tile_lookback(states, tile, agg);
+    if (threadIdx.x < 32) {
+      const int64_t e = tile_lookback_warp(states, tile, agg);
+      if (threadIdx.x == 0) sm_excl = e;
+    }
     __syncthreads();
     int64_t o = sm_excl + excl;
 #pragma unroll
-    for (int q = 0; q < TR_ITEMS; ++q) {
+    for (int q = 0; q < TH_ITEMS; ++q) {
       if (!hm[q]) continue;
       ng_ray r;
       load_ray(rays, pr[q], r);
