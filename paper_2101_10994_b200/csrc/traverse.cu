@@ -16,7 +16,7 @@ namespace ng {
 
 constexpr int TR_NT = 256;
 constexpr int TR_ITEMS = 4;   // candidate passes (API path)
-constexpr int TH_ITEMS = 12;  // hit-filtered passes (render path)
+constexpr int TH_ITEMS = 4;   // hit-filtered passes (render path)
 
 template <bool FINAL>
 __global__ void __launch_bounds__(TR_NT) k_traverse_level(
