@@ -155,6 +155,7 @@ _SIGS = {
     "ng_render_frame": (C.c_int, [P, P, P, P, P, P, P, P]),
     "ng_render_rays": (C.c_int, [P, P, P, P, C.c_int64, P, P, P, C.c_int32, P]),
     "ng_hit_points": (C.c_int, [P, P, P, C.c_int64, P, P]),
+    "ng_march_profile": (C.c_int, [P, C.c_int]),
 }
 
 EXPORTED = tuple(_SIGS)

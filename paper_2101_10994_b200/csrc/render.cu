@@ -132,7 +132,14 @@ struct MarchArgs {
   unsigned long long* d_hit_count;
   unsigned long long* work_counter;
   ng_counters* counters;
+  unsigned long long* prof;      // optional: 4 counters per group (steps, busy lanes, t0, t1)
 };
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 // One lane's query_field (render.py:155-171) result assembled from the
 // decoder outputs emitted by warp_eval (blend of predict(base), predict(base+1)).
@@ -267,10 +274,20 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_cons
     const bool act = ray >= 0;
     if constexpr (TC) {
       // the group's 4 warps step together (one 128-row GEMM per output level)
-      const int wf = __any_sync(FULL, act) ? 1 : 0;
+      const int wf = __popc(__ballot_sync(FULL, act));
       if (lane == 0) gflag[w] = wf;
       tc::named_sync(1 + g, 128);
-      if (!(gflag[4 * g] | gflag[4 * g + 1] | gflag[4 * g + 2] | gflag[4 * g + 3])) break;
+      const int active = gflag[4 * g] + gflag[4 * g + 1] + gflag[4 * g + 2] + gflag[4 * g + 3];
+      if (A.prof && (w & 3) == 0 && lane == 0) {  // debug profile: per-group steps and busy lanes
+        unsigned long long* pr = A.prof + 4 * (blockIdx.x * GROUPS + g);
+        if (pr[0] == 0) pr[2] = globaltimer_ns();
+        if (active) {
+          pr[0] += 1;
+          pr[1] += active;
+        }
+        pr[3] = globaltimer_ns();
+      }
+      if (!active) break;
     } else {
       if (!__any_sync(FULL, act)) break;
     }
@@ -706,6 +723,19 @@ static WsLayout layout(int64_t n, int64_t pair_cap, int64_t hit_cap) {
   return L;
 }
 
+// NG_MARCH_PROFILE=1: per-group march statistics (ng_march_profile).
+static unsigned long long* g_prof = nullptr;
+static unsigned long long* march_profile_buffer() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("NG_MARCH_PROFILE");
+    on = (e && e[0] == '1') ? 1 : 0;
+    if (on && cudaMalloc((void**)&g_prof, 4 * 8 * 4096) != cudaSuccess) on = 0;
+    if (on) cudaMemset(g_prof, 0, 4 * 8 * 4096);
+  }
+  return on ? g_prof : nullptr;
+}
+
 // Hit-filtered traversal of `rays` (root count already in counts[0]),
 // per-ray segments and the list of rays with a segment, then the march
 // arguments (outputs left to the caller).
@@ -756,6 +786,7 @@ static int trace_pass(const ng_octree& tree, const ng_render_cfg& cfg, const Lod
   A.seg_start = seg_start;
   A.seg_end = seg_end;
   A.work_counter = work_counter;
+  A.prof = march_profile_buffer();
   return NG_OK;
 }
 
@@ -929,6 +960,7 @@ int ng_sphere_trace(const ng_octree* tree, const ng_field* fld, const ng_render_
   A.d_hit_count = nullptr;
   A.work_counter = work;
   A.counters = d_counters;
+  A.prof = nullptr;
   (void)d_hit_count;
   r = launch_march(*tree, *fld, A, s);
   cudaFreeAsync(work, s);
@@ -966,6 +998,17 @@ int ng_shade(const uint8_t* hit, const double* normal, int64_t n, const ng_rende
   k_shade<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(hit, normal, n, *cfg, color);
   NG_CHECK_LAUNCH("ng_shade");
   return NG_OK;
+}
+
+// Debug: copy the march profile (4 x uint64 per group: steps, busy lanes,
+// first/last globaltimer ns) and reset it; 0 groups when profiling is off.
+int ng_march_profile(unsigned long long* host_out, int max_groups) {
+  if (!g_prof) return 0;
+  cudaDeviceSynchronize();
+  const int n = max_groups < 4096 ? max_groups : 4096;
+  cudaMemcpy(host_out, g_prof, (size_t)n * 32, cudaMemcpyDeviceToHost);
+  cudaMemset(g_prof, 0, 4 * 8 * 4096);
+  return n;
 }
 
 int ng_hit_points(const ng_ray* rays, const uint8_t* hit, const double* t, int64_t n, double* points,
