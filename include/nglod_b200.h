@@ -326,7 +326,7 @@ int ng_subdivide(const ng_octree* tree, const ng_ray* rays, int32_t t, const ng_
 int ng_compactify(const ng_pair* pairs, int64_t n, const int64_t* D, const int64_t* S, ng_pair* out,
                   void* stream);
 /* Debug (NG_MARCH_PROFILE=1): per tile group of the last march launches
- * {steps, busy lanes, first ns, last ns}; copies and resets; returns groups. */
+ * {steps, busy lanes, first ns, last ns, acquire ns, eval ns, 0, 0}; copies and resets. */
 int ng_march_profile(unsigned long long* host_out, int max_groups);
 /* Hit positions o + t*d for hit rays (FrameBuffer.points, render.py:395-396). */
 int ng_hit_points(const ng_ray* rays, const uint8_t* hit, const double* t, int64_t n,

@@ -214,7 +214,9 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_cons
     ray = -1;
   };
 
+  unsigned long long t_top = 0, t_acq = 0, t_eval = 0;
   while (true) {
+    if (A.prof && (w & 3) == 0 && lane == 0) t_top = globaltimer_ns();
     // ---- acquire rays and advance each to its next query point (render.py:200-238)
     while (true) {
       const bool want = (ray < 0) && !drained;
@@ -279,13 +281,16 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_cons
       tc::named_sync(1 + g, 128);
       const int active = gflag[4 * g] + gflag[4 * g + 1] + gflag[4 * g + 2] + gflag[4 * g + 3];
       if (A.prof && (w & 3) == 0 && lane == 0) {  // debug profile: per-group steps and busy lanes
-        unsigned long long* pr = A.prof + 4 * (blockIdx.x * GROUPS + g);
-        if (pr[0] == 0) pr[2] = globaltimer_ns();
+        unsigned long long* pr = A.prof + 8 * (blockIdx.x * GROUPS + g);
+        const unsigned long long now = globaltimer_ns();
+        if (pr[0] == 0) pr[2] = t_top;
         if (active) {
           pr[0] += 1;
           pr[1] += active;
         }
-        pr[3] = globaltimer_ns();
+        pr[3] = now;
+        pr[4] += now - t_top;  // acquire + advance + group barrier
+        t_acq = now;
       }
       if (!active) break;
     } else {
@@ -327,6 +332,10 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_cons
     if constexpr (TC) er = warp_eval(tree, c, ws, act, x, tcm, emit);
     else er = warp_eval(tree, c, ws, act, x, SimtMlp{c}, emit);
 
+    if (A.prof && (w & 3) == 0 && lane == 0) {
+      t_eval = globaltimer_ns();
+      A.prof[8 * (blockIdx.x * GROUPS + g) + 5] += t_eval - t_acq;  // gather + decoder
+    }
     // ---- stop rules (render.py:247-272)
     if (act) {
       double dval;
@@ -637,7 +646,6 @@ static int prep_kernel(K kernel, size_t smem, int nt, int& per_sm) {
   return NG_OK;
 }
 
-constexpr int R_NW_TC = 12;  // 3 tile groups of 4 warps
 
 static bool use_tc_decoder(const ng_field& f) {
   static int env = -1;
@@ -648,17 +656,40 @@ static bool use_tc_decoder(const ng_field& f) {
   return env && f.h == tc::N;
 }
 
-template <class KS, class KT, class Args>
-static int launch_eval_kernel(KS ksimt, KT ktc, const ng_field& f, const ng_octree& tree, const Args& A, int64_t max_units,
-                              bool cap_by_work, const char* name, cudaStream_t s) {
+static int tc_groups() {
+  static int g = -1;  // NG_TC_GROUPS: 4-warp tile groups per CTA (experiment knob; default 3)
+  if (g < 0) {
+    const char* e = getenv("NG_TC_GROUPS");
+    g = e ? atoi(e) : 3;
+    if (g < 1 || g > 3) g = 3;
+  }
+  return g;
+}
+
+template <class KT, class Args>
+static int launch_tc(KT ktc, int groups, const ng_field& f, const ng_octree& tree, const Args& A, int64_t max_units,
+                     bool cap_by_work, cudaStream_t s) {
+  const int ndec = A.dec_last - A.dec_first + 1;
+  const size_t smem = tc_smem_bytes(ndec, groups);
+  int per_sm, r;
+  if ((r = prep_kernel(ktc, smem, groups * 128, per_sm))) return r;
+  int64_t grid = (int64_t)sm_count() * per_sm;
+  if (cap_by_work) grid = std::max<int64_t>(1, std::min<int64_t>(grid, (max_units + 127) / 128));
+  ktc<<<(int)grid, groups * 128, smem, s>>>(tree, f, A);
+  return NG_OK;
+}
+
+template <class KS, class K1, class K2, class K3, class Args>
+static int launch_eval_kernel(KS ksimt, K1 k1, K2 k2, K3 k3, const ng_field& f, const ng_octree& tree,
+                              const Args& A, int64_t max_units, bool cap_by_work, const char* name, cudaStream_t s) {
   const int ndec = A.dec_last - A.dec_first + 1;
   int per_sm, r;
-  if (use_tc_decoder(f) && tc_smem_bytes(ndec, R_NW_TC / 4) <= 227 * 1024) {
-    const size_t smem = tc_smem_bytes(ndec, R_NW_TC / 4);
-    if ((r = prep_kernel(ktc, smem, R_NW_TC * 32, per_sm))) return r;
-    int64_t grid = (int64_t)sm_count() * per_sm;
-    if (cap_by_work) grid = std::max<int64_t>(1, std::min<int64_t>(grid, (max_units + 127) / 128));
-    ktc<<<(int)grid, R_NW_TC * 32, smem, s>>>(tree, f, A);
+  const int groups = tc_groups();
+  if (use_tc_decoder(f) && tc_smem_bytes(ndec, groups) <= 227 * 1024) {
+    if (groups == 1) r = launch_tc(k1, 1, f, tree, A, max_units, cap_by_work, s);
+    else if (groups == 2) r = launch_tc(k2, 2, f, tree, A, max_units, cap_by_work, s);
+    else r = launch_tc(k3, 3, f, tree, A, max_units, cap_by_work, s);
+    if (r) return r;
   } else {
     const size_t smem = (size_t)ndec * f.dec_stride * 4 + R_NW * sizeof(WarpScratch);
     if ((r = prep_kernel(ksimt, smem, R_NW * 32, per_sm))) return r;
@@ -677,11 +708,13 @@ static int launch_eval_kernel(KS ksimt, KT ktc, const ng_field& f, const ng_octr
 }
 
 static int launch_march(const ng_octree& tree, const ng_field& f, MarchArgs& A, cudaStream_t s) {
-  return launch_eval_kernel(k_march<R_NW, false>, k_march<R_NW_TC, true>, f, tree, A, 0, false, "k_march", s);
+  return launch_eval_kernel(k_march<R_NW, false>, k_march<4, true>, k_march<8, true>, k_march<12, true>, f, tree, A,
+                            0, false, "k_march", s);
 }
 
 static int launch_normals(const ng_octree& tree, const ng_field& f, NormalArgs& A, int64_t max_n, cudaStream_t s) {
-  return launch_eval_kernel(k_normals<R_NW, false>, k_normals<R_NW_TC, true>, f, tree, A, max_n, true, "k_normals", s);
+  return launch_eval_kernel(k_normals<R_NW, false>, k_normals<4, true>, k_normals<8, true>, k_normals<12, true>, f,
+                            tree, A, max_n, true, "k_normals", s);
 }
 
 static void background_u8(const ng_render_cfg& cfg, uint8_t bg[3]) {
@@ -730,8 +763,8 @@ static unsigned long long* march_profile_buffer() {
   if (on < 0) {
     const char* e = getenv("NG_MARCH_PROFILE");
     on = (e && e[0] == '1') ? 1 : 0;
-    if (on && cudaMalloc((void**)&g_prof, 4 * 8 * 4096) != cudaSuccess) on = 0;
-    if (on) cudaMemset(g_prof, 0, 4 * 8 * 4096);
+    if (on && cudaMalloc((void**)&g_prof, 8 * 8 * 4096) != cudaSuccess) on = 0;
+    if (on) cudaMemset(g_prof, 0, 8 * 8 * 4096);
   }
   return on ? g_prof : nullptr;
 }
@@ -1006,8 +1039,8 @@ int ng_march_profile(unsigned long long* host_out, int max_groups) {
   if (!g_prof) return 0;
   cudaDeviceSynchronize();
   const int n = max_groups < 4096 ? max_groups : 4096;
-  cudaMemcpy(host_out, g_prof, (size_t)n * 32, cudaMemcpyDeviceToHost);
-  cudaMemset(g_prof, 0, 4 * 8 * 4096);
+  cudaMemcpy(host_out, g_prof, (size_t)n * 64, cudaMemcpyDeviceToHost);
+  cudaMemset(g_prof, 0, 8 * 8 * 4096);
   return n;
 }
 

@@ -11,11 +11,11 @@ knot, svo, fld = bench.build_workload()
 cam = ng.Camera(bench.CAM["position"], bench.CAM["look_at"], bench.CAM["up"], bench.CAM["fov_y_deg"], 1280, 720)
 for _ in range(3):
     fb, rep = ng.render(cam, fld, ng.RenderConfig())
-buf = (ctypes.c_ulonglong * (4 * 4096))()
+buf = (ctypes.c_ulonglong * (8 * 4096))()
 _lib.lib().ng_march_profile(buf, 4096)  # reset
 fb, rep = ng.render(cam, fld, ng.RenderConfig())
 n = _lib.lib().ng_march_profile(buf, 4096)
-a = np.frombuffer(buf, dtype=np.uint64).reshape(-1, 4)[:n].astype(np.int64)
+a = np.frombuffer(buf, dtype=np.uint64).reshape(-1, 8)[:n].astype(np.int64)
 a = a[a[:, 0] > 0]
 t0 = a[:, 2].min()
 dur = (a[:, 3] - t0) / 1e3
@@ -23,7 +23,7 @@ steps, busy = a[:, 0], a[:, 1]
 print(f"groups {len(a)}  steps total {steps.sum()}  mean {steps.mean():.1f} max {steps.max()}")
 print(f"lane utilisation {busy.sum() / (steps.sum() * 128):.3f}  (trace evals {int(fb.evals.sum())})")
 print(f"group end (us): min {dur.min():.0f} median {np.median(dur):.0f} p90 {np.percentile(dur, 90):.0f} max {dur.max():.0f}")
-print(f"us per step (median group): {np.median(dur / steps):.2f}")
+print(f"us per step (median group): {np.median(dur / steps):.2f}  acquire {np.median(a[:, 4] / steps) / 1e3:.2f}  eval {np.median(a[:, 5] / steps) / 1e3:.2f}")
 it = fb.iterations[fb.iterations > 0]
 print(f"ray iterations: mean {it.mean():.2f} p99 {np.percentile(it, 99):.0f} max {it.max()}")
 order = np.argsort(dur)
