@@ -661,7 +661,7 @@ static int tc_groups() {
   if (g < 0) {
     const char* e = getenv("NG_TC_GROUPS");
     g = e ? atoi(e) : 3;
-    if (g < 1 || g > 3) g = 3;
+    if (g < 1 || g > 4) g = 3;
   }
   return g;
 }
@@ -679,16 +679,18 @@ static int launch_tc(KT ktc, int groups, const ng_field& f, const ng_octree& tre
   return NG_OK;
 }
 
-template <class KS, class K1, class K2, class K3, class Args>
-static int launch_eval_kernel(KS ksimt, K1 k1, K2 k2, K3 k3, const ng_field& f, const ng_octree& tree,
+template <class KS, class K1, class K2, class K3, class K4, class Args>
+static int launch_eval_kernel(KS ksimt, K1 k1, K2 k2, K3 k3, K4 k4, const ng_field& f, const ng_octree& tree,
                               const Args& A, int64_t max_units, bool cap_by_work, const char* name, cudaStream_t s) {
   const int ndec = A.dec_last - A.dec_first + 1;
   int per_sm, r;
-  const int groups = tc_groups();
+  int groups = tc_groups();
+  while (groups > 1 && tc_smem_bytes(ndec, groups) > 227 * 1024) --groups;
   if (use_tc_decoder(f) && tc_smem_bytes(ndec, groups) <= 227 * 1024) {
     if (groups == 1) r = launch_tc(k1, 1, f, tree, A, max_units, cap_by_work, s);
     else if (groups == 2) r = launch_tc(k2, 2, f, tree, A, max_units, cap_by_work, s);
-    else r = launch_tc(k3, 3, f, tree, A, max_units, cap_by_work, s);
+    else if (groups == 3) r = launch_tc(k3, 3, f, tree, A, max_units, cap_by_work, s);
+    else r = launch_tc(k4, 4, f, tree, A, max_units, cap_by_work, s);
     if (r) return r;
   } else {
     const size_t smem = (size_t)ndec * f.dec_stride * 4 + R_NW * sizeof(WarpScratch);
@@ -708,13 +710,13 @@ static int launch_eval_kernel(KS ksimt, K1 k1, K2 k2, K3 k3, const ng_field& f, 
 }
 
 static int launch_march(const ng_octree& tree, const ng_field& f, MarchArgs& A, cudaStream_t s) {
-  return launch_eval_kernel(k_march<R_NW, false>, k_march<4, true>, k_march<8, true>, k_march<12, true>, f, tree, A,
-                            0, false, "k_march", s);
+  return launch_eval_kernel(k_march<R_NW, false>, k_march<4, true>, k_march<8, true>, k_march<12, true>,
+                            k_march<16, true>, f, tree, A, 0, false, "k_march", s);
 }
 
 static int launch_normals(const ng_octree& tree, const ng_field& f, NormalArgs& A, int64_t max_n, cudaStream_t s) {
-  return launch_eval_kernel(k_normals<R_NW, false>, k_normals<4, true>, k_normals<8, true>, k_normals<12, true>, f,
-                            tree, A, max_n, true, "k_normals", s);
+  return launch_eval_kernel(k_normals<R_NW, false>, k_normals<4, true>, k_normals<8, true>, k_normals<12, true>,
+                            k_normals<16, true>, f, tree, A, max_n, true, "k_normals", s);
 }
 
 static void background_u8(const ng_render_cfg& cfg, uint8_t bg[3]) {
