@@ -112,6 +112,50 @@ __global__ void k_segments_active(const ng_hit_pair* __restrict__ hits, const in
   }
 }
 
+// Longest-first work order for the march: rays with more voxels in their
+// list (grazing / silhouette rays) take more sphere-trace steps, so they are
+// issued first and the persistent lanes do not end on a long serial tail.
+constexpr int LEN_BUCKETS = 64;
+
+__global__ void k_len_hist(const int32_t* __restrict__ active, const unsigned long long* __restrict__ d_n,
+                           const int64_t* __restrict__ seg_start, const int64_t* __restrict__ seg_end,
+                           unsigned int* __restrict__ hist) {
+  __shared__ unsigned int h[LEN_BUCKETS];
+  for (int i = threadIdx.x; i < LEN_BUCKETS; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  const int64_t n = (int64_t)*d_n;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t r = active[k];
+    const int64_t len = seg_end[r] - seg_start[r];
+    atomicAdd(&h[len < LEN_BUCKETS - 1 ? len : LEN_BUCKETS - 1], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < LEN_BUCKETS; i += blockDim.x)
+    if (h[i]) atomicAdd(&hist[i], h[i]);
+}
+
+__global__ void k_len_scatter(const int32_t* __restrict__ active, const unsigned long long* __restrict__ d_n,
+                              const int64_t* __restrict__ seg_start, const int64_t* __restrict__ seg_end,
+                              const unsigned int* __restrict__ hist, unsigned int* __restrict__ cursor,
+                              int32_t* __restrict__ sorted) {
+  __shared__ unsigned int off[LEN_BUCKETS];
+  if (threadIdx.x == 0) {
+    unsigned int run = 0;
+    for (int b = LEN_BUCKETS - 1; b >= 0; --b) {  // descending length
+      off[b] = run;
+      run += hist[b];
+    }
+  }
+  __syncthreads();
+  const int64_t n = (int64_t)*d_n;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t r = active[k];
+    const int64_t len = seg_end[r] - seg_start[r];
+    const int b = len < LEN_BUCKETS - 1 ? (int)len : LEN_BUCKETS - 1;
+    sorted[off[b] + atomicAdd(&cursor[b], 1u)] = r;
+  }
+}
+
 struct MarchArgs {
   ng_render_cfg cfg;
   int G, out_mask, dec_first, dec_last, passes;
@@ -730,6 +774,7 @@ static void background_u8(const ng_render_cfg& cfg, uint8_t bg[3]) {
 struct WsLayout {
   size_t rays, pairs_a, pairs_b, hits, seg_start, seg_end, active, hit_list, scratch, ctr, total;
   size_t s_rays, s_hit, s_t, s_it, s_ev;  // shadow-ray pass
+  size_t sorted, buckets;                 // longest-first march order
   size_t scratch_bytes;
 };
 
@@ -754,6 +799,8 @@ static WsLayout layout(int64_t n, int64_t pair_cap, int64_t hit_cap) {
   L.s_t = o; o = al(o + (size_t)n * 8);
   L.s_it = o; o = al(o + (size_t)n * 4);
   L.s_ev = o; o = al(o + (size_t)n * 4);
+  L.sorted = o; o = al(o + (size_t)n * 4);
+  L.buckets = o; o = al(o + 2 * LEN_BUCKETS * 4);
   L.total = o;
   return L;
 }
@@ -805,6 +852,14 @@ static int trace_pass(const ng_octree& tree, const ng_render_cfg& cfg, const Lod
   k_segments_active<<<grid_for(std::max<int64_t>(ws.hit_capacity, 1), 256), 256, 0, s>>>(
       hits, &counts[target], ws.hit_capacity, seg_start, seg_end, active, d_active);
   NG_CHECK_LAUNCH("k_segments_active");
+  int32_t* sorted = (int32_t*)(b + L.sorted);
+  unsigned int* buckets = (unsigned int*)(b + L.buckets);
+  if ((r = cuda_status(cudaMemsetAsync(buckets, 0, 2 * LEN_BUCKETS * 4, s), "bucket memset"))) return r;
+  k_len_hist<<<grid_for(n, 256), 256, 0, s>>>(active, d_active, seg_start, seg_end, buckets);
+  NG_CHECK_LAUNCH("k_len_hist");
+  k_len_scatter<<<grid_for(n, 256), 256, 0, s>>>(active, d_active, seg_start, seg_end, buckets,
+                                                  buckets + LEN_BUCKETS, sorted);
+  NG_CHECK_LAUNCH("k_len_scatter");
   A.cfg = cfg;
   A.G = P.G;
   A.out_mask = P.out_mask;
@@ -814,7 +869,7 @@ static int trace_pass(const ng_octree& tree, const ng_render_cfg& cfg, const Lod
   A.blend_base = P.blend_base;
   A.blend_alpha = P.alpha;
   A.rays = rays;
-  A.work = active;
+  A.work = sorted;
   A.d_n_work = d_active;
   A.n_work = 0;
   A.hits = hits;
