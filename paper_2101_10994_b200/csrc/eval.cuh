@@ -17,6 +17,10 @@
 
 #include "common.cuh"
 
+#ifndef NG_GATHER_BATCH
+#define NG_GATHER_BATCH 4  // points whose 8 corner rows are in flight together per warp
+#endif
+
 namespace ng {
 
 struct WarpScratch {
@@ -34,7 +38,14 @@ struct EvalCtx {
   int gather_level;                  // G: highest level interpolated
   int inside_level;                  // -1 or query_field level
   int out_mask;                      // decoder levels evaluated (bit L-1)
+  unsigned long long* dbg = nullptr; // debug (lane 0): ns in prologue, staging, gather, decoder
 };
+
+__device__ __forceinline__ unsigned long long dbg_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 // empty_space_value (field.py:185-191) in float64, numpy operation order.
 __device__ __forceinline__ double empty_value(const ng_octree& t, const double x[3]) {
@@ -119,6 +130,15 @@ template <class Mlp, class Emit>
 __device__ __forceinline__ EvalLane warp_eval(const ng_octree& tree, const EvalCtx& c, WarpScratch& ws,
                                               bool act, const double x[3], const Mlp& mlp, Emit&& emit) {
   const int lane = (int)lane_id();
+  const bool dbg = c.dbg && lane == 0;
+  unsigned long long t_mark = dbg ? dbg_now() : 0;
+  auto lap = [&](int slot) {
+    if (dbg) {
+      const unsigned long long t = dbg_now();
+      c.dbg[slot] += t - t_mark;
+      t_mark = t;
+    }
+  };
   EvalLane res;
   res.present = 0;
   res.inside = true;
@@ -173,6 +193,7 @@ __device__ __forceinline__ EvalLane warp_eval(const ng_octree& tree, const EvalC
     corners(1, idx_cur, ca, cb);
   }
 
+  lap(0);
   for (int l = 1; l <= G; ++l) {
     const int sh = G - l;
     const int resl = resG >> sh;
@@ -212,20 +233,21 @@ __device__ __forceinline__ EvalLane warp_eval(const ng_octree& tree, const EvalC
     ws.w[lane][1] = wb;
     unsigned pm = __ballot_sync(FULL, pres);
     __syncwarp();
+    lap(1);
     // lane = channel: coalesced 128-byte corner rows, 4 points (32 loads) in
     // flight per iteration; absent slots re-read a present point and are
     // masked out of the accumulation
     const float* __restrict__ Zc = c.Z + lane;
     while (pm) {
-      int pp[4];
+      int pp[NG_GATHER_BATCH];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < NG_GATHER_BATCH; ++q) {
         pp[q] = pm ? __ffs(pm) - 1 : -1;
         pm &= pm ? pm - 1 : 0u;
       }
-      float v[4][8];
+      float v[NG_GATHER_BATCH][8];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < NG_GATHER_BATCH; ++q) {
         const int p = pp[q] >= 0 ? pp[q] : pp[0];
         const int4 a = ws.ids[p][0], b = ws.ids[p][1];
         v[q][0] = __ldg(Zc + 32 * (int64_t)a.x);
@@ -238,7 +260,7 @@ __device__ __forceinline__ EvalLane warp_eval(const ng_octree& tree, const EvalC
         v[q][7] = __ldg(Zc + 32 * (int64_t)b.w);
       }
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < NG_GATHER_BATCH; ++q) {
         if (pp[q] < 0) continue;
         const float4 u0 = ws.w[pp[q]][0], u1 = ws.w[pp[q]][1];
         float acc = u0.x * v[q][0];
@@ -254,10 +276,12 @@ __device__ __forceinline__ EvalLane warp_eval(const ng_octree& tree, const EvalC
     }
     __syncwarp();
     if ((c.out_mask >> (l - 1)) & 1) {
+      lap(2);
       const bool any = __any_sync(FULL, dec && (res.present != 0));
       bool bad = false;
       const float d = mlp(l, xf, &ws.zt[lane][0], any, bad);
       emit(l, d, bad && dec && res.present != 0, res);
+      lap(3);
     }
     idx_cur = idx_nxt;
     ca = na;

@@ -224,8 +224,12 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_cons
   WarpScratch& ws = D.ws[w];
   uint32_t phase = 0;
   TcMlp tcm;
-  if constexpr (TC) tcm = tc_policy(D.t, D.tmem_base, A.dec_first, &phase);
+  if constexpr (TC) {
+    tcm = tc_policy(D.t, D.tmem_base, A.dec_first, &phase);
+    if (A.prof) tcm.prof = A.prof + 8 * (blockIdx.x * GROUPS + g);
+  }
   EvalCtx c;
+  if (A.prof && w == 0) c.dbg = A.prof + 8 * 4096 - 8 * 1024 + 8 * (blockIdx.x % 1024);
   c.Z = f.Z;
   c.dec = D.dec;
   c.dec_first = A.dec_first;

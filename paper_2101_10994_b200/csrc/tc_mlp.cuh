@@ -18,9 +18,12 @@ struct TcMlp {
   uint32_t* phase;
   int wg;
   int bar_id;
+  unsigned long long* prof = nullptr;  // debug: [6] += ns gather->decoder entry, [7] += ns in decoder
 
   __device__ __forceinline__ float operator()(int l, const float xf[3], const float* zrow, bool /*any*/,
                                               bool& bad) const {
+    unsigned long long t_in = 0;
+    if (prof && wg == 0 && lane_id() == 0) asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_in));
     const int lane = (int)lane_id();
     const int row = 32 * wg + lane;
     float v[36];
@@ -56,6 +59,12 @@ struct TcMlp {
       for (int i = 0; i < 32; ++i) acc = fmaf(W2[32 * c + i], fmaxf(h[i], 0.f), acc);
     }
     tc::fence_before_sync();
+    if (prof && wg == 0 && lane_id() == 0) {
+      unsigned long long t_out;
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_out));
+      prof[7] += t_out - t_in;
+      prof[6] = t_in;  // caller turns this into the gather time
+    }
     return acc;
   }
 };
