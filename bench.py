@@ -49,6 +49,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-query", action="store_true", help="skip the batched-query leg")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-extra", action="store_true", help="skip the configs[3]/[4] 1080p legs")
     return ap.parse_args()
 
 
@@ -278,6 +279,10 @@ def run_ours(args, rank: int, world: int):
                   "h2d_bytes_per_step": _sizeof("NgCamera") + _sizeof("NgRenderCfg"),
                   "d2h_bytes_per_step": d2h + _sizeof("NgFrameStats")}
 
+    # ---- configs[3] / configs[4] at 1920x1080 (tiled across the ranks when N > 1)
+    if not args.no_extra:
+        res["extra"] = extra_configs(args, world, dev, knot)
+
     # ---- batched SDF query (configs[2]): forward L = 1..5 over 2^24 points,
     # sharded by point range across ranks (no exchange)
     if not args.no_query:
@@ -305,6 +310,56 @@ def run_ours(args, rank: int, world: int):
         del out
     res["_svo"], res["_fld"] = svo, fld
     return res
+
+
+def _time_tiled(tiles, cam, cfg, steps, flush, world):
+    import torch
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for _ in range(2):
+        tiles.enqueue(cam, cfg)
+    torch.cuda.synchronize()
+    for a, b in ev:
+        flush.zero_()
+        a.record()
+        tiles.enqueue(cam, cfg)
+        if world > 1:
+            tiles.gather_color()
+        b.record()
+    torch.cuda.synchronize()
+    ms = statistics.median(a.elapsed_time(b) for a, b in ev)
+    if world > 1:
+        t = torch.tensor([ms], device=flush.device)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    return ms
+
+
+def extra_configs(args, world, dev, knot):
+    """configs[3]: LOD6 1920x1080 (image bands + NCCL gather when N > 1);
+    configs[4]: continuous LOD 4.5 with shadow rays at 1920x1080."""
+    import torch
+    import paper_2101_10994_b200 as ng
+    from paper_2101_10994_b200 import scenes
+    from paper_2101_10994_b200.parallel import TiledRenderer
+    from paper_2101_10994_b200.render import resolve_config, resolve_lod
+    _, samples = knot_scene()
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+    out = {}
+    svo6 = ng.build_octree(knot, 6, samples)
+    fld6 = scenes.planted_field(svo6, knot, seed=0)
+    cam = ng.Camera(CAM["position"], CAM["look_at"], CAM["up"], CAM["fov_y_deg"], 1920, 1080)
+    steps = max(3, min(args.steps, 10))
+    for name, fld, config in (
+            ("configs[3] LOD6 1920x1080", fld6, ng.RenderConfig()),
+            ("configs[4] LOD4.5 + shadow rays 1920x1080", fld6, ng.RenderConfig(lod=4.5, shadows=True))):
+        tiles = TiledRenderer(fld, 1920, 1080)
+        img, visible, evals = tiles.render(cam, config)
+        cfg = resolve_config(fld, config, resolve_lod(cam, fld, config))
+        ms = _time_tiled(tiles, cam, cfg, steps, flush, world)
+        st = tiles.sess.read_stats()
+        out[name] = {"frames_per_sec": 1000.0 / ms, "ms_per_frame": ms, "visible": visible, "decoder_evals": evals,
+                     "shadowed_local": int(st.shadowed), "voxels_finest": svo6.voxel_count(6), "n_gpus": world}
+    return out
 
 
 def _ref(x):
@@ -363,6 +418,8 @@ def main():
     }
     if "query" in res:
         line["query"] = res["query"]
+    if "extra" in res:
+        line["configs_3_4"] = res["extra"]
     if not args.no_cpu and world == 1:
         line["cpu_baseline"] = cpu_baseline(res)
     print(json.dumps(line))
