@@ -130,6 +130,7 @@ template <class Mlp, class Emit>
 __device__ __forceinline__ EvalLane warp_eval(const ng_octree& tree, const EvalCtx& c, WarpScratch& ws,
                                               bool act, const double x[3], const Mlp& mlp, Emit&& emit) {
   const int lane = (int)lane_id();
+#ifdef NG_PROFILE
   const bool dbg = c.dbg && lane == 0;
   unsigned long long t_mark = dbg ? dbg_now() : 0;
   auto lap = [&](int slot) {
@@ -139,6 +140,9 @@ __device__ __forceinline__ EvalLane warp_eval(const ng_octree& tree, const EvalC
       t_mark = t;
     }
   };
+#else
+  auto lap = [](int) {};
+#endif
   EvalLane res;
   res.present = 0;
   res.inside = true;

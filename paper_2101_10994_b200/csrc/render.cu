@@ -226,10 +226,14 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_cons
   TcMlp tcm;
   if constexpr (TC) {
     tcm = tc_policy(D.t, D.tmem_base, A.dec_first, &phase);
+#ifdef NG_PROFILE
     if (A.prof) tcm.prof = A.prof + 8 * (blockIdx.x * GROUPS + g);
+#endif
   }
   EvalCtx c;
+#ifdef NG_PROFILE
   if (A.prof && w == 0) c.dbg = A.prof + 8 * 4096 - 8 * 1024 + 8 * (blockIdx.x % 1024);
+#endif
   c.Z = f.Z;
   c.dec = D.dec;
   c.dec_first = A.dec_first;
@@ -264,7 +268,9 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_cons
 
   unsigned long long t_top = 0, t_acq = 0, t_eval = 0;
   while (true) {
+#ifdef NG_PROFILE
     if (A.prof && (w & 3) == 0 && lane == 0) t_top = globaltimer_ns();
+#endif
     // ---- acquire rays and advance each to its next query point (render.py:200-238)
     while (true) {
       const bool want = (ray < 0) && !drained;
@@ -328,6 +334,7 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_cons
       if (lane == 0) gflag[w] = wf;
       tc::named_sync(1 + g, 128);
       const int active = gflag[4 * g] + gflag[4 * g + 1] + gflag[4 * g + 2] + gflag[4 * g + 3];
+#ifdef NG_PROFILE
       if (A.prof && (w & 3) == 0 && lane == 0) {  // debug profile: per-group steps and busy lanes
         unsigned long long* pr = A.prof + 8 * (blockIdx.x * GROUPS + g);
         const unsigned long long now = globaltimer_ns();
@@ -340,6 +347,7 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_cons
         pr[4] += now - t_top;  // acquire + advance + group barrier
         t_acq = now;
       }
+#endif
       if (!active) break;
     } else {
       if (!__any_sync(FULL, act)) break;
@@ -380,10 +388,12 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_cons
     if constexpr (TC) er = warp_eval(tree, c, ws, act, x, tcm, emit);
     else er = warp_eval(tree, c, ws, act, x, SimtMlp{c}, emit);
 
+#ifdef NG_PROFILE
     if (A.prof && (w & 3) == 0 && lane == 0) {
       t_eval = globaltimer_ns();
       A.prof[8 * (blockIdx.x * GROUPS + g) + 5] += t_eval - t_acq;  // gather + decoder
     }
+#endif
     // ---- stop rules (render.py:247-272)
     if (act) {
       double dval;

@@ -22,8 +22,10 @@ struct TcMlp {
 
   __device__ __forceinline__ float operator()(int l, const float xf[3], const float* zrow, bool /*any*/,
                                               bool& bad) const {
+#ifdef NG_PROFILE
     unsigned long long t_in = 0;
     if (prof && wg == 0 && lane_id() == 0) asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_in));
+#endif
     const int lane = (int)lane_id();
     const int row = 32 * wg + lane;
     float v[36];
@@ -59,12 +61,13 @@ struct TcMlp {
       for (int i = 0; i < 32; ++i) acc = fmaf(W2[32 * c + i], fmaxf(h[i], 0.f), acc);
     }
     tc::fence_before_sync();
+#ifdef NG_PROFILE
     if (prof && wg == 0 && lane_id() == 0) {
       unsigned long long t_out;
       asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_out));
       prof[7] += t_out - t_in;
-      prof[6] = t_in;  // caller turns this into the gather time
     }
+#endif
     return acc;
   }
 };
