@@ -177,6 +177,12 @@ struct MarchArgs {
   unsigned long long* work_counter;
   ng_counters* counters;
   unsigned long long* prof;      // optional: 4 counters per group (steps, busy lanes, t0, t1)
+  // fused normals (render.py:277-300): after a hit the lane evaluates its
+  // 6 central-difference probes in the same persistent loop, then shades
+  int fuse_normals;
+  double* normal;
+  uint8_t* normal_ok;
+  uint8_t* color;                // null: shading happens later (shadow pass)
 };
 
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
@@ -190,6 +196,27 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
 struct FieldValue {
   double lo = 0.0, hi = 0.0;
 };
+
+// query_field value (render.py:155-171) from one lane's evaluation.
+__device__ __forceinline__ double field_value(const ng_octree& tree, const EvalLane& er, double lo, double hi,
+                                              double alpha, const double x[3]) {
+  if (!er.inside) return empty_value(tree, x);
+  if (alpha != 0.0) return dadd(dmul(dsub(1.0, alpha), lo), dmul(alpha, hi));
+  return lo;
+}
+
+// shade (render.py:303-314) for one hit pixel with an fp64 normal.
+__device__ __forceinline__ void shade_pixel(const ng_render_cfg& cfg, double n0, double n1, double n2,
+                                            uint8_t* rgb_out) {
+  double lam = dadd(dadd(dmul(n0, cfg.light[0]), dmul(n1, cfg.light[1])), dmul(n2, cfg.light[2]));
+  lam = lam < 0.0 ? 0.0 : (lam > 1.0 ? 1.0 : lam);
+#pragma unroll
+  for (int ch = 0; ch < 3; ++ch) {
+    double rgb = dmul(cfg.albedo[ch], dadd(cfg.ambient, dmul(dsub(1.0, cfg.ambient), lam)));
+    rgb = rgb < 0.0 ? 0.0 : (rgb > 1.0 ? 1.0 : rgb);
+    rgb_out[ch] = (uint8_t)dadd(dmul(rgb, 255.0), 0.5);
+  }
+}
 
 // Decoder policy setup shared by the march and normals kernels: SIMT stages
 // fp32 decoders; TC carves TMEM / A tiles / bf16 B tiles (tc_mlp.cuh).
@@ -257,6 +284,11 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_cons
   double t = 0.0, prev = NaN;
   int it = 0, ev = 0;
   double o[3] = {0, 0, 0}, d[3] = {0, 0, 0};
+  int probe = -1;               // -1 marching; 0..5 next normal probe (+x,+y,+z,-x,-y,-z)
+  double hp[3] = {0, 0, 0};     // hit point o + t_hit d
+  double vp0 = 0, vp1 = 0, vp2 = 0;  // plus-probe values
+  double g0 = 0, g1 = 0, g2 = 0;     // gradient
+  const double eps = A.cfg.normal_eps;
 
   auto finish = [&](bool is_hit, double th) {
     A.hit[ray] = is_hit ? 1 : 0;
@@ -286,6 +318,7 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_cons
             drained = true;
           } else {
             ray = A.work ? A.work[k] : (int)k;
+            probe = -1;
             cur = A.seg_start[ray];
             end = A.seg_end[ray];
             t = 0.0;
@@ -299,7 +332,7 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_cons
           }
         }
       }
-      if (ray >= 0 && !ready) {
+      if (ray >= 0 && !ready && probe < 0) {
         bool dead = false;
         while (true) {
           if (cur >= end || t > A.cfg.far_plane) {
@@ -353,9 +386,18 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_cons
       if (!__any_sync(FULL, act)) break;
     }
 
-    // ---- query point: x = o + t d clamped into the current voxel (render.py:244-245)
+    // ---- query point: x = o + t d clamped into the current voxel (render.py:244-245),
+    // or a normal probe clip(p +- eps e_axis, -1, 1) (render.py:289-293)
     double x[3] = {0.0, 0.0, 0.0};
-    if (act) {
+    if (act && probe >= 0) {
+      const int axis = probe % 3;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        double v = hp[a];
+        if (a == axis) v = (probe < 3) ? dadd(v, eps) : dsub(v, eps);
+        x[a] = np_min(np_max(v, -1.0), 1.0);
+      }
+    } else if (act) {
       const uint64_t code = __ldg(codes + A.hits[cur].voxel);
       const int cc[3] = {(int)compact3(code), (int)compact3(code >> 1), (int)compact3(code >> 2)};
 #pragma unroll
@@ -387,6 +429,9 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_cons
     EvalLane er;
     if constexpr (TC) er = warp_eval(tree, c, ws, act, x, tcm, emit);
     else er = warp_eval(tree, c, ws, act, x, SimtMlp{c}, emit);
+    auto dval_of = [&](const EvalLane& e, const FieldValue& v, const double* px) {
+      return field_value(tree, e, v.lo, v.hi, A.blend_alpha, px);
+    };
 
 #ifdef NG_PROFILE
     if (A.prof && (w & 3) == 0 && lane == 0) {
@@ -395,18 +440,32 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_cons
     }
 #endif
     // ---- stop rules (render.py:247-272)
-    if (act) {
-      double dval;
-      if (!er.inside) {
-        dval = empty_value(tree, x);
-        lc.empty += 1;
-      } else if (A.blend_alpha != 0.0) {
-        dval = dadd(dmul(dsub(1.0, A.blend_alpha), fv.lo), dmul(A.blend_alpha, fv.hi));
-      } else {
-        dval = fv.lo;
+    if (act && !er.inside) lc.empty += 1;  // query_field's own empty-space fallback
+    if (act && probe >= 0) {
+      // normals (render.py:294-299): g = (v+ - v-) / (2 eps), normalised
+      const double two_eps = 2.0 * eps;
+      if (probe == 0) vp0 = dval_of(er, fv, x);
+      else if (probe == 1) vp1 = dval_of(er, fv, x);
+      else if (probe == 2) vp2 = dval_of(er, fv, x);
+      else if (probe == 3) g0 = dsub(vp0, dval_of(er, fv, x)) / two_eps;
+      else if (probe == 4) g1 = dsub(vp1, dval_of(er, fv, x)) / two_eps;
+      else g2 = dsub(vp2, dval_of(er, fv, x)) / two_eps;
+      if (++probe == 6) {
+        const double nrm = __dsqrt_rn(dadd(dadd(dmul(g0, g0), dmul(g1, g1)), dmul(g2, g2)));
+        const bool ok = isfinite(nrm) && nrm > 1e-12;
+        const double n0 = ok ? g0 / nrm : 0.0, n1 = ok ? g1 / nrm : 0.0, n2 = ok ? g2 / nrm : 0.0;
+        A.normal[3 * ray] = n0;
+        A.normal[3 * ray + 1] = n1;
+        A.normal[3 * ray + 2] = n2;
+        A.normal_ok[ray] = ok ? 1 : 0;
+        if (A.color) shade_pixel(A.cfg, n0, n1, n2, A.color + 3 * ray);
+        ray = -1;
       }
+    } else if (act) {
+      double dval = dval_of(er, fv, x);
       ev += A.passes;
       it += 1;
+      const int ray_keep = ray;
       const bool is_hit = dval < A.cfg.delta;
       const bool stalled = !is_hit && (dval >= prev) && (fabs(dsub(dval, prev)) < A.cfg.osc_tol);
       if (is_hit) {
@@ -414,7 +473,14 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_cons
           const unsigned long long slot = atomicAdd(A.d_hit_count, 1ull);
           A.hit_list[slot] = ray;
         }
-        finish(true, dadd(t, dval));
+        const double th = dadd(t, dval);
+        finish(true, th);
+        if (A.fuse_normals) {  // keep the lane: its 6 normal probes come next
+          ray = ray_keep;
+          probe = 0;
+#pragma unroll
+          for (int a = 0; a < 3; ++a) hp[a] = dadd(o[a], dmul(th, d[a]));  // render.py:396
+        }
       } else if (stalled || it >= A.cfg.max_iters) {
         finish(false, 0.0);
       } else {
@@ -891,6 +957,10 @@ static int trace_pass(const ng_octree& tree, const ng_render_cfg& cfg, const Lod
   A.seg_end = seg_end;
   A.work_counter = work_counter;
   A.prof = march_profile_buffer();
+  A.fuse_normals = 0;
+  A.normal = nullptr;
+  A.normal_ok = nullptr;
+  A.color = nullptr;
   return NG_OK;
 }
 
@@ -941,13 +1011,24 @@ static int render_common(const ng_octree& tree, const ng_field& f, const ng_rend
   A.hit_list = hit_list;
   A.d_hit_count = ctr + 1;
   A.counters = &st->counters;
+  // normals ride in the march (probes fill lanes the march leaves idle)
+  static int fuse_env = -1;  // NG_FUSE_NORMALS=0 keeps the separate normals kernel
+  if (fuse_env < 0) {
+    const char* e = getenv("NG_FUSE_NORMALS");
+    fuse_env = (e && e[0] == '0') ? 0 : 1;
+  }
+  const bool fuse = do_normals && fuse_env;
+  A.fuse_normals = fuse ? 1 : 0;
+  A.normal = fr.normal;
+  A.normal_ok = fr.normal_ok;
+  A.color = cfg.shadows ? nullptr : fr.color;
   if (ws.ev_march_begin && (r = cuda_status(cudaEventRecord((cudaEvent_t)ws.ev_march_begin, s), "event record")))
     return r;
   if ((r = launch_march(tree, f, A, s))) return r;
   if (ws.ev_trace_done && (r = cuda_status(cudaEventRecord((cudaEvent_t)ws.ev_trace_done, s), "event record")))
     return r;
-  // ---- normals + shading (render.py:399-414, 440)
-  if (do_normals) {
+  // ---- normals + shading (render.py:399-414, 440), when not fused above
+  if (do_normals && !fuse) {
     NormalArgs B;
     B.cfg = cfg;
     B.G = P.G;
@@ -1065,6 +1146,10 @@ int ng_sphere_trace(const ng_octree* tree, const ng_field* fld, const ng_render_
   A.work_counter = work;
   A.counters = d_counters;
   A.prof = nullptr;
+  A.fuse_normals = 0;
+  A.normal = nullptr;
+  A.normal_ok = nullptr;
+  A.color = nullptr;
   (void)d_hit_count;
   r = launch_march(*tree, *fld, A, s);
   cudaFreeAsync(work, s);
