@@ -332,6 +332,71 @@ int ng_march_profile(unsigned long long* host_out, int max_groups);
 int ng_hit_points(const ng_ray* rays, const uint8_t* hit, const double* t, int64_t n,
                   double* points, void* stream);
 
+/* ---- training (field.py:286-409, trainer.py:87-296) ------- */
+/* fp64 master parameters and Adam moments (trainer.py:62-84, 176-190), all
+ * device memory owned by the caller. Z rows are padded to 32 channels; each
+ * decoder block holds W1b[h][36] (x weights, feature weights, b1 in column
+ * 35), W2[h], b2, zero padding to dec_stride doubles. */
+typedef struct ng_train_params {
+  double* Z;
+  double* Zm;
+  double* Zv;
+  double* dec;
+  double* decm;
+  double* decv;
+  int32_t m;
+  int32_t h;
+  int32_t n_decoders;
+  int32_t dec_stride;
+  int64_t corner_count;
+} ng_train_params;
+
+/* One batch (loss_batch + backward + adam_step, trainer.py:106-144, 87-103). */
+typedef struct ng_train_step {
+  int32_t active_mask;      /* loss levels, bit L-1 (trainer.py:119-125) */
+  int32_t update_decoders;  /* 0 for the frozen_decoder schedule (trainer.py:197) */
+  int32_t mode;             /* 0: Adam step; 1: gradients only (accumulated); 2: forward cache */
+  int32_t pad;
+  double denom;             /* loss denominator (trainer.py:127) */
+  double lr;
+  double c1;                /* 1 - beta1^step (trainer.py:92) */
+  double c2;                /* 1 - beta2^step (trainer.py:93) */
+  int64_t batch_index;      /* reported through status on divergence */
+} ng_train_step;
+
+size_t ng_train_workspace_bytes(const ng_octree* tree, int64_t batch_capacity, int32_t h, int32_t n_decoders,
+                                int64_t corner_count, int32_t dec_stride);
+/* One batch. upstream != NULL selects backward(cache, upstream) semantics
+ * (field.py:360-394) for the single level in active_mask. Mode 0 adds the
+ * per-level residual sums to level_sums[L-1] and runs Adam unless *status
+ * != 0; a non-finite loss or gradient sets *status = 1 + batch_index and
+ * stops all later updates (TrainingDiverged). Mode 1 writes level_sums,
+ * accumulates grad_Z (corner_count x 32) and grad_dec (n_decoders x
+ * dec_stride) and sets dec_touched[L-1] = 1 for decoders that received a
+ * gradient. psi_out (optional, n x max_active_level x 32) receives the
+ * per-level interpolated features. */
+int ng_train_batch(const ng_octree* tree, const ng_train_params* P, const ng_train_step* st, const double* pts,
+                   const double* dist, const double* upstream, int64_t n, int64_t batch_capacity, void* ws,
+                   size_t ws_bytes, double* level_sums, double* grad_Z, double* grad_dec, int32_t* dec_touched,
+                   double* psi_out, int64_t* status, void* stream);
+/* All mini-batches of one epoch (trainer.py:223-241) on already-permuted
+ * device points; Adam steps step0+1, step0+2, ... */
+int ng_train_epoch(const ng_octree* tree, const ng_train_params* P, const double* pts, const double* dist,
+                   int64_t n, int64_t batch_size, int32_t active_mask, int32_t update_decoders, double lr,
+                   int64_t step0, void* ws, size_t ws_bytes, double* level_sums, int64_t* status,
+                   void* stream);
+/* ForwardCache (field.py:321-357) of forward(x, level) with batch capacity
+ * n: per-level corner ids (n, level, 8; -1 where absent) and trilinear
+ * weights, per-level features psi (n, level, 32), pre-activations (n, h)
+ * and decoder inputs [x, z, 1] (n, 36); rows that are not decoded are 0. */
+int ng_train_export(const ng_octree* tree, const ng_train_params* P, int32_t level, const double* pts, int64_t n,
+                    void* ws, size_t ws_bytes, int32_t* ids, double* weights, double* psi, double* pre, double* inp,
+                    void* stream);
+/* adam_step (trainer.py:87-103) on one fp64 array; *d_bad = 1 (and no
+ * update) when the gradient has a non-finite entry. */
+int ng_adam_step(double* param, double* m, double* v, const double* grad, int64_t n, double lr, double c1,
+                 double c2, int64_t* d_bad, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -45,7 +45,15 @@ from .field import (
     predict,
     sum_features,
     trilinear,
+    DecoderGrads,
+    FieldGradients,
+    LevelInterp,
+    backward,
+    scatter_add_rows,
 )
+from .sampling import SampleSet, build_epoch_set, surface_points
+from .trainer import AdamState, EpochStats, TrainConfig, active_levels_for, adam_step, loss_batch, train
+from .modelio import load_model, save_model, serialized_bytes
 from .traversal import RayBundle, RayVoxelPairList, exclusive_sum, ray_segments, ray_trace_octree
 from .render import (
     Camera,
@@ -73,5 +81,7 @@ __all__ = [
     "exclusive_sum", "forward", "forward_levels", "locate", "morton_decode", "morton_encode", "new_field",
     "normals", "predict", "query_field", "ray_aabb_batch", "ray_segments", "ray_trace_octree", "render",
     "select_lod", "shade", "sphere_trace", "storage_bytes", "sum_features", "trace_rays", "trilinear",
-    "voxel_bounds", "write_ppm",
+    "voxel_bounds", "write_ppm", "DecoderGrads", "FieldGradients", "LevelInterp", "backward", "scatter_add_rows",
+    "SampleSet", "build_epoch_set", "surface_points", "AdamState", "EpochStats", "TrainConfig",
+    "active_levels_for", "adam_step", "loss_batch", "train", "load_model", "save_model", "serialized_bytes",
 ]

@@ -107,6 +107,18 @@ class NgFrameStats(C.Structure):
                 ("shadow_pairs", C.c_int64 * (MAX_TLEVELS + 1)), ("shadowed", C.c_int64)]
 
 
+class NgTrainParams(C.Structure):
+    _fields_ = [("Z", P), ("Zm", P), ("Zv", P), ("dec", P), ("decm", P), ("decv", P), ("m", C.c_int32),
+                ("h", C.c_int32), ("n_decoders", C.c_int32), ("dec_stride", C.c_int32),
+                ("corner_count", C.c_int64)]
+
+
+class NgTrainStep(C.Structure):
+    _fields_ = [("active_mask", C.c_int32), ("update_decoders", C.c_int32), ("mode", C.c_int32),
+                ("pad", C.c_int32), ("denom", C.c_double), ("lr", C.c_double), ("c1", C.c_double),
+                ("c2", C.c_double), ("batch_index", C.c_int64)]
+
+
 RAY_BYTES = 80
 PAIR_BYTES = 8
 HIT_PAIR_BYTES = 24
@@ -156,6 +168,12 @@ _SIGS = {
     "ng_render_rays": (C.c_int, [P, P, P, P, C.c_int64, P, P, P, C.c_int32, P]),
     "ng_hit_points": (C.c_int, [P, P, P, C.c_int64, P, P]),
     "ng_march_profile": (C.c_int, [P, C.c_int]),
+    "ng_train_workspace_bytes": (C.c_size_t, [P, C.c_int64, C.c_int32, C.c_int32, C.c_int64, C.c_int32]),
+    "ng_train_batch": (C.c_int, [P, P, P, P, P, P, C.c_int64, C.c_int64, P, C.c_size_t, P, P, P, P, P, P, P]),
+    "ng_train_epoch": (C.c_int, [P, P, P, P, C.c_int64, C.c_int64, C.c_int32, C.c_int32, C.c_double,
+                                 C.c_int64, P, C.c_size_t, P, P, P]),
+    "ng_train_export": (C.c_int, [P, P, C.c_int32, P, C.c_int64, P, C.c_size_t, P, P, P, P, P, P]),
+    "ng_adam_step": (C.c_int, [P, P, P, P, C.c_int64, C.c_double, C.c_double, C.c_double, P, P]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -296,26 +296,127 @@ def blend(svo, Z, decoders, x, L_tilde: float, counter: EvalCounter | None = Non
 
 
 @dataclass
-class ForwardCache:
-    """What a forward pass hands its caller (field.py:321-334). The backward
-    pass is outside this package's scope, so only the inputs
-    and outputs are kept."""
+class LevelInterp:
+    """Interpolation record for one feature level of a point batch (field.py:93-101)."""
 
-    svo: SparseVoxelOctree
-    Z: np.ndarray
-    decoder: Decoder
-    L: int
-    pts: np.ndarray
-    out: np.ndarray
+    level: int
+    mask: np.ndarray      # (n,)
+    ids: np.ndarray       # (k, 8) corner ids of the masked rows
+    weights: np.ndarray   # (k, 8) trilinear weights
+    psi: np.ndarray       # (n, m), zero where absent
+
+
+class ForwardCache:
+    """What backward needs from a forward pass (field.py:321-334).
+
+    `out` is computed eagerly. The per-level records, decoded rows, decoder
+    inputs and pre-activations (`recs`, `rows`, `inp`, `pre`) are exported
+    from the device forward pass (ng_train_export) on first access; the
+    backward pass itself recomputes them on the device."""
+
+    def __init__(self, svo, Z, decoders, L, pts, out):
+        self.svo = svo
+        self.Z = Z
+        self.decoders = decoders
+        self.decoder = decoders[L - 1]
+        self.L = L
+        self.pts = pts
+        self.out = out
+        self._export = None
+
+    def _exported(self):
+        if self._export is None:
+            from .trainer import DeviceTrainState
+            st = DeviceTrainState(self.svo, self.Z, self.decoders, moments=False)
+            self._export = st.export(self.pts, self.L)
+        return self._export
+
+    @property
+    def recs(self) -> list:
+        return self._exported()["recs"]
+
+    @property
+    def rows(self) -> np.ndarray:
+        return self._exported()["rows"]
+
+    @property
+    def inp(self) -> np.ndarray:
+        return self._exported()["inp"]
+
+    @property
+    def pre(self) -> np.ndarray:
+        return self._exported()["pre"]
 
 
 def forward(svo, Z, decoders, x, L: int, _dfield=None) -> tuple:
-    """predict plus a cache (field.py:337-357)."""
+    """predict plus a cache for the matching backward call (field.py:337-357)."""
     pts = np.atleast_2d(np.asarray(x, dtype=np.float64))
     _check_level(L, len(decoders))
     df = _dfield if _dfield is not None else DeviceField(Z, decoders)
     out = _run_query(svo, df, _dev_points(pts), out_levels=1 << (L - 1))[:, 0].cpu().numpy()
-    return out, ForwardCache(svo, Z, decoders[L - 1], L, pts, out)
+    return out, ForwardCache(svo, Z, decoders, L, pts, out)
+
+
+@dataclass
+class DecoderGrads:
+    """field.py:286-291."""
+
+    W1: np.ndarray
+    b1: np.ndarray
+    W2: np.ndarray
+    b2: np.ndarray
+
+
+@dataclass
+class FieldGradients:
+    """Accumulated partials for Z and each decoder; decoder slots stay None
+    until a backward pass touches that level (field.py:294-318)."""
+
+    dZ: np.ndarray
+    decoders: list
+
+    @classmethod
+    def zeros(cls, Z, n_decoders: int) -> "FieldGradients":
+        return cls(np.zeros(np.shape(Z)), [None] * n_decoders)
+
+    def decoder_slot(self, L: int, decoder: Decoder) -> DecoderGrads:
+        g = self.decoders[L - 1]
+        if g is None:
+            g = DecoderGrads(np.zeros(decoder.W1.shape), np.zeros(decoder.b1.shape), np.zeros(decoder.W2.shape),
+                             np.zeros(decoder.b2.shape))
+            self.decoders[L - 1] = g
+        return g
+
+
+def backward(cache: ForwardCache, upstream, grads: FieldGradients | None = None) -> FieldGradients:
+    """Reverse-mode partials of sum(upstream * out) w.r.t. the level-L decoder
+    and every contributing corner feature, accumulated into grads
+    (field.py:360-394). Runs on the device in fp64 (csrc/train.cu)."""
+    if not isinstance(cache, ForwardCache):
+        raise OctfieldError("backward needs the cache returned by forward")
+    if grads is None:
+        grads = FieldGradients.zeros(cache.Z, cache.svo.max_level)
+    up = np.atleast_1d(np.asarray(upstream, dtype=np.float64))
+    if up.shape != (len(cache.pts),):
+        raise StructuralError("upstream shape does not match the forward batch")
+    if len(up) == 0:
+        return grads
+    from .trainer import DeviceTrainState
+    st = DeviceTrainState(cache.svo, cache.Z, cache.decoders, moments=False)
+    st.gradients(cache.pts, None, 1 << (cache.L - 1), 1.0, grads, upstream=up)
+    return grads
+
+
+def scatter_add_rows(dst: np.ndarray, idx: np.ndarray, rows: np.ndarray) -> None:
+    """dst[idx] += rows with duplicates accumulated (field.py:397-409).
+    Host utility kept for API parity; the training step does this
+    reduction on the device (k_train_rows)."""
+    if len(idx) == 0:
+        return
+    order = np.argsort(idx, kind="stable")
+    idx_s = idx[order]
+    starts = np.concatenate([[0], np.flatnonzero(np.diff(idx_s)) + 1])
+    dst[idx_s[starts]] += np.add.reduceat(rows[order], starts, axis=0)
 
 
 def forward_levels_device(svo, dfield: DeviceField, pts: torch.Tensor, levels, counter=None) -> torch.Tensor:

@@ -369,6 +369,85 @@ def build_octree(oracle, max_level: int, surface_samples: np.ndarray, r0: int = 
                              corner_offsets=offsets, region=Aabb(lo, hi), virtual_levels=virtual, device=dev_tree)
 
 
+def octree_from_levels(r0: int, max_level: int, codes: list, parents: list, corners: list, corner_count: int,
+                       corner_offsets) -> SparseVoxelOctree:
+    """Device octree from stored levels (the model file's topology,
+    modelio.py:102-165): occupancy bitmaps from the given codes, the virtual
+    grids by parent closure of level 0, ranks and child tables on the device;
+    corner tables are taken as stored. The region AABB is recomputed from the
+    finest level (modelio.py:95-98)."""
+    if len(codes) != max_level + 1:
+        raise StructuralError("one code array per stored level is required")
+    dev = _dev()
+    st = stream_ptr()
+    nv = int(math.log2(r0))
+    T = nv + max_level + 1
+    resl = [_level_res(r0, t - nv) for t in range(T)]
+    bitmaps = [None] * T
+    for lv in range(max_level + 1):
+        c = np.asarray(codes[lv], dtype=np.uint64)
+        words = np.zeros(_words(resl[nv + lv]), dtype=np.uint64)
+        np.bitwise_or.at(words, (c >> np.uint64(6)).astype(np.int64), np.uint64(1) << (c & np.uint64(63)))
+        bitmaps[nv + lv] = torch.from_numpy(words.view(np.int64)).to(dev)
+    for t in range(nv - 1, -1, -1):
+        bitmaps[t] = torch.zeros(_words(resl[t]), dtype=torch.int64, device=dev)
+        call("ng_bitmap_parent", ptr(bitmaps[t + 1]), bitmaps[t + 1].numel(), ptr(bitmaps[t]), bitmaps[t].numel(),
+             st)
+    totals = torch.zeros(T, dtype=torch.int64, device=dev)
+    scratch = torch.empty(_scratch_words(max(b.numel() for b in bitmaps)), dtype=torch.int64, device=dev)
+    ranks = []
+    for t in range(T):
+        rk = torch.empty(bitmaps[t].numel(), dtype=torch.int32, device=dev)
+        call("ng_bitmap_rank", ptr(bitmaps[t]), bitmaps[t].numel(), ptr(rk), ptr(totals[t:t + 1]), ptr(scratch),
+             scratch.numel() * 8, st)
+        ranks.append(rk)
+    counts = totals.cpu().numpy()
+    d_codes = []
+    for t in range(T):
+        if t >= nv:
+            c = torch.from_numpy(np.ascontiguousarray(np.asarray(codes[t - nv], dtype=np.uint64).view(np.int64)))
+            d_codes.append(c.to(dev))
+        else:
+            c = torch.empty(int(counts[t]), dtype=torch.int64, device=dev)
+            call("ng_bitmap_extract", ptr(bitmaps[t]), ptr(ranks[t]), bitmaps[t].numel(), ptr(c), st)
+            d_codes.append(c)
+    child_start, child_mask, d_parents, d_corners = [], [], [], []
+    for t in range(T):
+        n = d_codes[t].numel()
+        lv = t - nv
+        if t + 1 < T:
+            cs = torch.empty(n, dtype=torch.int32, device=dev)
+            cm = torch.empty(n, dtype=torch.uint8, device=dev)
+            call("ng_level_children", ptr(d_codes[t]), n, ptr(bitmaps[t + 1]), ptr(ranks[t + 1]), ptr(cs), ptr(cm),
+                 st)
+        else:
+            cs = cm = None
+        child_start.append(cs)
+        child_mask.append(cm)
+        if lv >= 1:
+            d_parents.append(torch.from_numpy(np.ascontiguousarray(parents[lv], dtype=np.int32)).to(dev))
+            d_corners.append(torch.from_numpy(np.ascontiguousarray(corners[lv], dtype=np.int32).reshape(-1, 8)).to(dev))
+        elif lv == 0:
+            d_parents.append(torch.full((n,), -1, dtype=torch.int32, device=dev))
+            d_corners.append(None)
+        else:
+            d_parents.append(None)
+            d_corners.append(None)
+    res = r0 << max_level
+    ijk = morton_decode(np.asarray(codes[max_level], dtype=np.uint64))
+    org = cell_origin(ijk, res)
+    lo = org.min(axis=0)
+    hi = (org + _SPAN / res).max(axis=0)
+    half_diag = 0.5 * np.sqrt(3.0) * (_SPAN / res)
+    dev_tree = DeviceOctree(r0, max_level, d_codes, bitmaps, ranks, child_start, child_mask, d_corners, lo, hi,
+                            half_diag)
+    levels = [OctreeLevel(d_codes[nv + lv], d_parents[nv + lv], d_corners[nv + lv]) for lv in range(max_level + 1)]
+    virtual = [OctreeLevel(d_codes[t], None, None) for t in range(nv)]
+    return SparseVoxelOctree(r0=r0, max_level=max_level, levels=levels, corner_count=int(corner_count),
+                             corner_offsets=np.asarray(corner_offsets, dtype=np.int64), region=Aabb(lo, hi),
+                             virtual_levels=virtual, device=dev_tree)
+
+
 def _scratch_words(n_words: int) -> int:
     tiles = (n_words + 2047) // 2048
     return 4 + tiles + 16

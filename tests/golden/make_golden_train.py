@@ -126,6 +126,20 @@ def main():
         g.update(dec_arrays(f"run_{tag}_", out.decoders))
         g[f"run_{tag}_hist"] = np.stack([h.level_losses for h in hist])
 
+    # ---- model file bytes (modelio.py:47-69) and a max_lod=1 load (modelio.py:140-151)
+    import tempfile
+    from octfield import modelio as M
+    with tempfile.TemporaryDirectory() as tmp:
+        path = os.path.join(tmp, "tiny.nsdf")
+        M.save_model(path, fld)
+        with open(path, "rb") as fh:
+            g["model_bytes"] = np.frombuffer(fh.read(), dtype=np.uint8).copy()
+        cut = M.load_model(path, max_lod=1)
+        g["cut_corner_count"] = np.int64(cut.svo.corner_count)
+        g["cut_region_lo"], g["cut_region_hi"] = cut.svo.region.lo, cut.svo.region.hi
+        g["cut_Z"] = cut.Z
+        g["serialized_bytes"] = np.int64(M.serialized_bytes(fld))
+
     np.savez_compressed(os.path.join(HERE, "train.npz"), **g)
     print("wrote train.npz:", len(g), "arrays")
 

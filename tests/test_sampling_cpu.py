@@ -1,0 +1,25 @@
+"""The trainer's host data loader (paper_2101_10994_b200.sampling) against
+the reference's epoch sample sets (tests/golden/train.npz). CPU only."""
+
+import numpy as np
+
+from paper_2101_10994_b200 import sampling as S
+from paper_2101_10994_b200 import scenes
+
+
+def test_epoch_set_golden(golden):
+    g = golden("train")
+    ss = S.build_epoch_set(scenes.Sphere(0.5), 600, 10)
+    np.testing.assert_array_equal(ss.points, g["ep_points"])
+    np.testing.assert_array_equal(ss.distances, g["ep_dist"])
+    np.testing.assert_array_equal(ss.scheme_tags, g["ep_tags"])
+
+
+def test_split_counts_and_dump_roundtrip(tmp_path):
+    assert S.split_counts(10) == (4, 4, 2)
+    assert S.split_counts(7) == (4, 2, 1)
+    ss = S.SampleSet(np.array([[0.1, 0.2, 0.3]]), np.array([0.5]), np.zeros(1, np.int8))
+    S.dump_samples(tmp_path / "s.bin", ss)
+    back = S.load_samples(tmp_path / "s.bin")
+    np.testing.assert_allclose(back.points, ss.points.astype(np.float32))
+    assert back.scheme_tags[0] == S.SCHEME_UNIFORM
