@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--no-query", action="store_true", help="skip the batched-query leg")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-extra", action="store_true", help="skip the configs[3]/[4] 1080p legs")
+    ap.add_argument("--no-train", action="store_true", help="skip the training-step leg (SURVEY.md 8f)")
     return ap.parse_args()
 
 
@@ -308,8 +309,63 @@ def run_ours(args, rank: int, world: int):
                         "value": share * world / q_ms / 1e3, "unit": "Mpoints/s", "ms": q_ms}
         res["_query_pts"] = pts_h
         del out
+    # ---- training step: one epoch of loss + backward + Adam,
+    # batch 512, fp64 masters, random-init LOD5 field (rank 0 / N = 1 only: the
+    # reference trains in one process)
+    if not args.no_train and world == 1:
+        res["train"] = train_leg(knot, svo, dev, flush)
     res["_svo"], res["_fld"] = svo, fld
     return res
+
+
+TRAIN_POINTS = 500_000   # TrainConfig.points_per_epoch default (trainer.py:39)
+TRAIN_BATCH = 512        # TrainConfig.batch_size default (trainer.py:40)
+
+
+def train_leg(knot, svo, dev, flush):
+    import torch
+    import paper_2101_10994_b200 as ng
+    from paper_2101_10994_b200.trainer import DeviceTrainer
+    fld = ng.new_field(svo, seed=0)
+    pts_h = query_points(knot, TRAIN_POINTS, seed=1)
+    pts = torch.from_numpy(pts_h).to(dev)
+    dist = knot.device_eval(pts)
+    dist_h = dist.cpu().numpy()
+    work = ng.NeuralField(svo, fld.Z.astype(np.float64), [d.astype(np.float64) for d in fld.decoders])
+    tr = DeviceTrainer(work, TRAIN_BATCH)
+    act = list(range(1, MAX_LEVEL + 1))
+    tr.run_epoch(pts, dist, act, True, 1e-3)  # warm-up epoch (977 Adam steps)
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(3)]
+    for a, b in ev:
+        flush.zero_()
+        a.record()
+        tr.run_epoch(pts, dist, act, True, 1e-3)
+        b.record()
+    torch.cuda.synchronize()
+    ms = min(a.elapsed_time(b) for a, b in ev)
+    assert tr.diverged_at() < 0
+    # end to end: host points in (pinned), per-level epoch losses out
+    pin_p = torch.from_numpy(pts_h).pin_memory()
+    pin_d = torch.from_numpy(dist_h).pin_memory()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(2):
+        dp = pin_p.to(dev, non_blocking=True)
+        dd = pin_d.to(dev, non_blocking=True)
+        tr.run_epoch(dp, dd, act, True, 1e-3)
+        losses = tr.level_sums.cpu().numpy() / TRAIN_POINTS
+    e2e_s = (time.perf_counter() - t0) / 2
+    n_batches = (TRAIN_POINTS + TRAIN_BATCH - 1) // TRAIN_BATCH
+    return {"metric": "Mpoints/sec training step (loss + backward + Adam, fp64 masters)",
+            "value": TRAIN_POINTS / ms / 1e3, "unit": "Mpoints/s", "ms_per_epoch": ms,
+            "us_per_batch": ms * 1e3 / n_batches, "points_per_epoch": TRAIN_POINTS, "batch_size": TRAIN_BATCH,
+            "adam_steps_per_epoch": n_batches, "dtype": "fp64",
+            "workload": "LOD5 torus-knot octree, new_field(seed=0) m=32 h=128, 2:2:1 knot mix, joint schedule",
+            "launches_per_batch": 7, "level_losses": [float(x) for x in losses],
+            "e2e": {"value": TRAIN_POINTS / e2e_s / 1e6, "unit": "Mpoints/s",
+                    "h2d_bytes_per_step": int(pts_h.nbytes + dist_h.nbytes), "d2h_bytes_per_step": 8 * MAX_LEVEL},
+            "_pts": pts_h, "_dist": dist_h, "_fld": work}
 
 
 def _time_tiled(tiles, cam, cfg, steps, flush, world):
@@ -420,6 +476,8 @@ def main():
         line["query"] = res["query"]
     if "extra" in res:
         line["configs_3_4"] = res["extra"]
+    if "train" in res:
+        line["train"] = {k: v for k, v in res["train"].items() if not k.startswith("_")}
     if not args.no_cpu and world == 1:
         line["cpu_baseline"] = cpu_baseline(res)
     print(json.dumps(line))
@@ -466,7 +524,38 @@ def cpu_baseline(res):
         qs = cpu_query_sample(tree, res["_fld"], pts)
         out["query"] = {"value": len(pts) / qs / 1e6, "unit": "Mpoints/s",
                         "sample": f"{len(pts)} points, forward L=1..5, {qs:.1f} s"}
+    if "train" in res:
+        secs, npts = cpu_train_sample(tree, res["train"])
+        out["train"] = {"value": npts / secs / 1e6, "unit": "Mpoints/s", "cores": 1,
+                        "sample": f"{npts // TRAIN_BATCH} Adam steps of batch {TRAIN_BATCH} "
+                                  f"(oracle loss_batch + backward + dense Adam, fp64), {secs:.1f} s"}
     return out
+
+
+def cpu_train_sample(tree, tr, batches: int = 6):
+    """Oracle training steps (trainer.py:223-241 restated) on the same field
+    and points; bounded to a few batches."""
+    from oracle import train_oracle as TO
+    fld = tr["_fld"]
+    Z = np.array(fld.Z, dtype=np.float64)
+    decs = [TO.f64_decoder(d) for d in fld.decoders]
+    params = {"Z": Z}
+    for i, d in enumerate(decs):
+        for nm in ("W1", "b1", "W2", "b2"):
+            params[f"decoder{i + 1}.{nm}"] = getattr(d, nm)
+    st = TO.Adam.for_params(params)
+    act = list(range(1, MAX_LEVEL + 1))
+    t0 = time.perf_counter()
+    for b in range(batches):
+        sl = slice(b * TRAIN_BATCH, (b + 1) * TRAIN_BATCH)
+        loss, g, _ = TO._batch_pass(tree, Z, decs, tr["_pts"][sl], tr["_dist"][sl], act)
+        gd = {"Z": g.dZ}
+        for i, slot in enumerate(g.dec):
+            if slot is not None:
+                for nm, arr in zip(("W1", "b1", "W2", "b2"), slot):
+                    gd[f"decoder{i + 1}.{nm}"] = arr
+        TO.adam_step(params, gd, st, 1e-3)
+    return time.perf_counter() - t0, batches * TRAIN_BATCH
 
 
 # ------------------------------------------------------------------ reference arm

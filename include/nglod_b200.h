@@ -341,6 +341,7 @@ typedef struct ng_train_params {
   double* Z;
   double* Zm;
   double* Zv;
+  int32_t* Zlast;           /* per row: last Adam step applied (lazy zero-gradient steps) */
   double* dec;
   double* decm;
   double* decv;
@@ -359,11 +360,12 @@ typedef struct ng_train_step {
   int32_t pad;
   double denom;             /* loss denominator (trainer.py:127) */
   double lr;
-  double c1;                /* 1 - beta1^step (trainer.py:92) */
-  double c2;                /* 1 - beta2^step (trainer.py:93) */
+  int64_t step;             /* Adam step of this batch, 1-based (trainer.py:91) */
+  const double* adam_c;     /* device: (1 - beta1^t, 1 - beta2^t) of step t at [2(t-1)] (trainer.py:92-93) */
   int64_t batch_index;      /* reported through status on divergence */
 } ng_train_step;
 
+/* The workspace must be zero-filled once before its first use. */
 size_t ng_train_workspace_bytes(const ng_octree* tree, int64_t batch_capacity, int32_t h, int32_t n_decoders,
                                 int64_t corner_count, int32_t dec_stride);
 /* One batch. upstream != NULL selects backward(cache, upstream) semantics
@@ -380,11 +382,15 @@ int ng_train_batch(const ng_octree* tree, const ng_train_params* P, const ng_tra
                    size_t ws_bytes, double* level_sums, double* grad_Z, double* grad_dec, int32_t* dec_touched,
                    double* psi_out, int64_t* status, void* stream);
 /* All mini-batches of one epoch (trainer.py:223-241) on already-permuted
- * device points; Adam steps step0+1, step0+2, ... */
+ * device points; Adam steps step0+1, step0+2, ... (adam_c must cover them).
+ * Rows are flushed to the current step every flush_every batches and at the
+ * end, so P is fully up to date when the stream reaches the end. */
 int ng_train_epoch(const ng_octree* tree, const ng_train_params* P, const double* pts, const double* dist,
                    int64_t n, int64_t batch_size, int32_t active_mask, int32_t update_decoders, double lr,
-                   int64_t step0, void* ws, size_t ws_bytes, double* level_sums, int64_t* status,
-                   void* stream);
+                   int64_t step0, const double* adam_c, int32_t flush_every, void* ws, size_t ws_bytes,
+                   double* level_sums, int64_t* status, void* stream);
+/* Apply the zero-gradient Adam steps every row has missed, up to `step`. */
+int ng_train_flush(const ng_train_params* P, int64_t step, const double* adam_c, double lr, void* stream);
 /* ForwardCache (field.py:321-357) of forward(x, level) with batch capacity
  * n: per-level corner ids (n, level, 8; -1 where absent) and trilinear
  * weights, per-level features psi (n, level, 32), pre-activations (n, h)

@@ -108,15 +108,15 @@ class NgFrameStats(C.Structure):
 
 
 class NgTrainParams(C.Structure):
-    _fields_ = [("Z", P), ("Zm", P), ("Zv", P), ("dec", P), ("decm", P), ("decv", P), ("m", C.c_int32),
+    _fields_ = [("Z", P), ("Zm", P), ("Zv", P), ("Zlast", P), ("dec", P), ("decm", P), ("decv", P), ("m", C.c_int32),
                 ("h", C.c_int32), ("n_decoders", C.c_int32), ("dec_stride", C.c_int32),
                 ("corner_count", C.c_int64)]
 
 
 class NgTrainStep(C.Structure):
     _fields_ = [("active_mask", C.c_int32), ("update_decoders", C.c_int32), ("mode", C.c_int32),
-                ("pad", C.c_int32), ("denom", C.c_double), ("lr", C.c_double), ("c1", C.c_double),
-                ("c2", C.c_double), ("batch_index", C.c_int64)]
+                ("pad", C.c_int32), ("denom", C.c_double), ("lr", C.c_double), ("step", C.c_int64),
+                ("adam_c", P), ("batch_index", C.c_int64)]
 
 
 RAY_BYTES = 80
@@ -171,7 +171,8 @@ _SIGS = {
     "ng_train_workspace_bytes": (C.c_size_t, [P, C.c_int64, C.c_int32, C.c_int32, C.c_int64, C.c_int32]),
     "ng_train_batch": (C.c_int, [P, P, P, P, P, P, C.c_int64, C.c_int64, P, C.c_size_t, P, P, P, P, P, P, P]),
     "ng_train_epoch": (C.c_int, [P, P, P, P, C.c_int64, C.c_int64, C.c_int32, C.c_int32, C.c_double,
-                                 C.c_int64, P, C.c_size_t, P, P, P]),
+                                 C.c_int64, P, C.c_int32, P, C.c_size_t, P, P, P]),
+    "ng_train_flush": (C.c_int, [P, C.c_int64, P, C.c_double, P]),
     "ng_train_export": (C.c_int, [P, P, C.c_int32, P, C.c_int64, P, C.c_size_t, P, P, P, P, P, P]),
     "ng_adam_step": (C.c_int, [P, P, P, P, C.c_int64, C.c_double, C.c_double, C.c_double, P, P]),
 }

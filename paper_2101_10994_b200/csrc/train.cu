@@ -4,45 +4,67 @@
 // Reference: octfield/field.py:286-409 (forward cache, backward,
 // scatter_add_rows) and octfield/trainer.py:87-144, 165-296 (adam_step,
 // loss_batch, train, _batch_pass). The reference keeps float64 master
-// weights and computes in float64; so does this path (B200 has full-rate
-// fp64 relative to the work here, which is tiny per batch and bound by the
-// dense Adam sweep over Z).
+// weights and computes in float64; so does this path.
 //
-// One batch step, all on one stream, deterministic (no fp atomics):
-//   memset      corner counts / fill cursors / decoder-touched flags
-//   k_train_points   warp per point: locate + corner ids + trilinear weights at
-//                    levels 1..Lmax (fp64), running feature sums, then per active
-//                    level L the 35->h->1 decoder forward, residual, dout,
-//                    dpre (relu mask) and dz = dpre W1[:,3:]; the per-level
-//                    feature gradient G_l = sum_{L>=l} dz_L; integer counts of
-//                    (corner, record) contributions
-//   exclusive scan   counts -> segment offsets (scan.cu)
-//   k_train_fill     records -> corner segments (slot order is arbitrary)
-//   k_train_dec_grads  dW1|db1 = dpre^T [x z 1], dW2 = dout^T relu(pre), db2,
-//                      per-level residual sums; fixed-order reductions
-//   k_train_rows     warp per corner row: sort the segment's record keys,
-//                    sum w * G in key order (= dZ row, field.py:388-394),
-//                    Adam update of the row (dense: every row decays m, v)
-//   k_train_dec_adam Adam on the decoders that received a gradient
+// One mini-batch, six launches on one stream, deterministic (no
+// floating-point atomics; integer atomics only build index lists whose
+// order never reaches the arithmetic):
+//   k_train_locate   warp per point, lane = level: voxel lookup, 8 corner ids
+//                    and trilinear weights per level (field.py:104-135);
+//                    integer corner counts; first touch appends the corner
+//                    row to the touched-row list
+//   k_train_rowprep  warp per touched row: segment allocation; lazy Adam
+//                    catch-up of the row to step s-1 (see below)
+//   k_train_gather   warp per point, lane = channel: running feature sums z_l
+//                    of levels 1..Lmax (field.py:119, 154-169)
+//   k_train_dec      CTA per (active level L, 32-point group): decoder
+//                    forward [x z_L 1] W1b^T, relu, W2 (field.py:346-
+//                    357), residual + dout (trainer.py:139-143), dpre, dz =
+//                    dpre W1[:,3:] (field.py:381-387) and the group's partial
+//                    decoder gradients dW1b = dpre^T [x z 1], dW2, db2
+//                    (field.py:377-385), all as small smem-tiled GEMMs;
+//                    one extra row of blocks places the (corner, record) list
+//   k_train_dec_reduce  fixed-order sum of the group partials, per-level
+//                    residual sums (trainer.py:140), divergence flags; extra
+//                    blocks form G_l = sum over active L >= l of dz_L per point
+//   k_train_update   warp per touched row: record keys sorted, dZ row = sum
+//                    of w * G_l in key order (field.py:388-394,
+//                    scatter_add_rows 397-409), Adam step s; extra blocks run
+//                    Adam on the decoders that received a gradient
+//
+// Lazy Adam. adam_step (trainer.py:87-103) decays the moments of EVERY
+// parameter each step (the gradient dict always carries the dense dZ). A
+// row with a zero gradient follows m = m*b1, v = v*b2, p -= lr*(m/c1)/
+// (sqrt(v/c2)+eps): a fixed sequence of roundings that depends only on the
+// row's own state and the step. Each row records the last step applied
+// (Zlast) and replays the missed zero-gradient steps with the same
+// operations before it is read or updated, so the result is bit-identical
+// to a dense sweep while a batch touches only the rows it reads;
+// ng_train_flush brings every row to the current step (every `flush_every`
+// batches and at the end of an epoch). Rows whose moments are still zero
+// are exact no-ops and are skipped.
 #include "common.cuh"
 
 namespace ng {
 
-constexpr int TR_WARPS = 4;    // points per CTA in k_train_points
 constexpr int TR_LM = 12;      // max feature levels handled by the trainer
 constexpr int TR_HMAX = 128;   // max decoder width
+constexpr int TR_GP = 32;      // points per k_train_dec group
+constexpr int TR_NT = 256;     // k_train_dec threads
 constexpr int W1S = 37;        // smem row stride (doubles) of the staged W1b block
 constexpr double BETA1 = 0.9, BETA2 = 0.999, ADAM_EPS = 1e-8;  // trainer.py:29-31
 
 static inline int tr_grid(int64_t n, int nt) { return (int)((n + nt - 1) / nt); }
 
 struct TrainLayout {
-  size_t rec_w, rec_id, G, inp, pre, dpre, dout, sq, cnt, off, fill, list, sorted, scan, gdec, touched, total;
+  size_t rec_w, rec_id, pres, z, G, dz, sq, gpart, gdec, cnt, fill, seg, touched, list, sorted, ctr, total;
+  int64_t max_rows;
 };
 
-// Workspace carve-up for a batch capacity B, max level LM, A active-level
-// slots (= n_decoders), decoder width h, C corners and dec_stride doubles.
-static TrainLayout train_layout(int64_t B, int LM, int A, int h, int64_t C, int dec_stride) {
+// Workspace carve-up for a batch capacity B, LM levels, A level slots
+// (= n_decoders), C corner rows. cnt must start zeroed (the caller
+// zero-fills the workspace once); every batch leaves it zero.
+static TrainLayout train_layout(int64_t B, int LM, int A, int64_t C, int dec_stride) {
   TrainLayout L;
   size_t o = 0;
   auto take = [&](size_t bytes) {
@@ -50,22 +72,25 @@ static TrainLayout train_layout(int64_t B, int LM, int A, int h, int64_t C, int 
     o += (bytes + 255) & ~(size_t)255;
     return at;
   };
-  L.rec_w = take(sizeof(double) * B * LM * 8);
-  L.rec_id = take(sizeof(int32_t) * B * LM * 8);
+  const int64_t groups = (B + TR_GP - 1) / TR_GP;
+  const int64_t n_rec = B * LM * 8;
+  L.max_rows = n_rec < C ? n_rec : C;
+  L.rec_w = take(sizeof(double) * n_rec);
+  L.rec_id = take(sizeof(int32_t) * n_rec);
+  L.pres = take(sizeof(uint32_t) * B);
+  L.z = take(sizeof(double) * B * LM * 32);
   L.G = take(sizeof(double) * B * LM * 32);
-  L.inp = take(sizeof(double) * A * B * 36);
-  L.pre = take(sizeof(double) * A * B * h);
-  L.dpre = take(sizeof(double) * A * B * h);
-  L.dout = take(sizeof(double) * A * B);
+  L.dz = take(sizeof(double) * B * A * 32);
   L.sq = take(sizeof(double) * A * B);
-  L.cnt = take(sizeof(int64_t) * C);
-  L.fill = take(sizeof(int32_t) * C);
-  L.touched = take(sizeof(int32_t) * 32);
-  L.off = take(sizeof(int64_t) * C);
-  L.list = take(sizeof(int32_t) * B * LM * 8);
-  L.sorted = take(sizeof(int32_t) * B * LM * 8);
-  L.scan = take(ng_scan_scratch_bytes(C > 0 ? C : 1));
+  L.gpart = take(sizeof(double) * A * groups * dec_stride);
   L.gdec = take(sizeof(double) * A * dec_stride);
+  L.cnt = take(sizeof(int32_t) * C);
+  L.fill = take(sizeof(int32_t) * C);
+  L.seg = take(sizeof(int32_t) * C);
+  L.touched = take(sizeof(int32_t) * L.max_rows);
+  L.list = take(sizeof(int32_t) * n_rec);
+  L.sorted = take(sizeof(int32_t) * n_rec);
+  L.ctr = take(sizeof(int64_t) * 4 + sizeof(int32_t) * 32);  // n_touched, cursor, pad, pad | dtouch[32]
   L.total = o;
   return L;
 }
@@ -75,6 +100,7 @@ struct TrainArgs {
   double* Z;
   double* Zm;
   double* Zv;
+  int32_t* Zlast;
   double* dec;
   double* decm;
   double* decv;
@@ -87,323 +113,58 @@ struct TrainArgs {
   int64_t n;
   int LM;                  // levels interpolated: highest active level
   int active_mask;
+  int n_act;
   int update_decoders;
-  int mode;                // 0 Adam, 1 gradients only
+  int mode;                // 0 Adam, 1 gradients only, 2 forward cache export
   double two_over_n;       // 2.0 / denom (trainer.py:143)
-  double lr, c1, c2;
+  double lr;
+  int64_t step;            // Adam step s of this batch (1-based)
+  const double* adam_c;    // (c1, c2) of step t at [2(t-1)], [2(t-1)+1]
   int64_t batch_index;
+  int64_t groups;
+  int64_t max_rows;
   // workspace
   double* rec_w;
   int32_t* rec_id;
-  double* G;
-  double* inp;
-  double* pre;
-  double* dpre;
-  double* dout;
+  uint32_t* pres;
+  double* z;               // (n, LM, 32) running feature sums
+  double* G;               // (n, LM, 32) feature-gradient per level
+  double* dz;
   double* sq;
-  int64_t* cnt;
-  int64_t* off;
+  double* gpart;
+  double* gdec;
+  int32_t* cnt;
   int32_t* fill;
+  int32_t* seg;
+  int32_t* touched;
   int32_t* list;
   int32_t* sorted;
-  double* gdec;
-  int32_t* touched;
+  unsigned long long* ctr;  // [0] touched rows, [1] segment cursor
+  int32_t* dtouch;          // per level: a decoded point this batch
   // outputs
-  double* level_sums;      // (n_dec): += residual sums (mode 0: epoch accumulators)
+  double* level_sums;      // mode 0: += per-level residual sums; mode 1: =
   double* grad_Z;          // mode 1: (C, 32) +=
   double* grad_dec;        // mode 1: n_dec * dec_stride +=
   int32_t* dec_touched;    // mode 1: 1 where a decoder received a gradient
-  double* psi_out;         // optional (n, LM, 32): per-level interpolated features
+  double* psi_out;         // mode 2: (n, LM, 32)
+  double* pre_out;         // mode 2: (n, h)
+  double* inp_out;         // mode 2: (n, 36)
   int64_t* status;         // [0] = 1 + batch index of the first divergence
 };
 
 __device__ __forceinline__ int level_slot(int mask, int L) { return __popc(mask & ((1 << (L - 1)) - 1)); }
 
-__device__ __forceinline__ void flag_divergence(int64_t* status, int64_t batch) {
-  atomicCAS((unsigned long long*)status, 0ull, (unsigned long long)(batch + 1));
-}
-
-struct TrainWarp {
-  int ids[TR_LM][8];
-  double w[TR_LM][8];
-  double z[TR_LM][32];   // running feature sum through level l
-  double dz[TR_LM][32];  // dz of active slot a
-  double dpre[TR_HMAX];
-  double inp[36];
-};
-
-// Per point (one warp): interpolation, decoder forward/backward at every
-// active level, feature-gradient records (field.py:337-394, trainer.py:132-143).
-__global__ void __launch_bounds__(TR_WARPS * 32) k_train_points(const __grid_constant__ ng_octree tree,
-                                                                const __grid_constant__ TrainArgs A) {
-  extern __shared__ __align__(16) double tr_smem[];
-  double* sW1 = tr_smem;              // h x W1S: x weights, feature weights, (col 35) b1
-  double* sW2 = sW1 + TR_HMAX * W1S;  // h weights, then b2
-  TrainWarp* tws = reinterpret_cast<TrainWarp*>(sW2 + TR_HMAX + 4);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  TrainWarp& tw = tws[warp];
-  const int64_t p = (int64_t)blockIdx.x * TR_WARPS + warp;
-  const bool valid = p < A.n;
-  const int LM = A.LM, h = A.h, m = A.m;
-
-  double x[3] = {0.0, 0.0, 0.0};
-  if (valid) {
-    x[0] = __ldg(A.pts + 3 * p);
-    x[1] = __ldg(A.pts + 3 * p + 1);
-    x[2] = __ldg(A.pts + 3 * p + 2);
-  }
-  // ---- locate + corner ids + weights, lane l-1 handles level l (field.py:104-119)
-  bool pres = false;
-  if (valid && lane < LM) {
-    const int l = lane + 1;
-    const int res = tree.r0 << l;
-    const int tl = l + tree.n_virtual;
-    const int c0 = bin_axis(x[0], res), c1 = bin_axis(x[1], res), c2 = bin_axis(x[2], res);
-    const int64_t idx = rank_lookup(tree.bitmap[tl], tree.rank[tl], morton(c0, c1, c2));
-    pres = idx >= 0;
-    if (pres) {
-      const int4* cr = reinterpret_cast<const int4*>(tree.corners[tl] + 8 * idx);
-      const int4 a = __ldg(cr), b = __ldg(cr + 1);
-      tw.ids[lane][0] = a.x; tw.ids[lane][1] = a.y; tw.ids[lane][2] = a.z; tw.ids[lane][3] = a.w;
-      tw.ids[lane][4] = b.x; tw.ids[lane][5] = b.y; tw.ids[lane][6] = b.z; tw.ids[lane][7] = b.w;
-      // u = clip((x - DOMAIN_MIN) * (res / span) - cell, 0, 1); w_j = cx * cy * cz (field.py:115-135)
-      const double half = 0.5 * (double)res;
-      const int cc[3] = {c0, c1, c2};
-      double u[3];
-#pragma unroll
-      for (int a3 = 0; a3 < 3; ++a3) {
-        double f = dsub(dmul(dadd(x[a3], 1.0), half), (double)cc[a3]);
-        u[a3] = f < 0.0 ? 0.0 : (f > 1.0 ? 1.0 : f);
-      }
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const double wx = (j & 1) ? u[0] : dsub(1.0, u[0]);
-        const double wy = ((j >> 1) & 1) ? u[1] : dsub(1.0, u[1]);
-        const double wz = ((j >> 2) & 1) ? u[2] : dsub(1.0, u[2]);
-        tw.w[lane][j] = dmul(dmul(wx, wy), wz);
-      }
-    }
-  }
-  const unsigned present = __ballot_sync(FULL, pres);
-  __syncwarp();
-
-  // ---- running feature sums, lane = channel (field.py:119, 154-169)
-  {
-    double zrun = 0.0;
-    for (int l = 1; l <= LM; ++l) {
-      double psi = 0.0;
-      if ((present >> (l - 1)) & 1) {
-        const double* Zc = A.Z + lane;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) psi = dadd(psi, dmul(tw.w[l - 1][j], __ldg(Zc + 32 * (int64_t)tw.ids[l - 1][j])));
-      }
-      zrun = dadd(zrun, psi);
-      tw.z[l - 1][lane] = zrun;
-      if (A.psi_out && valid) A.psi_out[(p * LM + (l - 1)) * 32 + lane] = psi;
-    }
-  }
-  double dval = 0.0, upv = 0.0;
-  if (valid) {
-    if (A.upstream) upv = __ldg(A.upstream + p);
-    else if (A.dist) dval = __ldg(A.dist + p);
-  }
-
-  // ---- active levels, ascending (trainer.py:132-143)
-  for (int L = 1; L <= LM; ++L) {
-    if (!((A.active_mask >> (L - 1)) & 1)) continue;
-    const int a = level_slot(A.active_mask, L);
-    __syncthreads();
-    {
-      const double* blk = A.dec + (int64_t)(L - 1) * A.dec_stride;
-      for (int i = threadIdx.x; i < h * 36; i += blockDim.x) sW1[(i / 36) * W1S + (i % 36)] = blk[i];
-      for (int i = threadIdx.x; i <= h; i += blockDim.x) sW2[i] = blk[h * 36 + i];
-    }
-    __syncthreads();
-    const bool dec = valid && (present & ((1u << L) - 1u)) != 0u;
-    const int64_t row = (int64_t)a * A.n + p;
-    if (dec) {
-      if (lane < 3) tw.inp[lane] = x[lane];
-      tw.inp[3 + lane] = (lane < m) ? tw.z[L - 1][lane] : 0.0;
-      if (lane == 0) tw.inp[35] = 1.0;
-      __syncwarp();
-      double prev[TR_HMAX / 32];
-      double part = 0.0;
-#pragma unroll
-      for (int q = 0; q < TR_HMAX / 32; ++q) {
-        const int j = lane + 32 * q;
-        prev[q] = 0.0;
-        if (j < h) {
-          const double* wr = sW1 + j * W1S;
-          double s = 0.0;
-          for (int k = 0; k < 3 + m; ++k) s = fma(tw.inp[k], wr[k], s);
-          const double pr = dadd(s, wr[35]);  // inp @ W1.T + b1 (field.py:350)
-          prev[q] = pr;
-          part = fma(pr > 0.0 ? pr : 0.0, sW2[j], part);
-        }
-      }
-#pragma unroll
-      for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(FULL, part, o);
-      const double out = dadd(part, sW2[h]);
-      // resid = where(mask_L, out - d, 0); upstream = (2/n) resid (trainer.py:139-143)
-      const bool inL = (present >> (L - 1)) & 1;
-      const double resid = inL ? dsub(out, dval) : 0.0;
-      const double dout = A.upstream ? upv : dmul(A.two_over_n, resid);
-      // dhidden = dout * W2; dpre = where(pre > 0, dhidden, 0) (field.py:381-383)
-#pragma unroll
-      for (int q = 0; q < TR_HMAX / 32; ++q) {
-        const int j = lane + 32 * q;
-        if (j < h) {
-          const double dp = prev[q] > 0.0 ? dmul(dout, sW2[j]) : 0.0;
-          tw.dpre[j] = dp;
-          A.dpre[row * h + j] = dp;
-          A.pre[row * h + j] = prev[q];
-        }
-      }
-      A.inp[row * 36 + lane] = tw.inp[lane];
-      if (lane < 4) A.inp[row * 36 + 32 + lane] = tw.inp[32 + lane];
-      if (lane == 0) {
-        A.dout[row] = dout;
-        A.sq[row] = dmul(resid, resid);
-        A.touched[L - 1] = 1;
-      }
-      __syncwarp();
-      // dz = (dpre @ W1)[:, 3:] (field.py:386-387), lane = channel
-      double s = 0.0;
-      if (lane < m)
-        for (int j = 0; j < h; ++j) s = fma(tw.dpre[j], sW1[j * W1S + 3 + lane], s);
-      tw.dz[a][lane] = s;
-    } else if (valid) {
-      for (int j = lane; j < h; j += 32) {
-        A.dpre[row * h + j] = 0.0;
-        A.pre[row * h + j] = 0.0;
-      }
-      A.inp[row * 36 + lane] = 0.0;
-      if (lane < 4) A.inp[row * 36 + 32 + lane] = 0.0;
-      if (lane == 0) {
-        A.dout[row] = 0.0;
-        A.sq[row] = 0.0;
-      }
-      tw.dz[a][lane] = 0.0;
-    }
-  }
-  if (!valid) return;
-  __syncwarp();
-  // ---- per-level feature gradient G_l = sum over active L >= l of dz_L (field.py:388-394)
-  for (int l = 1; l <= LM; ++l) {
-    if (!((present >> (l - 1)) & 1)) continue;
-    double g = 0.0;
-    for (int L = l; L <= LM; ++L)
-      if ((A.active_mask >> (L - 1)) & 1) g = dadd(g, tw.dz[level_slot(A.active_mask, L)][lane]);
-    A.G[(p * LM + (l - 1)) * 32 + lane] = g;
-  }
-  // ---- contribution records: key = (p * LM + l - 1) * 8 + j
-  for (int s = lane; s < 8 * LM; s += 32) {
-    const int l = s / 8 + 1, j = s % 8;
-    const int64_t key = (p * LM + (l - 1)) * 8 + j;
-    if ((present >> (l - 1)) & 1) {
-      const int id = tw.ids[l - 1][j];
-      A.rec_id[key] = id;
-      A.rec_w[key] = tw.w[l - 1][j];
-      atomicAdd((unsigned long long*)(A.cnt + id), 1ull);
-    } else {
-      A.rec_id[key] = -1;
-    }
-  }
-}
-
-// Records into their corner's segment.
-__global__ void k_train_fill(const __grid_constant__ TrainArgs A, int64_t n_rec) {
-  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= n_rec) return;
-  const int id = A.rec_id[r];
-  if (id < 0) return;
-  const int64_t slot = A.off[id] + atomicAdd(A.fill + id, 1);
-  A.list[slot] = (int32_t)r;
-}
-
-// Decoder gradients (field.py:377-385) and per-level residual sums
-// (trainer.py:140): grid (active slot, 32-wide j block), 8 warps per CTA,
-// warp w reduces points w, w+8, ... in order; warps are combined in order.
-constexpr int DG_WARPS = 8;
-__global__ void __launch_bounds__(DG_WARPS * 32) k_train_dec_grads(const __grid_constant__ TrainArgs A) {
-  extern __shared__ __align__(16) double dg_smem[];  // [DG_WARPS][38][32]
-  const int a = blockIdx.x, jb = blockIdx.y;
-  int L = 0;
+__device__ __forceinline__ int slot_level(int mask, int a) {
   for (int l = 1, k = 0; l <= 31; ++l)
-    if ((A.active_mask >> (l - 1)) & 1) {
-      if (k == a) { L = l; break; }
+    if ((mask >> (l - 1)) & 1) {
+      if (k == a) return l;
       ++k;
     }
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int h = A.h;
-  const int j = jb * 32 + lane;
-  double acc[36];
-#pragma unroll
-  for (int k = 0; k < 36; ++k) acc[k] = 0.0;
-  double aw2 = 0.0, ab2 = 0.0;
-  if (j < h) {
-    for (int64_t p = warp; p < A.n; p += DG_WARPS) {
-      const int64_t row = (int64_t)a * A.n + p;
-      const double d = A.dpre[row * h + j];
-      const double dout = A.dout[row];
-      const double pr = A.pre[row * h + j];
-      aw2 = fma(dout, pr > 0.0 ? pr : 0.0, aw2);
-      ab2 = dadd(ab2, dout);
-      if (d != 0.0) {
-        const double2* ir = reinterpret_cast<const double2*>(A.inp + row * 36);
-#pragma unroll
-        for (int k = 0; k < 18; ++k) {
-          const double2 v = __ldg(ir + k);
-          acc[2 * k] = fma(d, v.x, acc[2 * k]);
-          acc[2 * k + 1] = fma(d, v.y, acc[2 * k + 1]);
-        }
-      }
-    }
-  }
-  double* mine = dg_smem + (size_t)warp * 38 * 32;
-#pragma unroll
-  for (int k = 0; k < 36; ++k) mine[k * 32 + lane] = acc[k];
-  mine[36 * 32 + lane] = aw2;
-  mine[37 * 32 + lane] = ab2;
-  __syncthreads();
-  const bool adam = A.mode == 0;
-  double* gblk = adam ? A.gdec + (int64_t)a * A.dec_stride : A.grad_dec + (int64_t)(L - 1) * A.dec_stride;
-  bool bad = false;       // non-finite decoder gradient (adam_step raises, trainer.py:96-97)
-  bool bad_loss = false;  // non-finite batch loss (trainer.py:233-236)
-  for (int t = threadIdx.x; t < 38 * 32; t += blockDim.x) {
-    const int k = t / 32, jj = jb * 32 + (t % 32);
-    if (jj >= h) continue;
-    if (k == 37 && (jb != 0 || jj != 0)) continue;  // b2 once
-    double s = 0.0;
-    for (int w = 0; w < DG_WARPS; ++w) s = dadd(s, dg_smem[(size_t)w * 38 * 32 + t]);
-    int64_t dst;
-    if (k < 36) {
-      if (k >= 3 + A.m && k != 35) continue;  // padding columns stay zero
-      dst = (int64_t)jj * 36 + k;
-    } else if (k == 36) {
-      dst = (int64_t)h * 36 + jj;
-    } else {
-      dst = (int64_t)h * 36 + h;
-    }
-    if (!isfinite(s)) bad = true;
-    if (adam) gblk[dst] = s;
-    else gblk[dst] += s;
-  }
-  // residual sum of this level: warp 0 of the first j block (fixed order)
-  if (jb == 0 && warp == 0) {
-    double s = 0.0;
-    for (int64_t p = lane; p < A.n; p += 32) s = dadd(s, A.sq[(int64_t)a * A.n + p]);
-#pragma unroll
-    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
-    if (lane == 0) {
-      if (!isfinite(s)) bad_loss = true;
-      if (adam) A.level_sums[L - 1] = dadd(A.level_sums[L - 1], s);
-      else A.level_sums[L - 1] = s;
-      if (!adam && A.dec_touched && A.touched[L - 1]) A.dec_touched[L - 1] = 1;
-    }
-  }
-  if (adam && (bad_loss || (bad && A.update_decoders && A.touched[L - 1])))
-    flag_divergence(A.status, A.batch_index);
+  return 0;
+}
+
+__device__ __forceinline__ void flag_divergence(int64_t* status, int64_t batch) {
+  atomicCAS((unsigned long long*)status, 0ull, (unsigned long long)(batch + 1));
 }
 
 // Adam moment update and parameter step for one element (trainer.py:95-103),
@@ -416,76 +177,488 @@ __device__ __forceinline__ void adam_elem(double& prm, double& mm, double& vv, d
   prm = dsub(prm, upd);
 }
 
-// One warp per corner row: dZ row = sum over the segment's records in key
-// order, then Adam (mode 0) or accumulate into grad_Z (mode 1).
-__global__ void __launch_bounds__(256) k_train_rows(const __grid_constant__ TrainArgs A) {
+// Zero-gradient Adam steps (last, upto] for one element: the dense sweep's
+// exact operation sequence; zero moments stay zero and leave p unchanged.
+__device__ __forceinline__ void adam_replay(double& prm, double& mm, double& vv, int64_t last, int64_t upto,
+                                            double lr, const double* __restrict__ c) {
+  if (mm == 0.0 && vv == 0.0) return;
+  for (int64_t t = last + 1; t <= upto; ++t) adam_elem(prm, mm, vv, 0.0, lr, c[2 * (t - 1)], c[2 * (t - 1) + 1]);
+}
+
+// ---------------------------------------------------------------- locate
+__global__ void __launch_bounds__(256) k_train_locate(const __grid_constant__ ng_octree tree,
+                                                      const __grid_constant__ TrainArgs A) {
   const int lane = threadIdx.x & 31;
-  const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (c >= A.C) return;
-  const int64_t S = A.cnt[c];
-  const int64_t base = A.off[c];
-  double g = 0.0;
-  auto add_rec = [&](int key) {
-    const int64_t gp = key >> 3;  // (p * LM + l - 1)
-    g = dadd(g, dmul(A.rec_w[key], A.G[gp * 32 + lane]));
-  };
-  if (S > 0 && S <= 32) {
-    const int key = lane < S ? A.list[base + lane] : 0x7fffffff;
-    int rank = 0;
-    for (int i = 0; i < (int)S; ++i) rank += __shfl_sync(FULL, key, i) < key;
-    for (int r = 0; r < (int)S; ++r) {
-      const unsigned who = __ballot_sync(FULL, lane < S && rank == r);
-      add_rec(__shfl_sync(FULL, key, __ffs(who) - 1));
+  const int64_t p = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (p >= A.n) return;
+  const int LM = A.LM;
+  bool pres = false;
+  if (lane < LM) {
+    const double x0 = __ldg(A.pts + 3 * p), x1 = __ldg(A.pts + 3 * p + 1), x2 = __ldg(A.pts + 3 * p + 2);
+    const int l = lane + 1;
+    const int res = tree.r0 << l;
+    const int tl = l + tree.n_virtual;
+    const int c0 = bin_axis(x0, res), c1 = bin_axis(x1, res), c2 = bin_axis(x2, res);
+    const int64_t idx = rank_lookup(tree.bitmap[tl], tree.rank[tl], morton(c0, c1, c2));
+    const int64_t key0 = (p * LM + lane) * 8;
+    pres = idx >= 0;
+    if (pres) {
+      const int4* cr = reinterpret_cast<const int4*>(tree.corners[tl] + 8 * idx);
+      const int4 a = __ldg(cr), b = __ldg(cr + 1);
+      const int ids[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+      // u = clip((x - DOMAIN_MIN) * (res / span) - cell, 0, 1); w_j = cx * cy * cz (field.py:115-135)
+      const double half = 0.5 * (double)res;
+      const double xs[3] = {x0, x1, x2};
+      const int cc[3] = {c0, c1, c2};
+      double u[3];
+#pragma unroll
+      for (int a3 = 0; a3 < 3; ++a3) {
+        const double f = dsub(dmul(dadd(xs[a3], 1.0), half), (double)cc[a3]);
+        u[a3] = f < 0.0 ? 0.0 : (f > 1.0 ? 1.0 : f);
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const double wx = (j & 1) ? u[0] : dsub(1.0, u[0]);
+        const double wy = ((j >> 1) & 1) ? u[1] : dsub(1.0, u[1]);
+        const double wz = ((j >> 2) & 1) ? u[2] : dsub(1.0, u[2]);
+        A.rec_w[key0 + j] = dmul(dmul(wx, wy), wz);
+        A.rec_id[key0 + j] = ids[j];
+        if (A.mode != 2 && atomicAdd(A.cnt + ids[j], 1) == 0) {
+          const unsigned long long at = atomicAdd(A.ctr, 1ull);
+          A.touched[at] = ids[j];
+        }
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) A.rec_id[key0 + j] = -1;
     }
-  } else if (S > 32) {
-    for (int64_t i0 = 0; i0 < S; i0 += 32) {
-      const bool own = i0 + lane < S;
-      const int key = own ? A.list[base + i0 + lane] : 0x7fffffff;
-      int64_t rank = 0;
-      for (int64_t i = 0; i < S; ++i) rank += A.list[base + i] < key;
-      if (own) A.sorted[base + rank] = key;
-    }
-    __syncwarp();
-    __threadfence_block();
-    for (int64_t r = 0; r < S; ++r) add_rec(A.sorted[base + r]);
   }
-  const int64_t e = c * 32 + lane;
-  if (A.mode == 0) {
-    if (*(volatile int64_t*)A.status) return;
-    if (!isfinite(g)) {
-      flag_divergence(A.status, A.batch_index);
-      return;
+  const unsigned bits = __ballot_sync(FULL, pres);
+  if (lane == 0) A.pres[p] = bits;
+}
+
+// ---------------------------------------------------------------- row prep
+__global__ void __launch_bounds__(256) k_train_rowprep(const __grid_constant__ TrainArgs A) {
+  const int lane = threadIdx.x & 31;
+  const int64_t n_rows = (int64_t)A.ctr[0];
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n_rows;
+       i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int id = A.touched[i];
+    if (lane == 0) {
+      A.seg[id] = (int32_t)atomicAdd(A.ctr + 1, (unsigned long long)A.cnt[id]);
+      A.fill[id] = 0;
     }
-    double prm = A.Z[e], mm = A.Zm[e], vv = A.Zv[e];
-    adam_elem(prm, mm, vv, g, A.lr, A.c1, A.c2);
-    A.Z[e] = prm;
-    A.Zm[e] = mm;
-    A.Zv[e] = vv;
-  } else if (S > 0) {
-    A.grad_Z[e] = dadd(A.grad_Z[e], g);
+    if (A.mode == 0) {
+      const int64_t e = (int64_t)id * 32 + lane;
+      const int64_t last = A.Zlast[id];
+      if (last < A.step - 1) {
+        double prm = A.Z[e], mm = A.Zm[e], vv = A.Zv[e];
+        if (!(mm == 0.0 && vv == 0.0)) {
+          adam_replay(prm, mm, vv, last, A.step - 1, A.lr, A.adam_c);
+          A.Z[e] = prm;
+          A.Zm[e] = mm;
+          A.Zv[e] = vv;
+        }
+        __syncwarp();
+        if (lane == 0) A.Zlast[id] = (int32_t)(A.step - 1);
+      }
+    }
   }
 }
 
-// Adam on every decoder that received a gradient this batch (trainer.py:100,
-// 290-296: untouched decoders keep their moments).
-__global__ void k_train_dec_adam(const __grid_constant__ TrainArgs A) {
-  const int a = blockIdx.y;
-  int L = 0;
-  for (int l = 1, k = 0; l <= 31; ++l)
-    if ((A.active_mask >> (l - 1)) & 1) {
-      if (k == a) { L = l; break; }
-      ++k;
+// ---------------------------------------------------------------- gather
+// z_l = sum_{l' <= l} sum_j w_j Z[id_j] for l = 1..LM; a level's 8 corner
+// rows are loaded together (lane = channel, 256 B per row).
+__global__ void __launch_bounds__(256) k_train_gather(const __grid_constant__ TrainArgs A) {
+  const int lane = threadIdx.x & 31;
+  const int64_t p = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (p >= A.n) return;
+  const int LM = A.LM;
+  const uint32_t pr = A.pres[p];
+  const int64_t key0 = p * LM * 8;
+  // lane i < 8 LM holds record i's (id, weight)
+  int idv[3];
+  double wv[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    const int i = c * 32 + lane;
+    const bool own = i < 8 * LM && ((pr >> (i >> 3)) & 1);
+    idv[c] = own ? A.rec_id[key0 + i] : 0;
+    wv[c] = own ? A.rec_w[key0 + i] : 0.0;
+  }
+  const double* Zc = A.Z + lane;
+  double z = 0.0;
+  for (int l = 1; l <= LM; ++l) {
+    double psi = 0.0;
+    if ((pr >> (l - 1)) & 1) {
+      double v[8], w[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int i = (l - 1) * 8 + j;
+        const int c = i >> 5;
+        const int src = i & 31;
+        const int id = __shfl_sync(FULL, c == 0 ? idv[0] : (c == 1 ? idv[1] : idv[2]), src);
+        w[j] = __shfl_sync(FULL, c == 0 ? wv[0] : (c == 1 ? wv[1] : wv[2]), src);
+        v[j] = Zc[32 * (int64_t)id];
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) psi = dadd(psi, dmul(w[j], v[j]));
     }
-  if (!A.touched[L - 1] || *(volatile int64_t*)A.status) return;
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    z = dadd(z, psi);
+    A.z[(p * LM + (l - 1)) * 32 + lane] = z;
+    if (A.psi_out) A.psi_out[(p * LM + (l - 1)) * 32 + lane] = psi;
+  }
+}
+
+// ---------------------------------------------------------------- decoder tiles
+static size_t dec_smem_bytes() {
+  return sizeof(double) * (TR_HMAX * W1S + TR_HMAX + 1 + TR_GP * 36 + 2 * TR_GP * TR_HMAX + TR_GP) +
+         sizeof(int) * TR_GP + 64;
+}
+
+__global__ void __launch_bounds__(TR_NT) k_train_dec(const __grid_constant__ TrainArgs A) {
+  extern __shared__ __align__(16) double dsm[];
+  const int h = A.h, m = A.m;
+  // one extra row of blocks (blockIdx.y == n_act): place records into their corner segments
+  if ((int)blockIdx.y == A.n_act) {
+    const int64_t n_rec = A.n * A.LM * 8;
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n_rec; r += (int64_t)gridDim.x * blockDim.x) {
+      const int id = A.rec_id[r];
+      if (id < 0) continue;
+      const int slot = A.seg[id] + atomicAdd(A.fill + id, 1);
+      A.list[slot] = (int32_t)r;
+    }
+    return;
+  }
+  double* sW1 = dsm;                          // [h][W1S]
+  double* sW2 = sW1 + TR_HMAX * W1S;          // [h + 1], b2 last
+  double* sInp = sW2 + TR_HMAX + 1;           // [TR_GP][36]: x, z_L (padded to 32), 1
+  double* sPre = sInp + TR_GP * 36;           // [TR_GP][TR_HMAX]
+  double* sDpre = sPre + TR_GP * TR_HMAX;     // [TR_GP][TR_HMAX]
+  double* sDout = sDpre + TR_GP * TR_HMAX;    // [TR_GP]
+  int* sDec = reinterpret_cast<int*>(sDout + TR_GP);
+  const int a = blockIdx.y;
+  const int L = slot_level(A.active_mask, a);
+  const int64_t g = blockIdx.x;
+  const int64_t p0 = g * TR_GP;
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+
+  // ---- stage decoder L (W1b rows, W2, b2): 16-byte loads, all in flight
+  {
+    const double2* blk2 = reinterpret_cast<const double2*>(A.dec + (int64_t)(L - 1) * A.dec_stride);
+    const int n2 = h * 18;
+#pragma unroll 9
+    for (int i = t; i < n2; i += TR_NT) {
+      const double2 v = __ldg(blk2 + i);
+      const int e = 2 * i;
+      sW1[(e / 36) * W1S + (e % 36)] = v.x;
+      sW1[((e + 1) / 36) * W1S + ((e + 1) % 36)] = v.y;
+    }
+    const double* blk = A.dec + (int64_t)(L - 1) * A.dec_stride;
+    for (int i = t; i <= h; i += TR_NT) sW2[i] = __ldg(blk + h * 36 + i);
+  }
+  // ---- decoder inputs [x, z_L, 1] (field.py:347): warp w owns points w, w+8, ...; lane = channel
+  for (int q = warp; q < TR_GP; q += TR_NT / 32) {
+    const int64_t p = p0 + q;
+    const bool valid = p < A.n;
+    const uint32_t pr = valid ? A.pres[p] : 0u;
+    const bool dec = valid && (pr & ((1u << L) - 1u)) != 0u;
+    const double z = dec ? A.z[(p * A.LM + (L - 1)) * 32 + lane] : 0.0;
+    double* ir = sInp + q * 36;
+    if (lane < 3) ir[lane] = valid ? __ldg(A.pts + 3 * p + lane) : 0.0;
+    ir[3 + lane] = (dec && lane < m) ? z : 0.0;
+    if (lane == 0) {
+      ir[35] = 1.0;
+      sDec[q] = dec ? 1 : 0;
+    }
+  }
+  __syncthreads();
+
+  // ---- forward: pre[p][j] = [x z] . W1b[j][0:3+m] + b1[j]; thread = (j, 16 points)
+  const int j = t & (TR_HMAX - 1);
+  const int half = t >> 7;
+  if (j < h) {
+    double w[36];
+#pragma unroll
+    for (int k = 0; k < 36; ++k) w[k] = sW1[j * W1S + k];
+    for (int q0 = half * 16; q0 < half * 16 + 16; q0 += 4) {
+      double s[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int k = 0; k < 35; ++k)
+        if (k < 3 + m) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) s[u] = fma(sInp[(q0 + u) * 36 + k], w[k], s[u]);
+        }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)  // inp @ W1.T + b1 (field.py:350)
+        sPre[(q0 + u) * TR_HMAX + j] = sDec[q0 + u] ? dadd(s[u], w[35]) : 0.0;
+    }
+  }
+  __syncthreads();
+
+  // ---- output, residual, dout (warp: 4 points)
+  for (int q = warp * 4; q < warp * 4 + 4; ++q) {
+    double part = 0.0;
+    for (int jj = lane; jj < h; jj += 32) {
+      const double pr = sPre[q * TR_HMAX + jj];
+      part = fma(pr > 0.0 ? pr : 0.0, sW2[jj], part);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(FULL, part, o);
+    if (lane == 0) {
+      const int64_t p = p0 + q;
+      double dout = 0.0, sq = 0.0;
+      if (sDec[q]) {
+        const double out = dadd(part, sW2[h]);
+        const bool inL = (A.pres[p] >> (L - 1)) & 1;
+        if (A.upstream) {
+          dout = __ldg(A.upstream + p);
+        } else if (A.dist) {
+          // resid = where(mask_L, out - d, 0); upstream = (2/n) resid (trainer.py:139-143)
+          const double resid = inL ? dsub(out, __ldg(A.dist + p)) : 0.0;
+          dout = dmul(A.two_over_n, resid);
+          sq = dmul(resid, resid);
+        }
+      }
+      sDout[q] = dout;
+      if (p < A.n) A.sq[(int64_t)a * A.n + p] = sq;
+    }
+  }
+  __syncthreads();
+
+  // ---- dpre = where(pre > 0, dout * W2, 0) (field.py:381-383)
+  if (j < h) {
+    const double w2 = sW2[j];
+    for (int q = half * 16; q < half * 16 + 16; ++q) {
+      const double pr = sPre[q * TR_HMAX + j];
+      sDpre[q * TR_HMAX + j] = (sDec[q] && pr > 0.0) ? dmul(sDout[q], w2) : 0.0;
+    }
+  }
+  __syncthreads();
+
+  if (A.mode == 2) {  // ForwardCache export
+    for (int q = warp; q < TR_GP; q += TR_NT / 32) {
+      const int64_t p = p0 + q;
+      if (p >= A.n) break;
+      for (int jj = lane; jj < h; jj += 32) A.pre_out[p * h + jj] = sPre[q * TR_HMAX + jj];
+      A.inp_out[p * 36 + lane] = sInp[q * 36 + lane];
+      if (lane < 4) A.inp_out[p * 36 + 32 + lane] = sInp[q * 36 + 32 + lane];
+    }
+    return;
+  }
+
+  // ---- dz = (dpre @ W1)[:, 3:] (field.py:386-387): thread = (channel, 4 points)
+  {
+    const int q0 = warp * 4;
+    double s[4] = {0.0, 0.0, 0.0, 0.0};
+    if (lane < m)
+      for (int jj = 0; jj < h; ++jj) {
+        const double wv = sW1[jj * W1S + 3 + lane];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) s[u] = fma(sDpre[(q0 + u) * TR_HMAX + jj], wv, s[u]);
+      }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t p = p0 + q0 + u;
+      if (p < A.n) A.dz[(p * A.n_dec + a) * 32 + lane] = sDec[q0 + u] ? s[u] : 0.0;
+    }
+  }
+  // ---- this group's partial decoder gradients (field.py:377-385): thread = (j, 18 columns)
+  if (j < h) {
+    double acc[18];
+#pragma unroll
+    for (int k = 0; k < 18; ++k) acc[k] = 0.0;
+    double aw2 = 0.0;
+    const int k0 = half * 18;
+    for (int q = 0; q < TR_GP; ++q) {
+      const double d = sDpre[q * TR_HMAX + j];
+      const double* ir = sInp + q * 36 + k0;
+#pragma unroll
+      for (int k = 0; k < 18; ++k) acc[k] = fma(d, ir[k], acc[k]);
+      if (half == 0) {
+        const double pr = sPre[q * TR_HMAX + j];
+        aw2 = fma(sDout[q], pr > 0.0 ? pr : 0.0, aw2);
+      }
+    }
+    double* gp = A.gpart + ((int64_t)a * A.groups + g) * A.dec_stride;
+#pragma unroll
+    for (int k = 0; k < 18; ++k) gp[j * 36 + k0 + k] = acc[k];
+    if (half == 0) gp[h * 36 + j] = aw2;
+    if (t == TR_HMAX) {  // db2 = sum dout
+      double ab2 = 0.0;
+      for (int q = 0; q < TR_GP; ++q) ab2 = dadd(ab2, sDout[q]);
+      gp[h * 36 + h] = ab2;
+    }
+  }
+  if (t == 0) {
+    int any = 0;
+    for (int q = 0; q < TR_GP; ++q) any |= sDec[q];
+    if (any) A.dtouch[L - 1] = 1;
+  }
+}
+
+// ---------------------------------------------------------------- decoder reduce
+__global__ void __launch_bounds__(256) k_train_dec_reduce(const __grid_constant__ TrainArgs A) {
+  if ((int)blockIdx.y == A.n_act) {  // G[p][l] = sum over active L >= l of dz_L (field.py:388-394)
+    const int64_t total = A.n * A.LM * 32;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+      const int k = (int)(e & 31);
+      const int64_t pl = e >> 5;
+      const int64_t p = pl / A.LM;
+      const int l = (int)(pl % A.LM) + 1;
+      double G = 0.0;
+      for (int Lk = l; Lk <= A.LM; ++Lk)
+        if ((A.active_mask >> (Lk - 1)) & 1) G = dadd(G, A.dz[(p * A.n_dec + level_slot(A.active_mask, Lk)) * 32 + k]);
+      A.G[e] = G;
+    }
+    return;
+  }
+  const int a = blockIdx.y;
+  const int L = slot_level(A.active_mask, a);
   const int64_t used = (int64_t)A.h * 36 + A.h + 1;
-  if (i >= used) return;
-  const int64_t e = (int64_t)(L - 1) * A.dec_stride + i;
-  double prm = A.dec[e], mm = A.decm[e], vv = A.decv[e];
-  adam_elem(prm, mm, vv, A.gdec[(int64_t)a * A.dec_stride + i], A.lr, A.c1, A.c2);
-  A.dec[e] = prm;
-  A.decm[e] = mm;
-  A.decv[e] = vv;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool adam = A.mode == 0;
+  bool bad = false;
+  if (i < used) {
+    double s = 0.0;
+    for (int64_t g = 0; g < A.groups; ++g) s = dadd(s, A.gpart[((int64_t)a * A.groups + g) * A.dec_stride + i]);
+    if (adam) A.gdec[(int64_t)a * A.dec_stride + i] = s;
+    else if (A.dtouch[L - 1]) A.grad_dec[(int64_t)(L - 1) * A.dec_stride + i] += s;
+    bad = !isfinite(s);
+  }
+  if (adam && A.update_decoders && A.dtouch[L - 1] && __any_sync(FULL, bad) && (threadIdx.x & 31) == 0)
+    flag_divergence(A.status, A.batch_index);
+  // residual sum of level L (trainer.py:140), fixed order
+  if (blockIdx.x == 0 && threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    double s = 0.0;
+    for (int64_t p = lane; p < A.n; p += 32) s = dadd(s, A.sq[(int64_t)a * A.n + p]);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
+    if (lane == 0) {
+      if (adam) {
+        A.level_sums[L - 1] = dadd(A.level_sums[L - 1], s);
+        if (!isfinite(s)) flag_divergence(A.status, A.batch_index);  // non-finite loss (trainer.py:233-236)
+      } else {
+        A.level_sums[L - 1] = s;
+        if (A.dec_touched && A.dtouch[L - 1]) A.dec_touched[L - 1] = 1;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- update
+// blocks [0, row_blocks): warp per touched row; the rest: decoder Adam.
+__global__ void __launch_bounds__(256) k_train_update(const __grid_constant__ TrainArgs A, int row_blocks) {
+  const int lane = threadIdx.x & 31;
+  if ((int)blockIdx.x >= row_blocks) {
+    if (A.mode != 0 || !A.update_decoders || *(volatile int64_t*)A.status) return;
+    const int64_t per = (int64_t)A.h * 36 + A.h + 1;  // elements per decoder
+    const double c1 = A.adam_c[2 * (A.step - 1)], c2 = A.adam_c[2 * (A.step - 1) + 1];
+    for (int64_t e = (int64_t)(blockIdx.x - row_blocks) * blockDim.x + threadIdx.x; e < per * A.n_act;
+         e += (int64_t)(gridDim.x - row_blocks) * blockDim.x) {
+      const int a = (int)(e / per);
+      const int64_t i = e % per;
+      const int L = slot_level(A.active_mask, a);
+      if (!A.dtouch[L - 1]) continue;  // untouched decoders keep their moments (trainer.py:100, 290-296)
+      const int64_t o = (int64_t)(L - 1) * A.dec_stride + i;
+      double prm = A.dec[o], mm = A.decm[o], vv = A.decv[o];
+      adam_elem(prm, mm, vv, A.gdec[(int64_t)a * A.dec_stride + i], A.lr, c1, c2);
+      A.dec[o] = prm;
+      A.decm[o] = mm;
+      A.decv[o] = vv;
+    }
+    return;
+  }
+  const int64_t n_rows = (int64_t)A.ctr[0];
+  const int LM8 = A.LM * 8;
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n_rows;
+       i += ((int64_t)row_blocks * blockDim.x) >> 5) {
+    const int id = A.touched[i];
+    const int S = A.cnt[id];
+    const int base = A.seg[id];
+    double g = 0.0;
+    // dZ row = sum of w * G over the records in key order: keys are ranked,
+    // then contributions are loaded 8 records at a time
+    auto accumulate = [&](const int* keys, int cnt) {
+      for (int r0 = 0; r0 < cnt; r0 += 8) {
+        double w[8], v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int key = keys[r0 + u < cnt ? r0 + u : r0];
+          w[u] = A.rec_w[key];
+          v[u] = A.G[(int64_t)(key >> 3) * 32 + lane];
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (r0 + u < cnt) g = dadd(g, dmul(w[u], v[u]));
+      }
+    };
+    if (S <= 32) {
+      __shared__ int sk[8][32];
+      const int wl = (threadIdx.x >> 5);
+      const int key = lane < S ? A.list[base + lane] : 0x7fffffff;
+      int rank = 0;
+      for (int q = 0; q < S; ++q) rank += __shfl_sync(FULL, key, q) < key;
+      if (lane < S) sk[wl][rank] = key;
+      __syncwarp();
+      accumulate(sk[wl], S);
+      __syncwarp();
+    } else {
+      for (int i0 = 0; i0 < S; i0 += 32) {
+        const bool own = i0 + lane < S;
+        const int key = own ? A.list[base + i0 + lane] : 0x7fffffff;
+        int rank = 0;
+        for (int c0 = 0; c0 < S; c0 += 32) {
+          const int other = c0 + lane < S ? A.list[base + c0 + lane] : 0x7fffffff;
+          for (int q = 0; q < 32; ++q) rank += __shfl_sync(FULL, other, q) < key;
+        }
+        if (own) A.sorted[base + rank] = key;
+      }
+      __syncwarp();
+      accumulate(A.sorted + base, S);
+    }
+    const int64_t e = (int64_t)id * 32 + lane;
+    if (A.mode == 0) {
+      if (!*(volatile int64_t*)A.status) {
+        if (!isfinite(g)) {
+          flag_divergence(A.status, A.batch_index);
+        } else {
+          double prm = A.Z[e], mm = A.Zm[e], vv = A.Zv[e];
+          adam_elem(prm, mm, vv, g, A.lr, A.adam_c[2 * (A.step - 1)], A.adam_c[2 * (A.step - 1) + 1]);
+          A.Z[e] = prm;
+          A.Zm[e] = mm;
+          A.Zv[e] = vv;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) A.Zlast[id] = (int32_t)A.step;
+    } else if (A.mode == 1) {
+      A.grad_Z[e] = dadd(A.grad_Z[e], g);
+    }
+    __syncwarp();
+    if (lane == 0) A.cnt[id] = 0;
+  }
+}
+
+// ---------------------------------------------------------------- flush
+__global__ void __launch_bounds__(256) k_train_flush(double* Z, double* Zm, double* Zv, int32_t* Zlast, int64_t C,
+                                                     int64_t upto, double lr, const double* __restrict__ c) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (r >= C) return;
+  const int64_t last = Zlast[r];
+  if (last >= upto) return;
+  const int64_t e = r * 32 + lane;
+  double prm = Z[e], mm = Zm[e], vv = Zv[e];
+  if (!(mm == 0.0 && vv == 0.0)) {
+    adam_replay(prm, mm, vv, last, upto, lr, c);
+    Z[e] = prm;
+    Zm[e] = mm;
+    Zv[e] = vv;
+  }
+  __syncwarp();
+  if (lane == 0) Zlast[r] = (int32_t)upto;
 }
 
 // Generic Adam over one parameter array (adam_step, trainer.py:87-103):
@@ -507,28 +680,45 @@ __global__ void k_adam_apply(double* p, double* m, double* v, const double* g, i
   v[i] = vv;
 }
 
-static size_t points_smem_bytes() {
-  return sizeof(double) * (TR_HMAX * W1S + TR_HMAX + 4) + sizeof(TrainWarp) * TR_WARPS;
-}
-
 static int highest_level(int mask) { return 32 - __builtin_clz((unsigned)mask); }
 
-}  // namespace ng
-
-using namespace ng;
-
-extern "C" {
-
-size_t ng_train_workspace_bytes(const ng_octree* tree, int64_t batch_capacity, int32_t h, int32_t n_decoders,
-                                int64_t corner_count, int32_t dec_stride) {
-  return train_layout(batch_capacity, tree->max_level, n_decoders, h, corner_count, dec_stride).total;
+static int launch_batch(const ng_octree* tree, TrainArgs& A, cudaStream_t s) {
+  int r = cuda_status(cudaMemsetAsync(A.ctr, 0, 4 * sizeof(int64_t) + 32 * sizeof(int32_t), s), "train memset");
+  if (r) return r;
+  static bool attr = false;
+  if (!attr) {
+    if ((r = cuda_status(cudaFuncSetAttribute(k_train_dec, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)dec_smem_bytes()), "train smem attr")))
+      return r;
+    attr = true;
+  }
+  const int cap_blocks = 4 * sm_count();
+  const int row_blocks = tr_grid(A.max_rows * 32, 256) < cap_blocks ? tr_grid(A.max_rows * 32, 256) : cap_blocks;
+  k_train_locate<<<tr_grid(A.n * 32, 256), 256, 0, s>>>(*tree, A);
+  NG_CHECK_LAUNCH("k_train_locate");
+  if (A.mode != 2) {
+    k_train_rowprep<<<row_blocks, 256, 0, s>>>(A);
+    NG_CHECK_LAUNCH("k_train_rowprep");
+  }
+  k_train_gather<<<tr_grid(A.n * 32, 256), 256, 0, s>>>(A);
+  NG_CHECK_LAUNCH("k_train_gather");
+  // grid.y = n_act decoder slots, plus one row of record-placement blocks
+  const int fill_rows = A.mode == 2 ? 0 : 1;
+  k_train_dec<<<dim3((unsigned)A.groups, A.n_act + fill_rows), TR_NT, dec_smem_bytes(), s>>>(A);
+  NG_CHECK_LAUNCH("k_train_dec");
+  if (A.mode == 2) return NG_OK;
+  const int64_t used = (int64_t)A.h * 36 + A.h + 1;
+  k_train_dec_reduce<<<dim3(tr_grid(used, 256), A.n_act + 1), 256, 0, s>>>(A);
+  NG_CHECK_LAUNCH("k_train_dec_reduce");
+  const int dec_blocks = (A.mode == 0 && A.update_decoders) ? tr_grid(used * A.n_act, 256) : 0;
+  k_train_update<<<row_blocks + dec_blocks, 256, 0, s>>>(A, row_blocks);
+  NG_CHECK_LAUNCH("k_train_update");
+  return NG_OK;
 }
 
-int ng_train_batch(const ng_octree* tree, const ng_train_params* P, const ng_train_step* st, const double* pts,
-                   const double* dist, const double* upstream, int64_t n, int64_t batch_capacity, void* ws,
-                   size_t ws_bytes, double* level_sums, double* grad_Z, double* grad_dec, int32_t* dec_touched,
-                   double* psi_out, int64_t* status, void* stream) {
-  cudaStream_t s = (cudaStream_t)stream;
+static int fill_args(const ng_octree* tree, const ng_train_params* P, const ng_train_step* st, const double* pts,
+                     const double* dist, const double* upstream, int64_t n, int64_t batch_capacity, void* ws,
+                     size_t ws_bytes, TrainArgs& A) {
   if (P->h < 1 || P->h > TR_HMAX || P->m < 1 || P->m > 32) {
     set_error("trainer supports 1 <= h <= %d and 1 <= m <= 32 (got h=%d, m=%d)", TR_HMAX, P->h, P->m);
     return NG_ERR_STRUCTURAL;
@@ -546,93 +736,111 @@ int ng_train_batch(const ng_octree* tree, const ng_train_params* P, const ng_tra
     set_error("batch of %lld points above the workspace capacity %lld", (long long)n, (long long)batch_capacity);
     return NG_ERR_CAPACITY;
   }
-  if (n <= 0) return NG_OK;
-  const TrainLayout Ly = train_layout(batch_capacity, tree->max_level, P->n_decoders, P->h, P->corner_count,
+  const TrainLayout Ly = train_layout(batch_capacity, tree->max_level, P->n_decoders, P->corner_count,
                                       P->dec_stride);
   if (ws_bytes < Ly.total) {
     set_error("train workspace %zu < %zu bytes", ws_bytes, Ly.total);
     return NG_ERR_CAPACITY;
   }
+  if (st->mode == 0 && (!P->Zm || !P->Zv || !P->Zlast || !st->adam_c || st->step < 1)) {
+    set_error("Adam mode needs moments, Zlast, the bias-correction table and step >= 1");
+    return NG_ERR_STRUCTURAL;
+  }
   char* b = (char*)ws;
-  TrainArgs A;
-  A.Z = P->Z; A.Zm = P->Zm; A.Zv = P->Zv;
+  A.Z = P->Z; A.Zm = P->Zm; A.Zv = P->Zv; A.Zlast = P->Zlast;
   A.dec = P->dec; A.decm = P->decm; A.decv = P->decv;
   A.m = P->m; A.h = P->h; A.n_dec = P->n_decoders; A.dec_stride = P->dec_stride; A.C = P->corner_count;
   A.pts = pts; A.dist = dist; A.upstream = upstream; A.n = n;
   A.LM = highest_level(mask);
   A.active_mask = mask;
+  A.n_act = __builtin_popcount((unsigned)mask);
   A.update_decoders = st->update_decoders;
   A.mode = st->mode;
   A.two_over_n = 2.0 / st->denom;
-  A.lr = st->lr; A.c1 = st->c1; A.c2 = st->c2;
+  A.lr = st->lr;
+  A.step = st->step;
+  A.adam_c = st->adam_c;
   A.batch_index = st->batch_index;
+  A.groups = (n + TR_GP - 1) / TR_GP;
+  A.max_rows = Ly.max_rows;
   A.rec_w = (double*)(b + Ly.rec_w);
   A.rec_id = (int32_t*)(b + Ly.rec_id);
+  A.pres = (uint32_t*)(b + Ly.pres);
+  A.z = (double*)(b + Ly.z);
   A.G = (double*)(b + Ly.G);
-  A.inp = (double*)(b + Ly.inp);
-  A.pre = (double*)(b + Ly.pre);
-  A.dpre = (double*)(b + Ly.dpre);
-  A.dout = (double*)(b + Ly.dout);
+  A.dz = (double*)(b + Ly.dz);
   A.sq = (double*)(b + Ly.sq);
-  A.cnt = (int64_t*)(b + Ly.cnt);
-  A.off = (int64_t*)(b + Ly.off);
+  A.gpart = (double*)(b + Ly.gpart);
+  A.gdec = (double*)(b + Ly.gdec);
+  A.cnt = (int32_t*)(b + Ly.cnt);
   A.fill = (int32_t*)(b + Ly.fill);
+  A.seg = (int32_t*)(b + Ly.seg);
+  A.touched = (int32_t*)(b + Ly.touched);
   A.list = (int32_t*)(b + Ly.list);
   A.sorted = (int32_t*)(b + Ly.sorted);
-  A.gdec = (double*)(b + Ly.gdec);
-  A.touched = (int32_t*)(b + Ly.touched);
+  A.ctr = (unsigned long long*)(b + Ly.ctr);
+  A.dtouch = (int32_t*)(b + Ly.ctr + 4 * sizeof(int64_t));
+  A.level_sums = A.grad_Z = A.grad_dec = nullptr;
+  A.dec_touched = nullptr;
+  A.psi_out = A.pre_out = A.inp_out = nullptr;
+  A.status = nullptr;
+  return NG_OK;
+}
+
+}  // namespace ng
+
+using namespace ng;
+
+extern "C" {
+
+size_t ng_train_workspace_bytes(const ng_octree* tree, int64_t batch_capacity, int32_t h, int32_t n_decoders,
+                                int64_t corner_count, int32_t dec_stride) {
+  (void)h;
+  return train_layout(batch_capacity, tree->max_level, n_decoders, corner_count, dec_stride).total;
+}
+
+int ng_train_batch(const ng_octree* tree, const ng_train_params* P, const ng_train_step* st, const double* pts,
+                   const double* dist, const double* upstream, int64_t n, int64_t batch_capacity, void* ws,
+                   size_t ws_bytes, double* level_sums, double* grad_Z, double* grad_dec, int32_t* dec_touched,
+                   double* psi_out, int64_t* status, void* stream) {
+  if (st->mode == 1 && (!grad_Z || !grad_dec)) {
+    set_error("gradient mode needs grad_Z and grad_dec");
+    return NG_ERR_STRUCTURAL;
+  }
+  if (st->mode != 2 && (!level_sums || !status)) {
+    set_error("level_sums and status are required");
+    return NG_ERR_STRUCTURAL;
+  }
+  TrainArgs A;
+  int r = fill_args(tree, P, st, pts, dist, upstream, n, batch_capacity, ws, ws_bytes, A);
+  if (r) return r;
+  if (n <= 0) return NG_OK;
   A.level_sums = level_sums;
   A.grad_Z = grad_Z;
   A.grad_dec = grad_dec;
   A.dec_touched = dec_touched;
   A.psi_out = psi_out;
   A.status = status;
-  if (A.mode == 1 && (!grad_Z || !grad_dec)) {
-    set_error("gradient mode needs grad_Z and grad_dec");
-    return NG_ERR_STRUCTURAL;
-  }
-  // counts, fill cursors and touched flags are contiguous in the layout
-  int r = cuda_status(cudaMemsetAsync(b + Ly.cnt, 0, Ly.off - Ly.cnt, s), "train memset");
-  if (r) return r;
-  const size_t smem = points_smem_bytes();
-  static bool attr = false;
-  if (!attr) {
-    if ((r = cuda_status(cudaFuncSetAttribute(k_train_points, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              (int)smem), "train smem attr")))
-      return r;
-    if ((r = cuda_status(cudaFuncSetAttribute(k_train_dec_grads, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              (int)(sizeof(double) * DG_WARPS * 38 * 32)), "train smem attr")))
-      return r;
-    attr = true;
-  }
-  k_train_points<<<tr_grid(n, TR_WARPS), TR_WARPS * 32, smem, s>>>(*tree, A);
-  NG_CHECK_LAUNCH("k_train_points");
-  if (A.mode == 2) return NG_OK;  // forward cache only (ng_train_export)
-  if ((r = ng_exclusive_sum_i64(A.cnt, A.C, A.off, b + Ly.scan, ng_scan_scratch_bytes(A.C), stream))) return r;
-  const int64_t n_rec = n * A.LM * 8;
-  k_train_fill<<<tr_grid(n_rec, 256), 256, 0, s>>>(A, n_rec);
-  NG_CHECK_LAUNCH("k_train_fill");
-  const int n_act = __builtin_popcount((unsigned)mask);
-  k_train_dec_grads<<<dim3(n_act, (A.h + 31) / 32), DG_WARPS * 32, sizeof(double) * DG_WARPS * 38 * 32, s>>>(A);
-  NG_CHECK_LAUNCH("k_train_dec_grads");
-  k_train_rows<<<tr_grid(A.C * 32, 256), 256, 0, s>>>(A);
-  NG_CHECK_LAUNCH("k_train_rows");
-  if (A.mode == 0 && A.update_decoders) {
-    const int64_t used = (int64_t)A.h * 36 + A.h + 1;
-    k_train_dec_adam<<<dim3(tr_grid(used, 256), n_act), 256, 0, s>>>(A);
-    NG_CHECK_LAUNCH("k_train_dec_adam");
-  }
+  return launch_batch(tree, A, (cudaStream_t)stream);
+}
+
+int ng_train_flush(const ng_train_params* P, int64_t step, const double* adam_c, double lr, void* stream) {
+  if (P->corner_count <= 0 || step < 1) return NG_OK;
+  k_train_flush<<<tr_grid(P->corner_count * 32, 256), 256, 0, (cudaStream_t)stream>>>(
+      P->Z, P->Zm, P->Zv, P->Zlast, P->corner_count, step, lr, adam_c);
+  NG_CHECK_LAUNCH("k_train_flush");
   return NG_OK;
 }
 
 int ng_train_epoch(const ng_octree* tree, const ng_train_params* P, const double* pts, const double* dist,
                    int64_t n, int64_t batch_size, int32_t active_mask, int32_t update_decoders, double lr,
-                   int64_t step0, void* ws, size_t ws_bytes, double* level_sums, int64_t* status,
-                   void* stream) {
+                   int64_t step0, const double* adam_c, int32_t flush_every, void* ws, size_t ws_bytes,
+                   double* level_sums, int64_t* status, void* stream) {
   if (batch_size < 1) {
     set_error("batch_size must be positive");
     return NG_ERR_CONFIG;
   }
+  cudaStream_t s = (cudaStream_t)stream;
   int64_t step = step0;
   for (int64_t s0 = 0, bi = 0; s0 < n; s0 += batch_size, ++bi) {
     const int64_t cnt = (n - s0 < batch_size) ? n - s0 : batch_size;
@@ -644,14 +852,15 @@ int ng_train_epoch(const ng_octree* tree, const ng_train_params* P, const double
     st.pad = 0;
     st.denom = (double)cnt;
     st.lr = lr;
-    st.c1 = 1.0 - pow(BETA1, (double)step);  // trainer.py:92-93
-    st.c2 = 1.0 - pow(BETA2, (double)step);
+    st.step = step;
+    st.adam_c = adam_c;
     st.batch_index = s0;
     int r = ng_train_batch(tree, P, &st, pts + 3 * s0, dist + s0, nullptr, cnt, batch_size, ws, ws_bytes,
-                           level_sums, nullptr, nullptr, nullptr, nullptr, status, stream);
+                           level_sums, nullptr, nullptr, nullptr, nullptr, status, s);
     if (r) return r;
+    if (flush_every > 0 && (bi + 1) % flush_every == 0 && (r = ng_train_flush(P, step, adam_c, lr, s))) return r;
   }
-  return NG_OK;
+  return ng_train_flush(P, step, adam_c, lr, s);
 }
 
 int ng_train_export(const ng_octree* tree, const ng_train_params* P, int32_t level, const double* pts, int64_t n,
@@ -668,25 +877,26 @@ int ng_train_export(const ng_octree* tree, const ng_train_params* P, int32_t lev
   st.mode = 2;
   st.pad = 0;
   st.denom = (double)n;
-  st.lr = st.c1 = st.c2 = 0.0;
+  st.lr = 0.0;
+  st.step = 0;
+  st.adam_c = nullptr;
   st.batch_index = 0;
-  int r = ng_train_batch(tree, P, &st, pts, nullptr, nullptr, n, n, ws, ws_bytes, nullptr, nullptr, nullptr,
-                         nullptr, psi, nullptr, stream);
+  TrainArgs A;
+  int r = fill_args(tree, P, &st, pts, nullptr, nullptr, n, n, ws, ws_bytes, A);
   if (r) return r;
-  const TrainLayout Ly = train_layout(n, tree->max_level, P->n_decoders, P->h, P->corner_count, P->dec_stride);
+  A.psi_out = psi;
+  A.pre_out = pre;
+  A.inp_out = inp;
   cudaStream_t s = (cudaStream_t)stream;
+  if ((r = launch_batch(tree, A, s))) return r;
+  const TrainLayout Ly = train_layout(n, tree->max_level, P->n_decoders, P->corner_count, P->dec_stride);
   const char* b = (const char*)ws;
+  // records are laid out [p][level][8] with LM = level
   if ((r = cuda_status(cudaMemcpyAsync(ids, b + Ly.rec_id, sizeof(int32_t) * n * level * 8,
                                        cudaMemcpyDeviceToDevice, s), "export ids")))
     return r;
-  if ((r = cuda_status(cudaMemcpyAsync(weights, b + Ly.rec_w, sizeof(double) * n * level * 8,
-                                       cudaMemcpyDeviceToDevice, s), "export weights")))
-    return r;
-  if ((r = cuda_status(cudaMemcpyAsync(pre, b + Ly.pre, sizeof(double) * n * P->h, cudaMemcpyDeviceToDevice, s),
-                       "export pre")))
-    return r;
-  return cuda_status(cudaMemcpyAsync(inp, b + Ly.inp, sizeof(double) * n * 36, cudaMemcpyDeviceToDevice, s),
-                     "export inp");
+  return cuda_status(cudaMemcpyAsync(weights, b + Ly.rec_w, sizeof(double) * n * level * 8,
+                                     cudaMemcpyDeviceToDevice, s), "export weights");
 }
 
 int ng_adam_step(double* param, double* m, double* v, const double* grad, int64_t n, double lr, double c1,

@@ -122,10 +122,11 @@ class DeviceTrainState:
         if moments:
             self.Zm, self.Zv = torch.zeros_like(self.Z), torch.zeros_like(self.Z)
             self.decm, self.decv = torch.zeros_like(self.dec), torch.zeros_like(self.dec)
+            self.Zlast = torch.zeros(self.C, dtype=torch.int32, device=dev)
         else:
-            self.Zm = self.Zv = self.decm = self.decv = None
+            self.Zm = self.Zv = self.decm = self.decv = self.Zlast = None
         s = _lib.NgTrainParams()
-        s.Z, s.Zm, s.Zv = ptr(self.Z), ptr(self.Zm), ptr(self.Zv)
+        s.Z, s.Zm, s.Zv, s.Zlast = ptr(self.Z), ptr(self.Zm), ptr(self.Zv), ptr(self.Zlast)
         s.dec, s.decm, s.decv = ptr(self.dec), ptr(self.decm), ptr(self.decv)
         s.m, s.h, s.n_decoders, s.dec_stride = self.m, self.h, self.n_dec, self.stride
         s.corner_count = self.C
@@ -137,7 +138,7 @@ class DeviceTrainState:
         if batch_capacity > self._ws_cap:
             nb = _lib.lib().ng_train_workspace_bytes(self.svo.device.ref(), batch_capacity, self.h, self.n_dec,
                                                      self.C, self.stride)
-            self._ws = torch.empty(int(nb), dtype=torch.uint8, device=self.Z.device)
+            self._ws = torch.zeros(int(nb), dtype=torch.uint8, device=self.Z.device)  # counters start at zero
             self._ws_cap = batch_capacity
         return self._ws
 
@@ -168,7 +169,7 @@ class DeviceTrainState:
         touched = torch.tensor([int(g is not None) for g in grads.decoders], dtype=torch.int32, device=dev)
         status = torch.zeros(1, dtype=torch.int64, device=dev)
         ws = self.workspace(n)
-        st = _lib.NgTrainStep(active_mask, 0, 1, 0, float(denom), 0.0, 0.0, 0.0, 0)
+        st = _lib.NgTrainStep(active_mask, 0, 1, 0, float(denom), 0.0, 0, None, 0)
         call("ng_train_batch", self.svo.device.ref(), ctypes.byref(self.struct), ctypes.byref(st), ptr(dp), ptr(dd),
              ptr(du), n, self._ws_cap, ptr(ws), ws.numel(), ptr(sums), ptr(gZ), ptr(gD), ptr(touched), None,
              ptr(status), stream_ptr())
@@ -194,7 +195,7 @@ class DeviceTrainState:
             # ng_train_export lays its workspace out for a capacity of exactly n
             nb = _lib.lib().ng_train_workspace_bytes(self.svo.device.ref(), n, self.h, self.n_dec, self.C,
                                                      self.stride)
-            ws = torch.empty(int(nb), dtype=torch.uint8, device=dev)
+            ws = torch.zeros(int(nb), dtype=torch.uint8, device=dev)
             call("ng_train_export", self.svo.device.ref(), ctypes.byref(self.struct), L, ptr(dp), n, ptr(ws),
                  ws.numel(), ptr(ids), ptr(w), ptr(psi), ptr(pre), ptr(inp), stream_ptr())
         ids_h, w_h, psi_h = ids.cpu().numpy(), w.cpu().numpy(), psi.cpu().numpy()
@@ -311,13 +312,28 @@ class DeviceTrainer:
     """The epoch loop's device half: parameters, moments, workspace and the
     Adam step counter persist across epochs in HBM."""
 
-    def __init__(self, fld: NeuralField, batch_size: int):
+    def __init__(self, fld: NeuralField, batch_size: int, flush_every: int = 32):
         self.state = DeviceTrainState(fld.svo, fld.Z, fld.decoders, moments=True)
         self.batch_size = batch_size
+        self.flush_every = flush_every
         self.step = 0
         dev = self.state.Z.device
         self.level_sums = torch.zeros(self.state.n_dec, dtype=torch.float64, device=dev)
         self.status = torch.zeros(1, dtype=torch.int64, device=dev)
+        self.adam_c = torch.zeros(0, dtype=torch.float64, device=dev)
+
+    def _bias_table(self, upto: int) -> None:
+        """(1 - beta1^t, 1 - beta2^t) for steps 1..upto, computed like
+        adam_step (trainer.py:92-93) and kept on the device."""
+        have = self.adam_c.numel() // 2
+        if upto <= have:
+            return
+        upto = max(upto, 2 * have)
+        c = np.empty((upto, 2), dtype=np.float64)
+        for t in range(1, upto + 1):
+            c[t - 1, 0] = 1.0 - ADAM_BETA1 ** t
+            c[t - 1, 1] = 1.0 - ADAM_BETA2 ** t
+        self.adam_c = torch.from_numpy(c.ravel()).to(self.state.Z.device)
 
     def run_epoch(self, pts_dev: torch.Tensor, dist_dev: torch.Tensor, active: list, update_decoders: bool,
                   lr: float) -> None:
@@ -329,10 +345,12 @@ class DeviceTrainer:
             mask |= 1 << (L - 1)
         self.level_sums.zero_()
         ws = st.workspace(self.batch_size)
+        n_batches = (n + self.batch_size - 1) // self.batch_size
+        self._bias_table(self.step + n_batches)
         call("ng_train_epoch", st.svo.device.ref(), ctypes.byref(st.struct), ptr(pts_dev), ptr(dist_dev), n,
-             self.batch_size, mask, int(update_decoders), float(lr), self.step, ptr(ws), ws.numel(),
-             ptr(self.level_sums), ptr(self.status), stream_ptr())
-        self.step += (n + self.batch_size - 1) // self.batch_size
+             self.batch_size, mask, int(update_decoders), float(lr), self.step, ptr(self.adam_c),
+             int(self.flush_every), ptr(ws), ws.numel(), ptr(self.level_sums), ptr(self.status), stream_ptr())
+        self.step += n_batches
 
     def diverged_at(self) -> int:
         """-1, or the start row of the first batch that diverged."""
