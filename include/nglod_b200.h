@@ -332,6 +332,20 @@ int ng_march_profile(unsigned long long* host_out, int max_groups);
 int ng_hit_points(const ng_ray* rays, const uint8_t* hit, const double* t, int64_t n,
                   double* points, void* stream);
 
+/* ---- evaluation (metrics.py) ------------------------ */
+/* trace_oracle_rays (metrics.py:145-178) for a built-in SDF (kinds as in
+ * ng_sdf_lattice): hit u8, t_hit fp64 (nan on miss). */
+int ng_trace_sdf(int32_t kind, const double* params, int32_t n_params, const double* origins, const double* dirs,
+                 int64_t n, double delta, double far_plane, int32_t max_iters, uint8_t* hit, double* t_hit,
+                 void* stream);
+/* Nearest occupied voxel of `level` for each point (first minimum of the
+ * squared box distance, metrics.py:236-250): the clamped anchor (n,3) and the
+ * separation (n,). */
+int ng_nearest_voxel(const ng_octree* tree, int32_t level, const double* pts, int64_t n, double* anchor, double* gap,
+                     void* stream);
+/* Distance from each query to its nearest point (PointGrid.nearest_dist, metrics.py:64-112). */
+int ng_nn_dist(const double* queries, int64_t nq, const double* points, int64_t np_, double* out, void* stream);
+
 /* ---- training (field.py:286-409, trainer.py:87-296) ------- */
 /* fp64 master parameters and Adam moments (trainer.py:62-84, 176-190), all
  * device memory owned by the caller. Z rows are padded to 32 channels; each

@@ -54,6 +54,17 @@ from .field import (
 from .sampling import SampleSet, build_epoch_set, surface_points
 from .trainer import AdamState, EpochStats, TrainConfig, active_levels_for, adam_step, loss_batch, train
 from .modelio import load_model, save_model, serialized_bytes
+from .metrics import (
+    EvalReport,
+    bench_frame,
+    chamfer_l1,
+    evaluate,
+    fibonacci_cameras,
+    giou,
+    image_metrics,
+    sample_predicted_surface,
+    surface_accuracy,
+)
 from .traversal import RayBundle, RayVoxelPairList, exclusive_sum, ray_segments, ray_trace_octree
 from .render import (
     Camera,
@@ -84,4 +95,6 @@ __all__ = [
     "voxel_bounds", "write_ppm", "DecoderGrads", "FieldGradients", "LevelInterp", "backward", "scatter_add_rows",
     "SampleSet", "build_epoch_set", "surface_points", "AdamState", "EpochStats", "TrainConfig",
     "active_levels_for", "adam_step", "loss_batch", "train", "load_model", "save_model", "serialized_bytes",
+    "EvalReport", "bench_frame", "chamfer_l1", "evaluate", "fibonacci_cameras", "giou", "image_metrics",
+    "sample_predicted_surface", "surface_accuracy",
 ]
