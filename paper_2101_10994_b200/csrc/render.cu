@@ -1063,6 +1063,9 @@ static int render_common(const ng_octree& tree, const ng_field& f, const ng_rend
     MarchArgs S;
     if ((r = trace_pass(tree, cfg, P, srays, n, st->shadow_pairs, L, ws, b, ctr + 3, ctr + 4, s, S))) return r;
     S.hit = (uint8_t*)(b + L.s_hit);
+    // the march writes only the rays that have a voxel segment: clear the rest
+    // (a shadow ray that leaves the octree without a segment is unshadowed)
+    if ((r = cuda_status(cudaMemsetAsync(S.hit, 0, (size_t)n, s), "shadow hit memset"))) return r;
     S.t = (double*)(b + L.s_t);
     S.iters = (int32_t*)(b + L.s_it);
     S.evals = (int32_t*)(b + L.s_ev);

@@ -407,6 +407,10 @@ def test_shadow_rays_match_oracle(ng, golden, O, lod):
     cam = dict(position=(0.0, 2.0, 3.5), look_at=(0.0, 0.0, 0.0), up=(0.0, 1.0, 0.0), fov_y_deg=30.0,
                width=96, height=72)
     fb, rep = ng.render(ng.Camera(**cam), fld, ng.RenderConfig(lod=lod, shadows=True))
+    for _ in range(2):  # repeated frames reuse the session workspace: results must not depend on it
+        fb2, rep2 = ng.render(ng.Camera(**cam), fld, ng.RenderConfig(lod=lod, shadows=True))
+        assert rep2.shadowed == rep.shadowed
+        np.testing.assert_array_equal(fb2.color, fb.color)
     fr = O.render(tree, fld.Z, decs, cam, O.RenderParams(lod=lod, shadows=True))
     assert np.mean(fb.hit == fr.hit) >= 0.999
     both = fb.hit & fr.hit
