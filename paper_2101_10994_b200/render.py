@@ -144,13 +144,15 @@ class FrameBuffer:
 
     _FIELDS = ("hit", "t", "points", "normal", "normal_ok", "iterations", "evals", "color")
 
-    def __init__(self, width, height, dev: dict, camera: Camera | None = None, rays: torch.Tensor | None = None):
+    def __init__(self, width, height, dev: dict, camera: Camera | None = None, rays: torch.Tensor | None = None,
+                 prefetched: dict | None = None):
         self.width = width
         self.height = height
         self.device = dev
         self._camera = camera
         self._rays = rays
         self._host = {}
+        self._pinned = prefetched or {}  # host copies already issued on the stream (pinned)
 
     def _shape(self, *tail):
         return (self.height, self.width) + tail
@@ -172,7 +174,8 @@ class FrameBuffer:
         elif name == "evals":
             v = d["evals"].cpu().numpy().astype(np.int64).reshape(self._shape())
         elif name == "color":
-            v = d["color"].cpu().numpy().reshape(self._shape(3))
+            src = self._pinned["color"] if "color" in self._pinned else d["color"].cpu()
+            v = src.numpy().reshape(self._shape(3))
         elif name == "points":
             n = self.width * self.height
             rays = self._rays if self._rays is not None else self._camera.device_rays()
@@ -509,6 +512,9 @@ def render(camera: Camera, fld: NeuralField, config: RenderConfig):
     while True:
         frame = sess.new_frame()
         sess.enqueue(cfg, frame, camera=camera, timed=True)
+        # the colour image rides the same stream synchronisation as the statistics
+        color_h = torch.empty(frame["color"].shape, dtype=torch.uint8, pin_memory=True)
+        color_h.copy_(frame["color"], non_blocking=True)
         st = sess.read_stats()
         if not sess.grow(st, n_levels):
             break
@@ -518,7 +524,7 @@ def render(camera: Camera, fld: NeuralField, config: RenderConfig):
         raise OctfieldError("internal: decoder ran outside the queried level's voxels")
     ms_trace = sess.ev0.elapsed_time(sess.ev1)
     ms_normals = sess.ev1.elapsed_time(sess.ev2)
-    fb = FrameBuffer(camera.width, camera.height, frame, camera=camera)
+    fb = FrameBuffer(camera.width, camera.height, frame, camera=camera, prefetched={"color": color_h})
     report = FrameReport(ms_trace=float(ms_trace), ms_normals=float(ms_normals),
                          evals=int(st.counters.decoder_evals), visible=int(st.visible), lod=lod,
                          shadowed=int(st.shadowed))

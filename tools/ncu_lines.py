@@ -1,6 +1,6 @@
 """Aggregate ncu warp-stall samples of one kernel by CUDA source line.
 
-    python tools/ncu_lines.py REPORT.ncu-rep OBJ.o KERNEL_SUBSTRING [top]
+    python tools/ncu_lines.py REPORT.ncu-rep OBJ.o KERNEL_SUBSTRING [top] [MANGLED_SUBSTRING]
 
 Maps SASS addresses in the report's source page to file:line through
 `nvdisasm -g` of the object's cubin (compile with -lineinfo)."""
@@ -8,6 +8,7 @@ import csv, io, os, re, subprocess, sys, tempfile, collections
 
 rep, obj, kname = sys.argv[1], sys.argv[2], sys.argv[3]
 top = int(sys.argv[4]) if len(sys.argv) > 4 else 40
+mangled = sys.argv[5] if len(sys.argv) > 5 else kname  # substring of the mangled name (template instance)
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass", "-k", f"regex:{kname}"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
@@ -36,7 +37,7 @@ for ln in dis.splitlines():
         cur_line = f"{os.path.basename(m.group(1))}:{m.group(2)}"
         continue
     m = re.match(r"\s*/\*([0-9a-f]{4,})\*/", ln)
-    if m and cur_fn and kname in cur_fn:
+    if m and cur_fn and mangled in cur_fn:
         line_of[int(m.group(1), 16)] = cur_line
 agg = collections.Counter()
 for a, v in samples:
