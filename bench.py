@@ -179,11 +179,14 @@ def run_ours(args, rank: int, world: int):
     from paper_2101_10994_b200.parallel import TiledRenderer
     from paper_2101_10994_b200.render import resolve_config, resolve_lod
 
-    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)) % torch.cuda.device_count())
     torch.cuda.set_device(dev)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        # NG_DIST_BACKEND=gloo lets several ranks share one GPU to exercise the
+        # multi-rank path on a single-GPU box; timed runs use NCCL
+        backend = os.environ.get("NG_DIST_BACKEND", "nccl")
+        dist.init_process_group(backend, device_id=dev if backend == "nccl" else None)
     knot, svo, fld = build_workload()
     cam = ng.Camera(CAM["position"], CAM["look_at"], CAM["up"], CAM["fov_y_deg"], WIDTH, HEIGHT)
     config = ng.RenderConfig()
