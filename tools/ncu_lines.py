@@ -9,12 +9,13 @@ import csv, io, os, re, subprocess, sys, tempfile, collections
 rep, obj, kname = sys.argv[1], sys.argv[2], sys.argv[3]
 top = int(sys.argv[4]) if len(sys.argv) > 4 else 40
 mangled = sys.argv[5] if len(sys.argv) > 5 else kname  # substring of the mangled name (template instance)
+column = sys.argv[6] if len(sys.argv) > 6 else "Warp Stall Sampling (All Samples)"  # or e.g. stall_wait
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass", "-k", f"regex:{kname}"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 hi = next(i for i, r in enumerate(rows) if "Address" in r and "Source" in r)
 h = rows[hi]
-ai, ci = h.index("Address"), h.index("Warp Stall Sampling (All Samples)")
+ai, ci = h.index("Address"), h.index(column)
 samples = []
 for r in rows[hi + 1:]:
     if len(r) > ci and r[ai].startswith("0x"):
