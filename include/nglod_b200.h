@@ -412,6 +412,9 @@ int ng_train_flush(const ng_train_params* P, int64_t step, const double* adam_c,
 int ng_train_export(const ng_octree* tree, const ng_train_params* P, int32_t level, const double* pts, int64_t n,
                     void* ws, size_t ws_bytes, int32_t* ids, double* weights, double* psi, double* pre, double* inp,
                     void* stream);
+/* Debug (NG_TRAIN_EVENTS=1): mean device ms per batch of each training kernel
+ * (locate, rowprep, gather, dec, reduce, update) since the last call; resets. */
+int ng_train_profile(double* host_out6);
 /* adam_step (trainer.py:87-103) on one fp64 array; *d_bad = 1 (and no
  * update) when the gradient has a non-finite entry. */
 int ng_adam_step(double* param, double* m, double* v, const double* grad, int64_t n, double lr, double c1,

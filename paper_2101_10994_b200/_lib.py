@@ -173,6 +173,7 @@ _SIGS = {
     "ng_train_epoch": (C.c_int, [P, P, P, P, C.c_int64, C.c_int64, C.c_int32, C.c_int32, C.c_double,
                                  C.c_int64, P, C.c_int32, P, C.c_size_t, P, P, P]),
     "ng_train_flush": (C.c_int, [P, C.c_int64, P, C.c_double, P]),
+    "ng_train_profile": (C.c_int, [P]),
     "ng_train_export": (C.c_int, [P, P, C.c_int32, P, C.c_int64, P, C.c_size_t, P, P, P, P, P, P]),
     "ng_trace_sdf": (C.c_int, [C.c_int32, P, C.c_int32, P, P, C.c_int64, C.c_double, C.c_double, C.c_int32, P, P,
                                P]),

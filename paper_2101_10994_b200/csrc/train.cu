@@ -49,8 +49,10 @@ namespace ng {
 
 constexpr int TR_LM = 12;      // max feature levels handled by the trainer
 constexpr int TR_HMAX = 128;   // max decoder width
-constexpr int TR_GP = 32;      // points per k_train_dec group
+constexpr int TR_GP = 16;      // points per decoder tile (one wave of tiles over the SMs at batch 512)
 constexpr int TR_NT = 256;     // k_train_dec threads
+constexpr int TR_PH = TR_GP / 2;            // points per thread half (forward / dpre)
+constexpr int TR_PW = TR_GP / (TR_NT / 32); // points per warp (output / dz)
 constexpr int W1S = 37;        // smem row stride (doubles) of the staged W1b block
 constexpr double BETA1 = 0.9, BETA2 = 0.999, ADAM_EPS = 1e-8;  // trainer.py:29-31
 
@@ -193,6 +195,7 @@ __global__ void __launch_bounds__(256) k_train_locate(const __grid_constant__ ng
   if (p >= A.n) return;
   const int LM = A.LM;
   bool pres = false;
+  int ids[8] = {-1, -1, -1, -1, -1, -1, -1, -1};
   if (lane < LM) {
     const double x0 = __ldg(A.pts + 3 * p), x1 = __ldg(A.pts + 3 * p + 1), x2 = __ldg(A.pts + 3 * p + 2);
     const int l = lane + 1;
@@ -205,7 +208,8 @@ __global__ void __launch_bounds__(256) k_train_locate(const __grid_constant__ ng
     if (pres) {
       const int4* cr = reinterpret_cast<const int4*>(tree.corners[tl] + 8 * idx);
       const int4 a = __ldg(cr), b = __ldg(cr + 1);
-      const int ids[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+      ids[0] = a.x; ids[1] = a.y; ids[2] = a.z; ids[3] = a.w;
+      ids[4] = b.x; ids[5] = b.y; ids[6] = b.z; ids[7] = b.w;
       // u = clip((x - DOMAIN_MIN) * (res / span) - cell, 0, 1); w_j = cx * cy * cz (field.py:115-135)
       const double half = 0.5 * (double)res;
       const double xs[3] = {x0, x1, x2};
@@ -223,14 +227,34 @@ __global__ void __launch_bounds__(256) k_train_locate(const __grid_constant__ ng
         const double wz = ((j >> 2) & 1) ? u[2] : dsub(1.0, u[2]);
         A.rec_w[key0 + j] = dmul(dmul(wx, wy), wz);
         A.rec_id[key0 + j] = ids[j];
-        if (A.mode != 2 && atomicAdd(A.cnt + ids[j], 1) == 0) {
-          const unsigned long long at = atomicAdd(A.ctr, 1ull);
-          A.touched[at] = ids[j];
-        }
       }
     } else {
 #pragma unroll
       for (int j = 0; j < 8; ++j) A.rec_id[key0 + j] = -1;
+    }
+  }
+  // corner counts; first touches append the row, one cursor atomic per warp and corner slot
+  if (A.mode != 2) {
+    int old[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) old[j] = pres ? atomicAdd(A.cnt + ids[j], 1) : 1;
+    int nfirst = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) nfirst += old[j] == 0;
+    int incl = nfirst;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(FULL, incl, o);
+      if ((int)lane >= o) incl += v;
+    }
+    const int total = __shfl_sync(FULL, incl, 31);
+    if (total) {
+      unsigned long long base = 0;
+      if (lane == 31) base = atomicAdd(A.ctr, (unsigned long long)total);
+      base = __shfl_sync(FULL, base, 31) + (unsigned long long)(incl - nfirst);
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (old[j] == 0) A.touched[base++] = ids[j];
     }
   }
   const unsigned bits = __ballot_sync(FULL, pres);
@@ -239,30 +263,48 @@ __global__ void __launch_bounds__(256) k_train_locate(const __grid_constant__ ng
 
 // ---------------------------------------------------------------- row prep
 __global__ void __launch_bounds__(256) k_train_rowprep(const __grid_constant__ TrainArgs A) {
-  const int lane = threadIdx.x & 31;
+  __shared__ int s_cnt[8];
+  __shared__ int s_base[8];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t n_rows = (int64_t)A.ctr[0];
-  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n_rows;
-       i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-    const int id = A.touched[i];
-    if (lane == 0) {
-      A.seg[id] = (int32_t)atomicAdd(A.ctr + 1, (unsigned long long)A.cnt[id]);
-      A.fill[id] = 0;
-    }
-    if (A.mode == 0) {
-      const int64_t e = (int64_t)id * 32 + lane;
-      const int64_t last = A.Zlast[id];
-      if (last < A.step - 1) {
-        double prm = A.Z[e], mm = A.Zm[e], vv = A.Zv[e];
-        if (!(mm == 0.0 && vv == 0.0)) {
-          adam_replay(prm, mm, vv, last, A.step - 1, A.lr, A.adam_c);
-          A.Z[e] = prm;
-          A.Zm[e] = mm;
-          A.Zv[e] = vv;
-        }
-        __syncwarp();
-        if (lane == 0) A.Zlast[id] = (int32_t)(A.step - 1);
+  // block-uniform loop: 8 rows per block iteration, one cursor atomic per block
+  for (int64_t i0 = (int64_t)blockIdx.x * 8; i0 < n_rows; i0 += (int64_t)gridDim.x * 8) {
+    const int64_t i = i0 + warp;
+    const int id = i < n_rows ? A.touched[i] : -1;
+    if (lane == 0) s_cnt[warp] = id >= 0 ? A.cnt[id] : 0;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int tot = 0;
+      for (int q = 0; q < 8; ++q) tot += s_cnt[q];
+      int base = (int)atomicAdd(A.ctr + 1, (unsigned long long)tot);
+      for (int q = 0; q < 8; ++q) {
+        s_base[q] = base;
+        base += s_cnt[q];
       }
     }
+    __syncthreads();
+    if (id >= 0) {
+      if (lane == 0) {
+        A.seg[id] = s_base[warp];
+        A.fill[id] = 0;
+      }
+      if (A.mode == 0) {
+        const int64_t e = (int64_t)id * 32 + lane;
+        const int64_t last = A.Zlast[id];
+        if (last < A.step - 1) {
+          double prm = A.Z[e], mm = A.Zm[e], vv = A.Zv[e];
+          if (!(mm == 0.0 && vv == 0.0)) {
+            adam_replay(prm, mm, vv, last, A.step - 1, A.lr, A.adam_c);
+            A.Z[e] = prm;
+            A.Zm[e] = mm;
+            A.Zv[e] = vv;
+          }
+          __syncwarp();
+          if (lane == 0) A.Zlast[id] = (int32_t)(A.step - 1);
+        }
+      }
+    }
+    __syncthreads();
   }
 }
 
@@ -374,14 +416,14 @@ __global__ void __launch_bounds__(TR_NT) k_train_dec(const __grid_constant__ Tra
   }
   __syncthreads();
 
-  // ---- forward: pre[p][j] = [x z] . W1b[j][0:3+m] + b1[j]; thread = (j, 16 points)
+  // ---- forward: pre[p][j] = [x z] . W1b[j][0:3+m] + b1[j]; thread = (j, TR_PH points)
   const int j = t & (TR_HMAX - 1);
   const int half = t >> 7;
   if (j < h) {
     double w[36];
 #pragma unroll
     for (int k = 0; k < 36; ++k) w[k] = sW1[j * W1S + k];
-    for (int q0 = half * 16; q0 < half * 16 + 16; q0 += 4) {
+    for (int q0 = half * TR_PH; q0 < half * TR_PH + TR_PH; q0 += 4) {
       double s[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
       for (int k = 0; k < 35; ++k)
@@ -396,8 +438,8 @@ __global__ void __launch_bounds__(TR_NT) k_train_dec(const __grid_constant__ Tra
   }
   __syncthreads();
 
-  // ---- output, residual, dout (warp: 4 points)
-  for (int q = warp * 4; q < warp * 4 + 4; ++q) {
+  // ---- output, residual, dout (warp: TR_PW points)
+  for (int q = warp * TR_PW; q < warp * TR_PW + TR_PW; ++q) {
     double part = 0.0;
     for (int jj = lane; jj < h; jj += 32) {
       const double pr = sPre[q * TR_HMAX + jj];
@@ -429,7 +471,7 @@ __global__ void __launch_bounds__(TR_NT) k_train_dec(const __grid_constant__ Tra
   // ---- dpre = where(pre > 0, dout * W2, 0) (field.py:381-383)
   if (j < h) {
     const double w2 = sW2[j];
-    for (int q = half * 16; q < half * 16 + 16; ++q) {
+    for (int q = half * TR_PH; q < half * TR_PH + TR_PH; ++q) {
       const double pr = sPre[q * TR_HMAX + j];
       sDpre[q * TR_HMAX + j] = (sDec[q] && pr > 0.0) ? dmul(sDout[q], w2) : 0.0;
     }
@@ -447,18 +489,20 @@ __global__ void __launch_bounds__(TR_NT) k_train_dec(const __grid_constant__ Tra
     return;
   }
 
-  // ---- dz = (dpre @ W1)[:, 3:] (field.py:386-387): thread = (channel, 4 points)
+  // ---- dz = (dpre @ W1)[:, 3:] (field.py:386-387): thread = (channel, TR_PW points)
   {
-    const int q0 = warp * 4;
-    double s[4] = {0.0, 0.0, 0.0, 0.0};
+    const int q0 = warp * TR_PW;
+    double s[TR_PW];
+#pragma unroll
+    for (int u = 0; u < TR_PW; ++u) s[u] = 0.0;
     if (lane < m)
       for (int jj = 0; jj < h; ++jj) {
         const double wv = sW1[jj * W1S + 3 + lane];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) s[u] = fma(sDpre[(q0 + u) * TR_HMAX + jj], wv, s[u]);
+        for (int u = 0; u < TR_PW; ++u) s[u] = fma(sDpre[(q0 + u) * TR_HMAX + jj], wv, s[u]);
       }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < TR_PW; ++u) {
       const int64_t p = p0 + q0 + u;
       if (p < A.n) A.dz[(p * A.n_dec + a) * 32 + lane] = sDec[q0 + u] ? s[u] : 0.0;
     }
@@ -506,9 +550,15 @@ __global__ void __launch_bounds__(256) k_train_dec_reduce(const __grid_constant_
       const int64_t pl = e >> 5;
       const int64_t p = pl / A.LM;
       const int l = (int)(pl % A.LM) + 1;
+      double v[TR_LM];
+#pragma unroll
+      for (int Lk = 1; Lk <= TR_LM; ++Lk)
+        v[Lk - 1] = (Lk >= l && Lk <= A.LM && ((A.active_mask >> (Lk - 1)) & 1))
+                        ? A.dz[(p * A.n_dec + level_slot(A.active_mask, Lk)) * 32 + k] : 0.0;
       double G = 0.0;
-      for (int Lk = l; Lk <= A.LM; ++Lk)
-        if ((A.active_mask >> (Lk - 1)) & 1) G = dadd(G, A.dz[(p * A.n_dec + level_slot(A.active_mask, Lk)) * 32 + k]);
+#pragma unroll
+      for (int Lk = 1; Lk <= TR_LM; ++Lk)
+        if (Lk >= l && Lk <= A.LM && ((A.active_mask >> (Lk - 1)) & 1)) G = dadd(G, v[Lk - 1]);
       A.G[e] = G;
     }
     return;
@@ -532,7 +582,14 @@ __global__ void __launch_bounds__(256) k_train_dec_reduce(const __grid_constant_
   if (blockIdx.x == 0 && threadIdx.x < 32) {
     const int lane = threadIdx.x;
     double s = 0.0;
-    for (int64_t p = lane; p < A.n; p += 32) s = dadd(s, A.sq[(int64_t)a * A.n + p]);
+    for (int64_t p0 = lane; p0 < A.n; p0 += 128) {
+      double v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = p0 + 32 * u < A.n ? A.sq[(int64_t)a * A.n + p0 + 32 * u] : 0.0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (p0 + 32 * u < A.n) s = dadd(s, v[u]);
+    }
 #pragma unroll
     for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
     if (lane == 0) {
@@ -682,7 +739,25 @@ __global__ void k_adam_apply(double* p, double* m, double* v, const double* g, i
 
 static int highest_level(int mask) { return 32 - __builtin_clz((unsigned)mask); }
 
+// Debug (NG_TRAIN_EVENTS=1): per-kernel device time from CUDA events around
+// each launch (one host sync per batch), read with ng_train_profile.
+static double g_phase_ms[8];
+static int64_t g_phase_batches = 0;
+
 static int launch_batch(const ng_octree* tree, TrainArgs& A, cudaStream_t s) {
+  static int ev_env = -1;
+  static cudaEvent_t ev[8];
+  if (ev_env < 0) {
+    const char* e = getenv("NG_TRAIN_EVENTS");
+    ev_env = (e && e[0] == '1') ? 1 : 0;
+    if (ev_env)
+      for (int k = 0; k < 8; ++k) cudaEventCreate(&ev[k]);
+  }
+  int nev = 0;
+  auto mark = [&]() {
+    if (ev_env) cudaEventRecord(ev[nev++], s);
+  };
+  mark();
   int r = cuda_status(cudaMemsetAsync(A.ctr, 0, 4 * sizeof(int64_t) + 32 * sizeof(int32_t), s), "train memset");
   if (r) return r;
   static bool attr = false;
@@ -696,23 +771,38 @@ static int launch_batch(const ng_octree* tree, TrainArgs& A, cudaStream_t s) {
   const int row_blocks = tr_grid(A.max_rows * 32, 256) < cap_blocks ? tr_grid(A.max_rows * 32, 256) : cap_blocks;
   k_train_locate<<<tr_grid(A.n * 32, 256), 256, 0, s>>>(*tree, A);
   NG_CHECK_LAUNCH("k_train_locate");
+  mark();
   if (A.mode != 2) {
     k_train_rowprep<<<row_blocks, 256, 0, s>>>(A);
     NG_CHECK_LAUNCH("k_train_rowprep");
+    mark();
   }
   k_train_gather<<<tr_grid(A.n * 32, 256), 256, 0, s>>>(A);
   NG_CHECK_LAUNCH("k_train_gather");
+  mark();
   // grid.y = n_act decoder slots, plus one row of record-placement blocks
   const int fill_rows = A.mode == 2 ? 0 : 1;
   k_train_dec<<<dim3((unsigned)A.groups, A.n_act + fill_rows), TR_NT, dec_smem_bytes(), s>>>(A);
   NG_CHECK_LAUNCH("k_train_dec");
+  mark();
   if (A.mode == 2) return NG_OK;
   const int64_t used = (int64_t)A.h * 36 + A.h + 1;
   k_train_dec_reduce<<<dim3(tr_grid(used, 256), A.n_act + 1), 256, 0, s>>>(A);
   NG_CHECK_LAUNCH("k_train_dec_reduce");
+  mark();
   const int dec_blocks = (A.mode == 0 && A.update_decoders) ? tr_grid(used * A.n_act, 256) : 0;
   k_train_update<<<row_blocks + dec_blocks, 256, 0, s>>>(A, row_blocks);
   NG_CHECK_LAUNCH("k_train_update");
+  mark();
+  if (ev_env && nev == 7) {
+    cudaEventSynchronize(ev[6]);
+    for (int k = 0; k < 6; ++k) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ev[k], ev[k + 1]);
+      g_phase_ms[k] += ms;
+    }
+    ++g_phase_batches;
+  }
   return NG_OK;
 }
 
@@ -897,6 +987,17 @@ int ng_train_export(const ng_octree* tree, const ng_train_params* P, int32_t lev
     return r;
   return cuda_status(cudaMemcpyAsync(weights, b + Ly.rec_w, sizeof(double) * n * level * 8,
                                      cudaMemcpyDeviceToDevice, s), "export weights");
+}
+
+/* Debug (NG_TRAIN_EVENTS=1): mean device ms per batch of each training
+ * kernel (locate, rowprep, gather, dec, reduce, update) since the last call; resets. */
+int ng_train_profile(double* host_out6) {
+  for (int k = 0; k < 6; ++k) {
+    host_out6[k] = g_phase_batches ? g_phase_ms[k] / (double)g_phase_batches : 0.0;
+    g_phase_ms[k] = 0.0;
+  }
+  g_phase_batches = 0;
+  return NG_OK;
 }
 
 int ng_adam_step(double* param, double* m, double* v, const double* grad, int64_t n, double lr, double c1,

@@ -30,11 +30,10 @@ sums = tr.level_sums.cpu().numpy() / npts
 print(json.dumps({"batch": bs, "points": npts, "epoch_ms": times, "Mpts_per_s": npts / (min(times) * 1e3),
                   "us_per_batch": min(times) * 1e3 / ((npts + bs - 1) // bs), "losses": sums.tolist(),
                   "status": int(tr.status.item()), "corners": svo.corner_count}))
-if os.environ.get("NG_TRAIN_PROFILE") == "1":
+if os.environ.get("NG_TRAIN_EVENTS") == "1":
     import ctypes
     from paper_2101_10994_b200 import _lib
-    buf = (ctypes.c_ulonglong * 8)()
+    buf = (ctypes.c_double * 6)()
     _lib.lib().ng_train_profile(buf)
-    nb = 5 * ((npts + bs - 1) // bs)  # warm + 3 timed + ... epochs run so far
-    names = ["locate", "rowprep", "gather", "dec+fill", "reduce", "update", "flush"]
-    print(json.dumps({k: round(buf[i] / nb / 1e3, 2) for i, k in enumerate(names)}), "us per batch (approx)")
+    names = ["locate", "rowprep", "gather", "dec", "reduce", "update"]
+    print(json.dumps({k: round(buf[i] * 1e3, 2) for i, k in enumerate(names)}), "us per batch (events, synced)")
