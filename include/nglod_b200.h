@@ -343,6 +343,11 @@ int ng_trace_sdf(int32_t kind, const double* params, int32_t n_params, const dou
  * separation (n,). */
 int ng_nearest_voxel(const ng_octree* tree, int32_t level, const double* pts, int64_t n, double* anchor, double* gap,
                      void* stream);
+/* sample_surface_sdf's tracer (sampling.py:109-149) for a built-in SDF: the
+ * surface point of each ray, NaN where the ray found none. */
+int ng_surface_trace(int32_t kind, const double* params, int32_t n_params, const double* origins,
+                     const double* dirs, int64_t n, double tol, double t_max, int32_t max_iters,
+                     int32_t bisect_iters, double* points, void* stream);
 /* Distance from each query to its nearest point (PointGrid.nearest_dist, metrics.py:64-112). */
 int ng_nn_dist(const double* queries, int64_t nq, const double* points, int64_t np_, double* out, void* stream);
 

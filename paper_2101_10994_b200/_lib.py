@@ -179,6 +179,8 @@ _SIGS = {
                                P]),
     "ng_nearest_voxel": (C.c_int, [P, C.c_int32, P, C.c_int64, P, P, P]),
     "ng_nn_dist": (C.c_int, [P, C.c_int64, P, C.c_int64, P, P]),
+    "ng_surface_trace": (C.c_int, [C.c_int32, P, C.c_int32, P, P, C.c_int64, C.c_double, C.c_double, C.c_int32,
+                                   C.c_int32, P, P]),
     "ng_adam_step": (C.c_int, [P, P, P, P, C.c_int64, C.c_double, C.c_double, C.c_double, P, P]),
 }
 

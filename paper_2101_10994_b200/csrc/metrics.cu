@@ -167,3 +167,72 @@ int ng_nn_dist(const double* queries, int64_t nq, const double* points, int64_t 
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------- epoch sampler
+// _trace_to_surface (sampling.py:109-139) and _bisect_crossing (142-149) for
+// a built-in SDF, one thread per ray, numpy's operation order: rays that
+// start inside trace the negated field; a sign change between steps is
+// refined by bisection. Writes the surface point (or NaN) per ray; the host
+// keeps the hits in ray order.
+namespace ng {
+__global__ void k_surface_trace(int kind, const double* __restrict__ prm, int np_, const double* __restrict__ o,
+                                const double* __restrict__ d, int64_t n, double tol, double t_max, int max_iters,
+                                int bisect_iters, double* __restrict__ pts) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double ox = o[3 * i], oy = o[3 * i + 1], oz = o[3 * i + 2];
+  const double dx = d[3 * i], dy = d[3 * i + 1], dz = d[3 * i + 2];
+  auto f_at = [&](double t) {
+    return sdf_builtin(kind, prm, np_, dadd(ox, dmul(t, dx)), dadd(oy, dmul(t, dy)), dadd(oz, dmul(t, dz)));
+  };
+  const double f0 = sdf_builtin(kind, prm, np_, ox, oy, oz);
+  const double side = f0 < 0.0 ? -1.0 : 1.0;
+  double t = 0.0, f_prev = dmul(side, f0), t_prev = 0.0;
+  double hit_t = NAN;
+  if (!(fabs(f0) >= tol)) {
+    hit_t = 0.0;
+  } else {
+    for (int it = 0; it < max_iters; ++it) {
+      t = dadd(t, f_prev);
+      const bool over = t > t_max;
+      const double f = dmul(side, f_at(t));
+      const bool done = (fabs(f) < tol) && !over;
+      if (done) {
+        hit_t = t;
+        break;
+      }
+      if (f < 0.0 && !over) {  // crossed: bisect between the last two steps
+        double lo = t_prev, hi = t;
+        for (int b = 0; b < bisect_iters; ++b) {
+          const double mid = dmul(0.5, dadd(lo, hi));
+          const bool hs = dmul(side, f_at(mid)) < 0.0;
+          hi = hs ? mid : hi;
+          lo = hs ? lo : mid;
+        }
+        hit_t = dmul(0.5, dadd(lo, hi));
+        break;
+      }
+      if (over) break;
+      f_prev = f;
+      t_prev = t;
+    }
+  }
+  pts[3 * i] = dadd(ox, dmul(hit_t, dx));
+  pts[3 * i + 1] = dadd(oy, dmul(hit_t, dy));
+  pts[3 * i + 2] = dadd(oz, dmul(hit_t, dz));
+}
+}  // namespace ng
+
+extern "C" int ng_surface_trace(int32_t kind, const double* params, int32_t n_params, const double* origins,
+                                const double* dirs, int64_t n, double tol, double t_max, int32_t max_iters,
+                                int32_t bisect_iters, double* points, void* stream) {
+  if (kind < 1 || kind > 3) {
+    ng::set_error("unknown built-in sdf kind %d", kind);
+    return NG_ERR_CONFIG;
+  }
+  if (n <= 0) return NG_OK;
+  ng::k_surface_trace<<<(int)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
+      kind, params, n_params, origins, dirs, n, tol, t_max, max_iters, bisect_iters, points);
+  NG_CHECK_LAUNCH("ng_surface_trace");
+  return NG_OK;
+}

@@ -282,3 +282,14 @@ def test_model_file_bytes_and_truncation(ng, scenes, golden, tmp_path):
     bad.write_bytes(g["model_bytes"].tobytes()[:-3])
     with pytest.raises(ng.FormatError):
         ng.load_model(bad)
+
+
+def test_device_epoch_sampler_golden(ng, scenes, golden):
+    """The GPU surface tracer + device SDF give the reference's epoch set
+    (sampling.py:177-196) for the sphere, bit for bit."""
+    from paper_2101_10994_b200 import sampling
+    g = golden("train")
+    ss = sampling.build_epoch_set(scenes.Sphere(0.5), 600, 10)
+    np.testing.assert_array_equal(ss.points, g["ep_points"])
+    np.testing.assert_array_equal(ss.distances, g["ep_dist"])
+    np.testing.assert_array_equal(ss.scheme_tags, g["ep_tags"])
