@@ -378,6 +378,8 @@ def octree_from_levels(r0: int, max_level: int, codes: list, parents: list, corn
     finest level (modelio.py:95-98)."""
     if len(codes) != max_level + 1:
         raise StructuralError("one code array per stored level is required")
+    if (r0 << max_level) > _MAX_RES:
+        raise StructuralError(f"finest resolution {r0 << max_level} above the device bitmap limit {_MAX_RES}")
     dev = _dev()
     st = stream_ptr()
     nv = int(math.log2(r0))
