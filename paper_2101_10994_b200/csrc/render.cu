@@ -271,6 +271,12 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_cons
   c.out_mask = A.out_mask;
   const int lane = (int)lane_id();
   const int64_t n_work = A.d_n_work ? (int64_t)*A.d_n_work : A.n_work;
+  // Spread light loads over every warp: with fewer rays than lanes, each
+  // warp marches at most `cap` rays at a time, so a step gathers fewer
+  // points per warp (fewer dependent load rounds) and all SMs take part.
+  const int64_t warps_total = (int64_t)gridDim.x * NW;
+  const int64_t per_warp = (n_work + warps_total - 1) / warps_total;
+  const int cap = per_warp >= 32 ? 32 : (per_warp < 1 ? 1 : (int)per_warp);
   const int tl = A.cfg.trace_level + tree.n_virtual;
   const int res = tree.r0 << A.cfg.trace_level;
   const double edge = 2.0 / (double)res;
@@ -305,7 +311,7 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_cons
 #endif
     // ---- acquire rays and advance each to its next query point (render.py:200-238)
     while (true) {
-      const bool want = (ray < 0) && !drained;
+      const bool want = (ray < 0) && !drained && lane < cap;
       const unsigned wm = __ballot_sync(FULL, want);
       if (wm) {
         const int leader = __ffs(wm) - 1;
@@ -358,7 +364,7 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_cons
         if (dead) finish(false, 0.0);
         else ready = true;
       }
-      if (!__any_sync(FULL, ray < 0 && !drained)) break;
+      if (!__any_sync(FULL, ray < 0 && !drained && lane < cap)) break;
     }
     const bool act = ray >= 0;
     if constexpr (TC) {
@@ -536,13 +542,20 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_normals(const __grid_co
   const double eps = A.cfg.normal_eps;
   LaneCounters lc;
   // work units: 32 points per warp (SIMT) or 128 per 4-warp group (TC)
-  constexpr int UNIT = TC ? 128 : 32;
+  // work units: PPW points per warp, 4 warps per unit (TC) or one (SIMT).
+  // PPW = 32 at full load; light loads are spread over every warp so each
+  // evaluation gathers fewer points per warp (fewer dependent load rounds).
+  constexpr int WPU = TC ? 4 : 1;
   constexpr int PER_CTA = TC ? NW / 4 : NW;
   const int my = TC ? w / 4 : w;
-  const int64_t n_units = (n + UNIT - 1) / UNIT;
-  for (int64_t u = (int64_t)blockIdx.x * PER_CTA + my; u < n_units; u += (int64_t)gridDim.x * PER_CTA) {
-    const int64_t i = u * UNIT + (TC ? 32 * (w % 4) : 0) + lane_id();
-    const bool act = i < n;
+  const int64_t units_total = (int64_t)gridDim.x * PER_CTA;
+  const int64_t per_warp = (n + units_total * WPU - 1) / (units_total * WPU);
+  const int ppw = per_warp >= 32 ? 32 : (per_warp < 1 ? 1 : (int)per_warp);
+  const int64_t unit = (int64_t)WPU * ppw;
+  const int64_t n_units = (n + unit - 1) / unit;
+  for (int64_t u = (int64_t)blockIdx.x * PER_CTA + my; u < n_units; u += units_total) {
+    const int64_t i = u * unit + (TC ? (int64_t)ppw * (w % 4) : 0) + lane_id();
+    const bool act = (int)lane_id() < ppw && i < n;
     int64_t dst = i;
     double p[3] = {0.0, 0.0, 0.0};
     if (act) {
