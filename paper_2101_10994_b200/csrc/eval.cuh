@@ -126,7 +126,7 @@ struct SimtMlp {
 // (ascending) the decoder policy `mlp` turns the lane's z_L into a value and
 // `emit(L, value_f32, nonfinite, lane)` is called warp-uniformly; lanes
 // decide what to do with it.
-template <class Mlp, class Emit>
+template <int GB = NG_GATHER_BATCH, class Mlp, class Emit>
 __device__ __forceinline__ EvalLane warp_eval(const ng_octree& tree, const EvalCtx& c, WarpScratch& ws,
                                               bool act, const double x[3], const Mlp& mlp, Emit&& emit) {
   const int lane = (int)lane_id();
@@ -243,15 +243,15 @@ __device__ __forceinline__ EvalLane warp_eval(const ng_octree& tree, const EvalC
     // masked out of the accumulation
     const float* __restrict__ Zc = c.Z + lane;
     while (pm) {
-      int pp[NG_GATHER_BATCH];
+      int pp[GB];
 #pragma unroll
-      for (int q = 0; q < NG_GATHER_BATCH; ++q) {
+      for (int q = 0; q < GB; ++q) {
         pp[q] = pm ? __ffs(pm) - 1 : -1;
         pm &= pm ? pm - 1 : 0u;
       }
-      float v[NG_GATHER_BATCH][8];
+      float v[GB][8];
 #pragma unroll
-      for (int q = 0; q < NG_GATHER_BATCH; ++q) {
+      for (int q = 0; q < GB; ++q) {
         const int p = pp[q] >= 0 ? pp[q] : pp[0];
         const int4 a = ws.ids[p][0], b = ws.ids[p][1];
         v[q][0] = __ldg(Zc + 32 * (int64_t)a.x);
@@ -264,7 +264,7 @@ __device__ __forceinline__ EvalLane warp_eval(const ng_octree& tree, const EvalC
         v[q][7] = __ldg(Zc + 32 * (int64_t)b.w);
       }
 #pragma unroll
-      for (int q = 0; q < NG_GATHER_BATCH; ++q) {
+      for (int q = 0; q < GB; ++q) {
         if (pp[q] < 0) continue;
         const float4 u0 = ws.w[pp[q]][0], u1 = ws.w[pp[q]][1];
         float acc = u0.x * v[q][0];

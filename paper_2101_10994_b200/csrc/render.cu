@@ -180,6 +180,7 @@ struct MarchArgs {
   // fused normals (render.py:277-300): after a hit the lane evaluates its
   // 6 central-difference probes in the same persistent loop, then shades
   int fuse_normals;
+  int lane_cap;                  // max rays a warp marches at once (NG_MARCH_CAP, default 32)
   double* normal;
   uint8_t* normal_ok;
   uint8_t* color;                // null: shading happens later (shadow pass)
@@ -276,7 +277,8 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_cons
   // points per warp (fewer dependent load rounds) and all SMs take part.
   const int64_t warps_total = (int64_t)gridDim.x * NW;
   const int64_t per_warp = (n_work + warps_total - 1) / warps_total;
-  const int cap = per_warp >= 32 ? 32 : (per_warp < 1 ? 1 : (int)per_warp);
+  int cap = per_warp >= 32 ? 32 : (per_warp < 1 ? 1 : (int)per_warp);
+  if (A.lane_cap > 0 && cap > A.lane_cap) cap = A.lane_cap;
   const int tl = A.cfg.trace_level + tree.n_virtual;
   const int res = tree.r0 << A.cfg.trace_level;
   const double edge = 2.0 / (double)res;
@@ -517,6 +519,13 @@ struct NormalArgs {
   ng_counters* counters;
 };
 
+// Corner rows in flight per gather round in k_normals. The 6 probes of a
+// unit are evaluated one after another, so their latency is on the frame's
+// critical path; 8 points per round (64 loads per warp) halves the rounds.
+#ifndef NORMALS_GATHER_BATCH
+#define NORMALS_GATHER_BATCH 8
+#endif
+
 // normals (render.py:277-300) + shade (render.py:303-314) for hit pixels.
 template <int NW, bool TC>
 __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_normals(const __grid_constant__ ng_octree tree, ng_field f,
@@ -595,8 +604,8 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_normals(const __grid_co
         if (L == A.blend_base) fv.lo = v; else fv.hi = v;
       };
       EvalLane er;
-      if constexpr (TC) er = warp_eval(tree, c, ws, act, x, tcm, emit);
-      else er = warp_eval(tree, c, ws, act, x, SimtMlp{c}, emit);
+      if constexpr (TC) er = warp_eval<NORMALS_GATHER_BATCH>(tree, c, ws, act, x, tcm, emit);
+      else er = warp_eval<NORMALS_GATHER_BATCH>(tree, c, ws, act, x, SimtMlp{c}, emit);
       double v = 0.0;
       if (act) {
         if (!er.inside) {
@@ -847,6 +856,12 @@ static int launch_eval_kernel(KS ksimt, K1 k1, K2 k2, K3 k3, K4 k4, const ng_fie
 }
 
 static int launch_march(const ng_octree& tree, const ng_field& f, MarchArgs& A, cudaStream_t s) {
+  static int cap_env = -1;
+  if (cap_env < 0) {
+    const char* e = getenv("NG_MARCH_CAP");
+    cap_env = e ? atoi(e) : 32;
+  }
+  A.lane_cap = cap_env;
   return launch_eval_kernel(k_march<R_NW, false>, k_march<4, true>, k_march<8, true>, k_march<12, true>,
                             k_march<16, true>, f, tree, A, 0, false, "k_march", s);
 }
