@@ -498,8 +498,10 @@ def _voxel_counts(svo):
 
 
 def _launches_per_frame(svo):
-    # camera rays, hit-filtered traversal passes, segments, march, normals, stats
-    return 1 + (MAX_LEVEL + svo.device.n_virtual) + 1 + 1 + 1 + 1
+    # camera rays, one hit-filtered traversal pass per level, segments, the
+    # longest-first order (histogram + scatter), march, normals, stats
+    # (cf. profiles/r01_final/launch_shares.md)
+    return 1 + (MAX_LEVEL + svo.device.n_virtual) + 1 + 2 + 1 + 1 + 1
 
 
 def _peak_hbm():
