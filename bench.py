@@ -251,6 +251,19 @@ def run_ours(args, rank: int, world: int):
         "total_evals": evals_all, "visible": visible_all, "clocks": clocks.summary(),
         "pairs": [int(st.pairs[i]) for i in range(n_levels + 1)], "active_rays": int(st.active_rays),
     }
+    # presummed feature tables: built once per field and (level, output levels),
+    # outside the per-frame work; their one-off cost is reported here
+    dfield = fld.device
+    if dfield.presum is not None:
+        key = dfield._presum_key
+        dfield._presum_key = None
+        p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        p0.record()
+        dfield.ensure_presum(svo, *key)
+        p1.record()
+        torch.cuda.synchronize()
+        res["presum"] = {"level": key[0], "out_mask": key[1], "build_ms": p0.elapsed_time(p1),
+                         "table_bytes": int(dfield.presum.numel() * 4)}
 
     # ---- end to end through the public API: host camera in, colour image out
     e2e_steps = max(3, min(args.steps, 20))
@@ -451,7 +464,11 @@ def main():
     ms = res["ms_per_step"]
     fps = 1000.0 / ms  # one full 1280x720 frame per step, split across the ranks
     march = statistics.median(res["march_ms"])
-    bytes_per_eval = EVAL_BYTES_BASE + EVAL_BYTES_PER_LEVEL * MAX_LEVEL
+    # with the presummed tables (csrc/presum.cu) an evaluation reads one
+    # level's node, corner ids and 8 table rows per output level; without
+    # them, every level 1..L
+    levels_read = 1 if res.get("presum") else MAX_LEVEL
+    bytes_per_eval = EVAL_BYTES_BASE + EVAL_BYTES_PER_LEVEL * levels_read
     algo_bytes = res["trace_evals"] * bytes_per_eval
     peak = _peak_hbm()
     achieved = algo_bytes / (march * 1e-3) / 1e9
@@ -479,8 +496,10 @@ def main():
                      "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic,
                      "algorithmic_bytes": algo_bytes,
-                     "note": f"{bytes_per_eval} B per eval x trace evals (SURVEY.md 8d); peak = measured hbm_gbs"},
+                     "note": f"{bytes_per_eval} B per eval x trace evals ({levels_read} level(s) read per eval: "
+                             "presummed S_L rows (SURVEY.md 8d per-level bytes)); peak = measured hbm_gbs"},
         "clocks": res["clocks"],
+        "presum": res.get("presum"),
     }
     if "query" in res:
         line["query"] = res["query"]

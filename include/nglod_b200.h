@@ -74,6 +74,15 @@ typedef struct ng_field {
   int32_t n_decoders;
   int32_t dec_stride;
   int64_t corner_count;
+  /* Optional presummed feature tables for the sphere tracer (ng_field_presum):
+   * S_L on the level-`presum_level` corner ids for each L in presum_mask
+   * (ascending), (n, presum_corners, 32) fp32. Used by the march / normals
+   * when their gather level and output levels match; NULL disables. */
+  const float* presum;
+  int64_t presum_offset;   /* first corner id of the level */
+  int64_t presum_corners;  /* corners of the level */
+  int32_t presum_level;
+  int32_t presum_mask;
 } ng_field;
 
 /* EvalCounter (field.py:79-90) plus a non-finite-input tally; device int64. */
@@ -331,6 +340,13 @@ int ng_march_profile(unsigned long long* host_out, int max_groups);
 /* Hit positions o + t*d for hit rays (FrameBuffer.points, render.py:395-396). */
 int ng_hit_points(const ng_ray* rays, const uint8_t* hit, const double* t, int64_t n,
                   double* points, void* stream);
+
+/* Presummed feature tables: S_L(c) = sum_{l <= L} psi_l(c) at every level-`level`
+ * corner c, for each L in out_mask (ascending), fp32 (n_out, n_corners, 32).
+ * Exact reassociation of sum_features (field.py:154-169) for points inside a
+ * level-`level` voxel (see presum.cu). owner_scratch: n_corners int32. */
+int ng_field_presum(const ng_octree* tree, const float* Z, int32_t level, int32_t out_mask, int64_t offset,
+                    int64_t n_corners, float* S, int32_t* owner_scratch, void* stream);
 
 /* ---- evaluation (metrics.py) ------------------------ */
 /* trace_oracle_rays (metrics.py:145-178) for a built-in SDF (kinds as in

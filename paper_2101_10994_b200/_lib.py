@@ -63,6 +63,8 @@ class NgField(C.Structure):
     _fields_ = [
         ("Z", P), ("decoders", P), ("m", C.c_int32), ("h", C.c_int32),
         ("n_decoders", C.c_int32), ("dec_stride", C.c_int32), ("corner_count", C.c_int64),
+        ("presum", P), ("presum_offset", C.c_int64), ("presum_corners", C.c_int64), ("presum_level", C.c_int32),
+        ("presum_mask", C.c_int32),
     ]
 
 
@@ -175,6 +177,7 @@ _SIGS = {
     "ng_train_flush": (C.c_int, [P, C.c_int64, P, C.c_double, P]),
     "ng_train_profile": (C.c_int, [P]),
     "ng_train_export": (C.c_int, [P, P, C.c_int32, P, C.c_int64, P, C.c_size_t, P, P, P, P, P, P]),
+    "ng_field_presum": (C.c_int, [P, P, C.c_int32, C.c_int32, C.c_int64, C.c_int64, P, P, P]),
     "ng_trace_sdf": (C.c_int, [C.c_int32, P, C.c_int32, P, P, C.c_int64, C.c_double, C.c_double, C.c_int32, P, P,
                                P]),
     "ng_nearest_voxel": (C.c_int, [P, C.c_int32, P, C.c_int64, P, P, P]),

@@ -39,6 +39,11 @@ struct EvalCtx {
   int inside_level;                  // -1 or query_field level
   int out_mask;                      // decoder levels evaluated (bit L-1)
   unsigned long long* dbg = nullptr; // debug (lane 0): ns in prologue, staging, gather, decoder
+  // presummed tables (presum.cu): S_L on the gather level's corner ids, one
+  // (corners, 32) block per output level; only valid with inside_level == G
+  const float* __restrict__ presum = nullptr;
+  int64_t presum_offset = 0;
+  int64_t presum_corners = 0;
 };
 
 __device__ __forceinline__ unsigned long long dbg_now() {
@@ -290,6 +295,113 @@ __device__ __forceinline__ EvalLane warp_eval(const ng_octree& tree, const EvalC
     idx_cur = idx_nxt;
     ca = na;
     cb = nb;
+  }
+  __syncwarp();
+  return res;
+}
+
+// warp_eval for points that are decoded only inside a level-G voxel
+// (query_field with inside_level == G: the march and the normal probes).
+// Every ancestor of the voxel exists, so all levels 1..G are present and
+// z_L = sum_j w_j^G S_L[c_j] (presum.cu): one voxel lookup and 8 corner rows
+// per output level instead of a lookup and 8 rows per level 1..L.
+template <int GB = NG_GATHER_BATCH, class Mlp, class Emit>
+__device__ __forceinline__ EvalLane warp_eval_presum(const ng_octree& tree, const EvalCtx& c, WarpScratch& ws,
+                                                     bool act, const double x[3], const Mlp& mlp, Emit&& emit) {
+  const int lane = (int)lane_id();
+  EvalLane res;
+  res.present = 0;
+  res.inside = true;
+  const int G = c.gather_level;
+  const int resG = tree.r0 << G;
+  const int tl = G + tree.n_virtual;
+  int cell[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) cell[a] = bin_axis(x[a], resG);
+  int64_t idx = -1;
+  int4 ia = make_int4(0, 0, 0, 0), ib = ia;
+  if (act) {
+    idx = rank_lookup(tree.bitmap[tl], tree.rank[tl], morton(cell[0], cell[1], cell[2]));
+    res.inside = idx >= 0;  // query_field's inside test at the trace level (render.py:159-166)
+    if (idx >= 0) {
+      const int4* cr = reinterpret_cast<const int4*>(tree.corners[tl] + 8 * idx);
+      ia = __ldg(cr);
+      ib = __ldg(cr + 1);
+    }
+  }
+  const bool pres = act && idx >= 0;
+  float4 wa = make_float4(0.f, 0.f, 0.f, 0.f), wb = wa;
+  if (pres) {
+    res.present = (G >= 32) ? 0xffffffffu : ((1u << G) - 1u);
+    const double half = 0.5 * (double)resG;
+    float u[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      double f = dsub(dmul(dadd(x[a], 1.0), half), (double)cell[a]);
+      f = f < 0.0 ? 0.0 : (f > 1.0 ? 1.0 : f);
+      u[a] = (float)f;
+    }
+    const float wx0 = 1.f - u[0], wy0 = 1.f - u[1], wz0 = 1.f - u[2];
+    wa = make_float4(wx0 * wy0 * wz0, u[0] * wy0 * wz0, wx0 * u[1] * wz0, u[0] * u[1] * wz0);
+    wb = make_float4(wx0 * wy0 * u[2], u[0] * wy0 * u[2], wx0 * u[1] * u[2], u[0] * u[1] * u[2]);
+    const int off = (int)c.presum_offset;
+    ia = make_int4(ia.x - off, ia.y - off, ia.z - off, ia.w - off);
+    ib = make_int4(ib.x - off, ib.y - off, ib.z - off, ib.w - off);
+  }
+  ws.ids[lane][0] = ia;
+  ws.ids[lane][1] = ib;
+  ws.w[lane][0] = wa;
+  ws.w[lane][1] = wb;
+  const unsigned pm0 = __ballot_sync(FULL, pres);
+  const float xf[3] = {(float)x[0], (float)x[1], (float)x[2]};
+  __syncwarp();
+  int slot = 0;
+  for (int L = 1; L <= G; ++L) {
+    if (!((c.out_mask >> (L - 1)) & 1)) continue;
+    const float* __restrict__ Sc = c.presum + (int64_t)slot * c.presum_corners * 32 + lane;
+    ++slot;
+    unsigned pm = pm0;
+    while (pm) {
+      int pp[GB];
+#pragma unroll
+      for (int q = 0; q < GB; ++q) {
+        pp[q] = pm ? __ffs(pm) - 1 : -1;
+        pm &= pm ? pm - 1 : 0u;
+      }
+      float v[GB][8];
+#pragma unroll
+      for (int q = 0; q < GB; ++q) {
+        const int p = pp[q] >= 0 ? pp[q] : pp[0];
+        const int4 a = ws.ids[p][0], b = ws.ids[p][1];
+        v[q][0] = __ldg(Sc + 32 * (int64_t)a.x);
+        v[q][1] = __ldg(Sc + 32 * (int64_t)a.y);
+        v[q][2] = __ldg(Sc + 32 * (int64_t)a.z);
+        v[q][3] = __ldg(Sc + 32 * (int64_t)a.w);
+        v[q][4] = __ldg(Sc + 32 * (int64_t)b.x);
+        v[q][5] = __ldg(Sc + 32 * (int64_t)b.y);
+        v[q][6] = __ldg(Sc + 32 * (int64_t)b.z);
+        v[q][7] = __ldg(Sc + 32 * (int64_t)b.w);
+      }
+#pragma unroll
+      for (int q = 0; q < GB; ++q) {
+        if (pp[q] < 0) continue;
+        const float4 u0 = ws.w[pp[q]][0], u1 = ws.w[pp[q]][1];
+        float acc = u0.x * v[q][0];
+        acc = fmaf(u0.y, v[q][1], acc);
+        acc = fmaf(u0.z, v[q][2], acc);
+        acc = fmaf(u0.w, v[q][3], acc);
+        acc = fmaf(u1.x, v[q][4], acc);
+        acc = fmaf(u1.y, v[q][5], acc);
+        acc = fmaf(u1.z, v[q][6], acc);
+        acc = fmaf(u1.w, v[q][7], acc);
+        ws.zt[pp[q]][lane] = acc;
+      }
+    }
+    __syncwarp();
+    const bool any = __any_sync(FULL, pres);
+    bool bad = false;
+    const float d = mlp(L, xf, &ws.zt[lane][0], any, bad);
+    emit(L, d, bad && pres, res);
   }
   __syncwarp();
   return res;

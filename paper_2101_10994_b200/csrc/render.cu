@@ -198,6 +198,18 @@ struct FieldValue {
   double lo = 0.0, hi = 0.0;
 };
 
+// The field's presummed tables serve this evaluation when they were built
+// for its gather level and output levels and points are decoded only
+// inside gather-level voxels (presum.cu).
+__device__ __forceinline__ void use_presum(const ng_field& f, EvalCtx& c) {
+  if (f.presum && f.presum_level == c.gather_level && f.presum_mask == c.out_mask &&
+      c.inside_level == c.gather_level) {
+    c.presum = f.presum;
+    c.presum_offset = f.presum_offset;
+    c.presum_corners = f.presum_corners;
+  }
+}
+
 // query_field value (render.py:155-171) from one lane's evaluation.
 __device__ __forceinline__ double field_value(const ng_octree& tree, const EvalLane& er, double lo, double hi,
                                               double alpha, const double x[3]) {
@@ -270,6 +282,7 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_cons
   c.gather_level = A.G;
   c.inside_level = A.cfg.trace_level;
   c.out_mask = A.out_mask;
+  use_presum(f, c);
   const int lane = (int)lane_id();
   const int64_t n_work = A.d_n_work ? (int64_t)*A.d_n_work : A.n_work;
   // Spread light loads over every warp: with fewer rays than lanes, each
@@ -435,8 +448,13 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_cons
       if (L == A.blend_base) fv.lo = v; else fv.hi = v;
     };
     EvalLane er;
-    if constexpr (TC) er = warp_eval(tree, c, ws, act, x, tcm, emit);
-    else er = warp_eval(tree, c, ws, act, x, SimtMlp{c}, emit);
+    if (c.presum) {
+      if constexpr (TC) er = warp_eval_presum(tree, c, ws, act, x, tcm, emit);
+      else er = warp_eval_presum(tree, c, ws, act, x, SimtMlp{c}, emit);
+    } else {
+      if constexpr (TC) er = warp_eval(tree, c, ws, act, x, tcm, emit);
+      else er = warp_eval(tree, c, ws, act, x, SimtMlp{c}, emit);
+    }
     auto dval_of = [&](const EvalLane& e, const FieldValue& v, const double* px) {
       return field_value(tree, e, v.lo, v.hi, A.blend_alpha, px);
     };
@@ -547,6 +565,7 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_normals(const __grid_co
   c.gather_level = A.G;
   c.inside_level = A.cfg.trace_level;
   c.out_mask = A.out_mask;
+  use_presum(f, c);
   const int64_t n = A.pts ? A.n_pts : (int64_t)*A.d_hit_count;
   const double eps = A.cfg.normal_eps;
   LaneCounters lc;
@@ -604,8 +623,13 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_normals(const __grid_co
         if (L == A.blend_base) fv.lo = v; else fv.hi = v;
       };
       EvalLane er;
-      if constexpr (TC) er = warp_eval<NORMALS_GATHER_BATCH>(tree, c, ws, act, x, tcm, emit);
-      else er = warp_eval<NORMALS_GATHER_BATCH>(tree, c, ws, act, x, SimtMlp{c}, emit);
+      if (c.presum) {
+        if constexpr (TC) er = warp_eval_presum<NORMALS_GATHER_BATCH>(tree, c, ws, act, x, tcm, emit);
+        else er = warp_eval_presum<NORMALS_GATHER_BATCH>(tree, c, ws, act, x, SimtMlp{c}, emit);
+      } else {
+        if constexpr (TC) er = warp_eval<NORMALS_GATHER_BATCH>(tree, c, ws, act, x, tcm, emit);
+        else er = warp_eval<NORMALS_GATHER_BATCH>(tree, c, ws, act, x, SimtMlp{c}, emit);
+      }
       double v = 0.0;
       if (act) {
         if (!er.inside) {

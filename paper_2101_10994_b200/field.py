@@ -142,9 +142,37 @@ class DeviceField:
         s.dec_stride = decoder_stride(self.h)
         s.corner_count = self.Z.shape[0]
         self.struct = s
+        self.presum = None
+        self._presum_key = None
 
     def ref(self):
         return ctypes.byref(self.struct)
+
+    def ensure_presum(self, svo, level: int, out_mask: int) -> None:
+        """Build (once per level / output set) the presummed feature tables
+        S_L on the level's corner ids that the sphere tracer and the normal
+        probes read instead of gathering every level (csrc/presum.cu)."""
+        key = (int(level), int(out_mask))
+        if self._presum_key == key:
+            return
+        dev = self.Z.device
+        offset = int(svo.corner_offsets[level])
+        end = int(svo.corner_offsets[level + 1]) if level < svo.max_level else int(svo.corner_count)
+        n = end - offset
+        n_out = bin(out_mask).count("1")
+        S = torch.empty((n_out, max(n, 1), _lib.FEAT_PAD), dtype=torch.float32, device=dev)
+        owner = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+        call("ng_field_presum", svo.device.ref(), ptr(self.Z), int(level), int(out_mask), offset, n, ptr(S),
+             ptr(owner), stream_ptr())
+        self.presum = S
+        self._presum_owner = owner  # kept until the kernel has run
+        self._presum_key = key
+        s = self.struct
+        s.presum = ptr(S)
+        s.presum_offset = offset
+        s.presum_corners = n
+        s.presum_level = int(level)
+        s.presum_mask = int(out_mask)
 
 
 def _as_points(x):

@@ -20,7 +20,7 @@ import torch.distributed as dist
 from . import _lib
 from ._lib import call, ptr, stream_ptr
 from .errors import OctfieldError
-from .render import Camera, RenderConfig, RenderSession, band_rows_of, resolve_config, resolve_lod
+from .render import prepare_presum, Camera, RenderConfig, RenderSession, band_rows_of, resolve_config, resolve_lod
 
 DEFAULT_BAND_ROWS = 8
 
@@ -76,6 +76,7 @@ class TiledRenderer:
         """Launch this rank's bands (no host sync)."""
         cs = camera.band_struct(self.band_rows, self.world, self.rank)
         fs = self.sess.frame_struct(self.frame)
+        prepare_presum(self.fld, cfg)
         if self.local_rows:
             call("ng_render_frame", self.fld.svo.device.ref(), self.fld.device.ref(), ctypes.byref(cfg),
                  ctypes.byref(cs), ctypes.byref(fs), ctypes.byref(self.sess.ws), ptr(self.sess.stats),

@@ -10,6 +10,8 @@ statistics -- no host synchronisation until the caller reads a result.
 
 from __future__ import annotations
 
+import os
+
 import ctypes
 import math
 from dataclasses import dataclass
@@ -253,6 +255,25 @@ def resolve_config(fld: NeuralField, config: RenderConfig, lod: float, eps: floa
     return c
 
 
+_PRESUM = os.environ.get("NG_PRESUM", "1") != "0"
+
+
+def prepare_presum(fld: NeuralField, cfg: _lib.NgRenderCfg) -> None:
+    """Presummed feature tables for this frame's gather level and output
+    levels (the LodPlan of render.cu: blend levels for a fractional lod);
+    NG_PRESUM=0 keeps the level-by-level gather."""
+    if not _PRESUM:
+        return
+    lod = max(float(cfg.lod), 1.0)
+    base = int(np.floor(lod))
+    if lod - base == 0.0:
+        mask, G = 1 << (base - 1), max(base, cfg.trace_level)
+    else:
+        mask, G = (1 << (base - 1)) | (1 << base), max(base + 1, cfg.trace_level)
+    if G == cfg.trace_level:
+        fld.device.ensure_presum(fld.svo, G, mask)
+
+
 def _lod_split(lod: float):
     L = max(float(lod), 1.0)
     base = int(np.floor(L))
@@ -453,6 +474,7 @@ class RenderSession:
         """Launch one frame on the current stream. With `timed`, ev0 / ev1 /
         ev2 bracket traversal+march and normals (ev1 is recorded by the C side)."""
         fs = self.frame_struct(frame)
+        prepare_presum(self.fld, cfg)
         if timed:
             self.ev1.record()  # materialise the handle; re-recorded mid-frame
             self.ws.ev_trace_done = self.ev1.cuda_event

@@ -36,7 +36,7 @@ def test_binding_covers_header():
 def test_struct_sizes_match_header_layout():
     from paper_2101_10994_b200 import _lib
     assert ctypes.sizeof(_lib.NgOctree) == 16 + 16 * 8 + 6 * 16 * 8 + 7 * 8
-    assert ctypes.sizeof(_lib.NgField) == 40
+    assert ctypes.sizeof(_lib.NgField) == 40 + 8 + 8 + 8 + 4 + 4  # + presum table pointer, offset, corners, level, mask
     assert ctypes.sizeof(_lib.NgQueryArgs) == 24
     assert ctypes.sizeof(_lib.NgCamera) == 12 * 8 + 2 * 8 + 6 * 4
     assert ctypes.sizeof(_lib.NgFrameStats) == (17 + 2 + 4 + 1 + 17 + 1) * 8

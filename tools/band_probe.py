@@ -7,12 +7,13 @@ import bench
 import paper_2101_10994_b200 as ng
 from paper_2101_10994_b200 import _lib
 from paper_2101_10994_b200.parallel import band_layout
-from paper_2101_10994_b200.render import RenderSession, resolve_config, resolve_lod
+from paper_2101_10994_b200.render import RenderSession, prepare_presum, resolve_config, resolve_lod
 
 knot, svo, fld = bench.build_workload()
 W, H = bench.WIDTH, bench.HEIGHT
 cam = ng.Camera(bench.CAM["position"], bench.CAM["look_at"], bench.CAM["up"], bench.CAM["fov_y_deg"], W, H)
 cfg = resolve_config(fld, ng.RenderConfig(), resolve_lod(cam, fld, ng.RenderConfig()))
+prepare_presum(fld, cfg)
 flush = torch.empty(bench.L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
 out = {}
 for world in [int(w) for w in os.environ.get("WORLDS", "1,2,4,8").split(",")]:
