@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <unordered_map>
 
 namespace ng {
 
@@ -252,7 +253,7 @@ struct DecoderSetup {
   }
 };
 
-template <int NW, bool TC>
+template <int NW, bool TC, bool PS>
 __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_constant__ ng_octree tree, ng_field f,
                                                               const __grid_constant__ MarchArgs A) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -282,7 +283,7 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_cons
   c.gather_level = A.G;
   c.inside_level = A.cfg.trace_level;
   c.out_mask = A.out_mask;
-  use_presum(f, c);
+  if constexpr (PS) use_presum(f, c);
   const int lane = (int)lane_id();
   const int64_t n_work = A.d_n_work ? (int64_t)*A.d_n_work : A.n_work;
   // Spread light loads over every warp: with fewer rays than lanes, each
@@ -448,7 +449,7 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_cons
       if (L == A.blend_base) fv.lo = v; else fv.hi = v;
     };
     EvalLane er;
-    if (c.presum) {
+    if constexpr (PS) {
       if constexpr (TC) er = warp_eval_presum(tree, c, ws, act, x, tcm, emit);
       else er = warp_eval_presum(tree, c, ws, act, x, SimtMlp{c}, emit);
     } else {
@@ -545,7 +546,7 @@ struct NormalArgs {
 #endif
 
 // normals (render.py:277-300) + shade (render.py:303-314) for hit pixels.
-template <int NW, bool TC>
+template <int NW, bool TC, bool PS>
 __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_normals(const __grid_constant__ ng_octree tree, ng_field f,
                                                                 const __grid_constant__ NormalArgs A) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -565,7 +566,7 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_normals(const __grid_co
   c.gather_level = A.G;
   c.inside_level = A.cfg.trace_level;
   c.out_mask = A.out_mask;
-  use_presum(f, c);
+  if constexpr (PS) use_presum(f, c);
   const int64_t n = A.pts ? A.n_pts : (int64_t)*A.d_hit_count;
   const double eps = A.cfg.normal_eps;
   LaneCounters lc;
@@ -623,7 +624,7 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_normals(const __grid_co
         if (L == A.blend_base) fv.lo = v; else fv.hi = v;
       };
       EvalLane er;
-      if (c.presum) {
+      if constexpr (PS) {
         if constexpr (TC) er = warp_eval_presum<NORMALS_GATHER_BATCH>(tree, c, ws, act, x, tcm, emit);
         else er = warp_eval_presum<NORMALS_GATHER_BATCH>(tree, c, ws, act, x, SimtMlp{c}, emit);
       } else {
@@ -803,12 +804,15 @@ static LodPlan plan_lod(const ng_render_cfg& cfg) {
 
 template <class K>
 static int prep_kernel(K kernel, size_t smem, int nt, int& per_sm) {
-  static size_t configured = 0;
-  if (smem > configured) {
+  // dynamic shared memory limit per kernel function (instances of one
+  // template share a pointer type, so the record is keyed by address)
+  static std::unordered_map<const void*, size_t> configured;
+  size_t& have = configured[(const void*)kernel];
+  if (smem > have) {
     cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)std::max<size_t>(smem, 48 * 1024));
     if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute");
-    configured = smem;
+    have = smem;
   }
   per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, nt, smem);
@@ -879,6 +883,12 @@ static int launch_eval_kernel(KS ksimt, K1 k1, K2 k2, K3 k3, K4 k4, const ng_fie
   return NG_OK;
 }
 
+// Host mirror of use_presum: the presummed kernels are launched only when
+// the field's tables match this evaluation.
+static bool presum_applies(const ng_field& f, int G, int out_mask, int trace_level) {
+  return f.presum && f.presum_level == G && f.presum_mask == out_mask && trace_level == G;
+}
+
 static int launch_march(const ng_octree& tree, const ng_field& f, MarchArgs& A, cudaStream_t s) {
   static int cap_env = -1;
   if (cap_env < 0) {
@@ -886,13 +896,21 @@ static int launch_march(const ng_octree& tree, const ng_field& f, MarchArgs& A, 
     cap_env = e ? atoi(e) : 32;
   }
   A.lane_cap = cap_env;
-  return launch_eval_kernel(k_march<R_NW, false>, k_march<4, true>, k_march<8, true>, k_march<12, true>,
-                            k_march<16, true>, f, tree, A, 0, false, "k_march", s);
+  if (presum_applies(f, A.G, A.out_mask, A.cfg.trace_level))
+    return launch_eval_kernel(k_march<R_NW, false, true>, k_march<4, true, true>, k_march<8, true, true>,
+                              k_march<12, true, true>, k_march<16, true, true>, f, tree, A, 0, false, "k_march", s);
+  return launch_eval_kernel(k_march<R_NW, false, false>, k_march<4, true, false>, k_march<8, true, false>,
+                            k_march<12, true, false>, k_march<16, true, false>, f, tree, A, 0, false, "k_march", s);
 }
 
 static int launch_normals(const ng_octree& tree, const ng_field& f, NormalArgs& A, int64_t max_n, cudaStream_t s) {
-  return launch_eval_kernel(k_normals<R_NW, false>, k_normals<4, true>, k_normals<8, true>, k_normals<12, true>,
-                            k_normals<16, true>, f, tree, A, max_n, true, "k_normals", s);
+  if (presum_applies(f, A.G, A.out_mask, A.cfg.trace_level))
+    return launch_eval_kernel(k_normals<R_NW, false, true>, k_normals<4, true, true>, k_normals<8, true, true>,
+                              k_normals<12, true, true>, k_normals<16, true, true>, f, tree, A, max_n, true,
+                              "k_normals", s);
+  return launch_eval_kernel(k_normals<R_NW, false, false>, k_normals<4, true, false>, k_normals<8, true, false>,
+                            k_normals<12, true, false>, k_normals<16, true, false>, f, tree, A, max_n, true,
+                            "k_normals", s);
 }
 
 static void background_u8(const ng_render_cfg& cfg, uint8_t bg[3]) {
