@@ -210,9 +210,12 @@ __global__ void __launch_bounds__(TR_NT) k_traverse_hits(
             double a0, b0;
             if (((m >> oct) & 1u) && child_hit(cs, oct, a0, b0)) hm[q] |= 1u << k;
           }
+          // the emit pass needs only the direction mask and the child mask
+          // (and, for the final level, the slabs again): keep them packed
+          if (hm[q]) hm[q] |= ((unsigned)dm << 8) | (m << 16);
         }
       }
-      sum += __popc(hm[q]);
+      sum += __popc(hm[q] & 0xffu);
     }
     int64_t excl;
     const int64_t agg = block_excl_scan<TR_NT>(sum, excl, sm_warp);
@@ -225,16 +228,17 @@ __global__ void __launch_bounds__(TR_NT) k_traverse_hits(
 #pragma unroll
     for (int q = 0; q < TH_ITEMS; ++q) {
       if (!hm[q]) continue;
-      ng_ray r;
-      load_ray(rays, pr[q], r);
-      const int dm = r.flags & 7;
-      const unsigned m = __ldg(cmask + pv[q]);
+      const int dm = (int)((hm[q] >> 8) & 7u);
+      const unsigned m = (hm[q] >> 16) & 0xffu;
       const int32_t first = __ldg(cstart + pv[q]);
-      const uint64_t c = __ldg(codes + pv[q]);
-      const int px = (int)compact3(c), py = (int)compact3(c >> 1), pz = (int)compact3(c >> 2);
       ChildSlabs cs;
-      if (NEXT_FINAL) child_slabs(r, px, py, pz, cres, cs);
-      for (unsigned bits = hm[q]; bits; bits &= bits - 1) {
+      if (NEXT_FINAL) {
+        ng_ray r;
+        load_ray(rays, pr[q], r);
+        const uint64_t c = __ldg(codes + pv[q]);
+        child_slabs(r, (int)compact3(c), (int)compact3(c >> 1), (int)compact3(c >> 2), cres, cs);
+      }
+      for (unsigned bits = hm[q] & 0xffu; bits; bits &= bits - 1) {
         const int k = __ffs(bits) - 1;
         const int oct = k ^ dm;
         const int32_t child = first + __popc(m & ((1u << oct) - 1u));
