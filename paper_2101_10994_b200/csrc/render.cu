@@ -22,7 +22,8 @@ int grid_for(int64_t n, int nt);
 size_t level_scratch_bytes(int64_t max_pairs);
 int traverse_hits(const ng_octree& tree, const ng_ray* rays, int t, bool next_final, const ng_pair* in,
                   const int64_t* d_count_in, int64_t in_cap, ng_pair* out_pairs, ng_hit_pair* out_hits,
-                  int64_t* d_count_out, int64_t out_cap, void* scratch, size_t scratch_bytes, cudaStream_t s);
+                  int64_t* d_count_out, int64_t out_cap, void* scratch, size_t scratch_bytes, cudaStream_t s,
+                  int64_t* seg_start, int64_t* seg_end);
 
 constexpr int R_NW = 8;  // warps per CTA for march / normals
 
@@ -86,33 +87,6 @@ __global__ void k_frame_defaults(ng_frame fr, int64_t n, uint8_t bg0, uint8_t bg
 }
 
 // ray_segments over the final list plus the list of rays that have one.
-__global__ void k_segments_active(const ng_hit_pair* __restrict__ hits, const int64_t* __restrict__ d_count,
-                                  int64_t cap, int64_t* __restrict__ seg_start, int64_t* __restrict__ seg_end,
-                                  int32_t* __restrict__ active, unsigned long long* d_active) {
-  int64_t n = *d_count;
-  if (n > cap) n = cap;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < n; base += stride) {
-    const int64_t i = base + threadIdx.x;
-    bool first = false;
-    int32_t r = -1;
-    if (i < n) {
-      r = hits[i].ray;
-      first = (i == 0 || hits[i - 1].ray != r);
-      if (first) seg_start[r] = i;
-      if (i == n - 1 || hits[i + 1].ray != r) seg_end[r] = i + 1;
-    }
-    const unsigned m = __ballot_sync(FULL, first);
-    if (m) {
-      unsigned long long b = 0;
-      const int leader = __ffs(m) - 1;
-      if ((int)lane_id() == leader) b = atomicAdd(d_active, (unsigned long long)__popc(m));
-      b = __shfl_sync(FULL, b, leader);
-      if (first) active[b + __popc(m & lanemask_lt())] = r;
-    }
-  }
-}
-
 // Longest-first work order for the march: rays with more voxels in their
 // list (grazing / silhouette rays) take more sphere-trace steps, so they are
 // issued first and the persistent lanes do not end on a long serial tail.
@@ -129,6 +103,35 @@ __global__ void k_len_hist(const int32_t* __restrict__ active, const unsigned lo
     const int32_t r = active[k];
     const int64_t len = seg_end[r] - seg_start[r];
     atomicAdd(&h[len < LEN_BUCKETS - 1 ? len : LEN_BUCKETS - 1], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < LEN_BUCKETS; i += blockDim.x)
+    if (h[i]) atomicAdd(&hist[i], h[i]);
+}
+
+// Active rays (a non-empty segment) and their list-length histogram, one
+// thread per ray: the active list for the march and the buckets of the
+// longest-first order.
+__global__ void k_active_hist(const int64_t* __restrict__ seg_start, const int64_t* __restrict__ seg_end, int64_t n,
+                              int32_t* __restrict__ active, unsigned long long* d_active,
+                              unsigned int* __restrict__ hist) {
+  __shared__ unsigned int h[LEN_BUCKETS];
+  for (int i = threadIdx.x; i < LEN_BUCKETS; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < n; base += stride) {
+    const int64_t r = base + threadIdx.x;
+    const int64_t len = r < n ? seg_end[r] - seg_start[r] : 0;
+    const bool has = len > 0;
+    if (has) atomicAdd(&h[len < LEN_BUCKETS - 1 ? len : LEN_BUCKETS - 1], 1u);
+    const unsigned m = __ballot_sync(FULL, has);
+    if (m) {
+      unsigned long long b = 0;
+      const int leader = __ffs(m) - 1;
+      if ((int)lane_id() == leader) b = atomicAdd(d_active, (unsigned long long)__popc(m));
+      b = __shfl_sync(FULL, b, leader);
+      if (has) active[b + __popc(m & lanemask_lt())] = (int32_t)r;
+    }
   }
   __syncthreads();
   for (int i = threadIdx.x; i < LEN_BUCKETS; i += blockDim.x)
@@ -988,25 +991,24 @@ static int trace_pass(const ng_octree& tree, const ng_render_cfg& cfg, const Lod
   const int target = cfg.trace_level + tree.n_virtual;
   const ng_pair* in = nullptr;
   int64_t in_cap = n;
+  // rays without final-level pairs keep the empty segment [0, 0)
+  if ((r = cuda_status(cudaMemsetAsync(seg_start, 0, n * 8, s), "seg memset"))) return r;
+  if ((r = cuda_status(cudaMemsetAsync(seg_end, 0, n * 8, s), "seg memset"))) return r;
   for (int t = 0; t < target; ++t) {
     const bool last = (t + 1 == target);
     ng_pair* out = (t % 2 == 0) ? pa : pb;
     r = traverse_hits(tree, rays, t, last, in, &counts[t], in_cap, last ? nullptr : out, last ? hits : nullptr,
-                      &counts[t + 1], last ? ws.hit_capacity : ws.pair_capacity, scratch, L.scratch_bytes, s);
+                      &counts[t + 1], last ? ws.hit_capacity : ws.pair_capacity, scratch, L.scratch_bytes, s,
+                      last ? seg_start : nullptr, last ? seg_end : nullptr);
     if (r) return r;
     in = out;
     in_cap = ws.pair_capacity;
   }
-  if ((r = cuda_status(cudaMemsetAsync(seg_start, 0, n * 8, s), "seg memset"))) return r;
-  if ((r = cuda_status(cudaMemsetAsync(seg_end, 0, n * 8, s), "seg memset"))) return r;
-  k_segments_active<<<grid_for(std::max<int64_t>(ws.hit_capacity, 1), 256), 256, 0, s>>>(
-      hits, &counts[target], ws.hit_capacity, seg_start, seg_end, active, d_active);
-  NG_CHECK_LAUNCH("k_segments_active");
   int32_t* sorted = (int32_t*)(b + L.sorted);
   unsigned int* buckets = (unsigned int*)(b + L.buckets);
   if ((r = cuda_status(cudaMemsetAsync(buckets, 0, 2 * LEN_BUCKETS * 4, s), "bucket memset"))) return r;
-  k_len_hist<<<grid_for(n, 256), 256, 0, s>>>(active, d_active, seg_start, seg_end, buckets);
-  NG_CHECK_LAUNCH("k_len_hist");
+  k_active_hist<<<grid_for(n, 256), 256, 0, s>>>(seg_start, seg_end, n, active, d_active, buckets);
+  NG_CHECK_LAUNCH("k_active_hist");
   k_len_scatter<<<grid_for(n, 256), 256, 0, s>>>(active, d_active, seg_start, seg_end, buckets,
                                                   buckets + LEN_BUCKETS, sorted);
   NG_CHECK_LAUNCH("k_len_scatter");

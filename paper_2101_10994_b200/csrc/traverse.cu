@@ -150,7 +150,7 @@ __global__ void __launch_bounds__(TR_NT) k_traverse_hits(
     const ng_pair* __restrict__ in, const int64_t* __restrict__ d_count_in, int64_t in_cap,
     ng_pair* __restrict__ out_pairs, ng_hit_pair* __restrict__ out_hits,
     int64_t* __restrict__ d_count_out, int64_t out_cap, unsigned long long* states,
-    unsigned int* tile_counter) {
+    unsigned int* tile_counter, int64_t* __restrict__ seg_start, int64_t* __restrict__ seg_end) {
   __shared__ int64_t sm_warp[TR_NT / 32 + 1];
   __shared__ int64_t sm_tile, sm_excl;
   int64_t n = *d_count_in;
@@ -227,6 +227,20 @@ __global__ void __launch_bounds__(TR_NT) k_traverse_hits(
     int64_t o = sm_excl + excl;
 #pragma unroll
     for (int q = 0; q < TH_ITEMS; ++q) {
+      // final level: each ray's [start, end) in the hit list (ray_segments,
+      // traversal.py:250-255). A ray's pairs are contiguous in the input, so
+      // its first pair knows the start and its last pair the end.
+      if (NEXT_FINAL && seg_start != nullptr && base + q < n) {
+        const int64_t i = base + q;
+        const int32_t r = pr[q];
+        const bool first = in == nullptr || i == 0 || in[i - 1].ray != r;
+        const bool last = in == nullptr || i == n - 1 || in[i + 1].ray != r;
+        if (first) seg_start[r] = o < out_cap ? o : out_cap;
+        if (last) {
+          const int64_t e = o + __popc(hm[q] & 0xffu);
+          seg_end[r] = e < out_cap ? e : out_cap;
+        }
+      }
       if (!hm[q]) continue;
       const int dm = (int)((hm[q] >> 8) & 7u);
       const unsigned m = (hm[q] >> 16) & 0xffu;
@@ -393,7 +407,8 @@ int traverse_level(const ng_octree& tree, const ng_ray* rays, int t, bool final,
 
 int traverse_hits(const ng_octree& tree, const ng_ray* rays, int t, bool next_final, const ng_pair* in,
                   const int64_t* d_count_in, int64_t in_cap, ng_pair* out_pairs, ng_hit_pair* out_hits,
-                  int64_t* d_count_out, int64_t out_cap, void* scratch, size_t scratch_bytes, cudaStream_t s) {
+                  int64_t* d_count_out, int64_t out_cap, void* scratch, size_t scratch_bytes, cudaStream_t s,
+                  int64_t* seg_start, int64_t* seg_end) {
   size_t need = level_scratch_bytes(in_cap);
   if (scratch_bytes < need) {
     set_error("traverse_hits: scratch %zu < %zu bytes", scratch_bytes, need);
@@ -408,10 +423,10 @@ int traverse_hits(const ng_octree& tree, const ng_ray* rays, int t, bool next_fi
   unsigned long long* states = (unsigned long long*)((char*)scratch + 16);
   if (next_final)
     k_traverse_hits<true><<<grid, TR_NT, 0, s>>>(tree, rays, t, in, d_count_in, in_cap, out_pairs, out_hits,
-                                                 d_count_out, out_cap, states, counter);
+                                                 d_count_out, out_cap, states, counter, seg_start, seg_end);
   else
     k_traverse_hits<false><<<grid, TR_NT, 0, s>>>(tree, rays, t, in, d_count_in, in_cap, out_pairs, out_hits,
-                                                  d_count_out, out_cap, states, counter);
+                                                  d_count_out, out_cap, states, counter, nullptr, nullptr);
   NG_CHECK_LAUNCH("k_traverse_hits");
   return NG_OK;
 }
