@@ -30,11 +30,16 @@ constexpr int R_NW = 8;  // warps per CTA for march / normals
 // Pixel-centre rays, bit-exact with Camera.rays (render.py:74-88), fused with
 // the per-pixel output defaults and the background colour.
 __global__ void k_camera_rays(ng_camera cam, ng_ray* __restrict__ rays, ng_frame fr, uint8_t bg0, uint8_t bg1,
-                              uint8_t bg2, int64_t* d_root_count) {
+                              uint8_t bg2, int64_t* d_root_count, int64_t* __restrict__ seg_start,
+                              int64_t* __restrict__ seg_end) {
   const int64_t n = (int64_t)cam.width * cam.local_rows;
   if (blockIdx.x == 0 && threadIdx.x == 0 && d_root_count) *d_root_count = n;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
+    if (seg_start) {  // rays without final-level pairs keep the empty segment
+      seg_start[i] = 0;
+      seg_end[i] = 0;
+    }
     if (rays) {
       const int px_i = (int)(i % cam.width);
       const int lrow = (int)(i / cam.width);
@@ -69,9 +74,32 @@ __global__ void k_camera_rays(ng_camera cam, ng_ray* __restrict__ rays, ng_frame
 
 __global__ void k_set_count(int64_t* p, int64_t v) { *p = v; }
 
-__global__ void k_frame_defaults(ng_frame fr, int64_t n, uint8_t bg0, uint8_t bg1, uint8_t bg2) {
+// Zero a handful of small device regions in one launch (frame statistics,
+// counters, traversal look-back states, histogram buckets) instead of one
+// memset per region on the frame's critical path.
+struct ZeroRegions {
+  void* p[6];
+  size_t bytes[6];
+  int n;
+};
+
+__global__ void k_zero_regions(ZeroRegions z) {
+  for (int k = 0; k < z.n; ++k) {
+    uint8_t* b = (uint8_t*)z.p[k];
+    const size_t n16 = z.bytes[k] / 16;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n16; i += (size_t)gridDim.x * blockDim.x)
+      reinterpret_cast<uint4*>(b)[i] = make_uint4(0, 0, 0, 0);
+    if (blockIdx.x == 0)
+      for (size_t i = n16 * 16 + threadIdx.x; i < z.bytes[k]; i += blockDim.x) b[i] = 0;
+  }
+}
+
+__global__ void k_frame_defaults(ng_frame fr, int64_t n, uint8_t bg0, uint8_t bg1, uint8_t bg2,
+                                 int64_t* __restrict__ seg_start, int64_t* __restrict__ seg_end) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
+    seg_start[i] = 0;
+    seg_end[i] = 0;
     fr.hit[i] = 0;
     fr.t[i] = __longlong_as_double(0x7ff8000000000000ll);
     fr.normal[3 * i] = 0.0;
@@ -944,8 +972,9 @@ static WsLayout layout(int64_t n, int64_t pair_cap, int64_t hit_cap) {
   L.seg_end = o; o = al(o + (size_t)n * 8);
   L.active = o; o = al(o + (size_t)n * 4);
   L.hit_list = o; o = al(o + (size_t)n * 4);
-  L.scratch_bytes = level_scratch_bytes(std::max<int64_t>(std::max<int64_t>(pair_cap, n), 1));
-  L.scratch = o; o = al(o + L.scratch_bytes);
+  // one look-back scratch region per traversal level, zeroed together once per pass
+  L.scratch_bytes = al(level_scratch_bytes(std::max<int64_t>(std::max<int64_t>(pair_cap, n), 1)));
+  L.scratch = o; o = al(o + L.scratch_bytes * NG_MAX_TLEVELS);
   L.ctr = o; o = al(o + 64);
   L.s_rays = o; o = al(o + (size_t)n * sizeof(ng_ray));
   L.s_hit = o; o = al(o + (size_t)n);
@@ -977,7 +1006,7 @@ static unsigned long long* march_profile_buffer() {
 static int trace_pass(const ng_octree& tree, const ng_render_cfg& cfg, const LodPlan& P, const ng_ray* rays,
                       int64_t n, int64_t* counts, const WsLayout& L, const ng_workspace& ws, char* b,
                       unsigned long long* d_active, unsigned long long* work_counter, cudaStream_t s,
-                      MarchArgs& A) {
+                      MarchArgs& A, bool zeroed) {
   ng_pair* pa = (ng_pair*)(b + L.pairs_a);
   ng_pair* pb = (ng_pair*)(b + L.pairs_b);
   ng_hit_pair* hits = (ng_hit_pair*)(b + L.hits);
@@ -991,22 +1020,33 @@ static int trace_pass(const ng_octree& tree, const ng_render_cfg& cfg, const Lod
   const int target = cfg.trace_level + tree.n_virtual;
   const ng_pair* in = nullptr;
   int64_t in_cap = n;
-  // rays without final-level pairs keep the empty segment [0, 0)
-  if ((r = cuda_status(cudaMemsetAsync(seg_start, 0, n * 8, s), "seg memset"))) return r;
-  if ((r = cuda_status(cudaMemsetAsync(seg_end, 0, n * 8, s), "seg memset"))) return r;
+  unsigned int* buckets = (unsigned int*)(b + L.buckets);
+  if (!zeroed) {  // the primary pass has these zeroed by k_zero_regions and the ray kernel
+    ZeroRegions z;
+    z.n = 4;
+    z.p[0] = scratch;
+    z.bytes[0] = L.scratch_bytes * (size_t)target;
+    z.p[1] = seg_start;
+    z.bytes[1] = (size_t)n * 8;
+    z.p[2] = seg_end;
+    z.bytes[2] = (size_t)n * 8;
+    z.p[3] = buckets;
+    z.bytes[3] = 2 * LEN_BUCKETS * 4;
+    k_zero_regions<<<grid_for(n / 2 + 1, 256), 256, 0, s>>>(z);
+    NG_CHECK_LAUNCH("k_zero_regions");
+  }
   for (int t = 0; t < target; ++t) {
     const bool last = (t + 1 == target);
     ng_pair* out = (t % 2 == 0) ? pa : pb;
     r = traverse_hits(tree, rays, t, last, in, &counts[t], in_cap, last ? nullptr : out, last ? hits : nullptr,
-                      &counts[t + 1], last ? ws.hit_capacity : ws.pair_capacity, scratch, L.scratch_bytes, s,
+                      &counts[t + 1], last ? ws.hit_capacity : ws.pair_capacity,
+                      (char*)scratch + (size_t)t * L.scratch_bytes, L.scratch_bytes, s,
                       last ? seg_start : nullptr, last ? seg_end : nullptr);
     if (r) return r;
     in = out;
     in_cap = ws.pair_capacity;
   }
   int32_t* sorted = (int32_t*)(b + L.sorted);
-  unsigned int* buckets = (unsigned int*)(b + L.buckets);
-  if ((r = cuda_status(cudaMemsetAsync(buckets, 0, 2 * LEN_BUCKETS * 4, s), "bucket memset"))) return r;
   k_active_hist<<<grid_for(n, 256), 256, 0, s>>>(seg_start, seg_end, n, active, d_active, buckets);
   NG_CHECK_LAUNCH("k_active_hist");
   k_len_scatter<<<grid_for(n, 256), 256, 0, s>>>(active, d_active, seg_start, seg_end, buckets,
@@ -1058,15 +1098,32 @@ static int render_common(const ng_octree& tree, const ng_field& f, const ng_rend
   // [0] active rays, [1] hits, [2] march work, [3] shadow active, [4] shadow work
   unsigned long long* ctr = (unsigned long long*)(b + L.ctr);
   int r;
-  if ((r = cuda_status(cudaMemsetAsync(st, 0, sizeof(ng_frame_stats), s), "stats memset"))) return r;
-  if ((r = cuda_status(cudaMemsetAsync(ctr, 0, 64, s), "ctr memset"))) return r;
+  int64_t* seg_start = (int64_t*)(b + L.seg_start);
+  int64_t* seg_end = (int64_t*)(b + L.seg_end);
+  {
+    // statistics, counters, the primary traversal's look-back states and the
+    // length buckets, in one launch
+    ZeroRegions z;
+    z.n = 4;
+    z.p[0] = st;
+    z.bytes[0] = sizeof(ng_frame_stats);
+    z.p[1] = ctr;
+    z.bytes[1] = 64;
+    z.p[2] = b + L.scratch;
+    z.bytes[2] = L.scratch_bytes * (size_t)(cfg.trace_level + tree.n_virtual);
+    z.p[3] = b + L.buckets;
+    z.bytes[3] = 2 * LEN_BUCKETS * 4;
+    k_zero_regions<<<64, 256, 0, s>>>(z);
+    NG_CHECK_LAUNCH("k_zero_regions");
+  }
   uint8_t bg[3];
   background_u8(cfg, bg);
   if (cam) {
-    k_camera_rays<<<grid_for(n, 256), 256, 0, s>>>(*cam, rays, fr, bg[0], bg[1], bg[2], &st->pairs[0]);
+    k_camera_rays<<<grid_for(n, 256), 256, 0, s>>>(*cam, rays, fr, bg[0], bg[1], bg[2], &st->pairs[0], seg_start,
+                                                   seg_end);
     NG_CHECK_LAUNCH("k_camera_rays");
   } else {
-    k_frame_defaults<<<grid_for(n, 256), 256, 0, s>>>(fr, n, bg[0], bg[1], bg[2]);
+    k_frame_defaults<<<grid_for(n, 256), 256, 0, s>>>(fr, n, bg[0], bg[1], bg[2], seg_start, seg_end);
     NG_CHECK_LAUNCH("k_frame_defaults");
     k_set_count<<<1, 1, 0, s>>>(&st->pairs[0], n);  // root list (i, 0) of n rays
     NG_CHECK_LAUNCH("k_set_count");
@@ -1075,7 +1132,7 @@ static int render_common(const ng_octree& tree, const ng_field& f, const ng_rend
   const int target = cfg.trace_level + tree.n_virtual;
   const LodPlan P = plan_lod(cfg);
   MarchArgs A;
-  if ((r = trace_pass(tree, cfg, P, rays, n, st->pairs, L, ws, b, ctr + 0, ctr + 2, s, A))) return r;
+  if ((r = trace_pass(tree, cfg, P, rays, n, st->pairs, L, ws, b, ctr + 0, ctr + 2, s, A, true))) return r;
   A.hit = fr.hit;
   A.t = fr.t;
   A.iters = fr.iterations;
@@ -1133,7 +1190,8 @@ static int render_common(const ng_octree& tree, const ng_field& f, const ng_rend
                                                   &st->shadow_pairs[0]);
     NG_CHECK_LAUNCH("k_shadow_rays");
     MarchArgs S;
-    if ((r = trace_pass(tree, cfg, P, srays, n, st->shadow_pairs, L, ws, b, ctr + 3, ctr + 4, s, S))) return r;
+    if ((r = trace_pass(tree, cfg, P, srays, n, st->shadow_pairs, L, ws, b, ctr + 3, ctr + 4, s, S, false)))
+      return r;
     S.hit = (uint8_t*)(b + L.s_hit);
     // the march writes only the rays that have a voxel segment: clear the rest
     // (a shadow ray that leaves the octree without a segment is unshadowed)
@@ -1162,7 +1220,8 @@ extern "C" {
 
 int ng_camera_rays(const ng_camera* cam, ng_ray* rays, void* stream) {
   int64_t n = (int64_t)cam->width * cam->local_rows;
-  k_camera_rays<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(*cam, rays, ng_frame{}, 0, 0, 0, nullptr);
+  k_camera_rays<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(*cam, rays, ng_frame{}, 0, 0, 0, nullptr, nullptr,
+                                                                            nullptr);
   NG_CHECK_LAUNCH("ng_camera_rays");
   return NG_OK;
 }

@@ -409,13 +409,12 @@ int traverse_hits(const ng_octree& tree, const ng_ray* rays, int t, bool next_fi
                   const int64_t* d_count_in, int64_t in_cap, ng_pair* out_pairs, ng_hit_pair* out_hits,
                   int64_t* d_count_out, int64_t out_cap, void* scratch, size_t scratch_bytes, cudaStream_t s,
                   int64_t* seg_start, int64_t* seg_end) {
+  // the caller zeroes `scratch` (tile counter and look-back states) beforehand
   size_t need = level_scratch_bytes(in_cap);
   if (scratch_bytes < need) {
     set_error("traverse_hits: scratch %zu < %zu bytes", scratch_bytes, need);
     return NG_ERR_CAPACITY;
   }
-  int r = cuda_status(cudaMemsetAsync(scratch, 0, need, s), "traverse_hits memset");
-  if (r) return r;
   const int64_t tile = (int64_t)TR_NT * TR_ITEMS;
   int64_t tiles = (in_cap + tile - 1) / tile;
   int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)sm_count() * 6));
