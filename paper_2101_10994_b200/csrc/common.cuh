@@ -184,6 +184,28 @@ __device__ __forceinline__ void load_ray(const ng_ray* __restrict__ rays, int64_
   r.pad = 0;
 }
 
+// A pinhole camera's rays share one origin: the traversal then loads only
+// the slab part of the record (1/d and the direction flags, bytes 48-79).
+struct SharedOrigin {
+  double o[3];
+  int shared;
+};
+
+__device__ __forceinline__ void load_ray_slab(const ng_ray* __restrict__ rays, int64_t i, const SharedOrigin& so,
+                                              ng_ray& r) {
+  if (!so.shared) {
+    load_ray(rays, i, r);
+    return;
+  }
+  const double2* p = reinterpret_cast<const double2*>(rays + i);
+  const double2 d = __ldg(p + 3), e = __ldg(p + 4);
+  r.o[0] = so.o[0]; r.o[1] = so.o[1]; r.o[2] = so.o[2];
+  r.d[0] = r.d[1] = r.d[2] = 0.0;  // not used by slab tests
+  r.inv[0] = d.x; r.inv[1] = d.y; r.inv[2] = e.x;
+  r.flags = __double_as_longlong(e.y) & 0xffffffff;
+  r.pad = 0;
+}
+
 __device__ __forceinline__ void make_ray(double ox, double oy, double oz, double dx, double dy,
                                          double dz, ng_ray& r) {
   r.o[0] = ox; r.o[1] = oy; r.o[2] = oz;

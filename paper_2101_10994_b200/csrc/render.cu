@@ -23,7 +23,7 @@ size_t level_scratch_bytes(int64_t max_pairs);
 int traverse_hits(const ng_octree& tree, const ng_ray* rays, int t, bool next_final, const ng_pair* in,
                   const int64_t* d_count_in, int64_t in_cap, ng_pair* out_pairs, ng_hit_pair* out_hits,
                   int64_t* d_count_out, int64_t out_cap, void* scratch, size_t scratch_bytes, cudaStream_t s,
-                  int64_t* seg_start, int64_t* seg_end);
+                  int64_t* seg_start, int64_t* seg_end, const double* shared_origin);
 
 constexpr int R_NW = 8;  // warps per CTA for march / normals
 
@@ -1006,7 +1006,7 @@ static unsigned long long* march_profile_buffer() {
 static int trace_pass(const ng_octree& tree, const ng_render_cfg& cfg, const LodPlan& P, const ng_ray* rays,
                       int64_t n, int64_t* counts, const WsLayout& L, const ng_workspace& ws, char* b,
                       unsigned long long* d_active, unsigned long long* work_counter, cudaStream_t s,
-                      MarchArgs& A, bool zeroed) {
+                      MarchArgs& A, bool zeroed, const double* shared_origin) {
   ng_pair* pa = (ng_pair*)(b + L.pairs_a);
   ng_pair* pb = (ng_pair*)(b + L.pairs_b);
   ng_hit_pair* hits = (ng_hit_pair*)(b + L.hits);
@@ -1041,7 +1041,7 @@ static int trace_pass(const ng_octree& tree, const ng_render_cfg& cfg, const Lod
     r = traverse_hits(tree, rays, t, last, in, &counts[t], in_cap, last ? nullptr : out, last ? hits : nullptr,
                       &counts[t + 1], last ? ws.hit_capacity : ws.pair_capacity,
                       (char*)scratch + (size_t)t * L.scratch_bytes, L.scratch_bytes, s,
-                      last ? seg_start : nullptr, last ? seg_end : nullptr);
+                      last ? seg_start : nullptr, last ? seg_end : nullptr, shared_origin);
     if (r) return r;
     in = out;
     in_cap = ws.pair_capacity;
@@ -1132,7 +1132,10 @@ static int render_common(const ng_octree& tree, const ng_field& f, const ng_rend
   const int target = cfg.trace_level + tree.n_virtual;
   const LodPlan P = plan_lod(cfg);
   MarchArgs A;
-  if ((r = trace_pass(tree, cfg, P, rays, n, st->pairs, L, ws, b, ctr + 0, ctr + 2, s, A, true))) return r;
+  // camera rays share the eye position (a host value, captured into the launches)
+  if ((r = trace_pass(tree, cfg, P, rays, n, st->pairs, L, ws, b, ctr + 0, ctr + 2, s, A, true,
+                      cam ? cam->position : nullptr)))
+    return r;
   A.hit = fr.hit;
   A.t = fr.t;
   A.iters = fr.iterations;
@@ -1190,7 +1193,8 @@ static int render_common(const ng_octree& tree, const ng_field& f, const ng_rend
                                                   &st->shadow_pairs[0]);
     NG_CHECK_LAUNCH("k_shadow_rays");
     MarchArgs S;
-    if ((r = trace_pass(tree, cfg, P, srays, n, st->shadow_pairs, L, ws, b, ctr + 3, ctr + 4, s, S, false)))
+    if ((r = trace_pass(tree, cfg, P, srays, n, st->shadow_pairs, L, ws, b, ctr + 3, ctr + 4, s, S, false,
+                        nullptr)))
       return r;
     S.hit = (uint8_t*)(b + L.s_hit);
     // the march writes only the rays that have a voxel segment: clear the rest

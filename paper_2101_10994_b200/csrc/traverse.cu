@@ -150,7 +150,8 @@ __global__ void __launch_bounds__(TR_NT) k_traverse_hits(
     const ng_pair* __restrict__ in, const int64_t* __restrict__ d_count_in, int64_t in_cap,
     ng_pair* __restrict__ out_pairs, ng_hit_pair* __restrict__ out_hits,
     int64_t* __restrict__ d_count_out, int64_t out_cap, unsigned long long* states,
-    unsigned int* tile_counter, int64_t* __restrict__ seg_start, int64_t* __restrict__ seg_end) {
+    unsigned int* tile_counter, int64_t* __restrict__ seg_start, int64_t* __restrict__ seg_end,
+    const SharedOrigin so) {
   __shared__ int64_t sm_warp[TR_NT / 32 + 1];
   __shared__ int64_t sm_tile, sm_excl;
   int64_t n = *d_count_in;
@@ -189,10 +190,10 @@ __global__ void __launch_bounds__(TR_NT) k_traverse_hits(
           const ng_pair p = in[i];
           pr[q] = p.ray;
           pv[q] = p.voxel;
-          load_ray(rays, pr[q], r);
+          load_ray_slab(rays, pr[q], so, r);
         } else {  // implicit root list: the root box itself must be hit
           pr[q] = (int32_t)i;
-          load_ray(rays, pr[q], r);
+          load_ray_slab(rays, pr[q], so, r);
           const double lo[3] = {-1.0, -1.0, -1.0}, hi[3] = {1.0, 1.0, 1.0};
           double a, b;
           parent_hit = slab_test(r, lo, hi, a, b);
@@ -248,7 +249,7 @@ __global__ void __launch_bounds__(TR_NT) k_traverse_hits(
       ChildSlabs cs;
       if (NEXT_FINAL) {
         ng_ray r;
-        load_ray(rays, pr[q], r);
+        load_ray_slab(rays, pr[q], so, r);
         const uint64_t c = __ldg(codes + pv[q]);
         child_slabs(r, (int)compact3(c), (int)compact3(c >> 1), (int)compact3(c >> 2), cres, cs);
       }
@@ -408,8 +409,11 @@ int traverse_level(const ng_octree& tree, const ng_ray* rays, int t, bool final,
 int traverse_hits(const ng_octree& tree, const ng_ray* rays, int t, bool next_final, const ng_pair* in,
                   const int64_t* d_count_in, int64_t in_cap, ng_pair* out_pairs, ng_hit_pair* out_hits,
                   int64_t* d_count_out, int64_t out_cap, void* scratch, size_t scratch_bytes, cudaStream_t s,
-                  int64_t* seg_start, int64_t* seg_end) {
+                  int64_t* seg_start, int64_t* seg_end, const double* shared_origin) {
   // the caller zeroes `scratch` (tile counter and look-back states) beforehand
+  SharedOrigin so;
+  so.shared = shared_origin != nullptr;
+  for (int a = 0; a < 3; ++a) so.o[a] = shared_origin ? shared_origin[a] : 0.0;
   size_t need = level_scratch_bytes(in_cap);
   if (scratch_bytes < need) {
     set_error("traverse_hits: scratch %zu < %zu bytes", scratch_bytes, need);
@@ -422,10 +426,10 @@ int traverse_hits(const ng_octree& tree, const ng_ray* rays, int t, bool next_fi
   unsigned long long* states = (unsigned long long*)((char*)scratch + 16);
   if (next_final)
     k_traverse_hits<true><<<grid, TR_NT, 0, s>>>(tree, rays, t, in, d_count_in, in_cap, out_pairs, out_hits,
-                                                 d_count_out, out_cap, states, counter, seg_start, seg_end);
+                                                 d_count_out, out_cap, states, counter, seg_start, seg_end, so);
   else
     k_traverse_hits<false><<<grid, TR_NT, 0, s>>>(tree, rays, t, in, d_count_in, in_cap, out_pairs, out_hits,
-                                                  d_count_out, out_cap, states, counter, nullptr, nullptr);
+                                                  d_count_out, out_cap, states, counter, nullptr, nullptr, so);
   NG_CHECK_LAUNCH("k_traverse_hits");
   return NG_OK;
 }
