@@ -170,21 +170,39 @@ __global__ void k_len_scatter(const int32_t* __restrict__ active, const unsigned
                               const int64_t* __restrict__ seg_start, const int64_t* __restrict__ seg_end,
                               const unsigned int* __restrict__ hist, unsigned int* __restrict__ cursor,
                               int32_t* __restrict__ sorted) {
+  // bucket offsets (descending length), then per block: count the block's
+  // rays per bucket in shared memory, reserve each bucket's range with one
+  // global atomic, and scatter (order inside a bucket does not matter)
   __shared__ unsigned int off[LEN_BUCKETS];
+  __shared__ unsigned int cnt[LEN_BUCKETS];
+  __shared__ unsigned int base[LEN_BUCKETS];
   if (threadIdx.x == 0) {
     unsigned int run = 0;
-    for (int b = LEN_BUCKETS - 1; b >= 0; --b) {  // descending length
+    for (int b = LEN_BUCKETS - 1; b >= 0; --b) {
       off[b] = run;
       run += hist[b];
     }
   }
-  __syncthreads();
   const int64_t n = (int64_t)*d_n;
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t r = active[k];
-    const int64_t len = seg_end[r] - seg_start[r];
-    const int b = len < LEN_BUCKETS - 1 ? (int)len : LEN_BUCKETS - 1;
-    sorted[off[b] + atomicAdd(&cursor[b], 1u)] = r;
+  for (int64_t k0 = blockIdx.x * (int64_t)blockDim.x; k0 < n; k0 += (int64_t)gridDim.x * blockDim.x) {
+    for (int i = threadIdx.x; i < LEN_BUCKETS; i += blockDim.x) cnt[i] = 0;
+    __syncthreads();
+    const int64_t k = k0 + threadIdx.x;
+    int32_t r = -1;
+    int b = 0;
+    unsigned int slot = 0;
+    if (k < n) {
+      r = active[k];
+      const int64_t len = seg_end[r] - seg_start[r];
+      b = len < LEN_BUCKETS - 1 ? (int)len : LEN_BUCKETS - 1;
+      slot = atomicAdd(&cnt[b], 1u);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < LEN_BUCKETS; i += blockDim.x)
+      base[i] = cnt[i] ? atomicAdd(&cursor[i], cnt[i]) : 0u;
+    __syncthreads();
+    if (r >= 0) sorted[off[b] + base[b] + slot] = r;
+    __syncthreads();
   }
 }
 
