@@ -143,23 +143,34 @@ __global__ void k_len_hist(const int32_t* __restrict__ active, const unsigned lo
 __global__ void k_active_hist(const int64_t* __restrict__ seg_start, const int64_t* __restrict__ seg_end, int64_t n,
                               int32_t* __restrict__ active, unsigned long long* d_active,
                               unsigned int* __restrict__ hist) {
+  // per block: bucket counts in shared memory, the block's active rays
+  // compacted with one global atomic (not one per warp)
   __shared__ unsigned int h[LEN_BUCKETS];
+  __shared__ unsigned int wcount[32];
+  __shared__ unsigned long long block_base;
   for (int i = threadIdx.x; i < LEN_BUCKETS; i += blockDim.x) h[i] = 0;
-  __syncthreads();
+  const int w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < n; base += stride) {
     const int64_t r = base + threadIdx.x;
     const int64_t len = r < n ? seg_end[r] - seg_start[r] : 0;
     const bool has = len > 0;
+    __syncthreads();
     if (has) atomicAdd(&h[len < LEN_BUCKETS - 1 ? len : LEN_BUCKETS - 1], 1u);
     const unsigned m = __ballot_sync(FULL, has);
-    if (m) {
-      unsigned long long b = 0;
-      const int leader = __ffs(m) - 1;
-      if ((int)lane_id() == leader) b = atomicAdd(d_active, (unsigned long long)__popc(m));
-      b = __shfl_sync(FULL, b, leader);
-      if (has) active[b + __popc(m & lanemask_lt())] = (int32_t)r;
+    if (lane_id() == 0) wcount[w] = __popc(m);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned int tot = 0;
+      for (int q = 0; q < nw; ++q) {
+        const unsigned int c = wcount[q];
+        wcount[q] = tot;
+        tot += c;
+      }
+      block_base = tot ? atomicAdd(d_active, (unsigned long long)tot) : 0ull;
     }
+    __syncthreads();
+    if (has) active[block_base + wcount[w] + __popc(m & lanemask_lt())] = (int32_t)r;
   }
   __syncthreads();
   for (int i = threadIdx.x; i < LEN_BUCKETS; i += blockDim.x)
