@@ -238,13 +238,7 @@ struct MarchArgs {
   unsigned long long* work_counter;
   ng_counters* counters;
   unsigned long long* prof;      // optional: 4 counters per group (steps, busy lanes, t0, t1)
-  // fused normals (render.py:277-300): after a hit the lane evaluates its
-  // 6 central-difference probes in the same persistent loop, then shades
-  int fuse_normals;
   int lane_cap;                  // max rays a warp marches at once (NG_MARCH_CAP, default 32)
-  double* normal;
-  uint8_t* normal_ok;
-  uint8_t* color;                // null: shading happens later (shadow pass)
 };
 
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
@@ -277,19 +271,6 @@ __device__ __forceinline__ double field_value(const ng_octree& tree, const EvalL
   if (!er.inside) return empty_value(tree, x);
   if (alpha != 0.0) return dadd(dmul(dsub(1.0, alpha), lo), dmul(alpha, hi));
   return lo;
-}
-
-// shade (render.py:303-314) for one hit pixel with an fp64 normal.
-__device__ __forceinline__ void shade_pixel(const ng_render_cfg& cfg, double n0, double n1, double n2,
-                                            uint8_t* rgb_out) {
-  double lam = dadd(dadd(dmul(n0, cfg.light[0]), dmul(n1, cfg.light[1])), dmul(n2, cfg.light[2]));
-  lam = lam < 0.0 ? 0.0 : (lam > 1.0 ? 1.0 : lam);
-#pragma unroll
-  for (int ch = 0; ch < 3; ++ch) {
-    double rgb = dmul(cfg.albedo[ch], dadd(cfg.ambient, dmul(dsub(1.0, cfg.ambient), lam)));
-    rgb = rgb < 0.0 ? 0.0 : (rgb > 1.0 ? 1.0 : rgb);
-    rgb_out[ch] = (uint8_t)dadd(dmul(rgb, 255.0), 0.5);
-  }
 }
 
 // Decoder policy setup shared by the march and normals kernels: SIMT stages
@@ -366,11 +347,6 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_cons
   double t = 0.0, prev = NaN;
   int it = 0, ev = 0;
   double o[3] = {0, 0, 0}, d[3] = {0, 0, 0};
-  int probe = -1;               // -1 marching; 0..5 next normal probe (+x,+y,+z,-x,-y,-z)
-  double hp[3] = {0, 0, 0};     // hit point o + t_hit d
-  double vp0 = 0, vp1 = 0, vp2 = 0;  // plus-probe values
-  double g0 = 0, g1 = 0, g2 = 0;     // gradient
-  const double eps = A.cfg.normal_eps;
 
   auto finish = [&](bool is_hit, double th) {
     A.hit[ray] = is_hit ? 1 : 0;
@@ -400,7 +376,6 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_cons
             drained = true;
           } else {
             ray = A.work ? A.work[k] : (int)k;
-            probe = -1;
             cur = A.seg_start[ray];
             end = A.seg_end[ray];
             t = 0.0;
@@ -414,7 +389,7 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_cons
           }
         }
       }
-      if (ray >= 0 && !ready && probe < 0) {
+      if (ray >= 0 && !ready) {
         bool dead = false;
         while (true) {
           if (cur >= end || t > A.cfg.far_plane) {
@@ -468,18 +443,9 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_cons
       if (!__any_sync(FULL, act)) break;
     }
 
-    // ---- query point: x = o + t d clamped into the current voxel (render.py:244-245),
-    // or a normal probe clip(p +- eps e_axis, -1, 1) (render.py:289-293)
+    // ---- query point: x = o + t d clamped into the current voxel (render.py:244-245)
     double x[3] = {0.0, 0.0, 0.0};
-    if (act && probe >= 0) {
-      const int axis = probe % 3;
-#pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        double v = hp[a];
-        if (a == axis) v = (probe < 3) ? dadd(v, eps) : dsub(v, eps);
-        x[a] = np_min(np_max(v, -1.0), 1.0);
-      }
-    } else if (act) {
+    if (act) {
       const uint64_t code = __ldg(codes + A.hits[cur].voxel);
       const int cc[3] = {(int)compact3(code), (int)compact3(code >> 1), (int)compact3(code >> 2)};
 #pragma unroll
@@ -528,31 +494,10 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_cons
 #endif
     // ---- stop rules (render.py:247-272)
     if (act && !er.inside) lc.empty += 1;  // query_field's own empty-space fallback
-    if (act && probe >= 0) {
-      // normals (render.py:294-299): g = (v+ - v-) / (2 eps), normalised
-      const double two_eps = 2.0 * eps;
-      if (probe == 0) vp0 = dval_of(er, fv, x);
-      else if (probe == 1) vp1 = dval_of(er, fv, x);
-      else if (probe == 2) vp2 = dval_of(er, fv, x);
-      else if (probe == 3) g0 = dsub(vp0, dval_of(er, fv, x)) / two_eps;
-      else if (probe == 4) g1 = dsub(vp1, dval_of(er, fv, x)) / two_eps;
-      else g2 = dsub(vp2, dval_of(er, fv, x)) / two_eps;
-      if (++probe == 6) {
-        const double nrm = __dsqrt_rn(dadd(dadd(dmul(g0, g0), dmul(g1, g1)), dmul(g2, g2)));
-        const bool ok = isfinite(nrm) && nrm > 1e-12;
-        const double n0 = ok ? g0 / nrm : 0.0, n1 = ok ? g1 / nrm : 0.0, n2 = ok ? g2 / nrm : 0.0;
-        A.normal[3 * ray] = n0;
-        A.normal[3 * ray + 1] = n1;
-        A.normal[3 * ray + 2] = n2;
-        A.normal_ok[ray] = ok ? 1 : 0;
-        if (A.color) shade_pixel(A.cfg, n0, n1, n2, A.color + 3 * ray);
-        ray = -1;
-      }
-    } else if (act) {
+    if (act) {
       double dval = dval_of(er, fv, x);
       ev += A.passes;
       it += 1;
-      const int ray_keep = ray;
       const bool is_hit = dval < A.cfg.delta;
       const bool stalled = !is_hit && (dval >= prev) && (fabs(dsub(dval, prev)) < A.cfg.osc_tol);
       if (is_hit) {
@@ -562,12 +507,6 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_cons
         }
         const double th = dadd(t, dval);
         finish(true, th);
-        if (A.fuse_normals) {  // keep the lane: its 6 normal probes come next
-          ray = ray_keep;
-          probe = 0;
-#pragma unroll
-          for (int a = 0; a < 3; ++a) hp[a] = dadd(o[a], dmul(th, d[a]));  // render.py:396
-        }
       } else if (stalled || it >= A.cfg.max_iters) {
         finish(false, 0.0);
       } else {
@@ -1098,10 +1037,6 @@ static int trace_pass(const ng_octree& tree, const ng_render_cfg& cfg, const Lod
   A.seg_end = seg_end;
   A.work_counter = work_counter;
   A.prof = march_profile_buffer();
-  A.fuse_normals = 0;
-  A.normal = nullptr;
-  A.normal_ok = nullptr;
-  A.color = nullptr;
   return NG_OK;
 }
 
@@ -1172,27 +1107,13 @@ static int render_common(const ng_octree& tree, const ng_field& f, const ng_rend
   A.hit_list = hit_list;
   A.d_hit_count = ctr + 1;
   A.counters = &st->counters;
-  // NG_FUSE_NORMALS=1 runs the normal probes inside the persistent march
-  // (lanes take their 6 probes after a hit). Measured slower on B200
-  // (2.159 vs 2.079 ms per 720p knot frame), so the separate normals kernel
-  // is the default.
-  static int fuse_env = -1;
-  if (fuse_env < 0) {
-    const char* e = getenv("NG_FUSE_NORMALS");
-    fuse_env = (e && e[0] == '1') ? 1 : 0;
-  }
-  const bool fuse = do_normals && fuse_env;
-  A.fuse_normals = fuse ? 1 : 0;
-  A.normal = fr.normal;
-  A.normal_ok = fr.normal_ok;
-  A.color = cfg.shadows ? nullptr : fr.color;
   if (ws.ev_march_begin && (r = cuda_status(cudaEventRecord((cudaEvent_t)ws.ev_march_begin, s), "event record")))
     return r;
   if ((r = launch_march(tree, f, A, s))) return r;
   if (ws.ev_trace_done && (r = cuda_status(cudaEventRecord((cudaEvent_t)ws.ev_trace_done, s), "event record")))
     return r;
-  // ---- normals + shading (render.py:399-414, 440), when not fused above
-  if (do_normals && !fuse) {
+  // ---- normals + shading (render.py:399-414, 440)
+  if (do_normals) {
     NormalArgs B;
     B.cfg = cfg;
     B.G = P.G;
@@ -1316,10 +1237,6 @@ int ng_sphere_trace(const ng_octree* tree, const ng_field* fld, const ng_render_
   A.work_counter = work;
   A.counters = d_counters;
   A.prof = nullptr;
-  A.fuse_normals = 0;
-  A.normal = nullptr;
-  A.normal_ok = nullptr;
-  A.color = nullptr;
   (void)d_hit_count;
   r = launch_march(*tree, *fld, A, s);
   cudaFreeAsync(work, s);
