@@ -204,6 +204,7 @@ typedef struct ng_frame_stats {
   int64_t overflow;              /* nonzero: a pair list exceeded its capacity */
   int64_t shadow_pairs[NG_MAX_TLEVELS + 1]; /* shadow-ray traversal (when cfg.shadows) */
   int64_t shadowed;              /* hit pixels whose shadow ray hit the surface */
+  int64_t pair_need;             /* after an overflow: pair capacity a rerun needs (tile traversal arena) */
 } ng_frame_stats;
 
 /* ---- library ----------------------------------------------------------- */

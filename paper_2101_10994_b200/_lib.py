@@ -106,7 +106,8 @@ class NgWorkspace(C.Structure):
 class NgFrameStats(C.Structure):
     _fields_ = [("pairs", C.c_int64 * (MAX_TLEVELS + 1)), ("visible", C.c_int64),
                 ("active_rays", C.c_int64), ("counters", NgCounters), ("overflow", C.c_int64),
-                ("shadow_pairs", C.c_int64 * (MAX_TLEVELS + 1)), ("shadowed", C.c_int64)]
+                ("shadow_pairs", C.c_int64 * (MAX_TLEVELS + 1)), ("shadowed", C.c_int64),
+                ("pair_need", C.c_int64)]
 
 
 class NgTrainParams(C.Structure):

@@ -24,6 +24,24 @@ int traverse_hits(const ng_octree& tree, const ng_ray* rays, int t, bool next_fi
                   const int64_t* d_count_in, int64_t in_cap, ng_pair* out_pairs, ng_hit_pair* out_hits,
                   int64_t* d_count_out, int64_t out_cap, void* scratch, size_t scratch_bytes, cudaStream_t s,
                   int64_t* seg_start, int64_t* seg_end, const double* shared_origin);
+int traverse_tiles(const ng_octree& tree, const ng_ray* rays, const int64_t* d_n, int target, int64_t* counts,
+                   ng_hit_pair* hits, int64_t hit_cap, void* ctl, int64_t* seg_start, int64_t* seg_end,
+                   void* arena, size_t arena_bytes, unsigned long long* d_need, const double* shared_origin,
+                   cudaStream_t s);
+int64_t tile_traverse_limit(size_t arena_bytes);
+int64_t tile_traverse_warps();
+int tile_traverse_scap();
+
+// NG_TILE_TRAVERSE=0 selects the level-by-level traversal launches
+// (k_traverse_hits) instead of the warp-per-tile kernel.
+static bool use_tile_traverse(int target) {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("NG_TILE_TRAVERSE");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on && target >= 1;
+}
 
 constexpr int R_NW = 8;  // warps per CTA for march / normals
 
@@ -98,8 +116,10 @@ __global__ void k_frame_defaults(ng_frame fr, int64_t n, uint8_t bg0, uint8_t bg
                                  int64_t* __restrict__ seg_start, int64_t* __restrict__ seg_end) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    seg_start[i] = 0;
-    seg_end[i] = 0;
+    if (seg_start) {
+      seg_start[i] = 0;
+      seg_end[i] = 0;
+    }
     fr.hit[i] = 0;
     fr.t[i] = __longlong_as_double(0x7ff8000000000000ll);
     fr.normal[3 * i] = 0.0;
@@ -706,11 +726,31 @@ __global__ void k_hit_points(const ng_ray* __restrict__ rays, const uint8_t* __r
   }
 }
 
+// Tile traversal: a tile list longer than the arena holds (`tile_need`
+// against `lim`) asks for a rerun with the pair capacity whose arena share
+// (10 bytes per pair per warp beyond the shared-memory lists, out of 16
+// bytes per unit of capacity) holds it, plus a quarter.
+struct TileOverflow {
+  const unsigned long long* need;  // null: level-by-level traversal
+  int64_t lim, scap, warps;
+};
+
+__device__ __forceinline__ int64_t tile_overflow(ng_frame_stats* st, const TileOverflow& T) {
+  if (T.need == nullptr || (int64_t)*T.need <= T.lim) return 0;
+  const int64_t spill = ((int64_t)*T.need - T.scap + 16) * 5 / 4;
+  const int64_t want = spill * 10 * T.warps / 16 + 4096;
+  if (want > st->pair_need) st->pair_need = want;
+  return 1;
+}
+
 __global__ void k_finish_stats(ng_frame_stats* st, int n_levels, int64_t pair_cap, int64_t hit_cap,
-                               const unsigned long long* d_hits, const unsigned long long* d_active) {
+                               const unsigned long long* d_hits, const unsigned long long* d_active,
+                               TileOverflow T) {
   int64_t over = 0;
-  for (int t = 1; t < n_levels; ++t) over |= (st->pairs[t] > pair_cap);
+  if (T.need == nullptr)
+    for (int t = 1; t < n_levels; ++t) over |= (st->pairs[t] > pair_cap);
   over |= (st->pairs[n_levels] > hit_cap);
+  over |= tile_overflow(st, T);
   st->overflow = over;
   st->visible = (int64_t)*d_hits;
   st->active_rays = (int64_t)*d_active;
@@ -764,10 +804,13 @@ __global__ void k_shade_shadowed(const int32_t* __restrict__ hit_list, const uns
   if ((threadIdx.x & 31) == 0 && local) atomicAdd((unsigned long long*)d_shadowed, (unsigned long long)local);
 }
 
-__global__ void k_shadow_overflow(ng_frame_stats* st, int n_levels, int64_t pair_cap, int64_t hit_cap) {
+__global__ void k_shadow_overflow(ng_frame_stats* st, int n_levels, int64_t pair_cap, int64_t hit_cap,
+                                  TileOverflow T) {
   int64_t over = 0;
-  for (int t = 1; t < n_levels; ++t) over |= (st->shadow_pairs[t] > pair_cap);
+  if (T.need == nullptr)
+    for (int t = 1; t < n_levels; ++t) over |= (st->shadow_pairs[t] > pair_cap);
   over |= (st->shadow_pairs[n_levels] > hit_cap);
+  over |= tile_overflow(st, T);
   if (over) st->overflow = 1;
 }
 
@@ -974,7 +1017,7 @@ static unsigned long long* march_profile_buffer() {
 static int trace_pass(const ng_octree& tree, const ng_render_cfg& cfg, const LodPlan& P, const ng_ray* rays,
                       int64_t n, int64_t* counts, const WsLayout& L, const ng_workspace& ws, char* b,
                       unsigned long long* d_active, unsigned long long* work_counter, cudaStream_t s,
-                      MarchArgs& A, bool zeroed, const double* shared_origin) {
+                      MarchArgs& A, bool zeroed, const double* shared_origin, TileOverflow& tov) {
   ng_pair* pa = (ng_pair*)(b + L.pairs_a);
   ng_pair* pb = (ng_pair*)(b + L.pairs_b);
   ng_hit_pair* hits = (ng_hit_pair*)(b + L.hits);
@@ -989,6 +1032,8 @@ static int trace_pass(const ng_octree& tree, const ng_render_cfg& cfg, const Lod
   const ng_pair* in = nullptr;
   int64_t in_cap = n;
   unsigned int* buckets = (unsigned int*)(b + L.buckets);
+  const bool tiles = use_tile_traverse(target);
+  tov.need = nullptr;
   if (!zeroed) {  // the primary pass has these zeroed by k_zero_regions and the ray kernel
     ZeroRegions z;
     z.n = 4;
@@ -1003,7 +1048,22 @@ static int trace_pass(const ng_octree& tree, const ng_render_cfg& cfg, const Lod
     k_zero_regions<<<grid_for(n / 2 + 1, 256), 256, 0, s>>>(z);
     NG_CHECK_LAUNCH("k_zero_regions");
   }
-  for (int t = 0; t < target; ++t) {
+  if (tiles) {
+    // one launch: level passes per 32-ray tile, the pair lists in shared
+    // memory with the two pair buffers as the spill arena; the control words
+    // (tile counter, hit cursor, longest tile list) live in the zeroed
+    // look-back scratch
+    const size_t arena_bytes = L.hits - L.pairs_a;
+    unsigned long long* need = (unsigned long long*)((char*)scratch + 16);
+    r = traverse_tiles(tree, rays, &counts[0], target, counts, hits, ws.hit_capacity, scratch, seg_start, seg_end,
+                       b + L.pairs_a, arena_bytes, need, shared_origin, s);
+    if (r) return r;
+    tov.need = need;
+    tov.lim = tile_traverse_limit(arena_bytes);
+    tov.scap = tile_traverse_scap();
+    tov.warps = tile_traverse_warps();
+  }
+  for (int t = 0; t < (tiles ? 0 : target); ++t) {
     const bool last = (t + 1 == target);
     ng_pair* out = (t % 2 == 0) ? pa : pb;
     r = traverse_hits(tree, rays, t, last, in, &counts[t], in_cap, last ? nullptr : out, last ? hits : nullptr,
@@ -1082,12 +1142,16 @@ static int render_common(const ng_octree& tree, const ng_field& f, const ng_rend
   }
   uint8_t bg[3];
   background_u8(cfg, bg);
+  const int target0 = cfg.trace_level + tree.n_virtual;
+  // the tile traversal writes every ray's segment itself
+  int64_t* zseg_s = use_tile_traverse(target0) ? nullptr : seg_start;
+  int64_t* zseg_e = use_tile_traverse(target0) ? nullptr : seg_end;
   if (cam) {
-    k_camera_rays<<<grid_for(n, 256), 256, 0, s>>>(*cam, rays, fr, bg[0], bg[1], bg[2], &st->pairs[0], seg_start,
-                                                   seg_end);
+    k_camera_rays<<<grid_for(n, 256), 256, 0, s>>>(*cam, rays, fr, bg[0], bg[1], bg[2], &st->pairs[0], zseg_s,
+                                                   zseg_e);
     NG_CHECK_LAUNCH("k_camera_rays");
   } else {
-    k_frame_defaults<<<grid_for(n, 256), 256, 0, s>>>(fr, n, bg[0], bg[1], bg[2], seg_start, seg_end);
+    k_frame_defaults<<<grid_for(n, 256), 256, 0, s>>>(fr, n, bg[0], bg[1], bg[2], zseg_s, zseg_e);
     NG_CHECK_LAUNCH("k_frame_defaults");
     k_set_count<<<1, 1, 0, s>>>(&st->pairs[0], n);  // root list (i, 0) of n rays
     NG_CHECK_LAUNCH("k_set_count");
@@ -1097,8 +1161,9 @@ static int render_common(const ng_octree& tree, const ng_field& f, const ng_rend
   const LodPlan P = plan_lod(cfg);
   MarchArgs A;
   // camera rays share the eye position (a host value, captured into the launches)
+  TileOverflow tov;
   if ((r = trace_pass(tree, cfg, P, rays, n, st->pairs, L, ws, b, ctr + 0, ctr + 2, s, A, true,
-                      cam ? cam->position : nullptr)))
+                      cam ? cam->position : nullptr, tov)))
     return r;
   A.hit = fr.hit;
   A.t = fr.t;
@@ -1134,7 +1199,7 @@ static int render_common(const ng_octree& tree, const ng_field& f, const ng_rend
     B.counters = &st->counters;
     if ((r = launch_normals(tree, f, B, n, s))) return r;
   }
-  k_finish_stats<<<1, 1, 0, s>>>(st, target, ws.pair_capacity, ws.hit_capacity, ctr + 1, ctr + 0);
+  k_finish_stats<<<1, 1, 0, s>>>(st, target, ws.pair_capacity, ws.hit_capacity, ctr + 1, ctr + 0, tov);
   NG_CHECK_LAUNCH("k_finish_stats");
   // ---- shadow rays toward the light (configs[4]) with the same traversal + march
   if (cfg.shadows && do_normals) {
@@ -1143,8 +1208,9 @@ static int render_common(const ng_octree& tree, const ng_field& f, const ng_rend
                                                   &st->shadow_pairs[0]);
     NG_CHECK_LAUNCH("k_shadow_rays");
     MarchArgs S;
+    TileOverflow stov;
     if ((r = trace_pass(tree, cfg, P, srays, n, st->shadow_pairs, L, ws, b, ctr + 3, ctr + 4, s, S, false,
-                        nullptr)))
+                        nullptr, stov)))
       return r;
     S.hit = (uint8_t*)(b + L.s_hit);
     // the march writes only the rays that have a voxel segment: clear the rest
@@ -1160,7 +1226,7 @@ static int render_common(const ng_octree& tree, const ng_field& f, const ng_rend
     k_shade_shadowed<<<grid_for(n, 256), 256, 0, s>>>(hit_list, ctr + 1, fr.normal, S.hit, cfg, fr.color,
                                                      &st->shadowed);
     NG_CHECK_LAUNCH("k_shade_shadowed");
-    k_shadow_overflow<<<1, 1, 0, s>>>(st, target, ws.pair_capacity, ws.hit_capacity);
+    k_shadow_overflow<<<1, 1, 0, s>>>(st, target, ws.pair_capacity, ws.hit_capacity, stov);
     NG_CHECK_LAUNCH("k_shadow_overflow");
   }
   return NG_OK;

@@ -276,6 +276,321 @@ __global__ void __launch_bounds__(TR_NT) k_traverse_hits(
   }
 }
 
+// Render-path traversal of a whole ray tile in one warp (all levels, one
+// launch). A warp takes 32 consecutive rays and runs the same hit-filtered
+// breadth-first passes as k_traverse_hits over its own pair lists, kept in
+// shared memory (spilling to a per-warp global arena for silhouette tiles):
+// decide + scan + subdivide become warp shuffles, with no grid-wide
+// look-back and no launch per level. Each ray's final pairs come out in the
+// reference's order (parents in list order, children front to back), so
+// per-ray segments are the reference's sub-lists; only the placement of a
+// tile's block in the final list depends on when the warp claims it (one
+// atomic per tile), which the march does not see.
+constexpr int TT_WPB = 8;      // warps per CTA
+constexpr int TT_SCAP = 640;   // pairs per warp-local list held in shared memory
+constexpr int TT_ITEMS = 2;    // pairs per lane per round
+
+struct TileWarp {
+  double o[32][3];
+  double inv[32][3];
+  int flags[32];
+  int seg_s[32], seg_e[32];
+  int32_t vox[2][TT_SCAP];
+  uint8_t ray[2][TT_SCAP];
+};
+
+struct TileList {
+  int32_t* svox;
+  uint8_t* sray;
+  int32_t* gvox;
+  uint8_t* gray;
+};
+
+__device__ __forceinline__ void tl_put(const TileList& b, int i, int32_t v, int r, int64_t gcap) {
+  if (i < TT_SCAP) {
+    b.svox[i] = v;
+    b.sray[i] = (uint8_t)r;
+  } else if (i - TT_SCAP < gcap) {
+    b.gvox[i - TT_SCAP] = v;
+    b.gray[i - TT_SCAP] = (uint8_t)r;
+  }
+}
+
+__device__ __forceinline__ void tl_get(const TileList& b, int i, int32_t& v, int& r) {
+  if (i < TT_SCAP) {
+    v = b.svox[i];
+    r = b.sray[i];
+  } else {
+    v = b.gvox[i - TT_SCAP];
+    r = b.gray[i - TT_SCAP];
+  }
+}
+
+__device__ __forceinline__ TileList tile_list(TileWarp* W, uint8_t* ga, int64_t gcap, int k) {
+  TileList b;
+  b.svox = W->vox[k];
+  b.sray = W->ray[k];
+  b.gvox = reinterpret_cast<int32_t*>(ga) + k * gcap;
+  b.gray = ga + 8 * gcap + k * gcap;
+  return b;
+}
+
+__device__ __forceinline__ void tw_ray(const TileWarp* W, int rl, ng_ray& r) {
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    r.o[a] = W->o[rl][a];
+    r.inv[a] = W->inv[rl][a];
+    r.d[a] = 0.0;
+  }
+  r.flags = W->flags[rl] & 0xff;
+  r.pad = 0;
+}
+
+// compact3 for codes below 2^30 (cells per axis <= 1024), in 32-bit ops.
+__device__ __forceinline__ uint32_t compact3_30(uint32_t v) {
+  v &= 0x09249249u;
+  v = (v ^ (v >> 2)) & 0x030c30c3u;
+  v = (v ^ (v >> 4)) & 0x0300f00fu;
+  v = (v ^ (v >> 8)) & 0xff0000ffu;
+  v = (v ^ (v >> 16)) & 0x000003ffu;
+  return v;
+}
+
+constexpr int TT_NAN_FREE = 1 << 8;  // ray flag: no slab value of this ray can be NaN
+
+// Hit bits (bit = octant) of the 8 children of parent cell pc for a ray
+// whose slab values are never NaN (finite origin, each axis either a zero
+// direction or a finite 1/d). Then numpy's NaN-propagating min / max equal
+// fmin / fmax and max / min over three axes do not depend on the order, so
+// near / far are formed from pairwise axis-0/1 bounds shared by 4 children
+// each. Same decisions as child_slabs + child_hit (ray_aabb_batch); the
+// sign of a zero t can differ, which no decision sees.
+__device__ __forceinline__ unsigned child_hits_nanfree(const TileWarp* W, int rl, const int pc[3], int cres) {
+  const double h = 2.0 / (double)cres;
+  const int fl = W->flags[rl];
+  double an[3][2], af[3][2];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const double o = W->o[rl][a];
+    // child planes: exact dyadic values, so the sums are exact (= cell_lo)
+    const double p0 = dadd(-1.0, dmul((double)(2 * pc[a]), h));
+    const double p1 = dadd(p0, h), p2 = dadd(p1, h);
+    if ((fl >> (3 + a)) & 1) {
+      const bool in0 = (o >= p0) && (o <= p1);
+      const bool in1 = (o >= p1) && (o <= p2);
+      an[a][0] = in0 ? -INFINITY : INFINITY;
+      af[a][0] = in0 ? INFINITY : -INFINITY;
+      an[a][1] = in1 ? -INFINITY : INFINITY;
+      af[a][1] = in1 ? INFINITY : -INFINITY;
+    } else {
+      const double inv = W->inv[rl][a];
+      const double t0 = dmul(dsub(p0, o), inv), t1 = dmul(dsub(p1, o), inv), t2 = dmul(dsub(p2, o), inv);
+      an[a][0] = fmin(t0, t1);
+      af[a][0] = fmax(t0, t1);
+      an[a][1] = fmin(t1, t2);
+      af[a][1] = fmax(t1, t2);
+    }
+  }
+  double n01[4], f01[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    n01[j] = fmax(an[0][j & 1], an[1][j >> 1]);
+    f01[j] = fmin(af[0][j & 1], af[1][j >> 1]);
+  }
+  unsigned hit = 0;
+#pragma unroll
+  for (int oct = 0; oct < 8; ++oct) {
+    const double near = fmax(n01[oct & 3], an[2][oct >> 2]);
+    const double far = fmin(f01[oct & 3], af[2][oct >> 2]);
+    hit |= ((near <= far) && (far >= 0.0) ? 1u : 0u) << oct;
+  }
+  return hit;
+}
+
+// Octant-indexed bits -> front-to-back order: bit k <- bit k ^ dm.
+__device__ __forceinline__ unsigned octants_front_to_back(unsigned x, int dm) {
+  if (dm & 1) x = ((x & 0x55u) << 1) | ((x >> 1) & 0x55u);
+  if (dm & 2) x = ((x & 0x33u) << 2) | ((x >> 2) & 0x33u);
+  if (dm & 4) x = ((x & 0x0fu) << 4) | ((x >> 4) & 0x0fu);
+  return x;
+}
+
+__global__ void __launch_bounds__(TT_WPB * 32) k_traverse_tiles(
+    const __grid_constant__ ng_octree tree, const ng_ray* __restrict__ rays, const int64_t* __restrict__ d_n,
+    int target, int64_t* counts, ng_hit_pair* __restrict__ hits, int64_t hit_cap, unsigned int* tile_counter,
+    unsigned long long* hit_cursor, int64_t* __restrict__ seg_start, int64_t* __restrict__ seg_end,
+    uint8_t* arena, int64_t gcap, unsigned long long* d_need, const SharedOrigin so) {
+  extern __shared__ __align__(16) uint8_t tt_smem[];
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  TileWarp* W = reinterpret_cast<TileWarp*>(tt_smem) + warp;
+  const int64_t gw = (int64_t)blockIdx.x * TT_WPB + warp;
+  uint8_t* ga = arena + gw * gcap * 10;  // [vox0 | vox1 | ray0 | ray1]
+  const int64_t n = *d_n;
+  const int64_t n_tiles = (n + 31) / 32;
+  const int lim = TT_SCAP + (int)gcap;
+  int64_t level_cnt = 0;  // lane t: pairs emitted at traversal level t
+  int need = 0;
+  while (true) {
+    unsigned int tile = 0;
+    if (lane == 0) tile = atomicAdd(tile_counter, 1u);
+    tile = __shfl_sync(FULL, tile, 0);
+    if ((int64_t)tile >= n_tiles) break;
+    const int64_t r0 = (int64_t)tile * 32;
+    const int nr = (int)((n - r0) < 32 ? (n - r0) : 32);
+    // ---- the tile's rays, and the root list: rays whose box test hits B
+    bool root = false;
+    if (lane < nr) {
+      ng_ray r;
+      load_ray_slab(rays, r0 + lane, so, r);
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        W->o[lane][a] = r.o[a];
+        W->inv[lane][a] = r.inv[a];
+      }
+      bool nan_free = true;
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+        nan_free = nan_free && isfinite(r.o[a]) && (((r.flags >> (3 + a)) & 1) || isfinite(r.inv[a]));
+      W->flags[lane] = r.flags | (nan_free ? TT_NAN_FREE : 0);
+      const double lo[3] = {-1.0, -1.0, -1.0}, hi[3] = {1.0, 1.0, 1.0};
+      double a0, b0;
+      root = slab_test(r, lo, hi, a0, b0);
+    }
+    W->seg_s[lane] = 0;
+    W->seg_e[lane] = 0;
+    const unsigned rb = __ballot_sync(FULL, root);
+    if (root) tl_put(tile_list(W, ga, gcap, 0), __popc(rb & lanemask_lt()), 0, lane, gcap);
+    int nc = __popc(rb);
+    __syncwarp();
+    // ---- level passes: hits at level t -> hit children at level t+1
+    for (int t = 0; t < target; ++t) {
+      const TileList src = tile_list(W, ga, gcap, t & 1);
+      const TileList dst = tile_list(W, ga, gcap, (t & 1) ^ 1);
+      const int cres = level_res(tree, t - tree.n_virtual + 1);
+      const bool small = cres <= 2048;  // parent codes below 2^30
+      const uint64_t* __restrict__ codes = tree.codes[t];
+      const int32_t* __restrict__ cstart = tree.child_start[t];
+      const uint8_t* __restrict__ cmask = tree.child_mask[t];
+      int out = 0;
+      for (int base = 0; base < nc; base += 32 * TT_ITEMS) {
+        int32_t pv[TT_ITEMS];
+        int pr[TT_ITEMS];
+        unsigned hm[TT_ITEMS];
+        int32_t first[TT_ITEMS];
+        int sum = 0;
+#pragma unroll
+        for (int q = 0; q < TT_ITEMS; ++q) {
+          const int i = base + lane * TT_ITEMS + q;
+          hm[q] = 0;
+          pv[q] = 0;
+          pr[q] = 0;
+          first[q] = 0;
+          if (i < nc) {
+            tl_get(src, i, pv[q], pr[q]);
+            const unsigned m = __ldg(cmask + pv[q]);
+            const uint64_t c = __ldg(codes + pv[q]);
+            first[q] = __ldg(cstart + pv[q]);
+            int pc[3];
+            if (small) {
+              const uint32_t c32 = (uint32_t)c;
+              pc[0] = (int)compact3_30(c32);
+              pc[1] = (int)compact3_30(c32 >> 1);
+              pc[2] = (int)compact3_30(c32 >> 2);
+            } else {
+              pc[0] = (int)compact3(c);
+              pc[1] = (int)compact3(c >> 1);
+              pc[2] = (int)compact3(c >> 2);
+            }
+            const int fl = W->flags[pr[q]];
+            const int dm = fl & 7;
+            unsigned ho;
+            if (fl & TT_NAN_FREE) {
+              ho = child_hits_nanfree(W, pr[q], pc, cres);
+            } else {
+              ng_ray r;
+              tw_ray(W, pr[q], r);
+              ChildSlabs cs;
+              child_slabs(r, pc[0], pc[1], pc[2], cres, cs);
+              ho = 0;
+#pragma unroll
+              for (int oct = 0; oct < 8; ++oct) {
+                double a0, b0;
+                if (child_hit(cs, oct, a0, b0)) ho |= 1u << oct;
+              }
+            }
+            hm[q] = octants_front_to_back(ho & m, dm);
+            if (hm[q]) hm[q] |= ((unsigned)dm << 8) | (m << 16);
+          }
+          sum += __popc(hm[q] & 0xffu);
+        }
+        const int incl = warp_incl_scan<int>(sum);
+        int o = out + incl - sum;
+#pragma unroll
+        for (int q = 0; q < TT_ITEMS; ++q) {
+          const int dm = (int)((hm[q] >> 8) & 7u);
+          const unsigned m = (hm[q] >> 16) & 0xffu;
+          for (unsigned bits = hm[q] & 0xffu; bits; bits &= bits - 1) {
+            const int oct = (__ffs(bits) - 1) ^ dm;
+            tl_put(dst, o, first[q] + __popc(m & ((1u << oct) - 1u)), pr[q], gcap);
+            ++o;
+          }
+        }
+        out += __shfl_sync(FULL, incl, 31);
+      }
+      __syncwarp();
+      if (lane == t + 1) level_cnt += out;
+      need = out > need ? out : need;
+      nc = out < lim ? out : lim;
+    }
+    // ---- final pairs: claim the tile's block of the hit list, write
+    // (ray, voxel, t_enter, t_exit) and the per-ray segments
+    const TileList fin = tile_list(W, ga, gcap, target & 1);
+    unsigned long long hb = 0;
+    if (lane == 0 && nc > 0) hb = atomicAdd(hit_cursor, (unsigned long long)nc);
+    const int64_t hbase = (int64_t)__shfl_sync(FULL, hb, 0);
+    const int fres = level_res(tree, target - tree.n_virtual);
+    const double fedge = 2.0 / (double)fres;
+    const uint64_t* __restrict__ fcodes = tree.codes[target];
+    for (int i = lane; i < nc; i += 32) {
+      int32_t v;
+      int rl;
+      tl_get(fin, i, v, rl);
+      int32_t pv_;
+      int prev = -1, next = -1;
+      if (i > 0) tl_get(fin, i - 1, pv_, prev);
+      if (i + 1 < nc) tl_get(fin, i + 1, pv_, next);
+      if (prev != rl) W->seg_s[rl] = i;
+      if (next != rl) W->seg_e[rl] = i + 1;
+      const uint64_t c = __ldg(fcodes + v);
+      const int cc[3] = {(int)compact3(c), (int)compact3(c >> 1), (int)compact3(c >> 2)};
+      double lo[3], hi[3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        lo[a] = cell_lo(cc[a], fres);
+        hi[a] = dadd(lo[a], fedge);
+      }
+      ng_ray r;
+      tw_ray(W, rl, r);
+      ng_hit_pair h;
+      h.ray = (int32_t)(r0 + rl);
+      h.voxel = v;
+      slab_test(r, lo, hi, h.t_enter, h.t_exit);
+      if (hbase + i < hit_cap) hits[hbase + i] = h;
+    }
+    __syncwarp();
+    if (lane < nr) {
+      const int64_t s0 = hbase + W->seg_s[lane], e0 = hbase + W->seg_e[lane];
+      seg_start[r0 + lane] = s0 < hit_cap ? s0 : hit_cap;
+      seg_end[r0 + lane] = e0 < hit_cap ? e0 : hit_cap;
+    }
+    __syncwarp();
+  }
+  if (lane >= 1 && lane <= target && level_cnt) atomicAdd((unsigned long long*)(counts + lane),
+                                                          (unsigned long long)level_cnt);
+  if (lane == 0 && need > TT_SCAP) atomicMax(d_need, (unsigned long long)need);
+}
+
 __global__ void k_segments(const ng_hit_pair* __restrict__ hits, const int64_t* __restrict__ d_count,
                            int64_t cap, int64_t n_rays, int64_t* __restrict__ seg_start,
                            int64_t* __restrict__ seg_end) {
@@ -432,6 +747,46 @@ int traverse_hits(const ng_octree& tree, const ng_ray* rays, int t, bool next_fi
                                                   d_count_out, out_cap, states, counter, nullptr, nullptr, so);
   NG_CHECK_LAUNCH("k_traverse_hits");
   return NG_OK;
+}
+
+size_t tile_traverse_smem() { return sizeof(TileWarp) * TT_WPB; }
+int tile_traverse_scap() { return TT_SCAP; }
+
+// Warps the tile traversal runs with (grid x TT_WPB); the per-warp global
+// arena is sized from this.
+int64_t tile_traverse_warps() {
+  static int per_sm = -1;
+  if (per_sm < 0) {
+    cudaFuncSetAttribute(k_traverse_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)tile_traverse_smem());
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_traverse_tiles, TT_WPB * 32,
+                                                      tile_traverse_smem()) != cudaSuccess || per_sm < 1)
+      per_sm = 1;
+  }
+  return (int64_t)sm_count() * per_sm * TT_WPB;
+}
+
+int traverse_tiles(const ng_octree& tree, const ng_ray* rays, const int64_t* d_n, int target, int64_t* counts,
+                   ng_hit_pair* hits, int64_t hit_cap, void* ctl, int64_t* seg_start, int64_t* seg_end,
+                   void* arena, size_t arena_bytes, unsigned long long* d_need, const double* shared_origin,
+                   cudaStream_t s) {
+  // `ctl` (zeroed by the caller): u32 tile counter at 0, u64 hit cursor at 8
+  SharedOrigin so;
+  so.shared = shared_origin != nullptr;
+  for (int a = 0; a < 3; ++a) so.o[a] = shared_origin ? shared_origin[a] : 0.0;
+  const int64_t warps = tile_traverse_warps();
+  const int64_t gcap = (int64_t)(arena_bytes / (size_t)(warps * 10)) & ~int64_t(15);
+  k_traverse_tiles<<<(int)(warps / TT_WPB), TT_WPB * 32, tile_traverse_smem(), s>>>(
+      tree, rays, d_n, target, counts, hits, hit_cap, (unsigned int*)ctl,
+      (unsigned long long*)((char*)ctl + 8), seg_start, seg_end, (uint8_t*)arena, gcap, d_need, so);
+  NG_CHECK_LAUNCH("k_traverse_tiles");
+  return NG_OK;
+}
+
+// Longest tile list the arena (the two pair buffers) holds.
+int64_t tile_traverse_limit(size_t arena_bytes) {
+  const int64_t warps = tile_traverse_warps();
+  return TT_SCAP + ((int64_t)(arena_bytes / (size_t)(warps * 10)) & ~int64_t(15));
 }
 
 int segments(const ng_hit_pair* hits, const int64_t* d_count, int64_t cap, int64_t n_rays,

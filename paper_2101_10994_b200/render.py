@@ -503,7 +503,7 @@ class RenderSession:
         if not st.overflow:
             return False
         need_pairs = max(st.pairs[t] for t in range(1, n_levels))
-        self.pair_cap = max(self.pair_cap, int(need_pairs) + 4096)
+        self.pair_cap = max(self.pair_cap, int(need_pairs) + 4096, int(st.pair_need))
         self.hit_cap = max(self.hit_cap, int(st.pairs[n_levels]) + 4096)
         self._alloc_ws()
         return True

@@ -39,7 +39,7 @@ def test_struct_sizes_match_header_layout():
     assert ctypes.sizeof(_lib.NgField) == 40 + 8 + 8 + 8 + 4 + 4  # + presum table pointer, offset, corners, level, mask
     assert ctypes.sizeof(_lib.NgQueryArgs) == 24
     assert ctypes.sizeof(_lib.NgCamera) == 12 * 8 + 2 * 8 + 6 * 4
-    assert ctypes.sizeof(_lib.NgFrameStats) == (17 + 2 + 4 + 1 + 17 + 1) * 8
+    assert ctypes.sizeof(_lib.NgFrameStats) == (17 + 2 + 4 + 1 + 17 + 1 + 1) * 8
     assert _lib.RAY_BYTES == 80 and _lib.HIT_PAIR_BYTES == 24
 
 
