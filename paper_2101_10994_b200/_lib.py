@@ -16,7 +16,10 @@ import torch
 from .errors import ConfigError, OctfieldError, StructuralError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libnglod_b200.so")
+# NG_LIB_VARIANT=name loads variants/libnglod_<name>.so (tools/build_variant.sh:
+# the same sources with different compile-time knobs, for A/B timing)
+LIB_PATH = (os.path.join(HERE, "variants", f"libnglod_{os.environ['NG_LIB_VARIANT']}.so")
+            if os.environ.get("NG_LIB_VARIANT") else os.path.join(HERE, "libnglod_b200.so"))
 
 NG_OK = 0
 NG_ERR_STRUCTURAL = 1

@@ -24,13 +24,15 @@ int traverse_hits(const ng_octree& tree, const ng_ray* rays, int t, bool next_fi
                   const int64_t* d_count_in, int64_t in_cap, ng_pair* out_pairs, ng_hit_pair* out_hits,
                   int64_t* d_count_out, int64_t out_cap, void* scratch, size_t scratch_bytes, cudaStream_t s,
                   int64_t* seg_start, int64_t* seg_end, const double* shared_origin);
-int traverse_tiles(const ng_octree& tree, const ng_ray* rays, const int64_t* d_n, int target, int64_t* counts,
+int traverse_tiles(const ng_octree& tree, const ng_ray* rays, const int64_t* d_n, int64_t n_max, int target,
+                   int64_t* counts,
                    ng_hit_pair* hits, int64_t hit_cap, void* ctl, int64_t* seg_start, int64_t* seg_end,
                    void* arena, size_t arena_bytes, unsigned long long* d_need, const double* shared_origin,
                    cudaStream_t s);
-int64_t tile_traverse_limit(size_t arena_bytes);
-int64_t tile_traverse_warps();
+int64_t tile_traverse_limit(size_t arena_bytes, int64_t n_max);
+int64_t tile_traverse_warps(int64_t n_max);
 int tile_traverse_scap();
+int tile_traverse_entry_bytes();
 
 // NG_TILE_TRAVERSE=0 selects the level-by-level traversal launches
 // (k_traverse_hits) instead of the warp-per-tile kernel.
@@ -40,7 +42,7 @@ static bool use_tile_traverse(int target) {
     const char* e = getenv("NG_TILE_TRAVERSE");
     on = (e && e[0] == '0') ? 0 : 1;
   }
-  return on && target >= 1;
+  return on && target >= 1 && target <= 10;  // packed cells: <= 1024 per axis
 }
 
 constexpr int R_NW = 8;  // warps per CTA for march / normals
@@ -728,17 +730,17 @@ __global__ void k_hit_points(const ng_ray* __restrict__ rays, const uint8_t* __r
 
 // Tile traversal: a tile list longer than the arena holds (`tile_need`
 // against `lim`) asks for a rerun with the pair capacity whose arena share
-// (10 bytes per pair per warp beyond the shared-memory lists, out of 16
-// bytes per unit of capacity) holds it, plus a quarter.
+// (`entry` bytes per pair per warp beyond the shared-memory lists, out of
+// 16 bytes per unit of capacity) holds it, plus a quarter.
 struct TileOverflow {
   const unsigned long long* need;  // null: level-by-level traversal
-  int64_t lim, scap, warps;
+  int64_t lim, scap, warps, entry;
 };
 
 __device__ __forceinline__ int64_t tile_overflow(ng_frame_stats* st, const TileOverflow& T) {
   if (T.need == nullptr || (int64_t)*T.need <= T.lim) return 0;
   const int64_t spill = ((int64_t)*T.need - T.scap + 16) * 5 / 4;
-  const int64_t want = spill * 10 * T.warps / 16 + 4096;
+  const int64_t want = spill * T.entry * T.warps / 16 + 4096;
   if (want > st->pair_need) st->pair_need = want;
   return 1;
 }
@@ -972,12 +974,18 @@ struct WsLayout {
 
 static size_t al(size_t x) { return (x + 255) & ~size_t(255); }
 
+constexpr int64_t TILE_ARENA_MIN = 2048;
+
 static WsLayout layout(int64_t n, int64_t pair_cap, int64_t hit_cap) {
   WsLayout L;
   size_t o = 0;
   L.rays = o; o = al(o + (size_t)n * sizeof(ng_ray));
-  L.pairs_a = o; o = al(o + (size_t)pair_cap * sizeof(ng_pair));
-  L.pairs_b = o; o = al(o + (size_t)pair_cap * sizeof(ng_pair));
+  // the two pair buffers double as the tile traversal's spill arena: at
+  // least TILE_ARENA_MIN list entries per warp whatever the frame size
+  const size_t tile_arena = (size_t)tile_traverse_warps(n) * TILE_ARENA_MIN * tile_traverse_entry_bytes();
+  const size_t pair_bytes = std::max((size_t)pair_cap * sizeof(ng_pair), tile_arena / 2);
+  L.pairs_a = o; o = al(o + pair_bytes);
+  L.pairs_b = o; o = al(o + pair_bytes);
   L.hits = o; o = al(o + (size_t)hit_cap * sizeof(ng_hit_pair));
   L.seg_start = o; o = al(o + (size_t)n * 8);
   L.seg_end = o; o = al(o + (size_t)n * 8);
@@ -1055,13 +1063,14 @@ static int trace_pass(const ng_octree& tree, const ng_render_cfg& cfg, const Lod
     // look-back scratch
     const size_t arena_bytes = L.hits - L.pairs_a;
     unsigned long long* need = (unsigned long long*)((char*)scratch + 16);
-    r = traverse_tiles(tree, rays, &counts[0], target, counts, hits, ws.hit_capacity, scratch, seg_start, seg_end,
+    r = traverse_tiles(tree, rays, &counts[0], n, target, counts, hits, ws.hit_capacity, scratch, seg_start, seg_end,
                        b + L.pairs_a, arena_bytes, need, shared_origin, s);
     if (r) return r;
     tov.need = need;
-    tov.lim = tile_traverse_limit(arena_bytes);
+    tov.lim = tile_traverse_limit(arena_bytes, n);
     tov.scap = tile_traverse_scap();
-    tov.warps = tile_traverse_warps();
+    tov.warps = tile_traverse_warps(n);
+    tov.entry = tile_traverse_entry_bytes();
   }
   for (int t = 0; t < (tiles ? 0 : target); ++t) {
     const bool last = (t + 1 == target);

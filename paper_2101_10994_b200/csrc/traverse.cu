@@ -277,68 +277,97 @@ __global__ void __launch_bounds__(TR_NT) k_traverse_hits(
 }
 
 // Render-path traversal of a whole ray tile in one warp (all levels, one
-// launch). A warp takes 32 consecutive rays and runs the same hit-filtered
-// breadth-first passes as k_traverse_hits over its own pair lists, kept in
-// shared memory (spilling to a per-warp global arena for silhouette tiles):
-// decide + scan + subdivide become warp shuffles, with no grid-wide
-// look-back and no launch per level. Each ray's final pairs come out in the
-// reference's order (parents in list order, children front to back), so
-// per-ray segments are the reference's sub-lists; only the placement of a
-// tile's block in the final list depends on when the warp claims it (one
-// atomic per tile), which the march does not see.
-constexpr int TT_WPB = 8;      // warps per CTA
-constexpr int TT_SCAP = 640;   // pairs per warp-local list held in shared memory
-constexpr int TT_ITEMS = 2;    // pairs per lane per round
+// launch). A warp takes TT_RAYS consecutive rays and runs the same
+// hit-filtered breadth-first passes as k_traverse_hits over its own pair
+// lists, kept in shared memory (spilling to a per-warp global arena for
+// silhouette tiles): decide + scan + subdivide become warp shuffles, with no
+// grid-wide look-back and no launch per level. Each ray's final pairs come
+// out in the reference's order (parents in list order, children front to
+// back), so per-ray segments are the reference's sub-lists; only the
+// placement of a tile's block in the final list depends on when the warp
+// claims it (one atomic per tile), which the march does not see.
+#ifndef NG_TT_RAYS
+#define NG_TT_RAYS 32
+#endif
+#ifndef NG_TT_SCAP
+#define NG_TT_SCAP 512
+#endif
+#ifndef NG_TT_ITEMS
+#define NG_TT_ITEMS 2
+#endif
+#ifndef NG_TT_WPB
+#define NG_TT_WPB 8
+#endif
+constexpr int TT_WPB = NG_TT_WPB;      // warps per CTA
+constexpr int TT_RAYS = NG_TT_RAYS;    // rays per tile (<= 256: list entries keep a u8 ray slot)
+constexpr int TT_SCAP = NG_TT_SCAP;    // pairs per warp-local list held in shared memory
+constexpr int TT_ITEMS = NG_TT_ITEMS;  // pairs per lane per round
+constexpr int TT_ENTRY = 9;            // list entry bytes: voxel i32, packed cell u32, ray u8
 
 struct TileWarp {
-  double o[32][3];
-  double inv[32][3];
-  int flags[32];
-  int seg_s[32], seg_e[32];
+  double o[TT_RAYS][3];  // per-ray origins (unused when the rays share one)
+  double inv[TT_RAYS][3];
+  int flags[TT_RAYS];
+  int seg_s[TT_RAYS], seg_e[TT_RAYS];
   int32_t vox[2][TT_SCAP];
+  uint32_t cell[2][TT_SCAP];  // x | y << 10 | z << 20 at the list's level
   uint8_t ray[2][TT_SCAP];
 };
 
 struct TileList {
   int32_t* svox;
+  uint32_t* scell;
   uint8_t* sray;
   int32_t* gvox;
+  uint32_t* gcell;
   uint8_t* gray;
 };
 
-__device__ __forceinline__ void tl_put(const TileList& b, int i, int32_t v, int r, int64_t gcap) {
+__device__ __forceinline__ void tl_put(const TileList& b, int i, int32_t v, uint32_t c, int r, int64_t gcap) {
   if (i < TT_SCAP) {
     b.svox[i] = v;
+    b.scell[i] = c;
     b.sray[i] = (uint8_t)r;
   } else if (i - TT_SCAP < gcap) {
     b.gvox[i - TT_SCAP] = v;
+    b.gcell[i - TT_SCAP] = c;
     b.gray[i - TT_SCAP] = (uint8_t)r;
   }
 }
 
-__device__ __forceinline__ void tl_get(const TileList& b, int i, int32_t& v, int& r) {
+__device__ __forceinline__ void tl_get(const TileList& b, int i, int32_t& v, uint32_t& c, int& r) {
   if (i < TT_SCAP) {
     v = b.svox[i];
+    c = b.scell[i];
     r = b.sray[i];
   } else {
     v = b.gvox[i - TT_SCAP];
+    c = b.gcell[i - TT_SCAP];
     r = b.gray[i - TT_SCAP];
   }
 }
 
+__device__ __forceinline__ int tl_ray(const TileList& b, int i) {
+  return i < TT_SCAP ? b.sray[i] : b.gray[i - TT_SCAP];
+}
+
+// arena per warp: [vox0 | vox1 | cell0 | cell1 | ray0 | ray1], gcap entries each
 __device__ __forceinline__ TileList tile_list(TileWarp* W, uint8_t* ga, int64_t gcap, int k) {
   TileList b;
   b.svox = W->vox[k];
+  b.scell = W->cell[k];
   b.sray = W->ray[k];
   b.gvox = reinterpret_cast<int32_t*>(ga) + k * gcap;
-  b.gray = ga + 8 * gcap + k * gcap;
+  b.gcell = reinterpret_cast<uint32_t*>(ga + 8 * gcap) + k * gcap;
+  b.gray = ga + 16 * gcap + k * gcap;
   return b;
 }
 
-__device__ __forceinline__ void tw_ray(const TileWarp* W, int rl, ng_ray& r) {
+template <bool SO>
+__device__ __forceinline__ void tw_ray(const TileWarp* W, const SharedOrigin& so, int rl, ng_ray& r) {
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
-    r.o[a] = W->o[rl][a];
+    r.o[a] = SO ? so.o[a] : W->o[rl][a];
     r.inv[a] = W->inv[rl][a];
     r.d[a] = 0.0;
   }
@@ -346,65 +375,51 @@ __device__ __forceinline__ void tw_ray(const TileWarp* W, int rl, ng_ray& r) {
   r.pad = 0;
 }
 
-// compact3 for codes below 2^30 (cells per axis <= 1024), in 32-bit ops.
-__device__ __forceinline__ uint32_t compact3_30(uint32_t v) {
-  v &= 0x09249249u;
-  v = (v ^ (v >> 2)) & 0x030c30c3u;
-  v = (v ^ (v >> 4)) & 0x0300f00fu;
-  v = (v ^ (v >> 8)) & 0xff0000ffu;
-  v = (v ^ (v >> 16)) & 0x000003ffu;
-  return v;
+// ray flag: finite origin, finite nonzero direction on every axis (then no
+// slab value is NaN and none of the zero-direction rules applies)
+constexpr int TT_GENERAL = 1 << 8;
+
+// Per-axis plane crossings of a cell's two child halves, in ray order:
+// q0 <= q1 <= q2 are t at the near face, the mid plane and the far face.
+// The planes are exact dyadic values and (p - o) * inv is monotone in p, so
+// these are the reference's t1 / t2 of each child box, sorted.
+__device__ __forceinline__ void axis_crossings(double o, double inv, bool neg, int pc, int cres, double& q0,
+                                               double& q1, double& q2) {
+  const double h = 2.0 / (double)cres;
+  const double pf = dmul((double)(2 * pc + (neg ? 2 : 0) - cres / 2), h);  // -1 + e h, exact
+  const double hs = neg ? -h : h;
+  const double pm = dadd(pf, hs), pl = dadd(pm, hs);
+  q0 = dmul(dsub(pf, o), inv);
+  q1 = dmul(dsub(pm, o), inv);
+  q2 = dmul(dsub(pl, o), inv);
 }
 
-constexpr int TT_NAN_FREE = 1 << 8;  // ray flag: no slab value of this ray can be NaN
-
-// Hit bits (bit = octant) of the 8 children of parent cell pc for a ray
-// whose slab values are never NaN (finite origin, each axis either a zero
-// direction or a finite 1/d). Then numpy's NaN-propagating min / max equal
-// fmin / fmax and max / min over three axes do not depend on the order, so
-// near / far are formed from pairwise axis-0/1 bounds shared by 4 children
-// each. Same decisions as child_slabs + child_hit (ray_aabb_batch); the
-// sign of a zero t can differ, which no decision sees.
-__device__ __forceinline__ unsigned child_hits_nanfree(const TileWarp* W, int rl, const int pc[3], int cres) {
-  const double h = 2.0 / (double)cres;
-  const int fl = W->flags[rl];
-  double an[3][2], af[3][2];
+// Hit bits of the 8 children of a hit parent cell, bit k = the k-th child
+// front to back (octant k ^ dm), for a TT_GENERAL ray. Child k has per-axis
+// interval [k_a ? q1 : q0, k_a ? q2 : q1]; ray_aabb_batch's test
+// max(near) <= min(far) && min(far) >= 0 is the set of pairwise conditions
+// near_a <= far_b and far_b >= 0. Those implied by the parent's own hit
+// (max q0 <= min q2, min q2 >= 0: the same plane values) or by q0 <= q1 <= q2
+// are dropped, leaving 21 comparisons.
+__device__ __forceinline__ unsigned child_hits_ordered(const double q0[3], const double q1[3], const double q2[3]) {
+  // children with local half v on axis a
+  auto half = [](int a, int v) -> unsigned {
+    const unsigned lo = a == 0 ? 0x55u : (a == 1 ? 0x33u : 0x0fu);
+    return v ? (~lo & 0xffu) : lo;
+  };
+  unsigned mask = 0xffu;
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
-    const double o = W->o[rl][a];
-    // child planes: exact dyadic values, so the sums are exact (= cell_lo)
-    const double p0 = dadd(-1.0, dmul((double)(2 * pc[a]), h));
-    const double p1 = dadd(p0, h), p2 = dadd(p1, h);
-    if ((fl >> (3 + a)) & 1) {
-      const bool in0 = (o >= p0) && (o <= p1);
-      const bool in1 = (o >= p1) && (o <= p2);
-      an[a][0] = in0 ? -INFINITY : INFINITY;
-      af[a][0] = in0 ? INFINITY : -INFINITY;
-      an[a][1] = in1 ? -INFINITY : INFINITY;
-      af[a][1] = in1 ? INFINITY : -INFINITY;
-    } else {
-      const double inv = W->inv[rl][a];
-      const double t0 = dmul(dsub(p0, o), inv), t1 = dmul(dsub(p1, o), inv), t2 = dmul(dsub(p2, o), inv);
-      an[a][0] = fmin(t0, t1);
-      af[a][0] = fmax(t0, t1);
-      an[a][1] = fmin(t1, t2);
-      af[a][1] = fmax(t1, t2);
+#pragma unroll
+    for (int b = 0; b < 3; ++b) {
+      if (a == b) continue;
+      if (!(q0[a] <= q1[b])) mask &= ~(half(a, 0) & half(b, 0));
+      if (!(q1[a] <= q2[b])) mask &= ~(half(a, 1) & half(b, 1));
+      if (!(q1[a] <= q1[b])) mask &= ~(half(a, 1) & half(b, 0));
     }
+    if (!(q1[a] >= 0.0)) mask &= ~half(a, 0);
   }
-  double n01[4], f01[4];
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    n01[j] = fmax(an[0][j & 1], an[1][j >> 1]);
-    f01[j] = fmin(af[0][j & 1], af[1][j >> 1]);
-  }
-  unsigned hit = 0;
-#pragma unroll
-  for (int oct = 0; oct < 8; ++oct) {
-    const double near = fmax(n01[oct & 3], an[2][oct >> 2]);
-    const double far = fmin(f01[oct & 3], af[2][oct >> 2]);
-    hit |= ((near <= far) && (far >= 0.0) ? 1u : 0u) << oct;
-  }
-  return hit;
+  return mask;
 }
 
 // Octant-indexed bits -> front-to-back order: bit k <- bit k ^ dm.
@@ -415,6 +430,9 @@ __device__ __forceinline__ unsigned octants_front_to_back(unsigned x, int dm) {
   return x;
 }
 
+__device__ __forceinline__ uint32_t pack_cell(uint32_t x, uint32_t y, uint32_t z) { return x | (y << 10) | (z << 20); }
+
+template <bool SO>
 __global__ void __launch_bounds__(TT_WPB * 32) k_traverse_tiles(
     const __grid_constant__ ng_octree tree, const ng_ray* __restrict__ rays, const int64_t* __restrict__ d_n,
     int target, int64_t* counts, ng_hit_pair* __restrict__ hits, int64_t hit_cap, unsigned int* tile_counter,
@@ -425,9 +443,9 @@ __global__ void __launch_bounds__(TT_WPB * 32) k_traverse_tiles(
   const int warp = threadIdx.x >> 5;
   TileWarp* W = reinterpret_cast<TileWarp*>(tt_smem) + warp;
   const int64_t gw = (int64_t)blockIdx.x * TT_WPB + warp;
-  uint8_t* ga = arena + gw * gcap * 10;  // [vox0 | vox1 | ray0 | ray1]
+  uint8_t* ga = arena + gw * gcap * (2 * TT_ENTRY);
   const int64_t n = *d_n;
-  const int64_t n_tiles = (n + 31) / 32;
+  const int64_t n_tiles = (n + TT_RAYS - 1) / TT_RAYS;
   const int lim = TT_SCAP + (int)gcap;
   int64_t level_cnt = 0;  // lane t: pairs emitted at traversal level t
   int need = 0;
@@ -436,91 +454,90 @@ __global__ void __launch_bounds__(TT_WPB * 32) k_traverse_tiles(
     if (lane == 0) tile = atomicAdd(tile_counter, 1u);
     tile = __shfl_sync(FULL, tile, 0);
     if ((int64_t)tile >= n_tiles) break;
-    const int64_t r0 = (int64_t)tile * 32;
-    const int nr = (int)((n - r0) < 32 ? (n - r0) : 32);
+    const int64_t r0 = (int64_t)tile * TT_RAYS;
+    const int nr = (int)((n - r0) < TT_RAYS ? (n - r0) : TT_RAYS);
     // ---- the tile's rays, and the root list: rays whose box test hits B
-    bool root = false;
-    if (lane < nr) {
-      ng_ray r;
-      load_ray_slab(rays, r0 + lane, so, r);
+    int nc = 0;
+    {
+      const TileList L0 = tile_list(W, ga, gcap, 0);
 #pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        W->o[lane][a] = r.o[a];
-        W->inv[lane][a] = r.inv[a];
+      for (int j0 = 0; j0 < TT_RAYS; j0 += 32) {
+        const int j = j0 + lane;
+        bool root = false;
+        if (j < nr) {
+          ng_ray r;
+          load_ray_slab(rays, r0 + j, so, r);
+          bool general = true;
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            if (!SO) W->o[j][a] = r.o[a];
+            W->inv[j][a] = r.inv[a];
+            general = general && isfinite(r.o[a]) && isfinite(r.inv[a]) && !((r.flags >> (3 + a)) & 1);
+          }
+          W->flags[j] = r.flags | (general ? TT_GENERAL : 0);
+          const double lo[3] = {-1.0, -1.0, -1.0}, hi[3] = {1.0, 1.0, 1.0};
+          double a0, b0;
+          root = slab_test(r, lo, hi, a0, b0);
+        }
+        W->seg_s[j] = 0;
+        W->seg_e[j] = 0;
+        const unsigned rb = __ballot_sync(FULL, root);
+        if (root) tl_put(L0, nc + __popc(rb & lanemask_lt()), 0, 0u, j, gcap);
+        nc += __popc(rb);
       }
-      bool nan_free = true;
-#pragma unroll
-      for (int a = 0; a < 3; ++a)
-        nan_free = nan_free && isfinite(r.o[a]) && (((r.flags >> (3 + a)) & 1) || isfinite(r.inv[a]));
-      W->flags[lane] = r.flags | (nan_free ? TT_NAN_FREE : 0);
-      const double lo[3] = {-1.0, -1.0, -1.0}, hi[3] = {1.0, 1.0, 1.0};
-      double a0, b0;
-      root = slab_test(r, lo, hi, a0, b0);
     }
-    W->seg_s[lane] = 0;
-    W->seg_e[lane] = 0;
-    const unsigned rb = __ballot_sync(FULL, root);
-    if (root) tl_put(tile_list(W, ga, gcap, 0), __popc(rb & lanemask_lt()), 0, lane, gcap);
-    int nc = __popc(rb);
     __syncwarp();
     // ---- level passes: hits at level t -> hit children at level t+1
     for (int t = 0; t < target; ++t) {
       const TileList src = tile_list(W, ga, gcap, t & 1);
       const TileList dst = tile_list(W, ga, gcap, (t & 1) ^ 1);
       const int cres = level_res(tree, t - tree.n_virtual + 1);
-      const bool small = cres <= 2048;  // parent codes below 2^30
-      const uint64_t* __restrict__ codes = tree.codes[t];
       const int32_t* __restrict__ cstart = tree.child_start[t];
       const uint8_t* __restrict__ cmask = tree.child_mask[t];
       int out = 0;
       for (int base = 0; base < nc; base += 32 * TT_ITEMS) {
-        int32_t pv[TT_ITEMS];
-        int pr[TT_ITEMS];
-        unsigned hm[TT_ITEMS];
         int32_t first[TT_ITEMS];
+        uint32_t pcell[TT_ITEMS];
+        int pr[TT_ITEMS];
+        unsigned hm[TT_ITEMS];  // bits 0-7 hit children front to back, 8-10 dm, 16-23 child mask
         int sum = 0;
 #pragma unroll
         for (int q = 0; q < TT_ITEMS; ++q) {
           const int i = base + lane * TT_ITEMS + q;
           hm[q] = 0;
-          pv[q] = 0;
-          pr[q] = 0;
           first[q] = 0;
+          pcell[q] = 0;
+          pr[q] = 0;
           if (i < nc) {
-            tl_get(src, i, pv[q], pr[q]);
-            const unsigned m = __ldg(cmask + pv[q]);
-            const uint64_t c = __ldg(codes + pv[q]);
-            first[q] = __ldg(cstart + pv[q]);
-            int pc[3];
-            if (small) {
-              const uint32_t c32 = (uint32_t)c;
-              pc[0] = (int)compact3_30(c32);
-              pc[1] = (int)compact3_30(c32 >> 1);
-              pc[2] = (int)compact3_30(c32 >> 2);
-            } else {
-              pc[0] = (int)compact3(c);
-              pc[1] = (int)compact3(c >> 1);
-              pc[2] = (int)compact3(c >> 2);
-            }
+            int32_t pv;
+            tl_get(src, i, pv, pcell[q], pr[q]);
+            const unsigned m = __ldg(cmask + pv);
+            first[q] = __ldg(cstart + pv);
+            const int pc[3] = {(int)(pcell[q] & 1023u), (int)((pcell[q] >> 10) & 1023u), (int)(pcell[q] >> 20)};
             const int fl = W->flags[pr[q]];
             const int dm = fl & 7;
-            unsigned ho;
-            if (fl & TT_NAN_FREE) {
-              ho = child_hits_nanfree(W, pr[q], pc, cres);
+            unsigned hk;  // front-to-back hit bits
+            if (fl & TT_GENERAL) {
+              double q0[3], q1[3], q2[3];
+#pragma unroll
+              for (int a = 0; a < 3; ++a)
+                axis_crossings(SO ? so.o[a] : W->o[pr[q]][a], W->inv[pr[q]][a], (dm >> a) & 1, pc[a], cres, q0[a],
+                               q1[a], q2[a]);
+              hk = child_hits_ordered(q0, q1, q2) & octants_front_to_back(m, dm);
             } else {
               ng_ray r;
-              tw_ray(W, pr[q], r);
+              tw_ray<SO>(W, so, pr[q], r);
               ChildSlabs cs;
               child_slabs(r, pc[0], pc[1], pc[2], cres, cs);
-              ho = 0;
+              unsigned ho = 0;
 #pragma unroll
               for (int oct = 0; oct < 8; ++oct) {
                 double a0, b0;
                 if (child_hit(cs, oct, a0, b0)) ho |= 1u << oct;
               }
+              hk = octants_front_to_back(ho & m, dm);
             }
-            hm[q] = octants_front_to_back(ho & m, dm);
-            if (hm[q]) hm[q] |= ((unsigned)dm << 8) | (m << 16);
+            if (hk) hm[q] = hk | ((unsigned)dm << 8) | (m << 16);
           }
           sum += __popc(hm[q] & 0xffu);
         }
@@ -530,9 +547,12 @@ __global__ void __launch_bounds__(TT_WPB * 32) k_traverse_tiles(
         for (int q = 0; q < TT_ITEMS; ++q) {
           const int dm = (int)((hm[q] >> 8) & 7u);
           const unsigned m = (hm[q] >> 16) & 0xffu;
+          const uint32_t c2 = pcell[q] << 1;  // 2 * (x, y, z), packed (parent cells < 512 per axis)
           for (unsigned bits = hm[q] & 0xffu; bits; bits &= bits - 1) {
             const int oct = (__ffs(bits) - 1) ^ dm;
-            tl_put(dst, o, first[q] + __popc(m & ((1u << oct) - 1u)), pr[q], gcap);
+            const uint32_t cc = c2 | (uint32_t)(oct & 1) | ((uint32_t)((oct >> 1) & 1) << 10) |
+                                ((uint32_t)(oct >> 2) << 20);
+            tl_put(dst, o, first[q] + __popc(m & ((1u << oct) - 1u)), cc, pr[q], gcap);
             ++o;
           }
         }
@@ -550,39 +570,59 @@ __global__ void __launch_bounds__(TT_WPB * 32) k_traverse_tiles(
     if (lane == 0 && nc > 0) hb = atomicAdd(hit_cursor, (unsigned long long)nc);
     const int64_t hbase = (int64_t)__shfl_sync(FULL, hb, 0);
     const int fres = level_res(tree, target - tree.n_virtual);
-    const double fedge = 2.0 / (double)fres;
-    const uint64_t* __restrict__ fcodes = tree.codes[target];
     for (int i = lane; i < nc; i += 32) {
       int32_t v;
+      uint32_t c;
       int rl;
-      tl_get(fin, i, v, rl);
-      int32_t pv_;
-      int prev = -1, next = -1;
-      if (i > 0) tl_get(fin, i - 1, pv_, prev);
-      if (i + 1 < nc) tl_get(fin, i + 1, pv_, next);
-      if (prev != rl) W->seg_s[rl] = i;
-      if (next != rl) W->seg_e[rl] = i + 1;
-      const uint64_t c = __ldg(fcodes + v);
-      const int cc[3] = {(int)compact3(c), (int)compact3(c >> 1), (int)compact3(c >> 2)};
-      double lo[3], hi[3];
-#pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        lo[a] = cell_lo(cc[a], fres);
-        hi[a] = dadd(lo[a], fedge);
-      }
-      ng_ray r;
-      tw_ray(W, rl, r);
+      tl_get(fin, i, v, c, rl);
+      if (i == 0 || tl_ray(fin, i - 1) != rl) W->seg_s[rl] = i;
+      if (i + 1 == nc || tl_ray(fin, i + 1) != rl) W->seg_e[rl] = i + 1;
+      const int cc[3] = {(int)(c & 1023u), (int)((c >> 10) & 1023u), (int)(c >> 20)};
       ng_hit_pair h;
       h.ray = (int32_t)(r0 + rl);
       h.voxel = v;
-      slab_test(r, lo, hi, h.t_enter, h.t_exit);
+      const int fl = W->flags[rl];
+      if (fl & TT_GENERAL) {
+        // the cell's slab interval per axis is [min, max] of its two plane
+        // crossings, sorted by the direction sign (monotone, as above)
+        double ne = 0.0, fa = 0.0;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          const bool neg = (fl >> a) & 1;
+          const double h2 = 2.0 / (double)fres;
+          const double pn = dmul((double)(cc[a] + (neg ? 1 : 0) - fres / 2), h2);
+          const double pfar = dadd(pn, neg ? -h2 : h2);
+          const double o = SO ? so.o[a] : W->o[rl][a];
+          const double inv = W->inv[rl][a];
+          const double tn = dmul(dsub(pn, o), inv), tf = dmul(dsub(pfar, o), inv);
+          ne = a == 0 ? tn : (tn > ne ? tn : ne);
+          fa = a == 0 ? tf : (tf < fa ? tf : fa);
+        }
+        h.t_enter = ne > 0.0 ? ne : 0.0;
+        h.t_exit = fa;
+      } else {
+        const double edge = 2.0 / (double)fres;
+        double lo[3], hi[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          lo[a] = cell_lo(cc[a], fres);
+          hi[a] = dadd(lo[a], edge);
+        }
+        ng_ray r;
+        tw_ray<SO>(W, so, rl, r);
+        slab_test(r, lo, hi, h.t_enter, h.t_exit);
+      }
       if (hbase + i < hit_cap) hits[hbase + i] = h;
     }
     __syncwarp();
-    if (lane < nr) {
-      const int64_t s0 = hbase + W->seg_s[lane], e0 = hbase + W->seg_e[lane];
-      seg_start[r0 + lane] = s0 < hit_cap ? s0 : hit_cap;
-      seg_end[r0 + lane] = e0 < hit_cap ? e0 : hit_cap;
+#pragma unroll
+    for (int j0 = 0; j0 < TT_RAYS; j0 += 32) {
+      const int j = j0 + lane;
+      if (j < nr) {
+        const int64_t s0 = hbase + W->seg_s[j], e0 = hbase + W->seg_e[j];
+        seg_start[r0 + j] = s0 < hit_cap ? s0 : hit_cap;
+        seg_end[r0 + j] = e0 < hit_cap ? e0 : hit_cap;
+      }
     }
     __syncwarp();
   }
@@ -751,22 +791,31 @@ int traverse_hits(const ng_octree& tree, const ng_ray* rays, int t, bool next_fi
 
 size_t tile_traverse_smem() { return sizeof(TileWarp) * TT_WPB; }
 int tile_traverse_scap() { return TT_SCAP; }
+int tile_traverse_entry_bytes() { return 2 * TT_ENTRY; }
 
-// Warps the tile traversal runs with (grid x TT_WPB); the per-warp global
+// Warps the tile traversal runs with for up to `n_rays` rays (grid x
+// TT_WPB: one resident wave, no more warps than tiles); the per-warp global
 // arena is sized from this.
-int64_t tile_traverse_warps() {
+int64_t tile_traverse_warps(int64_t n_rays) {
   static int per_sm = -1;
   if (per_sm < 0) {
-    cudaFuncSetAttribute(k_traverse_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    int a = 0, b = 0;
+    cudaFuncSetAttribute(k_traverse_tiles<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)tile_traverse_smem());
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_traverse_tiles, TT_WPB * 32,
-                                                      tile_traverse_smem()) != cudaSuccess || per_sm < 1)
-      per_sm = 1;
+    cudaFuncSetAttribute(k_traverse_tiles<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)tile_traverse_smem());
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_traverse_tiles<true>, TT_WPB * 32, tile_traverse_smem());
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_traverse_tiles<false>, TT_WPB * 32, tile_traverse_smem());
+    per_sm = std::max(1, std::min(a, b));
   }
-  return (int64_t)sm_count() * per_sm * TT_WPB;
+  const int64_t tiles = (n_rays + TT_RAYS - 1) / TT_RAYS;
+  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((int64_t)sm_count() * per_sm,
+                                                                  (tiles + TT_WPB - 1) / TT_WPB));
+  return blocks * TT_WPB;
 }
 
-int traverse_tiles(const ng_octree& tree, const ng_ray* rays, const int64_t* d_n, int target, int64_t* counts,
+int traverse_tiles(const ng_octree& tree, const ng_ray* rays, const int64_t* d_n, int64_t n_max, int target,
+                   int64_t* counts,
                    ng_hit_pair* hits, int64_t hit_cap, void* ctl, int64_t* seg_start, int64_t* seg_end,
                    void* arena, size_t arena_bytes, unsigned long long* d_need, const double* shared_origin,
                    cudaStream_t s) {
@@ -774,19 +823,20 @@ int traverse_tiles(const ng_octree& tree, const ng_ray* rays, const int64_t* d_n
   SharedOrigin so;
   so.shared = shared_origin != nullptr;
   for (int a = 0; a < 3; ++a) so.o[a] = shared_origin ? shared_origin[a] : 0.0;
-  const int64_t warps = tile_traverse_warps();
-  const int64_t gcap = (int64_t)(arena_bytes / (size_t)(warps * 10)) & ~int64_t(15);
-  k_traverse_tiles<<<(int)(warps / TT_WPB), TT_WPB * 32, tile_traverse_smem(), s>>>(
-      tree, rays, d_n, target, counts, hits, hit_cap, (unsigned int*)ctl,
-      (unsigned long long*)((char*)ctl + 8), seg_start, seg_end, (uint8_t*)arena, gcap, d_need, so);
+  const int64_t warps = tile_traverse_warps(n_max);
+  const int64_t gcap = (int64_t)(arena_bytes / (size_t)(warps * (2 * TT_ENTRY))) & ~int64_t(15);
+  auto k = so.shared ? k_traverse_tiles<true> : k_traverse_tiles<false>;
+  k<<<(int)(warps / TT_WPB), TT_WPB * 32, tile_traverse_smem(), s>>>(
+      tree, rays, d_n, target, counts, hits, hit_cap, (unsigned int*)ctl, (unsigned long long*)((char*)ctl + 8),
+      seg_start, seg_end, (uint8_t*)arena, gcap, d_need, so);
   NG_CHECK_LAUNCH("k_traverse_tiles");
   return NG_OK;
 }
 
 // Longest tile list the arena (the two pair buffers) holds.
-int64_t tile_traverse_limit(size_t arena_bytes) {
-  const int64_t warps = tile_traverse_warps();
-  return TT_SCAP + ((int64_t)(arena_bytes / (size_t)(warps * 10)) & ~int64_t(15));
+int64_t tile_traverse_limit(size_t arena_bytes, int64_t n_max) {
+  const int64_t warps = tile_traverse_warps(n_max);
+  return TT_SCAP + ((int64_t)(arena_bytes / (size_t)(warps * (2 * TT_ENTRY))) & ~int64_t(15));
 }
 
 int segments(const ng_hit_pair* hits, const int64_t* d_count, int64_t cap, int64_t n_rays,
