@@ -974,7 +974,16 @@ struct WsLayout {
 
 static size_t al(size_t x) { return (x + 255) & ~size_t(255); }
 
-constexpr int64_t TILE_ARENA_MIN = 2048;
+// list entries per warp the tile traversal's arena holds at least
+// (NG_TILE_ARENA_MIN overrides: a test knob for the overflow / rerun path)
+static int64_t tile_arena_min() {
+  static int64_t v = -1;
+  if (v < 0) {
+    const char* e = getenv("NG_TILE_ARENA_MIN");
+    v = e ? std::max(0, atoi(e)) : 2048;
+  }
+  return v;
+}
 
 static WsLayout layout(int64_t n, int64_t pair_cap, int64_t hit_cap) {
   WsLayout L;
@@ -982,7 +991,7 @@ static WsLayout layout(int64_t n, int64_t pair_cap, int64_t hit_cap) {
   L.rays = o; o = al(o + (size_t)n * sizeof(ng_ray));
   // the two pair buffers double as the tile traversal's spill arena: at
   // least TILE_ARENA_MIN list entries per warp whatever the frame size
-  const size_t tile_arena = (size_t)tile_traverse_warps(n) * TILE_ARENA_MIN * tile_traverse_entry_bytes();
+  const size_t tile_arena = (size_t)tile_traverse_warps(n) * tile_arena_min() * tile_traverse_entry_bytes();
   const size_t pair_bytes = std::max((size_t)pair_cap * sizeof(ng_pair), tile_arena / 2);
   L.pairs_a = o; o = al(o + pair_bytes);
   L.pairs_b = o; o = al(o + pair_bytes);

@@ -11,6 +11,7 @@
 #include "common.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace ng {
 
@@ -315,6 +316,7 @@ struct TileWarp {
 };
 
 struct TileList {
+  int scap;  // entries held in shared memory (<= TT_SCAP), the rest in the arena
   int32_t* svox;
   uint32_t* scell;
   uint8_t* sray;
@@ -324,36 +326,37 @@ struct TileList {
 };
 
 __device__ __forceinline__ void tl_put(const TileList& b, int i, int32_t v, uint32_t c, int r, int64_t gcap) {
-  if (i < TT_SCAP) {
+  if (i < b.scap) {
     b.svox[i] = v;
     b.scell[i] = c;
     b.sray[i] = (uint8_t)r;
-  } else if (i - TT_SCAP < gcap) {
-    b.gvox[i - TT_SCAP] = v;
-    b.gcell[i - TT_SCAP] = c;
-    b.gray[i - TT_SCAP] = (uint8_t)r;
+  } else if (i - b.scap < gcap) {
+    b.gvox[i - b.scap] = v;
+    b.gcell[i - b.scap] = c;
+    b.gray[i - b.scap] = (uint8_t)r;
   }
 }
 
 __device__ __forceinline__ void tl_get(const TileList& b, int i, int32_t& v, uint32_t& c, int& r) {
-  if (i < TT_SCAP) {
+  if (i < b.scap) {
     v = b.svox[i];
     c = b.scell[i];
     r = b.sray[i];
   } else {
-    v = b.gvox[i - TT_SCAP];
-    c = b.gcell[i - TT_SCAP];
-    r = b.gray[i - TT_SCAP];
+    v = b.gvox[i - b.scap];
+    c = b.gcell[i - b.scap];
+    r = b.gray[i - b.scap];
   }
 }
 
 __device__ __forceinline__ int tl_ray(const TileList& b, int i) {
-  return i < TT_SCAP ? b.sray[i] : b.gray[i - TT_SCAP];
+  return i < b.scap ? b.sray[i] : b.gray[i - b.scap];
 }
 
 // arena per warp: [vox0 | vox1 | cell0 | cell1 | ray0 | ray1], gcap entries each
-__device__ __forceinline__ TileList tile_list(TileWarp* W, uint8_t* ga, int64_t gcap, int k) {
+__device__ __forceinline__ TileList tile_list(TileWarp* W, uint8_t* ga, int64_t gcap, int k, int scap) {
   TileList b;
+  b.scap = scap;
   b.svox = W->vox[k];
   b.scell = W->cell[k];
   b.sray = W->ray[k];
@@ -437,7 +440,7 @@ __global__ void __launch_bounds__(TT_WPB * 32) k_traverse_tiles(
     const __grid_constant__ ng_octree tree, const ng_ray* __restrict__ rays, const int64_t* __restrict__ d_n,
     int target, int64_t* counts, ng_hit_pair* __restrict__ hits, int64_t hit_cap, unsigned int* tile_counter,
     unsigned long long* hit_cursor, int64_t* __restrict__ seg_start, int64_t* __restrict__ seg_end,
-    uint8_t* arena, int64_t gcap, unsigned long long* d_need, const SharedOrigin so) {
+    uint8_t* arena, int64_t gcap, int scap, unsigned long long* d_need, const SharedOrigin so) {
   extern __shared__ __align__(16) uint8_t tt_smem[];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -446,7 +449,7 @@ __global__ void __launch_bounds__(TT_WPB * 32) k_traverse_tiles(
   uint8_t* ga = arena + gw * gcap * (2 * TT_ENTRY);
   const int64_t n = *d_n;
   const int64_t n_tiles = (n + TT_RAYS - 1) / TT_RAYS;
-  const int lim = TT_SCAP + (int)gcap;
+  const int lim = scap + (int)gcap;
   int64_t level_cnt = 0;  // lane t: pairs emitted at traversal level t
   int need = 0;
   while (true) {
@@ -459,7 +462,7 @@ __global__ void __launch_bounds__(TT_WPB * 32) k_traverse_tiles(
     // ---- the tile's rays, and the root list: rays whose box test hits B
     int nc = 0;
     {
-      const TileList L0 = tile_list(W, ga, gcap, 0);
+      const TileList L0 = tile_list(W, ga, gcap, 0, scap);
 #pragma unroll
       for (int j0 = 0; j0 < TT_RAYS; j0 += 32) {
         const int j = j0 + lane;
@@ -489,8 +492,8 @@ __global__ void __launch_bounds__(TT_WPB * 32) k_traverse_tiles(
     __syncwarp();
     // ---- level passes: hits at level t -> hit children at level t+1
     for (int t = 0; t < target; ++t) {
-      const TileList src = tile_list(W, ga, gcap, t & 1);
-      const TileList dst = tile_list(W, ga, gcap, (t & 1) ^ 1);
+      const TileList src = tile_list(W, ga, gcap, t & 1, scap);
+      const TileList dst = tile_list(W, ga, gcap, (t & 1) ^ 1, scap);
       const int cres = level_res(tree, t - tree.n_virtual + 1);
       const int32_t* __restrict__ cstart = tree.child_start[t];
       const uint8_t* __restrict__ cmask = tree.child_mask[t];
@@ -565,7 +568,7 @@ __global__ void __launch_bounds__(TT_WPB * 32) k_traverse_tiles(
     }
     // ---- final pairs: claim the tile's block of the hit list, write
     // (ray, voxel, t_enter, t_exit) and the per-ray segments
-    const TileList fin = tile_list(W, ga, gcap, target & 1);
+    const TileList fin = tile_list(W, ga, gcap, target & 1, scap);
     unsigned long long hb = 0;
     if (lane == 0 && nc > 0) hb = atomicAdd(hit_cursor, (unsigned long long)nc);
     const int64_t hbase = (int64_t)__shfl_sync(FULL, hb, 0);
@@ -628,7 +631,7 @@ __global__ void __launch_bounds__(TT_WPB * 32) k_traverse_tiles(
   }
   if (lane >= 1 && lane <= target && level_cnt) atomicAdd((unsigned long long*)(counts + lane),
                                                           (unsigned long long)level_cnt);
-  if (lane == 0 && need > TT_SCAP) atomicMax(d_need, (unsigned long long)need);
+  if (lane == 0 && need > scap) atomicMax(d_need, (unsigned long long)need);
 }
 
 __global__ void k_segments(const ng_hit_pair* __restrict__ hits, const int64_t* __restrict__ d_count,
@@ -790,7 +793,16 @@ int traverse_hits(const ng_octree& tree, const ng_ray* rays, int t, bool next_fi
 }
 
 size_t tile_traverse_smem() { return sizeof(TileWarp) * TT_WPB; }
-int tile_traverse_scap() { return TT_SCAP; }
+// NG_TILE_SCAP=k (test knob) holds only k entries of each list in shared
+// memory, sending the rest through the arena.
+int tile_traverse_scap() {
+  static int scap = -1;
+  if (scap < 0) {
+    const char* e = getenv("NG_TILE_SCAP");
+    scap = e ? std::max(0, std::min(TT_SCAP, atoi(e))) : TT_SCAP;
+  }
+  return scap;
+}
 int tile_traverse_entry_bytes() { return 2 * TT_ENTRY; }
 
 // Warps the tile traversal runs with for up to `n_rays` rays (grid x
@@ -828,7 +840,7 @@ int traverse_tiles(const ng_octree& tree, const ng_ray* rays, const int64_t* d_n
   auto k = so.shared ? k_traverse_tiles<true> : k_traverse_tiles<false>;
   k<<<(int)(warps / TT_WPB), TT_WPB * 32, tile_traverse_smem(), s>>>(
       tree, rays, d_n, target, counts, hits, hit_cap, (unsigned int*)ctl, (unsigned long long*)((char*)ctl + 8),
-      seg_start, seg_end, (uint8_t*)arena, gcap, d_need, so);
+      seg_start, seg_end, (uint8_t*)arena, gcap, tile_traverse_scap(), d_need, so);
   NG_CHECK_LAUNCH("k_traverse_tiles");
   return NG_OK;
 }
@@ -836,7 +848,7 @@ int traverse_tiles(const ng_octree& tree, const ng_ray* rays, const int64_t* d_n
 // Longest tile list the arena (the two pair buffers) holds.
 int64_t tile_traverse_limit(size_t arena_bytes, int64_t n_max) {
   const int64_t warps = tile_traverse_warps(n_max);
-  return TT_SCAP + ((int64_t)(arena_bytes / (size_t)(warps * (2 * TT_ENTRY))) & ~int64_t(15));
+  return tile_traverse_scap() + ((int64_t)(arena_bytes / (size_t)(warps * (2 * TT_ENTRY))) & ~int64_t(15));
 }
 
 int segments(const ng_hit_pair* hits, const int64_t* d_count, int64_t cap, int64_t n_rays,
