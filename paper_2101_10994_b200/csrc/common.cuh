@@ -222,6 +222,38 @@ __device__ __forceinline__ void make_ray(double ox, double oy, double oz, double
   r.pad = 0;
 }
 
+// Pixel-centre ray i of a (band-tiled) pinhole camera, bit-exact with
+// Camera.rays (render.py:74-88). Every kernel that needs a camera ray
+// computes it with this one function, so a ray recomputed on the fly is
+// the same ray everywhere.
+__device__ __forceinline__ void camera_ray(const ng_camera& cam, int64_t i, ng_ray& r) {
+  const int px_i = (int)(i % cam.width);
+  const int lrow = (int)(i / cam.width);
+  const int band = lrow / cam.band_rows;
+  const int py_i = (band * cam.band_stride + cam.band_offset) * cam.band_rows + lrow % cam.band_rows;
+  const double px = dmul(dmul(dsub(dmul(2.0, dadd((double)px_i, 0.5)) / (double)cam.width, 1.0), cam.tan_half),
+                         cam.aspect);
+  const double py = dmul(dsub(1.0, dmul(2.0, dadd((double)py_i, 0.5)) / (double)cam.height), cam.tan_half);
+  double d[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) d[a] = dadd(dadd(cam.fwd[a], dmul(px, cam.right[a])), dmul(py, cam.up[a]));
+  const double nrm = __dsqrt_rn(dadd(dadd(dmul(d[0], d[0]), dmul(d[1], d[1])), dmul(d[2], d[2])));
+  make_ray(cam.position[0], cam.position[1], cam.position[2], d[0] / nrm, d[1] / nrm, d[2] / nrm, r);
+}
+
+// Rays of a pass: explicit records, or (`cam_rays`) the camera's rays
+// computed where they are used instead of stored.
+struct RaySrc {
+  const ng_ray* rays;
+  ng_camera cam;
+  int cam_rays;
+};
+
+__device__ __forceinline__ void ray_at(const RaySrc& S, int64_t i, ng_ray& r) {
+  if (S.cam_rays) camera_ray(S.cam, i, r);
+  else load_ray(S.rays, i, r);
+}
+
 // ---------------------------------------------------------------- warp utils
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31; }
 __device__ __forceinline__ unsigned lanemask_lt() {

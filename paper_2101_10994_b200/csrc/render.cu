@@ -28,7 +28,7 @@ int traverse_tiles(const ng_octree& tree, const ng_ray* rays, const int64_t* d_n
                    int64_t* counts,
                    ng_hit_pair* hits, int64_t hit_cap, void* ctl, int64_t* seg_start, int64_t* seg_end,
                    void* arena, size_t arena_bytes, unsigned long long* d_need, const double* shared_origin,
-                   cudaStream_t s);
+                   const ng_camera* cam_rays, cudaStream_t s);
 int64_t tile_traverse_limit(size_t arena_bytes, int64_t n_max);
 int64_t tile_traverse_warps(int64_t n_max);
 int tile_traverse_scap();
@@ -61,19 +61,8 @@ __global__ void k_camera_rays(ng_camera cam, ng_ray* __restrict__ rays, ng_frame
       seg_end[i] = 0;
     }
     if (rays) {
-      const int px_i = (int)(i % cam.width);
-      const int lrow = (int)(i / cam.width);
-      const int band = lrow / cam.band_rows;
-      const int py_i = (band * cam.band_stride + cam.band_offset) * cam.band_rows + lrow % cam.band_rows;
-      double px = dmul(dmul(dsub(dmul(2.0, dadd((double)px_i, 0.5)) / (double)cam.width, 1.0), cam.tan_half),
-                       cam.aspect);
-      double py = dmul(dsub(1.0, dmul(2.0, dadd((double)py_i, 0.5)) / (double)cam.height), cam.tan_half);
-      double d[3];
-#pragma unroll
-      for (int a = 0; a < 3; ++a) d[a] = dadd(dadd(cam.fwd[a], dmul(px, cam.right[a])), dmul(py, cam.up[a]));
-      double nrm = __dsqrt_rn(dadd(dadd(dmul(d[0], d[0]), dmul(d[1], d[1])), dmul(d[2], d[2])));
       ng_ray r;
-      make_ray(cam.position[0], cam.position[1], cam.position[2], d[0] / nrm, d[1] / nrm, d[2] / nrm, r);
+      camera_ray(cam, i, r);
       rays[i] = r;
     }
     if (fr.hit) {
@@ -244,7 +233,7 @@ struct MarchArgs {
   int G, out_mask, dec_first, dec_last, passes;
   int blend_base;
   double blend_alpha;
-  const ng_ray* rays;
+  RaySrc rays;                   // ray records, or the camera's rays computed on the fly
   const int32_t* work;           // ray ids to trace, or null for 0..n_work-1
   const unsigned long long* d_n_work;
   int64_t n_work;
@@ -405,9 +394,16 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_cons
             it = 0;
             ev = 0;
             ready = false;
-            const ng_ray* rp = A.rays + ray;
-            o[0] = rp->o[0]; o[1] = rp->o[1]; o[2] = rp->o[2];
-            d[0] = rp->d[0]; d[1] = rp->d[1]; d[2] = rp->d[2];
+            if (A.rays.cam_rays) {
+              ng_ray rr;
+              camera_ray(A.rays.cam, ray, rr);
+              o[0] = rr.o[0]; o[1] = rr.o[1]; o[2] = rr.o[2];
+              d[0] = rr.d[0]; d[1] = rr.d[1]; d[2] = rr.d[2];
+            } else {
+              const ng_ray* rp = A.rays.rays + ray;
+              o[0] = rp->o[0]; o[1] = rp->o[1]; o[2] = rp->o[2];
+              d[0] = rp->d[0]; d[1] = rp->d[1]; d[2] = rp->d[2];
+            }
           }
         }
       }
@@ -549,7 +545,7 @@ struct NormalArgs {
   double blend_alpha;
   const double* pts;                 // explicit points, or null: hit rays below
   int64_t n_pts;
-  const ng_ray* rays;
+  RaySrc rays;
   const int32_t* hit_list;
   const unsigned long long* d_hit_count;
   const double* t_hit;
@@ -615,10 +611,12 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_normals(const __grid_co
         p[2] = A.pts[3 * i + 2];
       } else {
         dst = A.hit_list[i];
-        const ng_ray* rp = A.rays + dst;
+        ng_ray rr;
+        if (A.rays.cam_rays) camera_ray(A.rays.cam, dst, rr);
+        else load_ray(A.rays.rays, dst, rr);
         const double th = A.t_hit[dst];
 #pragma unroll
-        for (int a = 0; a < 3; ++a) p[a] = dadd(rp->o[a], dmul(th, rp->d[a]));  // render.py:396
+        for (int a = 0; a < 3; ++a) p[a] = dadd(rr.o[a], dmul(th, rr.d[a]));  // render.py:396
       }
     }
     double vals[6];
@@ -759,7 +757,7 @@ __global__ void k_finish_stats(ng_frame_stats* st, int n_levels, int64_t pair_ca
 }
 
 // Shadow rays for the hit pixels: origin p + offset * n, direction = light.
-__global__ void k_shadow_rays(const ng_ray* __restrict__ rays, const int32_t* __restrict__ hit_list,
+__global__ void k_shadow_rays(const RaySrc rays, const int32_t* __restrict__ hit_list,
                               const unsigned long long* __restrict__ d_hits, const double* __restrict__ t_hit,
                               const double* __restrict__ normal, ng_render_cfg cfg, ng_ray* __restrict__ srays,
                               int64_t* d_root) {
@@ -767,7 +765,8 @@ __global__ void k_shadow_rays(const ng_ray* __restrict__ rays, const int32_t* __
   if (blockIdx.x == 0 && threadIdx.x == 0) *d_root = n;
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
     const int32_t px = hit_list[j];
-    const ng_ray& r = rays[px];
+    ng_ray r;
+    ray_at(rays, px, r);
     const double th = t_hit[px];
     double o[3];
 #pragma unroll
@@ -1034,7 +1033,8 @@ static unsigned long long* march_profile_buffer() {
 static int trace_pass(const ng_octree& tree, const ng_render_cfg& cfg, const LodPlan& P, const ng_ray* rays,
                       int64_t n, int64_t* counts, const WsLayout& L, const ng_workspace& ws, char* b,
                       unsigned long long* d_active, unsigned long long* work_counter, cudaStream_t s,
-                      MarchArgs& A, bool zeroed, const double* shared_origin, TileOverflow& tov) {
+                      MarchArgs& A, bool zeroed, const double* shared_origin, TileOverflow& tov,
+                      const ng_camera* cam_rays = nullptr) {
   ng_pair* pa = (ng_pair*)(b + L.pairs_a);
   ng_pair* pb = (ng_pair*)(b + L.pairs_b);
   ng_hit_pair* hits = (ng_hit_pair*)(b + L.hits);
@@ -1073,7 +1073,7 @@ static int trace_pass(const ng_octree& tree, const ng_render_cfg& cfg, const Lod
     const size_t arena_bytes = L.hits - L.pairs_a;
     unsigned long long* need = (unsigned long long*)((char*)scratch + 16);
     r = traverse_tiles(tree, rays, &counts[0], n, target, counts, hits, ws.hit_capacity, scratch, seg_start, seg_end,
-                       b + L.pairs_a, arena_bytes, need, shared_origin, s);
+                       b + L.pairs_a, arena_bytes, need, shared_origin, cam_rays, s);
     if (r) return r;
     tov.need = need;
     tov.lim = tile_traverse_limit(arena_bytes, n);
@@ -1106,7 +1106,9 @@ static int trace_pass(const ng_octree& tree, const ng_render_cfg& cfg, const Lod
   A.passes = P.passes;
   A.blend_base = P.blend_base;
   A.blend_alpha = P.alpha;
-  A.rays = rays;
+  A.rays.rays = rays;
+  A.rays.cam_rays = cam_rays != nullptr;
+  if (cam_rays) A.rays.cam = *cam_rays;
   A.work = sorted;
   A.d_n_work = d_active;
   A.n_work = 0;
@@ -1164,9 +1166,12 @@ static int render_common(const ng_octree& tree, const ng_field& f, const ng_rend
   // the tile traversal writes every ray's segment itself
   int64_t* zseg_s = use_tile_traverse(target0) ? nullptr : seg_start;
   int64_t* zseg_e = use_tile_traverse(target0) ? nullptr : seg_end;
+  // with the tile traversal, camera rays are computed where they are used
+  // (traversal, march, normals, shadow origins) instead of stored
+  const bool cam_rays = cam != nullptr && use_tile_traverse(target0);
   if (cam) {
-    k_camera_rays<<<grid_for(n, 256), 256, 0, s>>>(*cam, rays, fr, bg[0], bg[1], bg[2], &st->pairs[0], zseg_s,
-                                                   zseg_e);
+    k_camera_rays<<<grid_for(n, 256), 256, 0, s>>>(*cam, cam_rays ? nullptr : rays, fr, bg[0], bg[1], bg[2],
+                                                   &st->pairs[0], zseg_s, zseg_e);
     NG_CHECK_LAUNCH("k_camera_rays");
   } else {
     k_frame_defaults<<<grid_for(n, 256), 256, 0, s>>>(fr, n, bg[0], bg[1], bg[2], zseg_s, zseg_e);
@@ -1181,7 +1186,7 @@ static int render_common(const ng_octree& tree, const ng_field& f, const ng_rend
   // camera rays share the eye position (a host value, captured into the launches)
   TileOverflow tov;
   if ((r = trace_pass(tree, cfg, P, rays, n, st->pairs, L, ws, b, ctr + 0, ctr + 2, s, A, true,
-                      cam ? cam->position : nullptr, tov)))
+                      cam ? cam->position : nullptr, tov, cam_rays ? cam : nullptr)))
     return r;
   A.hit = fr.hit;
   A.t = fr.t;
@@ -1207,7 +1212,7 @@ static int render_common(const ng_octree& tree, const ng_field& f, const ng_rend
     B.blend_alpha = P.alpha;
     B.pts = nullptr;
     B.n_pts = 0;
-    B.rays = rays;
+    B.rays = A.rays;
     B.hit_list = hit_list;
     B.d_hit_count = ctr + 1;
     B.t_hit = fr.t;
@@ -1222,7 +1227,7 @@ static int render_common(const ng_octree& tree, const ng_field& f, const ng_rend
   // ---- shadow rays toward the light (configs[4]) with the same traversal + march
   if (cfg.shadows && do_normals) {
     ng_ray* srays = (ng_ray*)(b + L.s_rays);
-    k_shadow_rays<<<grid_for(n, 256), 256, 0, s>>>(rays, hit_list, ctr + 1, fr.t, fr.normal, cfg, srays,
+    k_shadow_rays<<<grid_for(n, 256), 256, 0, s>>>(A.rays, hit_list, ctr + 1, fr.t, fr.normal, cfg, srays,
                                                   &st->shadow_pairs[0]);
     NG_CHECK_LAUNCH("k_shadow_rays");
     MarchArgs S;
@@ -1305,7 +1310,8 @@ int ng_sphere_trace(const ng_octree* tree, const ng_field* fld, const ng_render_
   A.passes = P.passes;
   A.blend_base = P.blend_base;
   A.blend_alpha = P.alpha;
-  A.rays = rays;
+  A.rays.rays = rays;
+  A.rays.cam_rays = 0;
   A.work = nullptr;
   A.d_n_work = nullptr;
   A.n_work = n_rays;
@@ -1341,7 +1347,8 @@ int ng_normals(const ng_octree* tree, const ng_field* fld, const ng_render_cfg* 
   B.blend_alpha = P.alpha;
   B.pts = pts;
   B.n_pts = k;
-  B.rays = nullptr;
+  B.rays.rays = nullptr;
+  B.rays.cam_rays = 0;
   B.hit_list = nullptr;
   B.d_hit_count = nullptr;
   B.t_hit = nullptr;

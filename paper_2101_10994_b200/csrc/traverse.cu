@@ -440,7 +440,8 @@ __global__ void __launch_bounds__(TT_WPB * 32) k_traverse_tiles(
     const __grid_constant__ ng_octree tree, const ng_ray* __restrict__ rays, const int64_t* __restrict__ d_n,
     int target, int64_t* counts, ng_hit_pair* __restrict__ hits, int64_t hit_cap, unsigned int* tile_counter,
     unsigned long long* hit_cursor, int64_t* __restrict__ seg_start, int64_t* __restrict__ seg_end,
-    uint8_t* arena, int64_t gcap, int scap, unsigned long long* d_need, const SharedOrigin so) {
+    uint8_t* arena, int64_t gcap, int scap, unsigned long long* d_need, const SharedOrigin so,
+    const ng_camera cam, int cam_rays) {
   extern __shared__ __align__(16) uint8_t tt_smem[];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -469,7 +470,8 @@ __global__ void __launch_bounds__(TT_WPB * 32) k_traverse_tiles(
         bool root = false;
         if (j < nr) {
           ng_ray r;
-          load_ray_slab(rays, r0 + j, so, r);
+          if (SO && cam_rays) camera_ray(cam, r0 + j, r);  // the camera's ray, not stored
+          else load_ray_slab(rays, r0 + j, so, r);
           bool general = true;
 #pragma unroll
           for (int a = 0; a < 3; ++a) {
@@ -830,7 +832,7 @@ int traverse_tiles(const ng_octree& tree, const ng_ray* rays, const int64_t* d_n
                    int64_t* counts,
                    ng_hit_pair* hits, int64_t hit_cap, void* ctl, int64_t* seg_start, int64_t* seg_end,
                    void* arena, size_t arena_bytes, unsigned long long* d_need, const double* shared_origin,
-                   cudaStream_t s) {
+                   const ng_camera* cam_rays, cudaStream_t s) {
   // `ctl` (zeroed by the caller): u32 tile counter at 0, u64 hit cursor at 8
   SharedOrigin so;
   so.shared = shared_origin != nullptr;
@@ -840,7 +842,8 @@ int traverse_tiles(const ng_octree& tree, const ng_ray* rays, const int64_t* d_n
   auto k = so.shared ? k_traverse_tiles<true> : k_traverse_tiles<false>;
   k<<<(int)(warps / TT_WPB), TT_WPB * 32, tile_traverse_smem(), s>>>(
       tree, rays, d_n, target, counts, hits, hit_cap, (unsigned int*)ctl, (unsigned long long*)((char*)ctl + 8),
-      seg_start, seg_end, (uint8_t*)arena, gcap, tile_traverse_scap(), d_need, so);
+      seg_start, seg_end, (uint8_t*)arena, gcap, tile_traverse_scap(), d_need, so,
+      cam_rays ? *cam_rays : ng_camera{}, cam_rays != nullptr);
   NG_CHECK_LAUNCH("k_traverse_tiles");
   return NG_OK;
 }
