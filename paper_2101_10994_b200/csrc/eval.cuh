@@ -307,7 +307,8 @@ __device__ __forceinline__ EvalLane warp_eval(const ng_octree& tree, const EvalC
 // per output level instead of a lookup and 8 rows per level 1..L.
 template <int GB = NG_GATHER_BATCH, class Mlp, class Emit>
 __device__ __forceinline__ EvalLane warp_eval_presum(const ng_octree& tree, const EvalCtx& c, WarpScratch& ws,
-                                                     bool act, const double x[3], const Mlp& mlp, Emit&& emit) {
+                                                     bool act, const double x[3], const Mlp& mlp, Emit&& emit,
+                                                     int64_t known = -1) {
   const int lane = (int)lane_id();
   EvalLane res;
   res.present = 0;
@@ -321,7 +322,8 @@ __device__ __forceinline__ EvalLane warp_eval_presum(const ng_octree& tree, cons
   int64_t idx = -1;
   int4 ia = make_int4(0, 0, 0, 0), ib = ia;
   if (act) {
-    idx = rank_lookup(tree.bitmap[tl], tree.rank[tl], morton(cell[0], cell[1], cell[2]));
+    // `known`: the caller already holds the level-G voxel containing x
+    idx = known >= 0 ? known : rank_lookup(tree.bitmap[tl], tree.rank[tl], morton(cell[0], cell[1], cell[2]));
     res.inside = idx >= 0;  // query_field's inside test at the trace level (render.py:159-166)
     if (idx >= 0) {
       const int4* cr = reinterpret_cast<const int4*>(tree.corners[tl] + 8 * idx);

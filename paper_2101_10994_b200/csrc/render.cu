@@ -238,6 +238,7 @@ struct MarchArgs {
   const unsigned long long* d_n_work;
   int64_t n_work;
   const ng_hit_pair* hits;
+  int pair_cells;                // hits[].ray holds the voxel's packed cell (x | y << 10 | z << 20)
   const int64_t* seg_start;
   const int64_t* seg_end;
   uint8_t* hit;
@@ -358,6 +359,9 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_cons
   double t = 0.0, prev = NaN;
   int it = 0, ev = 0;
   double o[3] = {0, 0, 0}, d[3] = {0, 0, 0};
+  // the pair at `hidx`, kept in registers: a ray takes several steps per voxel
+  int64_t hidx = -1;
+  ng_hit_pair h{};
 
   auto finish = [&](bool is_hit, double th) {
     A.hit[ray] = is_hit ? 1 : 0;
@@ -414,7 +418,10 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_cons
             dead = true;
             break;
           }
-          const ng_hit_pair h = A.hits[cur];
+          if (hidx != cur) {
+            h = A.hits[cur];
+            hidx = cur;
+          }
           if (t >= h.t_exit) {
             ++cur;
             prev = NaN;
@@ -464,8 +471,18 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_cons
     // ---- query point: x = o + t d clamped into the current voxel (render.py:244-245)
     double x[3] = {0.0, 0.0, 0.0};
     if (act) {
-      const uint64_t code = __ldg(codes + A.hits[cur].voxel);
-      const int cc[3] = {(int)compact3(code), (int)compact3(code >> 1), (int)compact3(code >> 2)};
+      int cc[3];
+      if (A.pair_cells) {
+        const uint32_t pc = (uint32_t)h.ray;
+        cc[0] = (int)(pc & 1023u);
+        cc[1] = (int)((pc >> 10) & 1023u);
+        cc[2] = (int)(pc >> 20);
+      } else {
+        const uint64_t code = __ldg(codes + h.voxel);
+        cc[0] = (int)compact3(code);
+        cc[1] = (int)compact3(code >> 1);
+        cc[2] = (int)compact3(code >> 2);
+      }
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
         const double lo = cell_lo(cc[a], res);
@@ -494,8 +511,9 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_cons
     };
     EvalLane er;
     if constexpr (PS) {
-      if constexpr (TC) er = warp_eval_presum(tree, c, ws, act, x, tcm, emit);
-      else er = warp_eval_presum(tree, c, ws, act, x, SimtMlp{c}, emit);
+      // x lies in the pair's voxel (clamped above), which is locate's answer
+      if constexpr (TC) er = warp_eval_presum(tree, c, ws, act, x, tcm, emit, act ? (int64_t)h.voxel : -1);
+      else er = warp_eval_presum(tree, c, ws, act, x, SimtMlp{c}, emit, act ? (int64_t)h.voxel : -1);
     } else {
       if constexpr (TC) er = warp_eval(tree, c, ws, act, x, tcm, emit);
       else er = warp_eval(tree, c, ws, act, x, SimtMlp{c}, emit);
@@ -1113,6 +1131,7 @@ static int trace_pass(const ng_octree& tree, const ng_render_cfg& cfg, const Lod
   A.d_n_work = d_active;
   A.n_work = 0;
   A.hits = hits;
+  A.pair_cells = tiles ? 1 : 0;
   A.seg_start = seg_start;
   A.seg_end = seg_end;
   A.work_counter = work_counter;
@@ -1316,6 +1335,7 @@ int ng_sphere_trace(const ng_octree* tree, const ng_field* fld, const ng_render_
   A.d_n_work = nullptr;
   A.n_work = n_rays;
   A.hits = hits;
+  A.pair_cells = 0;
   A.seg_start = seg_start;
   A.seg_end = seg_end;
   A.hit = hit;

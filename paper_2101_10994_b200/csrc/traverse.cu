@@ -286,7 +286,9 @@ __global__ void __launch_bounds__(TR_NT) k_traverse_hits(
 // out in the reference's order (parents in list order, children front to
 // back), so per-ray segments are the reference's sub-lists; only the
 // placement of a tile's block in the final list depends on when the warp
-// claims it (one atomic per tile), which the march does not see.
+// claims it (one atomic per tile), which the march does not see. The march
+// knows each pair's ray from the segment it walks, so the `ray` field of
+// these render lists carries the voxel's packed cell coordinates instead.
 #ifndef NG_TT_RAYS
 #define NG_TT_RAYS 32
 #endif
@@ -584,7 +586,7 @@ __global__ void __launch_bounds__(TT_WPB * 32) k_traverse_tiles(
       if (i + 1 == nc || tl_ray(fin, i + 1) != rl) W->seg_e[rl] = i + 1;
       const int cc[3] = {(int)(c & 1023u), (int)((c >> 10) & 1023u), (int)(c >> 20)};
       ng_hit_pair h;
-      h.ray = (int32_t)(r0 + rl);
+      h.ray = (int32_t)c;  // render lists: the voxel's packed cell (the march knows its ray)
       h.voxel = v;
       const int fl = W->flags[rl];
       if (fl & TT_GENERAL) {
