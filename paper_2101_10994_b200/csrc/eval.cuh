@@ -310,6 +310,19 @@ __device__ __forceinline__ EvalLane warp_eval_presum(const ng_octree& tree, cons
                                                      bool act, const double x[3], const Mlp& mlp, Emit&& emit,
                                                      int64_t known = -1) {
   const int lane = (int)lane_id();
+#ifdef NG_PROFILE
+  const bool dbg = c.dbg && lane == 0;
+  unsigned long long t_mark = dbg ? dbg_now() : 0;
+  auto lap = [&](int slot) {
+    if (dbg) {
+      const unsigned long long t = dbg_now();
+      c.dbg[slot] += t - t_mark;
+      t_mark = t;
+    }
+  };
+#else
+  auto lap = [](int) {};
+#endif
   EvalLane res;
   res.present = 0;
   res.inside = true;
@@ -332,6 +345,7 @@ __device__ __forceinline__ EvalLane warp_eval_presum(const ng_octree& tree, cons
     }
   }
   const bool pres = act && idx >= 0;
+  lap(0);
   float4 wa = make_float4(0.f, 0.f, 0.f, 0.f), wb = wa;
   if (pres) {
     res.present = (G >= 32) ? 0xffffffffu : ((1u << G) - 1u);
@@ -357,6 +371,7 @@ __device__ __forceinline__ EvalLane warp_eval_presum(const ng_octree& tree, cons
   const unsigned pm0 = __ballot_sync(FULL, pres);
   const float xf[3] = {(float)x[0], (float)x[1], (float)x[2]};
   __syncwarp();
+  lap(1);
   int slot = 0;
   for (int L = 1; L <= G; ++L) {
     if (!((c.out_mask >> (L - 1)) & 1)) continue;
@@ -400,10 +415,12 @@ __device__ __forceinline__ EvalLane warp_eval_presum(const ng_octree& tree, cons
       }
     }
     __syncwarp();
+    lap(2);
     const bool any = __any_sync(FULL, pres);
     bool bad = false;
     const float d = mlp(L, xf, &ws.zt[lane][0], any, bad);
     emit(L, d, bad && pres, res);
+    lap(3);
   }
   __syncwarp();
   return res;

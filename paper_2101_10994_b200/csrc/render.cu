@@ -251,7 +251,20 @@ struct MarchArgs {
   ng_counters* counters;
   unsigned long long* prof;      // optional: 4 counters per group (steps, busy lanes, t0, t1)
   int lane_cap;                  // max rays a warp marches at once (NG_MARCH_CAP, default 32)
+  // normals (render.py:277-300) in the march: every hit publishes 6 probe
+  // items (slot * 6 + j); lanes without a ray evaluate them, and the lane
+  // completing a slot's sixth probe forms the normal and shades the pixel
+  int probes;
+  unsigned long long* probe_next;  // next probe item to claim
+  unsigned long long* rays_done;   // rays finished (hits published first)
+  unsigned int* probe_cnt;         // per slot: bit 31 published, low bits probes done
+  double* probe_val;               // per slot: the 6 probe values
+  double* normal;
+  uint8_t* normal_ok;
+  uint8_t* color;                  // null: shading happens later (shadow pass)
 };
+
+constexpr unsigned PROBE_READY = 0x80000000u;
 
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
   unsigned long long t;
@@ -285,6 +298,19 @@ __device__ __forceinline__ double field_value(const ng_octree& tree, const EvalL
   return lo;
 }
 
+// shade (render.py:303-314) of one hit pixel with its fp64 normal.
+__device__ __forceinline__ void shade_rgb(const ng_render_cfg& cfg, const double nv[3], uint8_t* rgb_out) {
+  double lam = dadd(dadd(dmul(nv[0], cfg.light[0]), dmul(nv[1], cfg.light[1])), dmul(nv[2], cfg.light[2]));
+  lam = lam < 0.0 ? 0.0 : (lam > 1.0 ? 1.0 : lam);
+  const double amb = cfg.ambient;
+#pragma unroll
+  for (int ch = 0; ch < 3; ++ch) {
+    double rgb = dmul(cfg.albedo[ch], dadd(amb, dmul(dsub(1.0, amb), lam)));
+    rgb = rgb < 0.0 ? 0.0 : (rgb > 1.0 ? 1.0 : rgb);
+    rgb_out[ch] = (uint8_t)dadd(dmul(rgb, 255.0), 0.5);
+  }
+}
+
 // Decoder policy setup shared by the march and normals kernels: SIMT stages
 // fp32 decoders; TC carves TMEM / A tiles / bf16 B tiles (tc_mlp.cuh).
 template <bool TC>
@@ -310,7 +336,7 @@ template <int NW, bool TC, bool PS>
 __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_constant__ ng_octree tree, ng_field f,
                                                               const __grid_constant__ MarchArgs A) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  __shared__ int gflag[NW];
+  __shared__ int gflag[2][NW];  // step parity: a warp is never two steps ahead of its group
   constexpr int GROUPS = TC ? NW / 4 : 1;
   DecoderSetup<TC> D(smem_raw, f, A.dec_first, A.dec_last, GROUPS);
   const int w = threadIdx.x >> 5;
@@ -362,6 +388,15 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_cons
   // the pair at `hidx`, kept in registers: a ray takes several steps per voxel
   int64_t hidx = -1;
   ng_hit_pair h{};
+  // probe item held by a lane without a ray (-1: none), and its point
+  int64_t pk = -1;
+  bool pready = false, probes_done = !A.probes;
+  int step_parity = 0;
+  // rays the group marched last step: probes are taken only by groups with
+  // none left, so they never lengthen the steps of a ray still marching
+  int group_marching = 1;
+  double px[3] = {0, 0, 0};
+  const double eps = A.cfg.normal_eps;
 
   auto finish = [&](bool is_hit, double th) {
     A.hit[ray] = is_hit ? 1 : 0;
@@ -437,18 +472,76 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_cons
           }
           break;
         }
-        if (dead) finish(false, 0.0);
-        else ready = true;
+        if (dead) {
+          finish(false, 0.0);
+          if (A.probes) atomicAdd(A.rays_done, 1ull);
+        } else {
+          ready = true;
+        }
       }
       if (!__any_sync(FULL, ray < 0 && !drained && lane < cap)) break;
     }
+    if (__any_sync(FULL, !probes_done)) {  // warp-uniform: the claim below is a warp collective
+      // lanes out of rays claim probe items (warp-aggregated) ...
+      const bool pw = !probes_done && ray < 0 && pk < 0 && (drained || lane >= cap) && (!TC || group_marching == 0);
+      const unsigned pm = __ballot_sync(FULL, pw);
+      if (pm) {
+        const int leader = __ffs(pm) - 1;
+        unsigned long long b = 0;
+        if (lane == leader) b = atomicAdd(A.probe_next, (unsigned long long)__popc(pm));
+        b = __shfl_sync(FULL, b, leader);
+        if (pw) {
+          pk = (int64_t)(b + __popc(pm & lanemask_lt()));
+          pready = false;
+        }
+      }
+      // ... and start one once its hit is published; an item past the last
+      // hit after every ray has finished ends the lane's probe work
+      if (pk >= 0 && !pready && pk / 6 >= n_work) {  // no such hit can exist
+        pk = -1;
+        probes_done = true;
+      }
+      if (pk >= 0 && !pready) {
+        const int64_t sl = pk / 6;
+        unsigned st;
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(st) : "l"(A.probe_cnt + sl) : "memory");
+        if (st & PROBE_READY) {  // acquire: the publisher's t and hit_list stores are visible
+          const int32_t pix = __ldcg(A.hit_list + sl);
+          const double th = __ldcg(A.t + pix);
+          ng_ray rr;
+          ray_at(A.rays, pix, rr);
+          const int j = (int)(pk % 6), axis = j % 3;
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            double v = dadd(rr.o[a], dmul(th, rr.d[a]));  // hit point (render.py:396)
+            if (a == axis) v = (j < 3) ? dadd(v, eps) : dsub(v, eps);
+            px[a] = np_min(np_max(v, -1.0), 1.0);  // render.py:289-293
+          }
+          pready = true;
+        } else if (*((volatile unsigned long long*)A.rays_done) >= (unsigned long long)n_work &&
+                   (unsigned long long)sl >= *((volatile unsigned long long*)A.d_hit_count)) {
+          pk = -1;
+          probes_done = true;
+        }
+      }
+    }
     const bool act = ray >= 0;
+    const bool pact = pk >= 0 && pready;
+    // a lane stays in the loop while it marches, holds a probe item or may
+    // still claim one
+    const bool alive = act || pk >= 0 || !probes_done || (!drained && lane < cap);
     if constexpr (TC) {
       // the group's 4 warps step together (one 128-row GEMM per output level)
-      const int wf = __popc(__ballot_sync(FULL, act));
-      if (lane == 0) gflag[w] = wf;
+      const int wf = __popc(__ballot_sync(FULL, act || pact));
+      const int wa = __popc(__ballot_sync(FULL, alive));
+      const int wm = __popc(__ballot_sync(FULL, act));
+      int* gf = gflag[step_parity];
+      step_parity ^= 1;
+      if (lane == 0) gf[w] = wf | (wa << 8) | (wm << 16);
       tc::named_sync(1 + g, 128);
-      const int active = gflag[4 * g] + gflag[4 * g + 1] + gflag[4 * g + 2] + gflag[4 * g + 3];
+      const int gs = gf[4 * g] + gf[4 * g + 1] + gf[4 * g + 2] + gf[4 * g + 3];
+      const int active = gs & 0xff, any_alive = (gs >> 8) & 0xff;
+      group_marching = gs >> 16;
 #ifdef NG_PROFILE
       if (A.prof && (w & 3) == 0 && lane == 0) {  // debug profile: per-group steps and busy lanes
         unsigned long long* pr = A.prof + 8 * (blockIdx.x * GROUPS + g);
@@ -463,13 +556,22 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_cons
         t_acq = now;
       }
 #endif
-      if (!active) break;
+      if (!any_alive) break;
+      if (!active) {  // waiting for hits to publish probe items
+        __nanosleep(256);
+        continue;
+      }
     } else {
-      if (!__any_sync(FULL, act)) break;
+      if (!__any_sync(FULL, alive)) break;
+      if (!__any_sync(FULL, act || pact)) {
+        __nanosleep(256);
+        continue;
+      }
     }
 
-    // ---- query point: x = o + t d clamped into the current voxel (render.py:244-245)
-    double x[3] = {0.0, 0.0, 0.0};
+    // ---- query point: x = o + t d clamped into the current voxel (render.py:244-245),
+    // or the lane's normal probe
+    double x[3] = {px[0], px[1], px[2]};
     if (act) {
       int cc[3];
       if (A.pair_cells) {
@@ -495,8 +597,9 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_cons
       }
     }
     FieldValue fv;
+    const bool eact = act || pact;
     auto emit = [&](int L, float dv, bool bad, const EvalLane& e) {
-      if (!act || !e.inside) return;
+      if (!eact || !e.inside) return;
       double v;
       if (e.present & ((1u << L) - 1u)) {
         v = (double)dv;
@@ -512,11 +615,12 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_cons
     EvalLane er;
     if constexpr (PS) {
       // x lies in the pair's voxel (clamped above), which is locate's answer
-      if constexpr (TC) er = warp_eval_presum(tree, c, ws, act, x, tcm, emit, act ? (int64_t)h.voxel : -1);
-      else er = warp_eval_presum(tree, c, ws, act, x, SimtMlp{c}, emit, act ? (int64_t)h.voxel : -1);
+      // (a probe point is located as usual)
+      if constexpr (TC) er = warp_eval_presum(tree, c, ws, eact, x, tcm, emit, act ? (int64_t)h.voxel : -1);
+      else er = warp_eval_presum(tree, c, ws, eact, x, SimtMlp{c}, emit, act ? (int64_t)h.voxel : -1);
     } else {
-      if constexpr (TC) er = warp_eval(tree, c, ws, act, x, tcm, emit);
-      else er = warp_eval(tree, c, ws, act, x, SimtMlp{c}, emit);
+      if constexpr (TC) er = warp_eval(tree, c, ws, eact, x, tcm, emit);
+      else er = warp_eval(tree, c, ws, eact, x, SimtMlp{c}, emit);
     }
     auto dval_of = [&](const EvalLane& e, const FieldValue& v, const double* px) {
       return field_value(tree, e, v.lo, v.hi, A.blend_alpha, px);
@@ -529,7 +633,37 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_cons
     }
 #endif
     // ---- stop rules (render.py:247-272)
-    if (act && !er.inside) lc.empty += 1;  // query_field's own empty-space fallback
+    if (eact && !er.inside) lc.empty += 1;  // query_field's own empty-space fallback
+    if (pact) {
+      // normals (render.py:294-299): g = (v+ - v-) / (2 eps) once all 6 are in
+      const int64_t sl = pk / 6;
+      A.probe_val[pk] = dval_of(er, fv, x);
+      __threadfence();
+      const unsigned old = atomicAdd(A.probe_cnt + sl, 1u);
+      if ((old & 0xffffu) == 5u) {
+        __threadfence();
+        double vals[6];
+#pragma unroll
+        for (int j = 0; j < 6; ++j) vals[j] = __ldcg(A.probe_val + 6 * sl + j);
+        const int32_t pix = __ldcg(A.hit_list + sl);
+        const double two_eps = 2.0 * eps;
+        double gr[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) gr[a] = dsub(vals[a], vals[3 + a]) / two_eps;
+        const double nrm = __dsqrt_rn(dadd(dadd(dmul(gr[0], gr[0]), dmul(gr[1], gr[1])), dmul(gr[2], gr[2])));
+        const bool ok = isfinite(nrm) && nrm > 1e-12;
+        double nv[3] = {0.0, 0.0, 0.0};
+        if (ok) {
+#pragma unroll
+          for (int a = 0; a < 3; ++a) nv[a] = gr[a] / nrm;
+        }
+#pragma unroll
+        for (int a = 0; a < 3; ++a) A.normal[3 * (int64_t)pix + a] = nv[a];
+        A.normal_ok[pix] = ok ? 1 : 0;
+        if (A.color) shade_rgb(A.cfg, nv, A.color + 3 * (int64_t)pix);
+      }
+      pk = -1;
+    }
     if (act) {
       double dval = dval_of(er, fv, x);
       ev += A.passes;
@@ -537,14 +671,21 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_cons
       const bool is_hit = dval < A.cfg.delta;
       const bool stalled = !is_hit && (dval >= prev) && (fabs(dsub(dval, prev)) < A.cfg.osc_tol);
       if (is_hit) {
-        if (A.hit_list) {
-          const unsigned long long slot = atomicAdd(A.d_hit_count, 1ull);
-          A.hit_list[slot] = ray;
-        }
+        const int r_id = ray;
         const double th = dadd(t, dval);
         finish(true, th);
+        if (A.hit_list) {
+          const unsigned long long slot = atomicAdd(A.d_hit_count, 1ull);
+          A.hit_list[slot] = r_id;
+          if (A.probes) {  // publish the slot's probes (t written above)
+            __threadfence();
+            atomicOr(A.probe_cnt + slot, PROBE_READY);
+          }
+        }
+        if (A.probes) atomicAdd(A.rays_done, 1ull);
       } else if (stalled || it >= A.cfg.max_iters) {
         finish(false, 0.0);
+        if (A.probes) atomicAdd(A.rays_done, 1ull);
       } else {
         prev = dval;
         t = dadd(t, dval);
@@ -696,19 +837,7 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_normals(const __grid_co
 #pragma unroll
       for (int a = 0; a < 3; ++a) A.normal[3 * dst + a] = nv[a];
       A.ok[dst] = ok ? 1 : 0;
-      if (A.color) {
-        // shade (render.py:303-314) with the fp64 normal
-        double lam = dadd(dadd(dmul(nv[0], A.cfg.light[0]), dmul(nv[1], A.cfg.light[1])),
-                          dmul(nv[2], A.cfg.light[2]));
-        lam = lam < 0.0 ? 0.0 : (lam > 1.0 ? 1.0 : lam);
-        const double amb = A.cfg.ambient;
-#pragma unroll
-        for (int ch = 0; ch < 3; ++ch) {
-          double rgb = dmul(A.cfg.albedo[ch], dadd(amb, dmul(dsub(1.0, amb), lam)));
-          rgb = rgb < 0.0 ? 0.0 : (rgb > 1.0 ? 1.0 : rgb);
-          A.color[3 * dst + ch] = (uint8_t)dadd(dmul(rgb, 255.0), 0.5);
-        }
-      }
+      if (A.color) shade_rgb(A.cfg, nv, A.color + 3 * dst);  // render.py:303-314, fp64 normal
     }
   }
   lc.flush(A.counters);
@@ -986,6 +1115,7 @@ struct WsLayout {
   size_t rays, pairs_a, pairs_b, hits, seg_start, seg_end, active, hit_list, scratch, ctr, total;
   size_t s_rays, s_hit, s_t, s_it, s_ev;  // shadow-ray pass
   size_t sorted, buckets;                 // longest-first march order
+  size_t probe_val, probe_cnt;            // normals evaluated in the march
   size_t scratch_bytes;
 };
 
@@ -1027,6 +1157,8 @@ static WsLayout layout(int64_t n, int64_t pair_cap, int64_t hit_cap) {
   L.s_it = o; o = al(o + (size_t)n * 4);
   L.s_ev = o; o = al(o + (size_t)n * 4);
   L.sorted = o; o = al(o + (size_t)n * 4);
+  L.probe_val = o; o = al(o + (size_t)n * 6 * 8);
+  L.probe_cnt = o; o = al(o + (size_t)n * 4);
   L.buckets = o; o = al(o + 2 * LEN_BUCKETS * 4);
   L.total = o;
   return L;
@@ -1136,6 +1268,7 @@ static int trace_pass(const ng_octree& tree, const ng_render_cfg& cfg, const Lod
   A.seg_end = seg_end;
   A.work_counter = work_counter;
   A.prof = march_profile_buffer();
+  A.probes = 0;
   return NG_OK;
 }
 
@@ -1158,7 +1291,8 @@ static int render_common(const ng_octree& tree, const ng_field& f, const ng_rend
   char* b = (char*)ws.base;
   ng_ray* rays = user_rays ? (ng_ray*)user_rays : (ng_ray*)(b + L.rays);
   int32_t* hit_list = (int32_t*)(b + L.hit_list);
-  // [0] active rays, [1] hits, [2] march work, [3] shadow active, [4] shadow work
+  // [0] active rays, [1] hits, [2] march work, [3] shadow active, [4] shadow work,
+  // [5] probe items claimed, [6] rays finished
   unsigned long long* ctr = (unsigned long long*)(b + L.ctr);
   int r;
   int64_t* seg_start = (int64_t*)(b + L.seg_start);
@@ -1176,6 +1310,9 @@ static int render_common(const ng_octree& tree, const ng_field& f, const ng_rend
     z.bytes[2] = L.scratch_bytes * (size_t)(cfg.trace_level + tree.n_virtual);
     z.p[3] = b + L.buckets;
     z.bytes[3] = 2 * LEN_BUCKETS * 4;
+    z.p[4] = b + L.probe_cnt;
+    z.bytes[4] = (size_t)n * 4;
+    z.n = 5;
     k_zero_regions<<<64, 256, 0, s>>>(z);
     NG_CHECK_LAUNCH("k_zero_regions");
   }
@@ -1214,13 +1351,29 @@ static int render_common(const ng_octree& tree, const ng_field& f, const ng_rend
   A.hit_list = hit_list;
   A.d_hit_count = ctr + 1;
   A.counters = &st->counters;
+  // normals: probe items inside the march (default), or the k_normals pass
+  // after it (NG_FUSED_PROBES=0)
+  static int fused_env = -1;
+  if (fused_env < 0) {
+    const char* e = getenv("NG_FUSED_PROBES");
+    fused_env = (e && e[0] == '0') ? 0 : 1;
+  }
+  const bool fused = do_normals && fused_env;
+  A.probes = fused ? 1 : 0;
+  A.probe_next = ctr + 5;
+  A.rays_done = ctr + 6;
+  A.probe_cnt = (unsigned int*)(b + L.probe_cnt);
+  A.probe_val = (double*)(b + L.probe_val);
+  A.normal = fr.normal;
+  A.normal_ok = fr.normal_ok;
+  A.color = cfg.shadows ? nullptr : fr.color;
   if (ws.ev_march_begin && (r = cuda_status(cudaEventRecord((cudaEvent_t)ws.ev_march_begin, s), "event record")))
     return r;
   if ((r = launch_march(tree, f, A, s))) return r;
   if (ws.ev_trace_done && (r = cuda_status(cudaEventRecord((cudaEvent_t)ws.ev_trace_done, s), "event record")))
     return r;
-  // ---- normals + shading (render.py:399-414, 440)
-  if (do_normals) {
+  // ---- normals + shading (render.py:399-414, 440), when not in the march
+  if (do_normals && !fused) {
     NormalArgs B;
     B.cfg = cfg;
     B.G = P.G;
@@ -1347,6 +1500,7 @@ int ng_sphere_trace(const ng_octree* tree, const ng_field* fld, const ng_render_
   A.work_counter = work;
   A.counters = d_counters;
   A.prof = nullptr;
+  A.probes = 0;
   (void)d_hit_count;
   r = launch_march(*tree, *fld, A, s);
   cudaFreeAsync(work, s);

@@ -1,6 +1,7 @@
 """The render path's warp-per-tile traversal (traverse.cu k_traverse_tiles)
 against the level-by-level kernels and the golden frame, including its
-shared-memory spill path and the overflow -> grow -> rerun loop. The knobs
+shared-memory spill path and the overflow -> grow -> rerun loop; and the
+normals evaluated inside the march against the separate normals pass. The knobs
 are read once per process, so each configuration renders in a subprocess
 (tests/tile_probe.py)."""
 import os
@@ -33,11 +34,12 @@ def frames(tmp_path_factory):
         "levels": _probe(tmp, "levels", {"NG_TILE_TRAVERSE": "0"}),
         "spill": _probe(tmp, "spill", {"NG_TILE_SCAP": "3"}),
         "overflow": _probe(tmp, "overflow", {"NG_TILE_SCAP": "0", "NG_TILE_ARENA_MIN": "0"}, "tiny_pairs"),
+        "normals_pass": _probe(tmp, "normals_pass", {"NG_FUSED_PROBES": "0"}),
     }
 
 
 def _same(a, b):
-    for k in ("hit", "t", "color", "iterations", "evals", "visible", "n_evals"):
+    for k in ("hit", "t", "color", "iterations", "evals", "visible", "n_evals", "normal", "normal_ok"):
         np.testing.assert_array_equal(a[k], b[k], err_msg=k)
 
 
@@ -63,3 +65,9 @@ def test_overflow_grows_and_reruns(frames):
     f = frames["overflow"]
     assert int(f["grows"]) >= 1
     _same(f, frames["tiles"])
+
+
+def test_probes_in_march_equal_normals_pass(frames):
+    """Normals evaluated as probe items inside the march (default) equal the
+    separate k_normals pass bit for bit (same evaluations, same counters)."""
+    _same(frames["tiles"], frames["normals_pass"])

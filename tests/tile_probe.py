@@ -44,5 +44,6 @@ svo = ng.build_octree(O.sdf_torus(0.5, 0.2), 4, go["samples_b"])
 fld = scenes.planted_field(svo, O.sdf_torus(0.5, 0.2), seed=0, device_sdf=False)
 cam = ng.Camera((0.0, 2.0, 3.5), (0.0, 0.0, 0.0), (0.0, 1.0, 0.0), 30.0, 96, 72)
 fb, rep = ng.render(cam, fld, ng.RenderConfig())
-np.savez(out, hit=fb.hit, t=fb.t, color=fb.color, iterations=fb.iterations, evals=fb.evals,
+np.savez(out, hit=fb.hit, t=fb.t, color=fb.color, iterations=fb.iterations, evals=fb.evals, normal=fb.normal,
+         normal_ok=fb.normal_ok,
          visible=rep.visible, n_evals=rep.evals, grows=grows[0])
