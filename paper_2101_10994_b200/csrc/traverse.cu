@@ -502,6 +502,8 @@ __global__ void __launch_bounds__(TT_WPB * 32) k_traverse_tiles(
       const int32_t* __restrict__ cstart = tree.child_start[t];
       const uint8_t* __restrict__ cmask = tree.child_mask[t];
       int out = 0;
+      const bool last_pass = t + 1 == target;
+      int carry_prev = -1;  // ray of the previous round's last item
       for (int base = 0; base < nc; base += 32 * TT_ITEMS) {
         int32_t first[TT_ITEMS];
         uint32_t pcell[TT_ITEMS];
@@ -514,7 +516,7 @@ __global__ void __launch_bounds__(TT_WPB * 32) k_traverse_tiles(
           hm[q] = 0;
           first[q] = 0;
           pcell[q] = 0;
-          pr[q] = 0;
+          pr[q] = -1;
           if (i < nc) {
             int32_t pv;
             tl_get(src, i, pv, pcell[q], pr[q]);
@@ -550,8 +552,25 @@ __global__ void __launch_bounds__(TT_WPB * 32) k_traverse_tiles(
         }
         const int incl = warp_incl_scan<int>(sum);
         int o = out + incl - sum;
+        // last pass: each ray's final segment runs from its first parent's
+        // first child to its last parent's last child (parents of a ray are
+        // contiguous); neighbours' rays come from the adjacent lanes
+        int nb_prev = 0, nb_next = 0;
+        if (last_pass) {
+          nb_prev = __shfl_up_sync(FULL, pr[TT_ITEMS - 1], 1);
+          nb_next = __shfl_down_sync(FULL, pr[0], 1);
+          if (lane == 0) nb_prev = carry_prev;
+          if (lane == 31) nb_next = base + 32 * TT_ITEMS < nc ? tl_ray(src, base + 32 * TT_ITEMS) : -1;
+          carry_prev = __shfl_sync(FULL, pr[TT_ITEMS - 1], 31);
+        }
 #pragma unroll
         for (int q = 0; q < TT_ITEMS; ++q) {
+          if (last_pass && pr[q] >= 0) {
+            const int prv = q > 0 ? pr[q - 1] : nb_prev;
+            const int nxt = q + 1 < TT_ITEMS ? pr[q + 1] : nb_next;
+            if (prv != pr[q]) W->seg_s[pr[q]] = o;
+            if (nxt != pr[q]) W->seg_e[pr[q]] = o + __popc(hm[q] & 0xffu);
+          }
           const int dm = (int)((hm[q] >> 8) & 7u);
           const unsigned m = (hm[q] >> 16) & 0xffu;
           const uint32_t c2 = pcell[q] << 1;  // 2 * (x, y, z), packed (parent cells < 512 per axis)
@@ -571,7 +590,7 @@ __global__ void __launch_bounds__(TT_WPB * 32) k_traverse_tiles(
       nc = out < lim ? out : lim;
     }
     // ---- final pairs: claim the tile's block of the hit list, write
-    // (ray, voxel, t_enter, t_exit) and the per-ray segments
+    // (cell, voxel, t_enter, t_exit) and the per-ray segments (set above)
     const TileList fin = tile_list(W, ga, gcap, target & 1, scap);
     unsigned long long hb = 0;
     if (lane == 0 && nc > 0) hb = atomicAdd(hit_cursor, (unsigned long long)nc);
@@ -582,8 +601,6 @@ __global__ void __launch_bounds__(TT_WPB * 32) k_traverse_tiles(
       uint32_t c;
       int rl;
       tl_get(fin, i, v, c, rl);
-      if (i == 0 || tl_ray(fin, i - 1) != rl) W->seg_s[rl] = i;
-      if (i + 1 == nc || tl_ray(fin, i + 1) != rl) W->seg_e[rl] = i + 1;
       const int cc[3] = {(int)(c & 1023u), (int)((c >> 10) & 1023u), (int)(c >> 20)};
       ng_hit_pair h;
       h.ray = (int32_t)c;  // render lists: the voxel's packed cell (the march knows its ray)
