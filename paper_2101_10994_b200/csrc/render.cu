@@ -25,7 +25,7 @@ int traverse_hits(const ng_octree& tree, const ng_ray* rays, int t, bool next_fi
                   int64_t* d_count_out, int64_t out_cap, void* scratch, size_t scratch_bytes, cudaStream_t s,
                   int64_t* seg_start, int64_t* seg_end, const double* shared_origin);
 int traverse_tiles(const ng_octree& tree, const ng_ray* rays, const int64_t* d_n, int64_t n_max, int target,
-                   int64_t* counts,
+                   int32_t* active, unsigned long long* d_active, int64_t* counts,
                    ng_hit_pair* hits, int64_t hit_cap, void* ctl, int64_t* seg_start, int64_t* seg_end,
                    void* arena, size_t arena_bytes, unsigned long long* d_need, const double* shared_origin,
                    const ng_camera* cam_rays, cudaStream_t s);
@@ -1222,7 +1222,7 @@ static int trace_pass(const ng_octree& tree, const ng_render_cfg& cfg, const Lod
     // look-back scratch
     const size_t arena_bytes = L.hits - L.pairs_a;
     unsigned long long* need = (unsigned long long*)((char*)scratch + 16);
-    r = traverse_tiles(tree, rays, &counts[0], n, target, counts, hits, ws.hit_capacity, scratch, seg_start, seg_end,
+    r = traverse_tiles(tree, rays, &counts[0], n, target, active, d_active, counts, hits, ws.hit_capacity, scratch, seg_start, seg_end,
                        b + L.pairs_a, arena_bytes, need, shared_origin, cam_rays, s);
     if (r) return r;
     tov.need = need;
@@ -1243,11 +1243,13 @@ static int trace_pass(const ng_octree& tree, const ng_render_cfg& cfg, const Lod
     in_cap = ws.pair_capacity;
   }
   int32_t* sorted = (int32_t*)(b + L.sorted);
-  k_active_hist<<<grid_for(n, 256), 256, 0, s>>>(seg_start, seg_end, n, active, d_active, buckets);
-  NG_CHECK_LAUNCH("k_active_hist");
-  k_len_scatter<<<grid_for(n, 256), 256, 0, s>>>(active, d_active, seg_start, seg_end, buckets,
-                                                  buckets + LEN_BUCKETS, sorted);
-  NG_CHECK_LAUNCH("k_len_scatter");
+  if (!tiles) {  // the tile traversal appends the work list itself (tile order)
+    k_active_hist<<<grid_for(n, 256), 256, 0, s>>>(seg_start, seg_end, n, active, d_active, buckets);
+    NG_CHECK_LAUNCH("k_active_hist");
+    k_len_scatter<<<grid_for(n, 256), 256, 0, s>>>(active, d_active, seg_start, seg_end, buckets,
+                                                    buckets + LEN_BUCKETS, sorted);
+    NG_CHECK_LAUNCH("k_len_scatter");
+  }
   A.cfg = cfg;
   A.G = P.G;
   A.out_mask = P.out_mask;
@@ -1259,7 +1261,10 @@ static int trace_pass(const ng_octree& tree, const ng_render_cfg& cfg, const Lod
   A.rays.rays = rays;
   A.rays.cam_rays = cam_rays != nullptr;
   if (cam_rays) A.rays.cam = *cam_rays;
-  A.work = sorted;
+  // level-by-level path: longest segments first; the tile path marches in
+  // tile order (measured the same on the 720p knot frame, and it saves the
+  // histogram and scatter launches)
+  A.work = tiles ? active : sorted;
   A.d_n_work = d_active;
   A.n_work = 0;
   A.hits = hits;
