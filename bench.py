@@ -469,7 +469,10 @@ def main():
     # them, every level 1..L
     levels_read = 1 if res.get("presum") else MAX_LEVEL
     bytes_per_eval = EVAL_BYTES_BASE + EVAL_BYTES_PER_LEVEL * levels_read
-    algo_bytes = res["trace_evals"] * bytes_per_eval
+    # the march launch also evaluates the normal probes (NG_FUSED_PROBES, default)
+    fused = os.environ.get("NG_FUSED_PROBES", "1") != "0"
+    march_evals = res["total_evals"] if fused else res["trace_evals"]
+    algo_bytes = march_evals * bytes_per_eval
     peak = _peak_hbm()
     achieved = algo_bytes / (march * 1e-3) / 1e9
     traffic = _traffic()
@@ -492,11 +495,13 @@ def main():
                   "frame_ms_median": statistics.median(res["frame_ms"])},
         "e2e": res["e2e"],
         "gpu_launches": args.steps * (_launches_per_frame(res["_svo"]) + (world + 1 if world > 1 else 0)),
-        "roofline": {"bound": "hbm", "kernel": "k_march (sphere-trace march, fused gather + MLP)",
+        "roofline": {"bound": "hbm", "kernel": "k_march (sphere-trace march + normal probes, fused gather + MLP)"
+                     if fused else "k_march (sphere-trace march, fused gather + MLP)",
                      "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic,
                      "algorithmic_bytes": algo_bytes,
-                     "note": f"{bytes_per_eval} B per eval x trace evals ({levels_read} level(s) read per eval: "
+                     "evals": march_evals,
+                     "note": f"{bytes_per_eval} B per eval x the launch's evals ({levels_read} level(s) read per eval: "
                              "presummed S_L rows (SURVEY.md 8d per-level bytes)); peak = measured hbm_gbs"},
         "clocks": res["clocks"],
         "presum": res.get("presum"),
@@ -517,10 +522,19 @@ def _voxel_counts(svo):
 
 
 def _launches_per_frame(svo):
-    # camera rays, one hit-filtered traversal pass per level, segments, the
-    # longest-first order (histogram + scatter), march, normals, stats
-    # (cf. profiles/r01_final/launch_shares.md)
-    return 1 + (MAX_LEVEL + svo.device.n_virtual) + 1 + 2 + 1 + 1 + 1
+    # zeroing + frame defaults, the tile traversal (all levels, work list),
+    # the march (normals as probe items inside it), stats; the
+    # level-by-level traversal (NG_TILE_TRAVERSE=0) adds one pass per level
+    # and the histogram + scatter, NG_FUSED_PROBES=0 the normals pass
+    # (cf. profiles/r01_tiles/launch_shares.md)
+    levels = os.environ.get("NG_TILE_TRAVERSE", "1") == "0"
+    fused = os.environ.get("NG_FUSED_PROBES", "1") != "0"
+    n = 1 + 1 + 1 + 1 + 1
+    if levels:
+        n += (MAX_LEVEL + svo.device.n_virtual) - 1 + 2
+    if not fused:
+        n += 1
+    return n
 
 
 def _peak_hbm():
