@@ -62,7 +62,21 @@ class Camera:
         true_up = np.cross(right, fwd)
         return fwd, right, true_up
 
+    def _key(self):
+        return (self.position.tobytes(), self.look_at.tobytes(), self.up.tobytes(), float(self.fov_y_deg),
+                int(self.width), int(self.height))
+
     def struct(self) -> _lib.NgCamera:
+        """The C camera (basis in fp64), cached on the camera for its current
+        parameters; callers get their own copy."""
+        key = self._key()
+        cached = self.__dict__.get("_struct_cache")
+        if cached is None or cached[0] != key:
+            cached = (key, self._make_struct())
+            self.__dict__["_struct_cache"] = cached
+        return _lib.NgCamera.from_buffer_copy(cached[1])
+
+    def _make_struct(self) -> _lib.NgCamera:
         fwd, right, up = self.basis()
         c = _lib.NgCamera()
         for a in range(3):
@@ -427,6 +441,42 @@ def resolve_lod(camera: Camera, fld: NeuralField, config: RenderConfig) -> float
     return max(lod, 1.0)
 
 
+class FrameTensors:
+    """One frame's device outputs in a single allocation. The C side gets
+    raw pointers (no per-field tensor ops on the per-frame path); a field's
+    tensor view is made on first access, `frame["color"]` etc."""
+
+    # name: (byte offset per pixel, bytes per pixel, dtype, trailing shape)
+    _LAYOUT = {"t": (0, 8, torch.float64, ()), "normal": (8, 24, torch.float64, (3,)),
+               "iterations": (32, 4, torch.int32, ()), "evals": (36, 4, torch.int32, ()),
+               "hit": (40, 1, torch.uint8, ()), "normal_ok": (41, 1, torch.uint8, ()),
+               "color": (42, 3, torch.uint8, (3,))}
+    BYTES_PER_PIXEL = 45
+
+    def __init__(self, n: int, dev):
+        self.n = n
+        self.buf = torch.empty(self.BYTES_PER_PIXEL * n, dtype=torch.uint8, device=dev)
+        self._views = {}
+
+    def struct(self) -> _lib.NgFrame:
+        b, n = self.buf.data_ptr(), self.n
+        off = {k: b + v[0] * n for k, v in self._LAYOUT.items()}
+        return _lib.NgFrame(off["hit"], off["t"], off["normal"], off["normal_ok"], off["iterations"], off["evals"],
+                            off["color"])
+
+    def __getitem__(self, name):
+        v = self._views.get(name)
+        if v is None:
+            o, w, dt, tail = self._LAYOUT[name]
+            n = self.n
+            v = self.buf[o * n:(o + w) * n].view(dt).view((n,) + tail)
+            self._views[name] = v
+        return v
+
+    def __contains__(self, name):
+        return name in self._LAYOUT
+
+
 class RenderSession:
     """Reusable device state for rendering frames of one size: workspace,
     frame buffers, statistics. `enqueue` launches a frame with no host sync;
@@ -452,20 +502,15 @@ class RenderSession:
         self.ws_buf = torch.empty(nbytes, dtype=torch.uint8, device=self.dev)
         self.ws = _lib.NgWorkspace(ptr(self.ws_buf), nbytes, self.pair_cap, self.hit_cap, None, None)
 
-    def new_frame(self) -> dict:
-        n, dev = self.n, self.dev
-        return {
-            "hit": torch.empty(n, dtype=torch.uint8, device=dev),
-            "t": torch.empty(n, dtype=torch.float64, device=dev),
-            "normal": torch.empty((n, 3), dtype=torch.float64, device=dev),
-            "normal_ok": torch.empty(n, dtype=torch.uint8, device=dev),
-            "iterations": torch.empty(n, dtype=torch.int32, device=dev),
-            "evals": torch.empty(n, dtype=torch.int32, device=dev),
-            "color": torch.empty((n, 3), dtype=torch.uint8, device=dev),
-        }
+    def new_frame(self) -> "FrameTensors":
+        """Fresh per-pixel output buffers (every frame owns its own, as the
+        reference returns fresh arrays)."""
+        return FrameTensors(self.n, self.dev)
 
     @staticmethod
-    def frame_struct(fr: dict) -> _lib.NgFrame:
+    def frame_struct(fr) -> _lib.NgFrame:
+        if isinstance(fr, FrameTensors):
+            return fr.struct()
         return _lib.NgFrame(ptr(fr["hit"]), ptr(fr["t"]), ptr(fr["normal"]), ptr(fr["normal_ok"]),
                             ptr(fr["iterations"]), ptr(fr["evals"]), ptr(fr["color"]))
 
