@@ -20,6 +20,9 @@
 #ifndef NG_GATHER_BATCH
 #define NG_GATHER_BATCH 4  // points whose 8 corner rows are in flight together per warp
 #endif
+#ifndef NG_QUAD_GATHER
+#define NG_QUAD_GATHER 1   // warp_eval: 16-byte row loads, 4 points per load instruction
+#endif
 
 namespace ng {
 
@@ -119,6 +122,7 @@ struct EvalLane {
 // of the warp needs a decode).
 struct SimtMlp {
   const EvalCtx& c;
+  __device__ __forceinline__ void prepare(int) const {}
   __device__ __forceinline__ float operator()(int l, const float xf[3], const float* zrow, bool any,
                                               bool& bad) const {
     bad = false;
@@ -243,6 +247,63 @@ __device__ __forceinline__ EvalLane warp_eval(const ng_octree& tree, const EvalC
     unsigned pm = __ballot_sync(FULL, pres);
     __syncwarp();
     lap(1);
+#if NG_QUAD_GATHER
+    // lane = (point slot lane / 8, channel quad lane % 8): a 128-byte corner
+    // row is 8 lanes' 16-byte loads, so one load instruction covers 4
+    // points' rows; GB points (2 GB rows per lane) are in flight per
+    // iteration; absent slots re-read a present point and are dropped
+    if constexpr (GB % 4 == 0) {
+      const int grp = lane >> 3, sub = lane & 7;
+      const float4* __restrict__ Z4 = reinterpret_cast<const float4*>(c.Z) + sub;
+      while (pm) {
+        int pp[GB];
+#pragma unroll
+        for (int q = 0; q < GB; ++q) {
+          pp[q] = pm ? __ffs(pm) - 1 : -1;
+          pm &= pm ? pm - 1 : 0u;
+        }
+        int mine[GB / 4];
+        float4 v[GB / 4][8];
+#pragma unroll
+        for (int k = 0; k < GB / 4; ++k) {
+          const int a0 = pp[4 * k], a1 = pp[4 * k + 1], a2 = pp[4 * k + 2], a3 = pp[4 * k + 3];
+          mine[k] = grp == 0 ? a0 : (grp == 1 ? a1 : (grp == 2 ? a2 : a3));
+          const int p = mine[k] >= 0 ? mine[k] : pp[0];
+          const int4 a = ws.ids[p][0], b = ws.ids[p][1];
+          v[k][0] = __ldg(Z4 + 8 * (int64_t)a.x);
+          v[k][1] = __ldg(Z4 + 8 * (int64_t)a.y);
+          v[k][2] = __ldg(Z4 + 8 * (int64_t)a.z);
+          v[k][3] = __ldg(Z4 + 8 * (int64_t)a.w);
+          v[k][4] = __ldg(Z4 + 8 * (int64_t)b.x);
+          v[k][5] = __ldg(Z4 + 8 * (int64_t)b.y);
+          v[k][6] = __ldg(Z4 + 8 * (int64_t)b.z);
+          v[k][7] = __ldg(Z4 + 8 * (int64_t)b.w);
+        }
+#pragma unroll
+        for (int k = 0; k < GB / 4; ++k) {
+          if (mine[k] < 0) continue;
+          const float4 u0 = ws.w[mine[k]][0], u1 = ws.w[mine[k]][1];
+          const float wj[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
+          float acc[4];
+          acc[0] = wj[0] * v[k][0].x;
+          acc[1] = wj[0] * v[k][0].y;
+          acc[2] = wj[0] * v[k][0].z;
+          acc[3] = wj[0] * v[k][0].w;
+#pragma unroll
+          for (int jj = 1; jj < 8; ++jj) {
+            acc[0] = fmaf(wj[jj], v[k][jj].x, acc[0]);
+            acc[1] = fmaf(wj[jj], v[k][jj].y, acc[1]);
+            acc[2] = fmaf(wj[jj], v[k][jj].z, acc[2]);
+            acc[3] = fmaf(wj[jj], v[k][jj].w, acc[3]);
+          }
+          float* zr = &ws.zt[mine[k]][4 * sub];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) zr[e] += acc[e];
+        }
+      }
+    } else
+#endif
+    {
     // lane = channel: coalesced 128-byte corner rows, 4 points (32 loads) in
     // flight per iteration; absent slots re-read a present point and are
     // masked out of the accumulation
@@ -283,9 +344,11 @@ __device__ __forceinline__ EvalLane warp_eval(const ng_octree& tree, const EvalC
         ws.zt[pp[q]][lane] += acc;
       }
     }
+    }
     __syncwarp();
     if ((c.out_mask >> (l - 1)) & 1) {
       lap(2);
+      mlp.prepare(l);  // decoder policies that stage one level at a time (k_query_tc)
       const bool any = __any_sync(FULL, dec && (res.present != 0));
       bool bad = false;
       const float d = mlp(l, xf, &ws.zt[lane][0], any, bad);

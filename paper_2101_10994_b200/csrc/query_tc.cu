@@ -22,7 +22,10 @@ namespace ng {
 
 int grid_for(int64_t n, int nt);
 
-constexpr int TQ_GROUPS = 2;
+// 4 groups (16 warps) per CTA: the CTA holds one decoder level at a time and
+// re-stages it per level (all groups step through the levels together), so
+// the five decoders' tiles do not cap the CTA at 2 groups
+constexpr int TQ_GROUPS = 4;
 constexpr int TQ_NW = 4 * TQ_GROUPS;
 
 __global__ void __launch_bounds__(TQ_NW * 32, 1) k_query_tc(const __grid_constant__ ng_octree tree, ng_field f,
@@ -31,13 +34,14 @@ __global__ void __launch_bounds__(TQ_NW * 32, 1) k_query_tc(const __grid_constan
                                                             double* __restrict__ out, int ncols,
                                                             ng_counters* counters) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  const int ndec = dec_last - dec_first + 1;
-  const TcSmem t = tc_carve(smem, ndec, TQ_GROUPS);
+  const TcSmem t = tc_carve(smem, 1, TQ_GROUPS);
   const int w = threadIdx.x >> 5;
   const int g = w / 4, wg = w % 4;
-  const uint32_t tmem_base = tc_setup(t, f.decoders, dec_first, dec_last, f.dec_stride, TQ_GROUPS);
+  const uint32_t tmem_base = tc_setup(t, f.decoders, dec_first, dec_first, f.dec_stride, TQ_GROUPS);
   uint32_t phase = 0;
-  const TcMlp mlp = tc_policy(t, tmem_base, dec_first, &phase);
+  TcMlp mlp = tc_policy(t, tmem_base, dec_first, &phase);
+  mlp.restage_src = f.decoders;
+  mlp.restage_stride = f.dec_stride;
 
   EvalCtx c;
   c.Z = f.Z;
@@ -53,7 +57,9 @@ __global__ void __launch_bounds__(TQ_NW * 32, 1) k_query_tc(const __grid_constan
   const double alpha = a.blend_alpha;
   LaneCounters lc;
   const int64_t n_tiles = (n + 127) / 128;
-  for (int64_t tile = (int64_t)blockIdx.x * TQ_GROUPS + g; tile < n_tiles; tile += (int64_t)gridDim.x * TQ_GROUPS) {
+  // the CTA's groups take tiles together (the level restaging is CTA-wide)
+  for (int64_t tb = (int64_t)blockIdx.x * TQ_GROUPS; tb < n_tiles; tb += (int64_t)gridDim.x * TQ_GROUPS) {
+    const int64_t tile = tb + g;
     const int64_t i = tile * 128 + 32 * wg + lane_id();
     const bool act = i < n;
     double x[3] = {0.0, 0.0, 0.0};
@@ -96,7 +102,7 @@ __global__ void __launch_bounds__(TQ_NW * 32, 1) k_query_tc(const __grid_constan
   tc_teardown(tmem_base, TQ_GROUPS);
 }
 
-size_t query_tc_smem_bytes(int ndec) { return tc_smem_bytes(ndec, TQ_GROUPS); }
+size_t query_tc_smem_bytes(int) { return tc_smem_bytes(1, TQ_GROUPS); }
 
 // Returns NG_ERR_CAPACITY when the tensor-core path cannot take the query
 // (hidden width != 128 or too many decoders for shared memory).

@@ -19,6 +19,12 @@ struct TcMlp {
   int wg;
   int bar_id;
   unsigned long long* prof = nullptr;  // debug: [6] += ns gather->decoder entry, [7] += ns in decoder
+  // one-level staging (k_query_tc): the CTA holds a single decoder's tiles
+  // and re-stages level l from these fp32 decoders before its GEMMs
+  const float* restage_src = nullptr;
+  int restage_stride = 0;
+
+  __device__ __forceinline__ void prepare(int l) const;
 
   __device__ __forceinline__ float operator()(int l, const float xf[3], const float* zrow, bool /*any*/,
                                               bool& bad) const {
@@ -43,7 +49,7 @@ struct TcMlp {
     tc::fence_proxy_async();
     tc::fence_before_sync();
     tc::named_sync(bar_id, 128);
-    const uint8_t* dt = dec_tiles + (size_t)(l - dec_first) * DEC_TC_BYTES;
+    const uint8_t* dt = dec_tiles + (restage_src ? (size_t)0 : (size_t)(l - dec_first) * DEC_TC_BYTES);
     if (wg == 0 && lane == 0)
       tc::issue_gemm(tmem, tc::smem_u32(a_hi), tc::smem_u32(a_lo), tc::smem_u32(dt), tc::smem_u32(dt + tc::TILE_BYTES),
                      mbar);
@@ -98,6 +104,19 @@ __device__ __forceinline__ void stage_decoder_tiles(uint8_t* dst, const float* _
   }
 }
 
+
+__device__ __forceinline__ void TcMlp::prepare(int l) const {
+  if (!restage_src) return;
+  // every group's previous GEMM has completed (each thread waited on its
+  // mbarrier before leaving the decoder), so the tiles can be replaced
+  tc::fence_before_sync();
+  __syncthreads();
+  stage_decoder_tiles(const_cast<uint8_t*>(dec_tiles), restage_src, l, l, restage_stride);
+  tc::fence_proxy_async();
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+}
 
 // Shared-memory carve-up for a kernel with `groups` 4-warp tile groups.
 struct TcSmem {
