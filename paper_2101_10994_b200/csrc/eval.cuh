@@ -18,7 +18,7 @@
 #include "common.cuh"
 
 #ifndef NG_GATHER_BATCH
-#define NG_GATHER_BATCH 4  // points whose 8 corner rows are in flight together per warp
+#define NG_GATHER_BATCH 8  // points whose 8 corner rows are in flight together per warp (2 quad loads)
 #endif
 #ifndef NG_QUAD_GATHER
 #define NG_QUAD_GATHER 1   // warp_eval: 16-byte row loads, 4 points per load instruction
@@ -441,6 +441,60 @@ __device__ __forceinline__ EvalLane warp_eval_presum(const ng_octree& tree, cons
     const float* __restrict__ Sc = c.presum + (int64_t)slot * c.presum_corners * 32 + lane;
     ++slot;
     unsigned pm = pm0;
+#if NG_QUAD_GATHER
+    if constexpr (GB % 4 == 0) {
+      // 16-byte row loads: lane = (point slot lane / 8, channel quad lane % 8)
+      const int grp = lane >> 3, sub = lane & 7;
+      const float4* __restrict__ S4 = reinterpret_cast<const float4*>(Sc - lane) + sub;
+      while (pm) {
+        int pp[GB];
+#pragma unroll
+        for (int q = 0; q < GB; ++q) {
+          pp[q] = pm ? __ffs(pm) - 1 : -1;
+          pm &= pm ? pm - 1 : 0u;
+        }
+        int mine[GB / 4];
+        float4 v[GB / 4][8];
+#pragma unroll
+        for (int k = 0; k < GB / 4; ++k) {
+          const int a0 = pp[4 * k], a1 = pp[4 * k + 1], a2 = pp[4 * k + 2], a3 = pp[4 * k + 3];
+          mine[k] = grp == 0 ? a0 : (grp == 1 ? a1 : (grp == 2 ? a2 : a3));
+          const int p = mine[k] >= 0 ? mine[k] : pp[0];
+          const int4 a = ws.ids[p][0], b = ws.ids[p][1];
+          v[k][0] = __ldg(S4 + 8 * (int64_t)a.x);
+          v[k][1] = __ldg(S4 + 8 * (int64_t)a.y);
+          v[k][2] = __ldg(S4 + 8 * (int64_t)a.z);
+          v[k][3] = __ldg(S4 + 8 * (int64_t)a.w);
+          v[k][4] = __ldg(S4 + 8 * (int64_t)b.x);
+          v[k][5] = __ldg(S4 + 8 * (int64_t)b.y);
+          v[k][6] = __ldg(S4 + 8 * (int64_t)b.z);
+          v[k][7] = __ldg(S4 + 8 * (int64_t)b.w);
+        }
+#pragma unroll
+        for (int k = 0; k < GB / 4; ++k) {
+          if (mine[k] < 0) continue;
+          const float4 u0 = ws.w[mine[k]][0], u1 = ws.w[mine[k]][1];
+          const float wj[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
+          float acc[4];
+          acc[0] = wj[0] * v[k][0].x;
+          acc[1] = wj[0] * v[k][0].y;
+          acc[2] = wj[0] * v[k][0].z;
+          acc[3] = wj[0] * v[k][0].w;
+#pragma unroll
+          for (int jj = 1; jj < 8; ++jj) {
+            acc[0] = fmaf(wj[jj], v[k][jj].x, acc[0]);
+            acc[1] = fmaf(wj[jj], v[k][jj].y, acc[1]);
+            acc[2] = fmaf(wj[jj], v[k][jj].z, acc[2]);
+            acc[3] = fmaf(wj[jj], v[k][jj].w, acc[3]);
+          }
+          float* zr = &ws.zt[mine[k]][4 * sub];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) zr[e] = acc[e];
+        }
+      }
+    } else
+#endif
+    {
     while (pm) {
       int pp[GB];
 #pragma unroll
@@ -476,6 +530,7 @@ __device__ __forceinline__ EvalLane warp_eval_presum(const ng_octree& tree, cons
         acc = fmaf(u1.w, v[q][7], acc);
         ws.zt[pp[q]][lane] = acc;
       }
+    }
     }
     __syncwarp();
     lap(2);

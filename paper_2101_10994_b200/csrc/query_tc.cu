@@ -9,7 +9,7 @@
 // B tiles stay resident in shared memory for the CTA's lifetime.
 // The batched query has no march control between evaluations, so it keeps
 // more corner rows in flight per warp than the render kernels (measured:
-// 1264 vs 1206 Mpoints/s at 8 vs 4 points per gather batch; the march prefers 4).
+// 1264 vs 1206 Mpoints/s at 8 vs 4 points per gather batch).
 #ifndef NG_GATHER_BATCH
 #define NG_GATHER_BATCH 8
 #endif
