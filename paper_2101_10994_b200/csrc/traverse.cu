@@ -301,6 +301,9 @@ __global__ void __launch_bounds__(TR_NT) k_traverse_hits(
 #ifndef NG_TT_WPB
 #define NG_TT_WPB 8
 #endif
+#ifndef NG_TT_MINB
+#define NG_TT_MINB 1  // CTAs per SM the register budget is sized for
+#endif
 constexpr int TT_WPB = NG_TT_WPB;      // warps per CTA
 constexpr int TT_RAYS = NG_TT_RAYS;    // rays per tile (<= 256: list entries keep a u8 ray slot)
 constexpr int TT_SCAP = NG_TT_SCAP;    // pairs per warp-local list held in shared memory
@@ -438,7 +441,7 @@ __device__ __forceinline__ unsigned octants_front_to_back(unsigned x, int dm) {
 __device__ __forceinline__ uint32_t pack_cell(uint32_t x, uint32_t y, uint32_t z) { return x | (y << 10) | (z << 20); }
 
 template <bool SO>
-__global__ void __launch_bounds__(TT_WPB * 32) k_traverse_tiles(
+__global__ void __launch_bounds__(TT_WPB * 32, NG_TT_MINB) k_traverse_tiles(
     const __grid_constant__ ng_octree tree, const ng_ray* __restrict__ rays, const int64_t* __restrict__ d_n,
     int target, int64_t* counts, ng_hit_pair* __restrict__ hits, int64_t hit_cap, unsigned int* tile_counter,
     unsigned long long* hit_cursor, int64_t* __restrict__ seg_start, int64_t* __restrict__ seg_end,
