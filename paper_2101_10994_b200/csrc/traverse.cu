@@ -302,7 +302,7 @@ __global__ void __launch_bounds__(TR_NT) k_traverse_hits(
 #define NG_TT_WPB 8
 #endif
 #ifndef NG_TT_MINB
-#define NG_TT_MINB 1  // CTAs per SM the register budget is sized for
+#define NG_TT_MINB 2  // CTAs per SM the register budget is sized for (1 lets ptxas take 150 registers: half the warps)
 #endif
 constexpr int TT_WPB = NG_TT_WPB;      // warps per CTA
 constexpr int TT_RAYS = NG_TT_RAYS;    // rays per tile (<= 256: list entries keep a u8 ray slot)
