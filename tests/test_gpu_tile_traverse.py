@@ -71,3 +71,54 @@ def test_probes_in_march_equal_normals_pass(frames):
     """Normals evaluated as probe items inside the march (default) equal the
     separate k_normals pass bit for bit (same evaluations, same counters)."""
     _same(frames["tiles"], frames["normals_pass"])
+
+
+def _degenerate_rays():
+    """Rays the tile traversal's fast test excludes (a zero direction
+    component) or whose slab values tie: axis-aligned and diagonal
+    directions from origins on the LOD4 lattice planes and edges."""
+    rng = np.random.default_rng(11)
+    h = 2.0 / 64  # LOD4 cell edge (res 64)
+    o, d = [], []
+    axes = [np.array(v, float) for v in [(1, 0, 0), (-1, 0, 0), (0, 1, 0), (0, -1, 0), (0, 0, 1), (0, 0, -1)]]
+    diag = [np.array(v, float) / np.linalg.norm(v) for v in [(1, 1, 0), (1, -1, 0), (0, 1, -1), (1, 1, 1), (-1, 1, -1)]]
+    for _ in range(1500):
+        k = rng.integers(-40, 41, size=3)
+        p = k * h  # lattice points and planes
+        jitter = rng.uniform(-0.6, 0.6, size=3)
+        mask = rng.integers(0, 2, size=3).astype(bool)
+        p = np.where(mask, p, jitter)  # some coordinates on planes, others free
+        dirs = axes + diag
+        dv = dirs[rng.integers(0, len(dirs))]
+        start = p - 1.7 * dv  # start outside the shape, travel through p
+        o.append(start)
+        d.append(dv)
+    return np.array(o), np.array(d)
+
+
+def test_degenerate_rays_match_oracle(golden):
+    """Explicit rays through the render path (tile traversal with per-ray
+    origins, both the ordered and the literal slab paths, then the march)
+    against the oracle's traversal + march."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2101_10994_b200 as ng
+    from paper_2101_10994_b200 import scenes
+    from paper_2101_10994_b200.render import trace_rays
+    from oracle import nglod_oracle as O
+    from conftest import oracle_tree_from_golden
+    go = golden("octree")
+    svo = ng.build_octree(O.sdf_torus(0.5, 0.2), 4, go["samples_b"])
+    tree = oracle_tree_from_golden(go, "b_")
+    fld = scenes.planted_field(svo, O.sdf_torus(0.5, 0.2), seed=0, device_sdf=False)
+    decs = [O.OracleDecoder(dd.W1, dd.b1, dd.W2, dd.b2) for dd in fld.decoders]
+    o, d = _degenerate_rays()
+    assert (d == 0).any(axis=1).sum() > 500  # many rays take the literal path
+    hit, t = trace_rays(fld, ng.RayBundle(o, d), 4.0)
+    ofin = O.traverse(tree, o, d, 4)[-1]
+    ohit, ot, _, _ = O.march(tree, fld.Z, decs, o, d, ofin, 4.0, O.RenderParams())
+    assert hit.sum() > 300
+    assert np.mean(hit == ohit) >= 0.999
+    both = hit & ohit
+    assert np.abs(t[both] - ot[both]).max(initial=0.0) <= 2e-3
