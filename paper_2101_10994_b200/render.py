@@ -441,6 +441,11 @@ def resolve_lod(camera: Camera, fld: NeuralField, config: RenderConfig) -> float
     return max(lod, 1.0)
 
 
+def _graphs_enabled() -> bool:
+    """NG_GRAPHS=0 launches every frame's kernels directly."""
+    return os.environ.get("NG_GRAPHS", "1") != "0"
+
+
 class FrameTensors:
     """One frame's device outputs in a single allocation. The C side gets
     raw pointers (no per-field tensor ops on the per-frame path); a field's
@@ -496,6 +501,7 @@ class RenderSession:
         self.ev0 = torch.cuda.Event(enable_timing=True)
         self.ev1 = torch.cuda.Event(enable_timing=True)
         self.ev2 = torch.cuda.Event(enable_timing=True)
+        self._graphs, self._graph_misses = {}, 0
 
     def _alloc_ws(self):
         nbytes = _lib.lib().ng_render_workspace_bytes(self.n, self.pair_cap, self.hit_cap)
@@ -520,16 +526,45 @@ class RenderSession:
         ev2 bracket traversal+march and normals (ev1 is recorded by the C side)."""
         fs = self.frame_struct(frame)
         prepare_presum(self.fld, cfg)
-        if timed:
+        graphed = camera is not None and _graphs_enabled() and self._graph_misses < 8
+        if timed and not graphed:
             self.ev1.record()  # materialise the handle; re-recorded mid-frame
             self.ws.ev_trace_done = self.ev1.cuda_event
             self.ev0.record()
         else:
             self.ws.ev_trace_done = None
+            if timed:
+                self.ev0.record()
         if camera is not None:
-            call("ng_render_frame", self.fld.svo.device.ref(), self.fld.device.ref(), ctypes.byref(cfg),
-                 ctypes.byref(camera.struct()), ctypes.byref(fs), ctypes.byref(self.ws), ptr(self.stats),
-                 stream_ptr())
+            tree, field, cs = self.fld.svo.device.ref(), self.fld.device.ref(), camera.struct()
+
+            def launch():
+                call("ng_render_frame", tree, field, ctypes.byref(cfg), ctypes.byref(cs), ctypes.byref(fs),
+                     ctypes.byref(self.ws), ptr(self.stats), stream_ptr())
+            if graphed:
+                # the frame's launches as one CUDA graph, replayed while every
+                # argument is unchanged (render() reusing a freed frame buffer
+                # gets the same address back from the caching allocator);
+                # timed graphed frames are timed as a whole (ev0 -> ev1), the
+                # normals being evaluated inside the march
+                key = (bytes(self.fld.svo.device.struct), bytes(self.fld.device.struct), bytes(cfg), bytes(cs),
+                       bytes(fs), bytes(self.ws))
+                g = self._graphs.get(key)
+                if g is None:  # a few graphs: consecutive frames alternate buffers
+                    self._graph_misses += 1
+                    if len(self._graphs) >= 4:
+                        self._graphs.pop(next(iter(self._graphs)))
+                    g = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(g):
+                        launch()
+                    self._graphs[key] = g
+                else:
+                    self._graph_misses = 0
+                g.replay()
+                if timed:
+                    self.ev1.record()
+            else:
+                launch()
         else:
             call("ng_render_rays", self.fld.svo.device.ref(), self.fld.device.ref(), ctypes.byref(cfg), ptr(rays),
                  self.n, ctypes.byref(fs), ctypes.byref(self.ws), ptr(self.stats), int(do_normals), stream_ptr())
