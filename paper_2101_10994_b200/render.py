@@ -443,7 +443,7 @@ def resolve_lod(camera: Camera, fld: NeuralField, config: RenderConfig) -> float
 
 def _graphs_enabled() -> bool:
     """NG_GRAPHS=0 launches every frame's kernels directly."""
-    return os.environ.get("NG_GRAPHS", "1") != "0"
+    return os.environ.get("NG_GRAPHS", "1") != "0" and os.environ.get("NG_MARCH_PROFILE") != "1"
 
 
 class FrameTensors:
@@ -501,7 +501,7 @@ class RenderSession:
         self.ev0 = torch.cuda.Event(enable_timing=True)
         self.ev1 = torch.cuda.Event(enable_timing=True)
         self.ev2 = torch.cuda.Event(enable_timing=True)
-        self._graphs, self._graph_misses = {}, 0
+        self._graphs, self._graph_seen, self._graph_misses = {}, set(), 0
 
     def _alloc_ws(self):
         nbytes = _lib.lib().ng_render_workspace_bytes(self.n, self.pair_cap, self.hit_cap)
@@ -550,17 +550,22 @@ class RenderSession:
                 key = (bytes(self.fld.svo.device.struct), bytes(self.fld.device.struct), bytes(cfg), bytes(cs),
                        bytes(fs), bytes(self.ws))
                 g = self._graphs.get(key)
-                if g is None:  # a few graphs: consecutive frames alternate buffers
+                if g is None and key not in self._graph_seen:
+                    # first sight: launch directly (lazy one-off set-up stays
+                    # outside any capture); captured on the next occurrence
+                    self._graph_seen.add(key)
                     self._graph_misses += 1
-                    if len(self._graphs) >= 4:
-                        self._graphs.pop(next(iter(self._graphs)))
-                    g = torch.cuda.CUDAGraph()
-                    with torch.cuda.graph(g):
-                        launch()
-                    self._graphs[key] = g
+                    launch()
                 else:
+                    if g is None:  # a few graphs: consecutive frames alternate buffers
+                        if len(self._graphs) >= 4:
+                            self._graphs.pop(next(iter(self._graphs)))
+                        g = torch.cuda.CUDAGraph()
+                        with torch.cuda.graph(g):
+                            launch()
+                        self._graphs[key] = g
                     self._graph_misses = 0
-                g.replay()
+                    g.replay()
                 if timed:
                     self.ev1.record()
             else:
