@@ -25,7 +25,10 @@ int grid_for(int64_t n, int nt);
 // 4 groups (16 warps) per CTA: the CTA holds one decoder level at a time and
 // re-stages it per level (all groups step through the levels together), so
 // the five decoders' tiles do not cap the CTA at 2 groups
-constexpr int TQ_GROUPS = 4;
+#ifndef NG_TQ_GROUPS
+#define NG_TQ_GROUPS 4
+#endif
+constexpr int TQ_GROUPS = NG_TQ_GROUPS;
 constexpr int TQ_NW = 4 * TQ_GROUPS;
 
 __global__ void __launch_bounds__(TQ_NW * 32, 1) k_query_tc(const __grid_constant__ ng_octree tree, ng_field f,
