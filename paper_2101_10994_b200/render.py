@@ -502,6 +502,7 @@ class RenderSession:
         self.ev1 = torch.cuda.Event(enable_timing=True)
         self.ev2 = torch.cuda.Event(enable_timing=True)
         self._graphs, self._graph_seen, self._graph_misses = {}, set(), 0
+        self.graph_replays = 0
 
     def _alloc_ws(self):
         nbytes = _lib.lib().ng_render_workspace_bytes(self.n, self.pair_cap, self.hit_cap)
@@ -565,6 +566,7 @@ class RenderSession:
                             launch()
                         self._graphs[key] = g
                     self._graph_misses = 0
+                    self.graph_replays += 1
                     g.replay()
                 if timed:
                     self.ev1.record()

@@ -417,3 +417,34 @@ def test_shadow_rays_match_oracle(ng, golden, O, lod):
     assert fr.shadowed[both].sum() > 0, "test scene should cast shadows"
     assert abs(rep.shadowed - int(fr.shadowed.sum())) <= max(3, int(fr.shadowed.sum()) // 50)
     assert np.mean(np.all(fb.color == fr.color, axis=-1)) >= 0.99
+
+
+def test_render_graph_replay_matches_direct(ng, golden, O):
+    """render() replays a frame's launches as a CUDA graph once a launch key
+    repeats (render.py RenderSession.enqueue): replayed frames equal the
+    directly launched ones, and a changed camera or config is not served
+    from a stale graph."""
+    from paper_2101_10994_b200 import scenes
+    go = golden("octree")
+    svo = ng.build_octree(O.sdf_torus(0.5, 0.2), 4, go["samples_b"])
+    fld = scenes.planted_field(svo, O.sdf_torus(0.5, 0.2), seed=0, device_sdf=False)
+    cams = [ng.Camera((0.0, 2.0, 3.5), (0.0, 0.0, 0.0), (0.0, 1.0, 0.0), 30.0, 80, 60),
+            ng.Camera((1.0, 1.0, 3.0), (0.0, 0.1, 0.0), (0.0, 1.0, 0.0), 35.0, 80, 60)]
+    cfgs = [ng.RenderConfig(), ng.RenderConfig(lod=3.5)]
+    first = {}
+    for rnd in range(4):  # keys repeat from the second round: captured, then replayed
+        for ci, cam in enumerate(cams):
+            for ki, cfg in enumerate(cfgs):
+                fb, rep = ng.render(cam, fld, cfg)
+                got = (fb.color.copy(), fb.t.copy(), fb.iterations.copy(), rep.evals, rep.visible)
+                if (ci, ki) not in first:
+                    first[(ci, ki)] = got
+                else:
+                    ref = first[(ci, ki)]
+                    np.testing.assert_array_equal(got[0], ref[0])
+                    np.testing.assert_array_equal(got[1], ref[1])
+                    np.testing.assert_array_equal(got[2], ref[2])
+                    assert got[3:] == ref[3:]
+    assert not np.array_equal(first[(0, 0)][0], first[(1, 0)][0])
+    from paper_2101_10994_b200.render import _session
+    assert _session(fld, 80, 60).graph_replays > 0
