@@ -25,7 +25,7 @@ int traverse_hits(const ng_octree& tree, const ng_ray* rays, int t, bool next_fi
                   int64_t* d_count_out, int64_t out_cap, void* scratch, size_t scratch_bytes, cudaStream_t s,
                   int64_t* seg_start, int64_t* seg_end, const double* shared_origin);
 int traverse_tiles(const ng_octree& tree, const ng_ray* rays, const int64_t* d_n, int64_t n_max, int target,
-                   int32_t* active, unsigned long long* d_active, int64_t* counts,
+                   int4* items, unsigned long long* d_active, int64_t* counts,
                    ng_hit_pair* hits, int64_t hit_cap, void* ctl, int64_t* seg_start, int64_t* seg_end,
                    void* arena, size_t arena_bytes, unsigned long long* d_need, const double* shared_origin,
                    const ng_camera* cam_rays, cudaStream_t s);
@@ -235,6 +235,7 @@ struct MarchArgs {
   double blend_alpha;
   RaySrc rays;                   // ray records, or the camera's rays computed on the fly
   const int32_t* work;           // ray ids to trace, or null for 0..n_work-1
+  const int4* items;             // or work items (ray, segment length, segment start lo / hi) from the tile traversal
   const unsigned long long* d_n_work;
   int64_t n_work;
   const ng_hit_pair* hits;
@@ -425,9 +426,16 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_cons
           if (k >= n_work) {
             drained = true;
           } else {
-            ray = A.work ? A.work[k] : (int)k;
-            cur = A.seg_start[ray];
-            end = A.seg_end[ray];
+            if (A.items) {  // one load: ray and segment
+              const int4 wi = A.items[k];
+              ray = wi.x;
+              cur = (int64_t)(uint32_t)wi.z | ((int64_t)wi.w << 32);
+              end = cur + wi.y;
+            } else {
+              ray = A.work ? A.work[k] : (int)k;
+              cur = A.seg_start[ray];
+              end = A.seg_end[ray];
+            }
             t = 0.0;
             prev = NaN;
             it = 0;
@@ -1145,7 +1153,7 @@ static WsLayout layout(int64_t n, int64_t pair_cap, int64_t hit_cap) {
   L.hits = o; o = al(o + (size_t)hit_cap * sizeof(ng_hit_pair));
   L.seg_start = o; o = al(o + (size_t)n * 8);
   L.seg_end = o; o = al(o + (size_t)n * 8);
-  L.active = o; o = al(o + (size_t)n * 4);
+  L.active = o; o = al(o + (size_t)n * 16);  // ray ids, or the tile traversal's 16-byte work items
   L.hit_list = o; o = al(o + (size_t)n * 4);
   // one look-back scratch region per traversal level, zeroed together once per pass
   L.scratch_bytes = al(level_scratch_bytes(std::max<int64_t>(std::max<int64_t>(pair_cap, n), 1)));
@@ -1222,7 +1230,7 @@ static int trace_pass(const ng_octree& tree, const ng_render_cfg& cfg, const Lod
     // look-back scratch
     const size_t arena_bytes = L.hits - L.pairs_a;
     unsigned long long* need = (unsigned long long*)((char*)scratch + 16);
-    r = traverse_tiles(tree, rays, &counts[0], n, target, active, d_active, counts, hits, ws.hit_capacity, scratch, seg_start, seg_end,
+    r = traverse_tiles(tree, rays, &counts[0], n, target, reinterpret_cast<int4*>(active), d_active, counts, hits, ws.hit_capacity, scratch, seg_start, seg_end,
                        b + L.pairs_a, arena_bytes, need, shared_origin, cam_rays, s);
     if (r) return r;
     tov.need = need;
@@ -1264,7 +1272,8 @@ static int trace_pass(const ng_octree& tree, const ng_render_cfg& cfg, const Lod
   // level-by-level path: longest segments first; the tile path marches in
   // tile order (measured the same on the 720p knot frame, and it saves the
   // histogram and scatter launches)
-  A.work = tiles ? active : sorted;
+  A.work = tiles ? nullptr : sorted;
+  A.items = tiles ? reinterpret_cast<const int4*>(active) : nullptr;
   A.d_n_work = d_active;
   A.n_work = 0;
   A.hits = hits;
@@ -1490,6 +1499,7 @@ int ng_sphere_trace(const ng_octree* tree, const ng_field* fld, const ng_render_
   A.rays.rays = rays;
   A.rays.cam_rays = 0;
   A.work = nullptr;
+  A.items = nullptr;
   A.d_n_work = nullptr;
   A.n_work = n_rays;
   A.hits = hits;

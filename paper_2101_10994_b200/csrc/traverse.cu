@@ -446,7 +446,7 @@ __global__ void __launch_bounds__(TT_WPB * 32, NG_TT_MINB) k_traverse_tiles(
     int target, int64_t* counts, ng_hit_pair* __restrict__ hits, int64_t hit_cap, unsigned int* tile_counter,
     unsigned long long* hit_cursor, int64_t* __restrict__ seg_start, int64_t* __restrict__ seg_end,
     uint8_t* arena, int64_t gcap, int scap, unsigned long long* d_need, const SharedOrigin so,
-    const ng_camera cam, int cam_rays, int32_t* __restrict__ active, unsigned long long* d_active) {
+    const ng_camera cam, int cam_rays, int4* __restrict__ items, unsigned long long* d_active) {
   extern __shared__ __align__(16) uint8_t tt_smem[];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -646,8 +646,10 @@ __global__ void __launch_bounds__(TT_WPB * 32, NG_TT_MINB) k_traverse_tiles(
     for (int j0 = 0; j0 < TT_RAYS; j0 += 32) {
       const int j = j0 + lane;
       bool has = false;
+      int64_t s0 = 0, e0 = 0;
       if (j < nr) {
-        int64_t s0 = hbase + W->seg_s[j], e0 = hbase + W->seg_e[j];
+        s0 = hbase + W->seg_s[j];
+        e0 = hbase + W->seg_e[j];
         s0 = s0 < hit_cap ? s0 : hit_cap;
         e0 = e0 < hit_cap ? e0 : hit_cap;
         seg_start[r0 + j] = s0;
@@ -659,7 +661,9 @@ __global__ void __launch_bounds__(TT_WPB * 32, NG_TT_MINB) k_traverse_tiles(
       unsigned long long ab = 0;
       if (lane == 0 && am) ab = atomicAdd(d_active, (unsigned long long)__popc(am));
       ab = __shfl_sync(FULL, ab, 0);
-      if (has) active[ab + __popc(am & lanemask_lt())] = (int32_t)(r0 + j);
+      if (has)  // (ray, segment length, segment start)
+        items[ab + __popc(am & lanemask_lt())] =
+            make_int4((int)(r0 + j), (int)(e0 - s0), (int)(uint32_t)s0, (int)(s0 >> 32));
     }
     __syncwarp();
   }
@@ -861,7 +865,7 @@ int64_t tile_traverse_warps(int64_t n_rays) {
 }
 
 int traverse_tiles(const ng_octree& tree, const ng_ray* rays, const int64_t* d_n, int64_t n_max, int target,
-                   int32_t* active, unsigned long long* d_active, int64_t* counts,
+                   int4* items, unsigned long long* d_active, int64_t* counts,
                    ng_hit_pair* hits, int64_t hit_cap, void* ctl, int64_t* seg_start, int64_t* seg_end,
                    void* arena, size_t arena_bytes, unsigned long long* d_need, const double* shared_origin,
                    const ng_camera* cam_rays, cudaStream_t s) {
@@ -875,7 +879,7 @@ int traverse_tiles(const ng_octree& tree, const ng_ray* rays, const int64_t* d_n
   k<<<(int)(warps / TT_WPB), TT_WPB * 32, tile_traverse_smem(), s>>>(
       tree, rays, d_n, target, counts, hits, hit_cap, (unsigned int*)ctl, (unsigned long long*)((char*)ctl + 8),
       seg_start, seg_end, (uint8_t*)arena, gcap, tile_traverse_scap(), d_need, so,
-      cam_rays ? *cam_rays : ng_camera{}, cam_rays != nullptr, active, d_active);
+      cam_rays ? *cam_rays : ng_camera{}, cam_rays != nullptr, items, d_active);
   NG_CHECK_LAUNCH("k_traverse_tiles");
   return NG_OK;
 }
