@@ -28,7 +28,8 @@ int traverse_tiles(const ng_octree& tree, const ng_ray* rays, const int64_t* d_n
                    int4* items, unsigned long long* d_active, int64_t* counts,
                    ng_hit_pair* hits, int64_t hit_cap, void* ctl, int64_t* seg_start, int64_t* seg_end,
                    void* arena, size_t arena_bytes, unsigned long long* d_need, const double* shared_origin,
-                   const ng_camera* cam_rays, cudaStream_t s);
+                   const ng_camera* cam_rays, const ng_frame* defaults, uint32_t bg, int64_t n_host,
+                   cudaStream_t s);
 int64_t tile_traverse_limit(size_t arena_bytes, int64_t n_max);
 int64_t tile_traverse_warps(int64_t n_max);
 int tile_traverse_scap();
@@ -1192,7 +1193,8 @@ static int trace_pass(const ng_octree& tree, const ng_render_cfg& cfg, const Lod
                       int64_t n, int64_t* counts, const WsLayout& L, const ng_workspace& ws, char* b,
                       unsigned long long* d_active, unsigned long long* work_counter, cudaStream_t s,
                       MarchArgs& A, bool zeroed, const double* shared_origin, TileOverflow& tov,
-                      const ng_camera* cam_rays = nullptr) {
+                      const ng_camera* cam_rays = nullptr, const ng_frame* defaults = nullptr, uint32_t bg = 0,
+                      int64_t n_host = -1) {
   ng_pair* pa = (ng_pair*)(b + L.pairs_a);
   ng_pair* pb = (ng_pair*)(b + L.pairs_b);
   ng_hit_pair* hits = (ng_hit_pair*)(b + L.hits);
@@ -1231,7 +1233,7 @@ static int trace_pass(const ng_octree& tree, const ng_render_cfg& cfg, const Lod
     const size_t arena_bytes = L.hits - L.pairs_a;
     unsigned long long* need = (unsigned long long*)((char*)scratch + 16);
     r = traverse_tiles(tree, rays, &counts[0], n, target, reinterpret_cast<int4*>(active), d_active, counts, hits, ws.hit_capacity, scratch, seg_start, seg_end,
-                       b + L.pairs_a, arena_bytes, need, shared_origin, cam_rays, s);
+                       b + L.pairs_a, arena_bytes, need, shared_origin, cam_rays, defaults, bg, n_host, s);
     if (r) return r;
     tov.need = need;
     tov.lim = tile_traverse_limit(arena_bytes, n);
@@ -1339,7 +1341,12 @@ static int render_common(const ng_octree& tree, const ng_field& f, const ng_rend
   // with the tile traversal, camera rays are computed where they are used
   // (traversal, march, normals, shadow origins) instead of stored
   const bool cam_rays = cam != nullptr && use_tile_traverse(target0);
-  if (cam) {
+  // with camera rays computed on the fly the tile traversal also writes the
+  // frame's per-pixel defaults and the root count: no separate ray kernel
+  const uint32_t bg_packed = (uint32_t)bg[0] | ((uint32_t)bg[1] << 8) | ((uint32_t)bg[2] << 16);
+  if (cam && cam_rays) {
+    // (nothing: folded into k_traverse_tiles)
+  } else if (cam) {
     k_camera_rays<<<grid_for(n, 256), 256, 0, s>>>(*cam, cam_rays ? nullptr : rays, fr, bg[0], bg[1], bg[2],
                                                    &st->pairs[0], zseg_s, zseg_e);
     NG_CHECK_LAUNCH("k_camera_rays");
@@ -1356,7 +1363,8 @@ static int render_common(const ng_octree& tree, const ng_field& f, const ng_rend
   // camera rays share the eye position (a host value, captured into the launches)
   TileOverflow tov;
   if ((r = trace_pass(tree, cfg, P, rays, n, st->pairs, L, ws, b, ctr + 0, ctr + 2, s, A, true,
-                      cam ? cam->position : nullptr, tov, cam_rays ? cam : nullptr)))
+                      cam ? cam->position : nullptr, tov, cam_rays ? cam : nullptr, cam_rays ? &fr : nullptr,
+                      bg_packed, cam_rays ? n : -1)))
     return r;
   A.hit = fr.hit;
   A.t = fr.t;

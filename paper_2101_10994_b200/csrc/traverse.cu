@@ -446,14 +446,18 @@ __global__ void __launch_bounds__(TT_WPB * 32, NG_TT_MINB) k_traverse_tiles(
     int target, int64_t* counts, ng_hit_pair* __restrict__ hits, int64_t hit_cap, unsigned int* tile_counter,
     unsigned long long* hit_cursor, int64_t* __restrict__ seg_start, int64_t* __restrict__ seg_end,
     uint8_t* arena, int64_t gcap, int scap, unsigned long long* d_need, const SharedOrigin so,
-    const ng_camera cam, int cam_rays, int4* __restrict__ items, unsigned long long* d_active) {
+    const ng_camera cam, int cam_rays, int4* __restrict__ items, unsigned long long* d_active,
+    const ng_frame fr, uint32_t bg, int64_t n_host) {
   extern __shared__ __align__(16) uint8_t tt_smem[];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   TileWarp* W = reinterpret_cast<TileWarp*>(tt_smem) + warp;
   const int64_t gw = (int64_t)blockIdx.x * TT_WPB + warp;
   uint8_t* ga = arena + gw * gcap * (2 * TT_ENTRY);
-  const int64_t n = *d_n;
+  // the ray count: the caller's (then published as the root list length), or
+  // the device count (shadow rays)
+  const int64_t n = n_host >= 0 ? n_host : *d_n;
+  if (n_host >= 0 && blockIdx.x == 0 && threadIdx.x == 0) *const_cast<int64_t*>(d_n) = n_host;
   const int64_t n_tiles = (n + TT_RAYS - 1) / TT_RAYS;
   const int lim = scap + (int)gcap;
   int64_t level_cnt = 0;  // lane t: pairs emitted at traversal level t
@@ -473,6 +477,20 @@ __global__ void __launch_bounds__(TT_WPB * 32, NG_TT_MINB) k_traverse_tiles(
       for (int j0 = 0; j0 < TT_RAYS; j0 += 32) {
         const int j = j0 + lane;
         bool root = false;
+        if (j < nr && fr.hit) {  // per-pixel output defaults (the march overwrites its rays')
+          const int64_t i = r0 + j;
+          fr.hit[i] = 0;
+          fr.t[i] = __longlong_as_double(0x7ff8000000000000ll);
+          fr.normal[3 * i] = 0.0;
+          fr.normal[3 * i + 1] = 0.0;
+          fr.normal[3 * i + 2] = 0.0;
+          fr.normal_ok[i] = 0;
+          fr.iterations[i] = 0;
+          fr.evals[i] = 0;
+          fr.color[3 * i] = (uint8_t)(bg & 0xffu);
+          fr.color[3 * i + 1] = (uint8_t)((bg >> 8) & 0xffu);
+          fr.color[3 * i + 2] = (uint8_t)((bg >> 16) & 0xffu);
+        }
         if (j < nr) {
           ng_ray r;
           if (SO && cam_rays) camera_ray(cam, r0 + j, r);  // the camera's ray, not stored
@@ -868,7 +886,8 @@ int traverse_tiles(const ng_octree& tree, const ng_ray* rays, const int64_t* d_n
                    int4* items, unsigned long long* d_active, int64_t* counts,
                    ng_hit_pair* hits, int64_t hit_cap, void* ctl, int64_t* seg_start, int64_t* seg_end,
                    void* arena, size_t arena_bytes, unsigned long long* d_need, const double* shared_origin,
-                   const ng_camera* cam_rays, cudaStream_t s) {
+                   const ng_camera* cam_rays, const ng_frame* defaults, uint32_t bg, int64_t n_host,
+                   cudaStream_t s) {
   // `ctl` (zeroed by the caller): u32 tile counter at 0, u64 hit cursor at 8
   SharedOrigin so;
   so.shared = shared_origin != nullptr;
@@ -879,7 +898,8 @@ int traverse_tiles(const ng_octree& tree, const ng_ray* rays, const int64_t* d_n
   k<<<(int)(warps / TT_WPB), TT_WPB * 32, tile_traverse_smem(), s>>>(
       tree, rays, d_n, target, counts, hits, hit_cap, (unsigned int*)ctl, (unsigned long long*)((char*)ctl + 8),
       seg_start, seg_end, (uint8_t*)arena, gcap, tile_traverse_scap(), d_need, so,
-      cam_rays ? *cam_rays : ng_camera{}, cam_rays != nullptr, items, d_active);
+      cam_rays ? *cam_rays : ng_camera{}, cam_rays != nullptr, items, d_active, defaults ? *defaults : ng_frame{},
+      bg, n_host);
   NG_CHECK_LAUNCH("k_traverse_tiles");
   return NG_OK;
 }
