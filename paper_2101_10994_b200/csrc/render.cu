@@ -267,6 +267,9 @@ struct MarchArgs {
 };
 
 constexpr unsigned PROBE_READY = 0x80000000u;
+#ifndef NG_PROBE_GROUP_MAX
+#define NG_PROBE_GROUP_MAX 0  // a group takes probe items while it marches at most this many rays
+#endif
 
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
   unsigned long long t;
@@ -492,7 +495,7 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_cons
     }
     if (__any_sync(FULL, !probes_done)) {  // warp-uniform: the claim below is a warp collective
       // lanes out of rays claim probe items (warp-aggregated) ...
-      const bool pw = !probes_done && ray < 0 && pk < 0 && (drained || lane >= cap) && (!TC || group_marching == 0);
+      const bool pw = !probes_done && ray < 0 && pk < 0 && (drained || lane >= cap) && (!TC || group_marching <= NG_PROBE_GROUP_MAX);
       const unsigned pm = __ballot_sync(FULL, pw);
       if (pm) {
         const int leader = __ffs(pm) - 1;
@@ -1323,7 +1326,10 @@ static int render_common(const ng_octree& tree, const ng_field& f, const ng_rend
     z.p[1] = ctr;
     z.bytes[1] = 64;
     z.p[2] = b + L.scratch;
-    z.bytes[2] = L.scratch_bytes * (size_t)(cfg.trace_level + tree.n_virtual);
+    // (the tile traversal uses only its control words at the start)
+    z.bytes[2] = use_tile_traverse(cfg.trace_level + tree.n_virtual)
+                     ? 64
+                     : L.scratch_bytes * (size_t)(cfg.trace_level + tree.n_virtual);
     z.p[3] = b + L.buckets;
     z.bytes[3] = 2 * LEN_BUCKETS * 4;
     z.p[4] = b + L.probe_cnt;
