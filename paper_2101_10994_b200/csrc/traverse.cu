@@ -430,6 +430,33 @@ __device__ __forceinline__ unsigned child_hits_ordered(const double q0[3], const
   return mask;
 }
 
+// The literal child tests (child_slabs / child_hit, numpy's NaN rules) for
+// the rare rays the ordered test excludes. Out of line, so the compiler
+// cannot if-convert it into every item's instruction stream.
+__device__ __noinline__ unsigned literal_child_hits(const ng_ray r, int px, int py, int pz, int cres) {
+  ChildSlabs cs;
+  child_slabs(r, px, py, pz, cres, cs);
+  unsigned ho = 0;
+#pragma unroll
+  for (int oct = 0; oct < 8; ++oct) {
+    double a0, b0;
+    if (child_hit(cs, oct, a0, b0)) ho |= 1u << oct;
+  }
+  return ho;
+}
+
+// The literal slab values of one box (slab_test), out of line as above.
+__device__ __noinline__ void literal_slab(const ng_ray r, const int cc[3], int res, double& t_enter, double& t_exit) {
+  const double edge = 2.0 / (double)res;
+  double lo[3], hi[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    lo[a] = cell_lo(cc[a], res);
+    hi[a] = dadd(lo[a], edge);
+  }
+  slab_test(r, lo, hi, t_enter, t_exit);
+}
+
 // Octant-indexed bits -> front-to-back order: bit k <- bit k ^ dm.
 __device__ __forceinline__ unsigned octants_front_to_back(unsigned x, int dm) {
   if (dm & 1) x = ((x & 0x55u) << 1) | ((x >> 1) & 0x55u);
@@ -557,15 +584,7 @@ __global__ void __launch_bounds__(TT_WPB * 32, NG_TT_MINB) k_traverse_tiles(
             } else {
               ng_ray r;
               tw_ray<SO>(W, so, pr[q], r);
-              ChildSlabs cs;
-              child_slabs(r, pc[0], pc[1], pc[2], cres, cs);
-              unsigned ho = 0;
-#pragma unroll
-              for (int oct = 0; oct < 8; ++oct) {
-                double a0, b0;
-                if (child_hit(cs, oct, a0, b0)) ho |= 1u << oct;
-              }
-              hk = octants_front_to_back(ho & m, dm);
+              hk = octants_front_to_back(literal_child_hits(r, pc[0], pc[1], pc[2], cres) & m, dm);
             }
             if (hk) hm[q] = hk | ((unsigned)dm << 8) | (m << 16);
           }
@@ -646,16 +665,9 @@ __global__ void __launch_bounds__(TT_WPB * 32, NG_TT_MINB) k_traverse_tiles(
         h.t_enter = ne > 0.0 ? ne : 0.0;
         h.t_exit = fa;
       } else {
-        const double edge = 2.0 / (double)fres;
-        double lo[3], hi[3];
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-          lo[a] = cell_lo(cc[a], fres);
-          hi[a] = dadd(lo[a], edge);
-        }
         ng_ray r;
         tw_ray<SO>(W, so, rl, r);
-        slab_test(r, lo, hi, h.t_enter, h.t_exit);
+        literal_slab(r, cc, fres, h.t_enter, h.t_exit);
       }
       if (hbase + i < hit_cap) hits[hbase + i] = h;
     }
