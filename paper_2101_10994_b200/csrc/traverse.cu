@@ -474,7 +474,7 @@ __global__ void __launch_bounds__(TT_WPB * 32, NG_TT_MINB) k_traverse_tiles(
     unsigned long long* hit_cursor, int64_t* __restrict__ seg_start, int64_t* __restrict__ seg_end,
     uint8_t* arena, int64_t gcap, int scap, unsigned long long* d_need, const SharedOrigin so,
     const ng_camera cam, int cam_rays, int4* __restrict__ items, unsigned long long* d_active,
-    const ng_frame fr, uint32_t bg, int64_t n_host) {
+    const ng_frame fr, uint32_t bg, int64_t n_host, int cull) {
   extern __shared__ __align__(16) uint8_t tt_smem[];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -533,6 +533,12 @@ __global__ void __launch_bounds__(TT_WPB * 32, NG_TT_MINB) k_traverse_tiles(
           const double lo[3] = {-1.0, -1.0, -1.0}, hi[3] = {1.0, 1.0, 1.0};
           double a0, b0;
           root = slab_test(r, lo, hi, a0, b0);
+          // a ray missing the box of the occupied finest voxels (the trace
+          // level being the finest) hits none of them: each voxel box lies
+          // inside it on the same dyadic planes, so the slab values nest
+          // (the ordered-test argument); the rare rays with a zero
+          // direction component or a non-finite value are not culled
+          if (root && cull && general) root = slab_test(r, tree.region_lo, tree.region_hi, a0, b0);
         }
         W->seg_s[j] = 0;
         W->seg_e[j] = 0;
@@ -911,7 +917,7 @@ int traverse_tiles(const ng_octree& tree, const ng_ray* rays, const int64_t* d_n
       tree, rays, d_n, target, counts, hits, hit_cap, (unsigned int*)ctl, (unsigned long long*)((char*)ctl + 8),
       seg_start, seg_end, (uint8_t*)arena, gcap, tile_traverse_scap(), d_need, so,
       cam_rays ? *cam_rays : ng_camera{}, cam_rays != nullptr, items, d_active, defaults ? *defaults : ng_frame{},
-      bg, n_host);
+      bg, n_host, target == tree.n_tlevels - 1);
   NG_CHECK_LAUNCH("k_traverse_tiles");
   return NG_OK;
 }
