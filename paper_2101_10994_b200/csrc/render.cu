@@ -43,7 +43,7 @@ static bool use_tile_traverse(int target) {
     const char* e = getenv("NG_TILE_TRAVERSE");
     on = (e && e[0] == '0') ? 0 : 1;
   }
-  return on && target >= 1 && target <= 10;  // packed cells: <= 1024 per axis
+  return on && target >= 1 && target <= 9;  // list cells: <= 512 per axis
 }
 
 constexpr int R_NW = 8;  // warps per CTA for march / normals

@@ -305,69 +305,52 @@ __global__ void __launch_bounds__(TR_NT) k_traverse_hits(
 #define NG_TT_MINB 2  // CTAs per SM the register budget is sized for (1 lets ptxas take 150 registers: half the warps)
 #endif
 constexpr int TT_WPB = NG_TT_WPB;      // warps per CTA
-constexpr int TT_RAYS = NG_TT_RAYS;    // rays per tile (<= 256: list entries keep a u8 ray slot)
+constexpr int TT_RAYS = NG_TT_RAYS;    // rays per tile (<= 32: the ray slot is 5 bits of a list entry)
 constexpr int TT_SCAP = NG_TT_SCAP;    // pairs per warp-local list held in shared memory
 constexpr int TT_ITEMS = NG_TT_ITEMS;  // pairs per lane per round
-constexpr int TT_ENTRY = 9;            // list entry bytes: voxel i32, packed cell u32, ray u8
+constexpr int TT_ENTRY = 8;            // list entry: voxel i32 | cell x, y, z (9 bits each) + ray slot << 27
+static_assert(TT_RAYS <= 32, "list entries keep a 5-bit ray slot");
 
 struct TileWarp {
   double o[TT_RAYS][3];  // per-ray origins (unused when the rays share one)
   double inv[TT_RAYS][3];
   int flags[TT_RAYS];
   int seg_s[TT_RAYS], seg_e[TT_RAYS];
-  int32_t vox[2][TT_SCAP];
-  uint32_t cell[2][TT_SCAP];  // x | y << 10 | z << 20 at the list's level
-  uint8_t ray[2][TT_SCAP];
+  int2 ent[2][TT_SCAP];
 };
 
+// A warp's pair list: entries in shared memory, the rest in its arena share.
+// Cells are packed x | y << 9 | z << 18 (<= 512 per axis at the list's level).
 struct TileList {
-  int scap;  // entries held in shared memory (<= TT_SCAP), the rest in the arena
-  int32_t* svox;
-  uint32_t* scell;
-  uint8_t* sray;
-  int32_t* gvox;
-  uint32_t* gcell;
-  uint8_t* gray;
+  int scap;  // entries held in shared memory (<= TT_SCAP)
+  int2* s;
+  int2* g;
 };
 
 __device__ __forceinline__ void tl_put(const TileList& b, int i, int32_t v, uint32_t c, int r, int64_t gcap) {
-  if (i < b.scap) {
-    b.svox[i] = v;
-    b.scell[i] = c;
-    b.sray[i] = (uint8_t)r;
-  } else if (i - b.scap < gcap) {
-    b.gvox[i - b.scap] = v;
-    b.gcell[i - b.scap] = c;
-    b.gray[i - b.scap] = (uint8_t)r;
-  }
+  const int2 e = make_int2(v, (int)(c | ((uint32_t)r << 27)));
+  if (i < b.scap) b.s[i] = e;
+  else if (i - b.scap < gcap) b.g[i - b.scap] = e;
 }
 
 __device__ __forceinline__ void tl_get(const TileList& b, int i, int32_t& v, uint32_t& c, int& r) {
-  if (i < b.scap) {
-    v = b.svox[i];
-    c = b.scell[i];
-    r = b.sray[i];
-  } else {
-    v = b.gvox[i - b.scap];
-    c = b.gcell[i - b.scap];
-    r = b.gray[i - b.scap];
-  }
+  const int2 e = i < b.scap ? b.s[i] : b.g[i - b.scap];
+  v = e.x;
+  c = (uint32_t)e.y & 0x7ffffffu;
+  r = (int)((uint32_t)e.y >> 27);
 }
 
 __device__ __forceinline__ int tl_ray(const TileList& b, int i) {
-  return i < b.scap ? b.sray[i] : b.gray[i - b.scap];
+  const int y = i < b.scap ? b.s[i].y : b.g[i - b.scap].y;
+  return (int)((uint32_t)y >> 27);
 }
 
-// arena per warp: [vox0 | vox1 | cell0 | cell1 | ray0 | ray1], gcap entries each
+// arena per warp: [list 0 | list 1], gcap entries each
 __device__ __forceinline__ TileList tile_list(TileWarp* W, uint8_t* ga, int64_t gcap, int k, int scap) {
   TileList b;
   b.scap = scap;
-  b.svox = W->vox[k];
-  b.scell = W->cell[k];
-  b.sray = W->ray[k];
-  b.gvox = reinterpret_cast<int32_t*>(ga) + k * gcap;
-  b.gcell = reinterpret_cast<uint32_t*>(ga + 8 * gcap) + k * gcap;
-  b.gray = ga + 16 * gcap + k * gcap;
+  b.s = W->ent[k];
+  b.g = reinterpret_cast<int2*>(ga) + k * gcap;
   return b;
 }
 
@@ -465,7 +448,6 @@ __device__ __forceinline__ unsigned octants_front_to_back(unsigned x, int dm) {
   return x;
 }
 
-__device__ __forceinline__ uint32_t pack_cell(uint32_t x, uint32_t y, uint32_t z) { return x | (y << 10) | (z << 20); }
 
 template <bool SO>
 __global__ void __launch_bounds__(TT_WPB * 32, NG_TT_MINB) k_traverse_tiles(
@@ -576,7 +558,7 @@ __global__ void __launch_bounds__(TT_WPB * 32, NG_TT_MINB) k_traverse_tiles(
             tl_get(src, i, pv, pcell[q], pr[q]);
             const unsigned m = __ldg(cmask + pv);
             first[q] = __ldg(cstart + pv);
-            const int pc[3] = {(int)(pcell[q] & 1023u), (int)((pcell[q] >> 10) & 1023u), (int)(pcell[q] >> 20)};
+            const int pc[3] = {(int)(pcell[q] & 511u), (int)((pcell[q] >> 9) & 511u), (int)(pcell[q] >> 18)};
             const int fl = W->flags[pr[q]];
             const int dm = fl & 7;
             unsigned hk;  // front-to-back hit bits
@@ -619,11 +601,11 @@ __global__ void __launch_bounds__(TT_WPB * 32, NG_TT_MINB) k_traverse_tiles(
           }
           const int dm = (int)((hm[q] >> 8) & 7u);
           const unsigned m = (hm[q] >> 16) & 0xffu;
-          const uint32_t c2 = pcell[q] << 1;  // 2 * (x, y, z), packed (parent cells < 512 per axis)
+          const uint32_t c2 = pcell[q] << 1;  // 2 * (x, y, z), packed (parent cells < 256 per axis)
           for (unsigned bits = hm[q] & 0xffu; bits; bits &= bits - 1) {
             const int oct = (__ffs(bits) - 1) ^ dm;
-            const uint32_t cc = c2 | (uint32_t)(oct & 1) | ((uint32_t)((oct >> 1) & 1) << 10) |
-                                ((uint32_t)(oct >> 2) << 20);
+            const uint32_t cc = c2 | (uint32_t)(oct & 1) | ((uint32_t)((oct >> 1) & 1) << 9) |
+                                ((uint32_t)(oct >> 2) << 18);
             tl_put(dst, o, first[q] + __popc(m & ((1u << oct) - 1u)), cc, pr[q], gcap);
             ++o;
           }
@@ -647,9 +629,10 @@ __global__ void __launch_bounds__(TT_WPB * 32, NG_TT_MINB) k_traverse_tiles(
       uint32_t c;
       int rl;
       tl_get(fin, i, v, c, rl);
-      const int cc[3] = {(int)(c & 1023u), (int)((c >> 10) & 1023u), (int)(c >> 20)};
+      const int cc[3] = {(int)(c & 511u), (int)((c >> 9) & 511u), (int)(c >> 18)};
       ng_hit_pair h;
-      h.ray = (int32_t)c;  // render lists: the voxel's packed cell (the march knows its ray)
+      // render lists: the voxel's cell x | y << 10 | z << 20 (the march knows its ray)
+      h.ray = (int32_t)((uint32_t)cc[0] | ((uint32_t)cc[1] << 10) | ((uint32_t)cc[2] << 20));
       h.voxel = v;
       const int fl = W->flags[rl];
       if (fl & TT_GENERAL) {
