@@ -293,7 +293,7 @@ __global__ void __launch_bounds__(TR_NT) k_traverse_hits(
 #define NG_TT_RAYS 32
 #endif
 #ifndef NG_TT_SCAP
-#define NG_TT_SCAP 512
+#define NG_TT_SCAP 768  // 2 CTAs of 8 warps per SM at 14.2 KB per warp
 #endif
 #ifndef NG_TT_ITEMS
 #define NG_TT_ITEMS 2
