@@ -440,6 +440,22 @@ __device__ __noinline__ void literal_slab(const ng_ray r, const int cc[3], int r
   slab_test(r, lo, hi, t_enter, t_exit);
 }
 
+// ray_aabb_batch's hit decision for a general ray (finite origin, finite
+// nonzero 1/d): per axis the face crossings in ray order (monotone in the
+// plane), then max(near) <= min(far) && min(far) >= 0; no NaN can occur.
+__device__ __forceinline__ bool box_hit_ordered(const ng_ray& r, const double lo[3], const double hi[3]) {
+  double ne = 0.0, fa = 0.0;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const bool neg = (r.flags >> a) & 1;
+    const double tn = dmul(dsub(neg ? hi[a] : lo[a], r.o[a]), r.inv[a]);
+    const double tf = dmul(dsub(neg ? lo[a] : hi[a], r.o[a]), r.inv[a]);
+    ne = a == 0 ? tn : (tn > ne ? tn : ne);
+    fa = a == 0 ? tf : (tf < fa ? tf : fa);
+  }
+  return ne <= fa && fa >= 0.0;
+}
+
 // Octant-indexed bits -> front-to-back order: bit k <- bit k ^ dm.
 __device__ __forceinline__ unsigned octants_front_to_back(unsigned x, int dm) {
   if (dm & 1) x = ((x & 0x55u) << 1) | ((x >> 1) & 0x55u);
@@ -513,14 +529,18 @@ __global__ void __launch_bounds__(TT_WPB * 32, NG_TT_MINB) k_traverse_tiles(
           }
           W->flags[j] = r.flags | (general ? TT_GENERAL : 0);
           const double lo[3] = {-1.0, -1.0, -1.0}, hi[3] = {1.0, 1.0, 1.0};
-          double a0, b0;
-          root = slab_test(r, lo, hi, a0, b0);
-          // a ray missing the box of the occupied finest voxels (the trace
-          // level being the finest) hits none of them: each voxel box lies
-          // inside it on the same dyadic planes, so the slab values nest
-          // (the ordered-test argument); the rare rays with a zero
-          // direction component or a non-finite value are not culled
-          if (root && cull && general) root = slab_test(r, tree.region_lo, tree.region_hi, a0, b0);
+          if (general) {
+            root = box_hit_ordered(r, lo, hi);
+            // a ray missing the box of the occupied finest voxels (the trace
+            // level being the finest) hits none of them: each voxel box lies
+            // inside it on the same dyadic planes, so the slab values nest
+            // (the ordered-test argument); rays off the general path are not
+            // culled
+            if (root && cull) root = box_hit_ordered(r, tree.region_lo, tree.region_hi);
+          } else {
+            double a0, b0;
+            root = slab_test(r, lo, hi, a0, b0);
+          }
         }
         W->seg_s[j] = 0;
         W->seg_e[j] = 0;
