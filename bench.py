@@ -525,17 +525,17 @@ def _voxel_counts(svo):
 
 def _launches_per_frame(svo):
     # zeroing, the tile traversal (all levels, frame defaults, work list),
-    # the march (normals as probe items inside it), stats; the
+    # the march (normals as probe items inside it, statistics); the
     # level-by-level traversal (NG_TILE_TRAVERSE=0) adds the camera-ray
     # kernel, one pass per level and the histogram + scatter,
     # NG_FUSED_PROBES=0 the normals pass (cf. profiles/r01_tiles/launch_shares.md)
     levels = os.environ.get("NG_TILE_TRAVERSE", "1") == "0"
     fused = os.environ.get("NG_FUSED_PROBES", "1") != "0"
-    n = 1 + 1 + 1 + 1
+    n = 1 + 1 + 1  # (the march's last CTA writes the frame statistics)
     if levels:
         n += 1 + (MAX_LEVEL + svo.device.n_virtual) - 1 + 2
     if not fused:
-        n += 1
+        n += 2  # normals pass, statistics kernel
     return n
 
 

@@ -229,6 +229,48 @@ __global__ void k_len_scatter(const int32_t* __restrict__ active, const unsigned
   }
 }
 
+// Tile traversal: a tile list longer than the arena holds (`tile_need`
+// against `lim`) asks for a rerun with the pair capacity whose arena share
+// (`entry` bytes per pair per warp beyond the shared-memory lists, out of
+// 16 bytes per unit of capacity) holds it, plus a quarter.
+struct TileOverflow {
+  const unsigned long long* need;  // null: level-by-level traversal
+  int64_t lim, scap, warps, entry;
+};
+
+__device__ __forceinline__ int64_t tile_overflow(ng_frame_stats* st, const TileOverflow& T) {
+  if (T.need == nullptr || (int64_t)*T.need <= T.lim) return 0;
+  const int64_t spill = ((int64_t)*T.need - T.scap + 16) * 5 / 4;
+  const int64_t want = spill * T.entry * T.warps / 16 + 4096;
+  if (want > st->pair_need) st->pair_need = want;
+  return 1;
+}
+
+__device__ __forceinline__ void finish_stats(ng_frame_stats* st, int n_levels, int64_t pair_cap, int64_t hit_cap,
+                                             const unsigned long long* d_hits, const unsigned long long* d_active,
+                                             const TileOverflow& T) {
+  int64_t over = 0;
+  if (T.need == nullptr)
+    for (int t = 1; t < n_levels; ++t) over |= (st->pairs[t] > pair_cap);
+  over |= (st->pairs[n_levels] > hit_cap);
+  over |= tile_overflow(st, T);
+  st->overflow = over;
+  st->visible = (int64_t)*((volatile const unsigned long long*)d_hits);
+  st->active_rays = (int64_t)*((volatile const unsigned long long*)d_active);
+}
+
+// The frame statistics, run by the last CTA of the primary march (no
+// separate launch).
+struct FinishArgs {
+  ng_frame_stats* st;  // null: not this launch's job
+  int n_levels;
+  int64_t pair_cap, hit_cap;
+  const unsigned long long* d_hits;
+  const unsigned long long* d_active;
+  unsigned int* done;  // CTAs finished (zeroed per frame)
+  TileOverflow tov;
+};
+
 struct MarchArgs {
   ng_render_cfg cfg;
   int G, out_mask, dec_first, dec_last, passes;
@@ -253,6 +295,7 @@ struct MarchArgs {
   ng_counters* counters;
   unsigned long long* prof;      // optional: 4 counters per group (steps, busy lanes, t0, t1)
   int lane_cap;                  // max rays a warp marches at once (NG_MARCH_CAP, default 32)
+  FinishArgs fin;
   // normals (render.py:277-300) in the march: every hit publishes 6 probe
   // items (slot * 6 + j); lanes without a ray evaluate them, and the lane
   // completing a slot's sixth probe forms the normal and shades the pixel
@@ -706,6 +749,17 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_cons
     }
   }
   lc.flush(A.counters);
+  if (A.fin.st) {  // last CTA out writes the frame statistics
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      if (atomicAdd(A.fin.done, 1u) == gridDim.x - 1) {
+        __threadfence();
+        finish_stats(A.fin.st, A.fin.n_levels, A.fin.pair_cap, A.fin.hit_cap, A.fin.d_hits, A.fin.d_active,
+                     A.fin.tov);
+      }
+    }
+  }
   if constexpr (TC) tc_teardown(D.tmem_base, GROUPS);
 }
 
@@ -885,34 +939,10 @@ __global__ void k_hit_points(const ng_ray* __restrict__ rays, const uint8_t* __r
   }
 }
 
-// Tile traversal: a tile list longer than the arena holds (`tile_need`
-// against `lim`) asks for a rerun with the pair capacity whose arena share
-// (`entry` bytes per pair per warp beyond the shared-memory lists, out of
-// 16 bytes per unit of capacity) holds it, plus a quarter.
-struct TileOverflow {
-  const unsigned long long* need;  // null: level-by-level traversal
-  int64_t lim, scap, warps, entry;
-};
-
-__device__ __forceinline__ int64_t tile_overflow(ng_frame_stats* st, const TileOverflow& T) {
-  if (T.need == nullptr || (int64_t)*T.need <= T.lim) return 0;
-  const int64_t spill = ((int64_t)*T.need - T.scap + 16) * 5 / 4;
-  const int64_t want = spill * T.entry * T.warps / 16 + 4096;
-  if (want > st->pair_need) st->pair_need = want;
-  return 1;
-}
-
 __global__ void k_finish_stats(ng_frame_stats* st, int n_levels, int64_t pair_cap, int64_t hit_cap,
                                const unsigned long long* d_hits, const unsigned long long* d_active,
                                TileOverflow T) {
-  int64_t over = 0;
-  if (T.need == nullptr)
-    for (int t = 1; t < n_levels; ++t) over |= (st->pairs[t] > pair_cap);
-  over |= (st->pairs[n_levels] > hit_cap);
-  over |= tile_overflow(st, T);
-  st->overflow = over;
-  st->visible = (int64_t)*d_hits;
-  st->active_rays = (int64_t)*d_active;
+  finish_stats(st, n_levels, pair_cap, hit_cap, d_hits, d_active, T);
 }
 
 // Shadow rays for the hit pixels: origin p + offset * n, direction = light.
@@ -1288,6 +1318,7 @@ static int trace_pass(const ng_octree& tree, const ng_render_cfg& cfg, const Lod
   A.work_counter = work_counter;
   A.prof = march_profile_buffer();
   A.probes = 0;
+  A.fin.st = nullptr;
   return NG_OK;
 }
 
@@ -1311,7 +1342,7 @@ static int render_common(const ng_octree& tree, const ng_field& f, const ng_rend
   ng_ray* rays = user_rays ? (ng_ray*)user_rays : (ng_ray*)(b + L.rays);
   int32_t* hit_list = (int32_t*)(b + L.hit_list);
   // [0] active rays, [1] hits, [2] march work, [3] shadow active, [4] shadow work,
-  // [5] probe items claimed, [6] rays finished
+  // [5] probe items claimed, [6] rays finished, [7] march CTAs finished
   unsigned long long* ctr = (unsigned long long*)(b + L.ctr);
   int r;
   int64_t* seg_start = (int64_t*)(b + L.seg_start);
@@ -1395,6 +1426,16 @@ static int render_common(const ng_octree& tree, const ng_field& f, const ng_rend
   A.normal = fr.normal;
   A.normal_ok = fr.normal_ok;
   A.color = cfg.shadows ? nullptr : fr.color;
+  if (fused) {  // the statistics are final when the march ends: its last CTA writes them
+    A.fin.st = st;
+    A.fin.n_levels = target;
+    A.fin.pair_cap = ws.pair_capacity;
+    A.fin.hit_cap = ws.hit_capacity;
+    A.fin.d_hits = ctr + 1;
+    A.fin.d_active = ctr + 0;
+    A.fin.done = reinterpret_cast<unsigned int*>(ctr + 7);
+    A.fin.tov = tov;
+  }
   if (ws.ev_march_begin && (r = cuda_status(cudaEventRecord((cudaEvent_t)ws.ev_march_begin, s), "event record")))
     return r;
   if ((r = launch_march(tree, f, A, s))) return r;
@@ -1422,8 +1463,10 @@ static int render_common(const ng_octree& tree, const ng_field& f, const ng_rend
     B.counters = &st->counters;
     if ((r = launch_normals(tree, f, B, n, s))) return r;
   }
-  k_finish_stats<<<1, 1, 0, s>>>(st, target, ws.pair_capacity, ws.hit_capacity, ctr + 1, ctr + 0, tov);
-  NG_CHECK_LAUNCH("k_finish_stats");
+  if (!fused) {
+    k_finish_stats<<<1, 1, 0, s>>>(st, target, ws.pair_capacity, ws.hit_capacity, ctr + 1, ctr + 0, tov);
+    NG_CHECK_LAUNCH("k_finish_stats");
+  }
   // ---- shadow rays toward the light (configs[4]) with the same traversal + march
   if (cfg.shadows && do_normals) {
     ng_ray* srays = (ng_ray*)(b + L.s_rays);
@@ -1530,6 +1573,7 @@ int ng_sphere_trace(const ng_octree* tree, const ng_field* fld, const ng_render_
   A.counters = d_counters;
   A.prof = nullptr;
   A.probes = 0;
+  A.fin.st = nullptr;
   (void)d_hit_count;
   r = launch_march(*tree, *fld, A, s);
   cudaFreeAsync(work, s);
