@@ -1244,7 +1244,10 @@ static int trace_pass(const ng_octree& tree, const ng_render_cfg& cfg, const Lod
   unsigned int* buckets = (unsigned int*)(b + L.buckets);
   const bool tiles = use_tile_traverse(target);
   tov.need = nullptr;
-  if (!zeroed) {  // the primary pass has these zeroed by k_zero_regions and the ray kernel
+  if (!zeroed && tiles) {  // the tile path reads only its control words (the march takes work items)
+    int rz = cuda_status(cudaMemsetAsync(scratch, 0, 64, s), "tile traversal control words");
+    if (rz) return rz;
+  } else if (!zeroed) {  // the primary pass has these zeroed by k_zero_regions and the ray kernel
     ZeroRegions z;
     z.n = 4;
     z.p[0] = scratch;
