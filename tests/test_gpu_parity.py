@@ -448,3 +448,28 @@ def test_render_graph_replay_matches_direct(ng, golden, O):
     assert not np.array_equal(first[(0, 0)][0], first[(1, 0)][0])
     from paper_2101_10994_b200.render import _session
     assert _session(fld, 80, 60).graph_replays > 0
+
+
+@pytest.mark.parametrize("pos,look", [((0.1, 0.05, 0.0), (1.0, 0.2, 0.3)),     # inside the torus region, looking out
+                                      ((0.0, 0.9, 0.0), (0.0, 0.0, 0.05)),     # inside the domain, above the ring
+                                      ((0.55, 0.0, 0.0), (0.55, 0.0, 1.0))])   # inside the tube (origin in a voxel)
+def test_render_camera_inside_domain_matches_oracle(ng, golden, O, pos, look):
+    """Cameras inside the octree's domain and region: t_enter clamps to 0 for
+    the boxes containing the eye (octree.py:311-333), the region cull keeps
+    these rays, and the frame matches the oracle's render."""
+    from paper_2101_10994_b200 import scenes
+    go = golden("octree")
+    svo = ng.build_octree(O.sdf_torus(0.5, 0.2), 4, go["samples_b"])
+    tree = oracle_tree_from_golden(go, "b_")
+    fld = scenes.planted_field(svo, O.sdf_torus(0.5, 0.2), seed=0, device_sdf=False)
+    decs = [O.OracleDecoder(d.W1, d.b1, d.W2, d.b2) for d in fld.decoders]
+    cam = ng.Camera(pos, look, (0.0, 1.0, 0.0) if abs(look[1] - pos[1]) < 0.5 else (1.0, 0.0, 0.0), 60.0, 40, 30)
+    fb, rep = ng.render(cam, fld, ng.RenderConfig())
+    fr = O.render(tree, fld.Z, decs, dict(position=cam.position, look_at=cam.look_at, up=cam.up,
+                                          fov_y_deg=cam.fov_y_deg, width=40, height=30), O.RenderParams())
+    hit, ohit = fb.hit.reshape(-1), np.asarray(fr.hit).reshape(-1)
+    assert ohit.sum() > 20  # the view sees surface
+    assert np.mean(hit == ohit) >= 0.99
+    both = hit & ohit
+    assert np.abs(fb.t.reshape(-1)[both] - np.asarray(fr.t).reshape(-1)[both]).max(initial=0.0) <= DEPTH_TOL
+    assert np.mean(np.all(fb.color.reshape(-1, 3) == np.asarray(fr.color).reshape(-1, 3), axis=-1)) >= 0.98
