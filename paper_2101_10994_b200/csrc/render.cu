@@ -310,6 +310,9 @@ struct MarchArgs {
 };
 
 constexpr unsigned PROBE_READY = 0x80000000u;
+#ifndef NG_PROBE_GROUP_MAX_HEAVY
+#define NG_PROBE_GROUP_MAX_HEAVY 64
+#endif
 #ifndef NG_PROBE_GROUP_MAX
 #define NG_PROBE_GROUP_MAX 0  // a group takes probe items while it marches at most this many rays
 #endif
@@ -443,6 +446,13 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_cons
   // rays the group marched last step: probes are taken only by groups with
   // none left, so they never lengthen the steps of a ray still marching
   int group_marching = 1;
+  // with several rays queued per lane, groups rarely run dry before the end,
+  // so lightly marching groups (<= 64 of 128 rays) also take probe items;
+  // otherwise only groups with no rays left do (measured: 720p prefers 0,
+  // 1080p LOD6 64)
+  // (single-decoder frames only: with the LOD blend every probe costs two)
+  const int probe_group_max = (n_work > 4 * (int64_t)gridDim.x * NW * 32 && A.passes == 1) ? NG_PROBE_GROUP_MAX_HEAVY
+                                                                                          : NG_PROBE_GROUP_MAX;
   double px[3] = {0, 0, 0};
   const double eps = A.cfg.normal_eps;
 
@@ -538,7 +548,8 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_cons
     }
     if (__any_sync(FULL, !probes_done)) {  // warp-uniform: the claim below is a warp collective
       // lanes out of rays claim probe items (warp-aggregated) ...
-      const bool pw = !probes_done && ray < 0 && pk < 0 && (drained || lane >= cap) && (!TC || group_marching <= NG_PROBE_GROUP_MAX);
+      const bool pw = !probes_done && ray < 0 && pk < 0 && (drained || lane >= cap) &&
+                      (!TC || group_marching <= probe_group_max);
       const unsigned pm = __ballot_sync(FULL, pw);
       if (pm) {
         const int leader = __ffs(pm) - 1;
