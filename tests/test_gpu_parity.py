@@ -473,3 +473,26 @@ def test_render_camera_inside_domain_matches_oracle(ng, golden, O, pos, look):
     both = hit & ohit
     assert np.abs(fb.t.reshape(-1)[both] - np.asarray(fr.t).reshape(-1)[both]).max(initial=0.0) <= DEPTH_TOL
     assert np.mean(np.all(fb.color.reshape(-1, 3) == np.asarray(fr.color).reshape(-1, 3), axis=-1)) >= 0.98
+
+
+@pytest.mark.parametrize("lod", [1.0, 1.5, 2.0, 2.75])
+def test_render_low_lods_match_oracle(ng, golden, O, lod):
+    """Coarse trace levels (1-3: short tile traversals, presummed tables of
+    one or two levels, the LOD blend between coarse decoders) against the
+    oracle's render."""
+    from paper_2101_10994_b200 import scenes
+    go = golden("octree")
+    svo = ng.build_octree(O.sdf_torus(0.5, 0.2), 4, go["samples_b"])
+    tree = oracle_tree_from_golden(go, "b_")
+    fld = scenes.planted_field(svo, O.sdf_torus(0.5, 0.2), seed=0, device_sdf=False)
+    decs = [O.OracleDecoder(d.W1, d.b1, d.W2, d.b2) for d in fld.decoders]
+    cam = ng.Camera((0.0, 2.0, 3.5), (0.0, 0.0, 0.0), (0.0, 1.0, 0.0), 30.0, 64, 48)
+    fb, rep = ng.render(cam, fld, ng.RenderConfig(lod=lod))
+    fr = O.render(tree, fld.Z, decs, dict(position=cam.position, look_at=cam.look_at, up=cam.up,
+                                          fov_y_deg=cam.fov_y_deg, width=64, height=48), O.RenderParams(lod=lod))
+    hit, ohit = fb.hit.reshape(-1), np.asarray(fr.hit).reshape(-1)
+    assert ohit.sum() > 100
+    assert np.mean(hit == ohit) >= 0.995
+    both = hit & ohit
+    assert np.abs(fb.t.reshape(-1)[both] - np.asarray(fr.t).reshape(-1)[both]).max(initial=0.0) <= DEPTH_TOL
+    assert np.mean(np.all(fb.color.reshape(-1, 3) == np.asarray(fr.color).reshape(-1, 3), axis=-1)) >= 0.98
