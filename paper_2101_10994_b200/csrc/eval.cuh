@@ -122,7 +122,10 @@ struct EvalLane {
 // of the warp needs a decode).
 struct SimtMlp {
   const EvalCtx& c;
+  static constexpr bool kDirectZ = false;  // reads z rows from the warp's z tile
   __device__ __forceinline__ void prepare(int) const {}
+  __device__ __forceinline__ void put_z4(int, int, const float*) const {}
+  __device__ __forceinline__ float decode_direct(int, const float*, bool&) const { return 0.f; }
   __device__ __forceinline__ float operator()(int l, const float xf[3], const float* zrow, bool any,
                                               bool& bad) const {
     bad = false;
@@ -441,6 +444,7 @@ __device__ __forceinline__ EvalLane warp_eval_presum(const ng_octree& tree, cons
     const float* __restrict__ Sc = c.presum + (int64_t)slot * c.presum_corners * 32 + lane;
     ++slot;
     unsigned pm = pm0;
+    unsigned zbad = 0;  // (direct z) points whose z has a non-finite channel on this lane
 #if NG_QUAD_GATHER
     if constexpr (GB % 4 == 0) {
       // 16-byte row loads: lane = (point slot lane / 8, channel quad lane % 8)
@@ -487,9 +491,15 @@ __device__ __forceinline__ EvalLane warp_eval_presum(const ng_octree& tree, cons
             acc[2] = fmaf(wj[jj], v[k][jj].z, acc[2]);
             acc[3] = fmaf(wj[jj], v[k][jj].w, acc[3]);
           }
-          float* zr = &ws.zt[mine[k]][4 * sub];
+          if constexpr (Mlp::kDirectZ) {  // z straight into the decoder's operand row
+            mlp.put_z4(mine[k], sub, acc);
+            zbad |= (isfinite(acc[0]) && isfinite(acc[1]) && isfinite(acc[2]) && isfinite(acc[3]) ? 0u : 1u)
+                    << mine[k];
+          } else {
+            float* zr = &ws.zt[mine[k]][4 * sub];
 #pragma unroll
-          for (int e = 0; e < 4; ++e) zr[e] = acc[e];
+            for (int e = 0; e < 4; ++e) zr[e] = acc[e];
+          }
         }
       }
     } else
@@ -534,9 +544,17 @@ __device__ __forceinline__ EvalLane warp_eval_presum(const ng_octree& tree, cons
     }
     __syncwarp();
     lap(2);
-    const bool any = __any_sync(FULL, pres);
     bool bad = false;
-    const float d = mlp(L, xf, &ws.zt[lane][0], any, bad);
+    float d;
+    if constexpr (Mlp::kDirectZ && GB % 4 == 0 && NG_QUAD_GATHER) {
+      // this lane's point: non-finite z on any channel lane, or non-finite x
+      const unsigned zb = __reduce_or_sync(FULL, zbad);
+      d = mlp.decode_direct(L, xf, bad);
+      bad = bad || ((zb >> lane) & 1u);
+    } else {
+      const bool any = __any_sync(FULL, pres);
+      d = mlp(L, xf, &ws.zt[lane][0], any, bad);
+    }
     emit(L, d, bad && pres, res);
     lap(3);
   }

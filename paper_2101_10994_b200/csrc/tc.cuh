@@ -131,15 +131,23 @@ __device__ __forceinline__ void split_bf16(float a, __nv_bfloat16& hi, __nv_bflo
   lo = __float2bfloat16_rn(a - __bfloat162float(hi));
 }
 
-// Write one operand row (48 values) as hi / lo tiles; v[k] for k < 36, zero after.
+// Operand column layout (K = 48): x0 x1 x2 | bias input | 0 0 0 0 |
+// z0..z31 | 0 x 8. z starts on a 16-byte chunk, so 4 consecutive channels
+// are one 8-byte store of a row (the presummed gather writes z this way).
+constexpr int KZ = 8;  // first z column
+__device__ __forceinline__ int input_of_column(int k) {  // index into [x(3), z(32), 1] or -1 (zero)
+  return k < 3 ? k : (k == 3 ? 35 : (k >= KZ && k < KZ + 32 ? 3 + (k - KZ) : -1));
+}
+
+// Write one operand row (48 values) as hi / lo tiles from v36 = [x, z, 1].
 __device__ __forceinline__ void write_row(uint8_t* hi_tile, uint8_t* lo_tile, int row, const float* v36) {
 #pragma unroll
   for (int c = 0; c < CHUNKS; ++c) {
     __align__(16) __nv_bfloat16 h[8], l[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      const int k = c * 8 + j;
-      const float a = (k < 36) ? v36[k] : 0.f;
+      const int src = input_of_column(c * 8 + j);
+      const float a = src >= 0 ? v36[src] : 0.f;
       split_bf16(a, h[j], l[j]);
     }
     const int off = tile_off(row, c * 8);

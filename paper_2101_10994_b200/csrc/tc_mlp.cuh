@@ -26,6 +26,19 @@ struct TcMlp {
 
   __device__ __forceinline__ void prepare(int l) const;
 
+  // The presummed gather writes z straight into the operand rows (lane =
+  // channel quad), and the decoder then adds only x and the bias input.
+  static constexpr bool kDirectZ = true;
+  __device__ __forceinline__ void put_z4(int p, int sub, const float* acc) const {
+    __align__(8) __nv_bfloat16 h[4], l4[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) tc::split_bf16(acc[e], h[e], l4[e]);
+    const int off = tc::tile_off(32 * wg + p, tc::KZ + 4 * sub);
+    *reinterpret_cast<uint2*>(a_hi + off) = *reinterpret_cast<const uint2*>(h);
+    *reinterpret_cast<uint2*>(a_lo + off) = *reinterpret_cast<const uint2*>(l4);
+  }
+  __device__ __forceinline__ float decode_direct(int l, const float xf[3], bool& bad) const;
+
   __device__ __forceinline__ float operator()(int l, const float xf[3], const float* zrow, bool /*any*/,
                                               bool& bad) const {
 #ifdef NG_PROFILE
@@ -78,6 +91,46 @@ struct TcMlp {
   }
 };
 
+__device__ __forceinline__ float TcMlp::decode_direct(int l, const float xf[3], bool& bad) const {
+  const int lane = (int)lane_id();
+  const int row = 32 * wg + lane;
+  bad = !(isfinite(xf[0]) && isfinite(xf[1]) && isfinite(xf[2]));
+  // chunk 0: x, the bias input, zeros; chunk 5: zeros (z is chunks 1-4)
+  {
+    const float c0[8] = {xf[0], xf[1], xf[2], 1.f, 0.f, 0.f, 0.f, 0.f};
+    __align__(16) __nv_bfloat16 h[8], lo[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) tc::split_bf16(c0[j], h[j], lo[j]);
+    const int off0 = tc::tile_off(row, 0), off5 = tc::tile_off(row, 40);
+    *reinterpret_cast<uint4*>(a_hi + off0) = *reinterpret_cast<const uint4*>(h);
+    *reinterpret_cast<uint4*>(a_lo + off0) = *reinterpret_cast<const uint4*>(lo);
+    *reinterpret_cast<uint4*>(a_hi + off5) = make_uint4(0, 0, 0, 0);
+    *reinterpret_cast<uint4*>(a_lo + off5) = make_uint4(0, 0, 0, 0);
+  }
+  tc::fence_proxy_async();
+  tc::fence_before_sync();
+  tc::named_sync(bar_id, 128);
+  const uint8_t* dt = dec_tiles + (restage_src ? (size_t)0 : (size_t)(l - dec_first) * DEC_TC_BYTES);
+  if (wg == 0 && lane == 0)
+    tc::issue_gemm(tmem, tc::smem_u32(a_hi), tc::smem_u32(a_lo), tc::smem_u32(dt), tc::smem_u32(dt + tc::TILE_BYTES),
+                   mbar);
+  tc::mbar_wait(mbar, *phase & 1u);
+  *phase += 1;
+  tc::fence_after_sync();
+  const float* W2 = reinterpret_cast<const float*>(dt + 2 * tc::TILE_BYTES);
+  float acc = W2[128];  // b2
+  const uint32_t taddr = tmem + ((uint32_t)(32 * wg) << 16);
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    float hh[32];
+    tc::tmem_ld32(taddr + 32 * c, hh);
+#pragma unroll
+    for (int i = 0; i < 32; ++i) acc = fmaf(W2[32 * c + i], fmaxf(hh[i], 0.f), acc);
+  }
+  tc::fence_before_sync();
+  return acc;
+}
+
 // Convert packed fp32 decoders (ng_field layout) into bf16 hi/lo B tiles.
 __device__ __forceinline__ void stage_decoder_tiles(uint8_t* dst, const float* __restrict__ src, int first, int last, int stride) {
   const int ndec = last - first + 1;
@@ -89,8 +142,8 @@ __device__ __forceinline__ void stage_decoder_tiles(uint8_t* dst, const float* _
     __align__(16) __nv_bfloat16 h[8], lo[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
-      const int k = c * 8 + q;
-      tc::split_bf16(k < NG_W1_STRIDE ? __ldg(row + k) : 0.f, h[q], lo[q]);
+      const int src = tc::input_of_column(c * 8 + q);  // W1b row = [x weights, z weights, b1]
+      tc::split_bf16(src >= 0 ? __ldg(row + src) : 0.f, h[q], lo[q]);
     }
     uint8_t* t = dst + (size_t)d * DEC_TC_BYTES;
     const int off = tc::tile_off(j, c * 8);
