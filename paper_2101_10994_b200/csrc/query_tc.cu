@@ -35,7 +35,7 @@ __global__ void __launch_bounds__(TQ_NW * 32, 1) k_query_tc(const __grid_constan
                                                             ng_query_args a, int G, int out_mask, int dec_first,
                                                             int dec_last, const double* __restrict__ pts, int64_t n,
                                                             double* __restrict__ out, int ncols,
-                                                            ng_counters* counters) {
+                                                            ng_counters* counters, const uint8_t* tiles) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const TcSmem t = tc_carve(smem, 1, TQ_GROUPS);
   const int w = threadIdx.x >> 5;
@@ -45,6 +45,7 @@ __global__ void __launch_bounds__(TQ_NW * 32, 1) k_query_tc(const __grid_constan
   TcMlp mlp = tc_policy(t, tmem_base, dec_first, &phase);
   mlp.restage_src = f.decoders;
   mlp.restage_stride = f.dec_stride;
+  mlp.restage_tiles = tiles;
 
   EvalCtx c;
   c.Z = f.Z;
@@ -107,6 +108,12 @@ __global__ void __launch_bounds__(TQ_NW * 32, 1) k_query_tc(const __grid_constan
 
 size_t query_tc_smem_bytes(int) { return tc_smem_bytes(1, TQ_GROUPS); }
 
+// The requested decoders as bf16 hi / lo B tiles (+ W2, b2), converted once
+// per query so each CTA's per-level restage is a plain copy.
+__global__ void k_query_tiles(ng_field f, int dec_first, int dec_last, uint8_t* tiles) {
+  stage_decoder_tiles(tiles, f.decoders, dec_first, dec_last, f.dec_stride);
+}
+
 // Returns NG_ERR_CAPACITY when the tensor-core path cannot take the query
 // (hidden width != 128 or too many decoders for shared memory).
 int run_query_tc(const ng_octree& tree, const ng_field& f, const ng_query_args& a, int G, int out_mask,
@@ -124,10 +131,16 @@ int run_query_tc(const ng_octree& tree, const ng_field& f, const ng_query_args& 
   }
   const int64_t tiles = (n + 127) / 128;
   const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((tiles + TQ_GROUPS - 1) / TQ_GROUPS, sm_count()));
+  const int ndec = dec_last - dec_first + 1;
+  uint8_t* dtiles = nullptr;
+  int r = cuda_status(cudaMallocAsync((void**)&dtiles, (size_t)ndec * DEC_TC_BYTES, s), "query tiles alloc");
+  if (r) return r;
+  k_query_tiles<<<1, 512, 0, s>>>(f, dec_first, dec_last, dtiles);
+  NG_CHECK_LAUNCH("k_query_tiles");
   k_query_tc<<<(int)grid, TQ_NW * 32, smem, s>>>(tree, f, a, G, out_mask, dec_first, dec_last, pts, n, out, ncols,
-                                                 counters);
+                                                 counters, dtiles);
   NG_CHECK_LAUNCH("k_query_tc");
-  return NG_OK;
+  return cuda_status(cudaFreeAsync(dtiles, s), "query tiles free");
 }
 
 }  // namespace ng

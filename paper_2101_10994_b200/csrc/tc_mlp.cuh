@@ -23,6 +23,7 @@ struct TcMlp {
   // and re-stages level l from these fp32 decoders before its GEMMs
   const float* restage_src = nullptr;
   int restage_stride = 0;
+  const uint8_t* restage_tiles = nullptr;  // or pre-converted tiles (DEC_TC_BYTES per level, dec_first first)
 
   __device__ __forceinline__ void prepare(int l) const;
 
@@ -164,7 +165,13 @@ __device__ __forceinline__ void TcMlp::prepare(int l) const {
   // mbarrier before leaving the decoder), so the tiles can be replaced
   tc::fence_before_sync();
   __syncthreads();
-  stage_decoder_tiles(const_cast<uint8_t*>(dec_tiles), restage_src, l, l, restage_stride);
+  if (restage_tiles) {  // a plain copy of the pre-converted tiles
+    const uint4* src4 = reinterpret_cast<const uint4*>(restage_tiles + (size_t)(l - dec_first) * DEC_TC_BYTES);
+    uint4* dst4 = reinterpret_cast<uint4*>(const_cast<uint8_t*>(dec_tiles));
+    for (int i = threadIdx.x; i < DEC_TC_BYTES / 16; i += blockDim.x) dst4[i] = __ldg(src4 + i);
+  } else {
+    stage_decoder_tiles(const_cast<uint8_t*>(dec_tiles), restage_src, l, l, restage_stride);
+  }
   tc::fence_proxy_async();
   tc::fence_before_sync();
   __syncthreads();
