@@ -226,7 +226,9 @@ __device__ __forceinline__ void make_ray(double ox, double oy, double oz, double
 // Camera.rays (render.py:74-88). Every kernel that needs a camera ray
 // computes it with this one function, so a ray recomputed on the fly is
 // the same ray everywhere.
-__device__ __forceinline__ void camera_ray(const ng_camera& cam, int64_t i, ng_ray& r) {
+// The unit direction of camera ray i (render.py:74-88); camera_ray below
+// adds the origin and the slab fields (1/d, signs).
+__device__ __forceinline__ void camera_dir(const ng_camera& cam, int64_t i, double dir[3]) {
   const int px_i = (int)(i % cam.width);
   const int lrow = (int)(i / cam.width);
   const int band = lrow / cam.band_rows;
@@ -238,7 +240,14 @@ __device__ __forceinline__ void camera_ray(const ng_camera& cam, int64_t i, ng_r
 #pragma unroll
   for (int a = 0; a < 3; ++a) d[a] = dadd(dadd(cam.fwd[a], dmul(px, cam.right[a])), dmul(py, cam.up[a]));
   const double nrm = __dsqrt_rn(dadd(dadd(dmul(d[0], d[0]), dmul(d[1], d[1])), dmul(d[2], d[2])));
-  make_ray(cam.position[0], cam.position[1], cam.position[2], d[0] / nrm, d[1] / nrm, d[2] / nrm, r);
+#pragma unroll
+  for (int a = 0; a < 3; ++a) dir[a] = d[a] / nrm;
+}
+
+__device__ __forceinline__ void camera_ray(const ng_camera& cam, int64_t i, ng_ray& r) {
+  double d[3];
+  camera_dir(cam, i, d);
+  make_ray(cam.position[0], cam.position[1], cam.position[2], d[0], d[1], d[2], r);
 }
 
 // Rays of a pass: explicit records, or (`cam_rays`) the camera's rays

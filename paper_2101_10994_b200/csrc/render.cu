@@ -499,10 +499,8 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_cons
             ev = 0;
             ready = false;
             if (A.rays.cam_rays) {
-              ng_ray rr;
-              camera_ray(A.rays.cam, ray, rr);
-              o[0] = rr.o[0]; o[1] = rr.o[1]; o[2] = rr.o[2];
-              d[0] = rr.d[0]; d[1] = rr.d[1]; d[2] = rr.d[2];
+              camera_dir(A.rays.cam, ray, d);  // (the march needs no slab fields)
+              o[0] = A.rays.cam.position[0]; o[1] = A.rays.cam.position[1]; o[2] = A.rays.cam.position[2];
             } else {
               const ng_ray* rp = A.rays.rays + ray;
               o[0] = rp->o[0]; o[1] = rp->o[1]; o[2] = rp->o[2];
