@@ -744,7 +744,8 @@ static int highest_level(int mask) { return 32 - __builtin_clz((unsigned)mask); 
 static double g_phase_ms[8];
 static int64_t g_phase_batches = 0;
 
-static int launch_batch(const ng_octree* tree, TrainArgs& A, cudaStream_t s) {
+// parts: 1 = counters reset + point location, 2 = the rest of the step
+static int launch_batch(const ng_octree* tree, TrainArgs& A, cudaStream_t s, int parts = 3) {
   static int ev_env = -1;
   static cudaEvent_t ev[8];
   if (ev_env < 0) {
@@ -757,9 +758,7 @@ static int launch_batch(const ng_octree* tree, TrainArgs& A, cudaStream_t s) {
   auto mark = [&]() {
     if (ev_env) cudaEventRecord(ev[nev++], s);
   };
-  mark();
-  int r = cuda_status(cudaMemsetAsync(A.ctr, 0, 4 * sizeof(int64_t) + 32 * sizeof(int32_t), s), "train memset");
-  if (r) return r;
+  int r = 0;
   static bool attr = false;
   if (!attr) {
     if ((r = cuda_status(cudaFuncSetAttribute(k_train_dec, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -769,9 +768,15 @@ static int launch_batch(const ng_octree* tree, TrainArgs& A, cudaStream_t s) {
   }
   const int cap_blocks = 4 * sm_count();
   const int row_blocks = tr_grid(A.max_rows * 32, 256) < cap_blocks ? tr_grid(A.max_rows * 32, 256) : cap_blocks;
-  k_train_locate<<<tr_grid(A.n * 32, 256), 256, 0, s>>>(*tree, A);
-  NG_CHECK_LAUNCH("k_train_locate");
-  mark();
+  if (parts & 1) {
+    mark();
+    if ((r = cuda_status(cudaMemsetAsync(A.ctr, 0, 4 * sizeof(int64_t) + 32 * sizeof(int32_t), s), "train memset")))
+      return r;
+    k_train_locate<<<tr_grid(A.n * 32, 256), 256, 0, s>>>(*tree, A);
+    NG_CHECK_LAUNCH("k_train_locate");
+    mark();
+  }
+  if (!(parts & 2)) return NG_OK;
   if (A.mode != 2) {
     k_train_rowprep<<<row_blocks, 256, 0, s>>>(A);
     NG_CHECK_LAUNCH("k_train_rowprep");
@@ -886,7 +891,10 @@ extern "C" {
 size_t ng_train_workspace_bytes(const ng_octree* tree, int64_t batch_capacity, int32_t h, int32_t n_decoders,
                                 int64_t corner_count, int32_t dec_stride) {
   (void)h;
-  return train_layout(batch_capacity, tree->max_level, n_decoders, corner_count, dec_stride).total;
+  // two batch buffers: ng_train_epoch locates batch b+1 in one while batch b
+  // runs in the other (single-batch calls use the first)
+  const size_t one = train_layout(batch_capacity, tree->max_level, n_decoders, corner_count, dec_stride).total;
+  return 2 * ((one + 255) & ~(size_t)255);
 }
 
 int ng_train_batch(const ng_octree* tree, const ng_train_params* P, const ng_train_step* st, const double* pts,
@@ -931,10 +939,21 @@ int ng_train_epoch(const ng_octree* tree, const ng_train_params* P, const double
     return NG_ERR_CONFIG;
   }
   cudaStream_t s = (cudaStream_t)stream;
-  int64_t step = step0;
-  for (int64_t s0 = 0, bi = 0; s0 < n; s0 += batch_size, ++bi) {
+  // Batch b+1's point location depends only on the points and the octree,
+  // so it runs on a side stream in the other workspace buffer while batch
+  // b's step runs (a buffer is reused once the step two batches back has
+  // left its corner counters at zero). NG_TRAIN_OVERLAP=0: one stream.
+  static int overlap_env = -1;
+  if (overlap_env < 0) {
+    const char* e = getenv("NG_TRAIN_OVERLAP");
+    const char* ev = getenv("NG_TRAIN_EVENTS");
+    overlap_env = (e && e[0] == '0') || (ev && ev[0] == '1') ? 0 : 1;
+  }
+  const size_t half = ws_bytes / 2;
+  const int64_t nb = (n + batch_size - 1) / batch_size;
+  auto args_for = [&](int64_t bi, TrainArgs& A) -> int {
+    const int64_t s0 = bi * batch_size;
     const int64_t cnt = (n - s0 < batch_size) ? n - s0 : batch_size;
-    ++step;
     ng_train_step st;
     st.active_mask = active_mask;
     st.update_decoders = update_decoders;
@@ -942,12 +961,60 @@ int ng_train_epoch(const ng_octree* tree, const ng_train_params* P, const double
     st.pad = 0;
     st.denom = (double)cnt;
     st.lr = lr;
-    st.step = step;
+    st.step = step0 + bi + 1;
     st.adam_c = adam_c;
     st.batch_index = s0;
-    int r = ng_train_batch(tree, P, &st, pts + 3 * s0, dist + s0, nullptr, cnt, batch_size, ws, ws_bytes,
-                           level_sums, nullptr, nullptr, nullptr, nullptr, status, s);
+    char* wsb = (char*)ws + (overlap_env ? (size_t)(bi & 1) * half : 0);
+    int r = fill_args(tree, P, &st, pts + 3 * s0, dist + s0, nullptr, cnt, batch_size, wsb,
+                      overlap_env ? half : ws_bytes, A);
     if (r) return r;
+    A.level_sums = level_sums;
+    A.grad_Z = nullptr;
+    A.grad_dec = nullptr;
+    A.dec_touched = nullptr;
+    A.psi_out = nullptr;
+    A.status = status;
+    return NG_OK;
+  };
+  static cudaStream_t side = nullptr;
+  static cudaEvent_t e_loc[2], e_done[2];
+  if (overlap_env && !side) {
+    cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking);
+    for (int k = 0; k < 2; ++k) {
+      cudaEventCreateWithFlags(&e_loc[k], cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&e_done[k], cudaEventDisableTiming);
+    }
+  }
+  int64_t step = step0;
+  if (nb > 0) {
+    TrainArgs A;
+    int r = args_for(0, A);
+    if (r) return r;
+    if ((r = launch_batch(tree, A, s, overlap_env ? 1 : 3))) return r;
+    if (!overlap_env) {
+      ++step;
+      if (flush_every > 0 && 1 % flush_every == 0 && (r = ng_train_flush(P, step, adam_c, lr, s))) return r;
+    }
+  }
+  for (int64_t bi = overlap_env ? 0 : 1; bi < nb; ++bi) {
+    TrainArgs A;
+    int r = args_for(bi, A);
+    if (r) return r;
+    if (overlap_env) {
+      if (bi + 1 < nb) {  // locate the next batch on the side stream
+        TrainArgs An;
+        if ((r = args_for(bi + 1, An))) return r;
+        if (bi >= 1 && (r = cuda_status(cudaStreamWaitEvent(side, e_done[(bi + 1) & 1], 0), "train wait"))) return r;
+        if ((r = launch_batch(tree, An, side, 1))) return r;
+        if ((r = cuda_status(cudaEventRecord(e_loc[(bi + 1) & 1], side), "train record"))) return r;
+      }
+      if (bi >= 1 && (r = cuda_status(cudaStreamWaitEvent(s, e_loc[bi & 1], 0), "train wait"))) return r;
+      if ((r = launch_batch(tree, A, s, 2))) return r;
+      if ((r = cuda_status(cudaEventRecord(e_done[bi & 1], s), "train record"))) return r;
+    } else {
+      if ((r = launch_batch(tree, A, s, 3))) return r;
+    }
+    ++step;
     if (flush_every > 0 && (bi + 1) % flush_every == 0 && (r = ng_train_flush(P, step, adam_c, lr, s))) return r;
   }
   return ng_train_flush(P, step, adam_c, lr, s);
