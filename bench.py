@@ -311,7 +311,7 @@ def run_ours(args, rank: int, world: int):
         for _ in range(2):
             out = forward_levels_device(svo, fld.device, pts, [1, 2, 3, 4, 5])
         torch.cuda.synchronize()
-        qe = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(3)]
+        qe = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(7)]
         for a, b in qe:
             flush.zero_()
             a.record()

@@ -977,13 +977,19 @@ int ng_train_epoch(const ng_octree* tree, const ng_train_params* P, const double
     return NG_OK;
   };
   static cudaStream_t side = nullptr;
-  static cudaEvent_t e_loc[2], e_done[2];
+  static cudaEvent_t e_loc[2], e_done[2], e_start;
   if (overlap_env && !side) {
     cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking);
     for (int k = 0; k < 2; ++k) {
       cudaEventCreateWithFlags(&e_loc[k], cudaEventDisableTiming);
       cudaEventCreateWithFlags(&e_done[k], cudaEventDisableTiming);
     }
+    cudaEventCreateWithFlags(&e_start, cudaEventDisableTiming);
+  }
+  if (overlap_env) {  // the side stream starts after everything already queued on the caller's stream
+    int r0 = cuda_status(cudaEventRecord(e_start, s), "train record");
+    if (!r0) r0 = cuda_status(cudaStreamWaitEvent(side, e_start, 0), "train wait");
+    if (r0) return r0;
   }
   int64_t step = step0;
   if (nb > 0) {
