@@ -293,3 +293,31 @@ def test_device_epoch_sampler_golden(ng, scenes, golden):
     np.testing.assert_array_equal(ss.points, g["ep_points"])
     np.testing.assert_array_equal(ss.distances, g["ep_dist"])
     np.testing.assert_array_equal(ss.scheme_tags, g["ep_tags"])
+
+
+def test_epoch_inputs_copied_asynchronously(ng, scenes, golden):
+    """The epoch's next-batch location runs on a side stream: inputs that are
+    still being copied (non-blocking from pinned memory) when the epoch is
+    enqueued must give the same result as synchronised inputs."""
+    import torch
+    from paper_2101_10994_b200.trainer import DeviceTrainer
+    g = golden("train")
+    fld = _tiny(ng, scenes, g)
+    rng = np.random.default_rng(21)
+    pts = rng.uniform(-0.9, 0.9, size=(5000, 3))
+    dist = np.linalg.norm(pts, axis=1) - 0.5
+    outs = []
+    for asynchronous in (False, True):
+        tr = DeviceTrainer(ng.NeuralField(fld.svo, fld.Z.copy(), [d.astype(np.float64) for d in fld.decoders]),
+                           256)
+        for _ in range(2):
+            if asynchronous:
+                p = torch.from_numpy(pts).pin_memory().to("cuda", non_blocking=True)
+                d = torch.from_numpy(dist).pin_memory().to("cuda", non_blocking=True)
+            else:
+                p = torch.from_numpy(pts).cuda()
+                d = torch.from_numpy(dist).cuda()
+                torch.cuda.synchronize()
+            tr.run_epoch(p, d, [1, 2], True, 1e-3)
+        outs.append(tr.state.Z_numpy())
+    np.testing.assert_array_equal(outs[0], outs[1])
