@@ -298,10 +298,6 @@ def run_ours(args, rank: int, world: int):
                   "h2d_bytes_per_step": _sizeof("NgCamera") + _sizeof("NgRenderCfg"),
                   "d2h_bytes_per_step": d2h + _sizeof("NgFrameStats")}
 
-    # ---- configs[3] / configs[4] at 1920x1080 (tiled across the ranks when N > 1)
-    if not args.no_extra:
-        res["extra"] = extra_configs(args, world, dev, knot)
-
     # ---- batched SDF query (configs[2]): forward L = 1..5 over 2^24 points,
     # sharded by point range across ranks (no exchange)
     if not args.no_query:
@@ -327,6 +323,10 @@ def run_ours(args, rank: int, world: int):
                         "value": share * world / q_ms / 1e3, "unit": "Mpoints/s", "ms": q_ms}
         res["_query_pts"] = pts_h
         del out
+    # ---- configs[3] / configs[4] at 1920x1080 (tiled across the ranks when N > 1)
+    if not args.no_extra:
+        res["extra"] = extra_configs(args, world, dev, knot)
+
     # ---- training step: one epoch of loss + backward + Adam,
     # batch 512, fp64 masters, random-init LOD5 field (rank 0 / N = 1 only: the
     # reference trains in one process)
