@@ -14,8 +14,14 @@ for _ in range(2):
     out = forward_levels_device(svo, fld.device, pts, [1, 2, 3, 4, 5])
 torch.cuda.synchronize()
 ms = []
+mode = os.environ.get("QP_FLUSH", "write")  # write (as bench.py) | read | none
+acc = torch.zeros((), dtype=torch.int64, device=dev)
 for _ in range(7):
-    flush.zero_()
+    if mode == "write":
+        flush.zero_()
+    elif mode == "read":
+        acc += flush.view(torch.int64).max()
+    torch.cuda.synchronize()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
     out = forward_levels_device(svo, fld.device, pts, [1, 2, 3, 4, 5])
@@ -23,5 +29,5 @@ for _ in range(7):
     torch.cuda.synchronize()
     ms.append(a.elapsed_time(b))
 z = fld.device.Z
-print(f"best {bench.QUERY_POINTS / min(ms) / 1e3:.0f} Mpts/s  median {bench.QUERY_POINTS / sorted(ms)[3] / 1e3:.0f}"
+print(f"flush {mode}  best {bench.QUERY_POINTS / min(ms) / 1e3:.0f} Mpts/s  median {bench.QUERY_POINTS / sorted(ms)[3] / 1e3:.0f}"
       f"  Z {z.data_ptr():#x} ({z.numel() * 4 >> 20} MiB)  pts {pts.data_ptr():#x}  out {out.data_ptr():#x}")
