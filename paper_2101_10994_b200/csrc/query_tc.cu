@@ -29,13 +29,18 @@ int grid_for(int64_t n, int nt);
 #define NG_TQ_GROUPS 4
 #endif
 constexpr int TQ_GROUPS = NG_TQ_GROUPS;
+// tiles claimed from a counter (1) or strided over the grid (0)
+#ifndef NG_QUERY_DYNAMIC
+#define NG_QUERY_DYNAMIC 1
+#endif
 constexpr int TQ_NW = 4 * TQ_GROUPS;
 
 __global__ void __launch_bounds__(TQ_NW * 32, 1) k_query_tc(const __grid_constant__ ng_octree tree, ng_field f,
                                                             ng_query_args a, int G, int out_mask, int dec_first,
                                                             int dec_last, const double* __restrict__ pts, int64_t n,
                                                             double* __restrict__ out, int ncols,
-                                                            ng_counters* counters, const uint8_t* tiles) {
+                                                            ng_counters* counters, const uint8_t* tiles,
+                                                            unsigned int* claim) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const TcSmem t = tc_carve(smem, 1, TQ_GROUPS);
   const int w = threadIdx.x >> 5;
@@ -61,8 +66,19 @@ __global__ void __launch_bounds__(TQ_NW * 32, 1) k_query_tc(const __grid_constan
   const double alpha = a.blend_alpha;
   LaneCounters lc;
   const int64_t n_tiles = (n + 127) / 128;
-  // the CTA's groups take tiles together (the level restaging is CTA-wide)
+  // the CTA's groups take tiles together (the level restaging is CTA-wide),
+  // claimed from a counter so a slow SM does not hold up the query's end
+#if NG_QUERY_DYNAMIC
+  __shared__ int64_t s_tb;
+  while (true) {
+    if (threadIdx.x == 0) s_tb = (int64_t)atomicAdd(claim, 1u) * TQ_GROUPS;
+    __syncthreads();
+    const int64_t tb = s_tb;
+    __syncthreads();
+    if (tb >= n_tiles) break;
+#else
   for (int64_t tb = (int64_t)blockIdx.x * TQ_GROUPS; tb < n_tiles; tb += (int64_t)gridDim.x * TQ_GROUPS) {
+#endif
     const int64_t tile = tb + g;
     const int64_t i = tile * 128 + 32 * wg + lane_id();
     const bool act = i < n;
@@ -110,7 +126,8 @@ size_t query_tc_smem_bytes(int) { return tc_smem_bytes(1, TQ_GROUPS); }
 
 // The requested decoders as bf16 hi / lo B tiles (+ W2, b2), converted once
 // per query so each CTA's per-level restage is a plain copy.
-__global__ void k_query_tiles(ng_field f, int dec_first, int dec_last, uint8_t* tiles) {
+__global__ void k_query_tiles(ng_field f, int dec_first, int dec_last, uint8_t* tiles, unsigned int* claim) {
+  if (threadIdx.x == 0) *claim = 0u;  // k_query_tc's tile counter
   stage_decoder_tiles(tiles, f.decoders, dec_first, dec_last, f.dec_stride);
 }
 
@@ -133,12 +150,13 @@ int run_query_tc(const ng_octree& tree, const ng_field& f, const ng_query_args& 
   const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((tiles + TQ_GROUPS - 1) / TQ_GROUPS, sm_count()));
   const int ndec = dec_last - dec_first + 1;
   uint8_t* dtiles = nullptr;
-  int r = cuda_status(cudaMallocAsync((void**)&dtiles, (size_t)ndec * DEC_TC_BYTES, s), "query tiles alloc");
+  int r = cuda_status(cudaMallocAsync((void**)&dtiles, (size_t)ndec * DEC_TC_BYTES + 256, s), "query tiles alloc");
   if (r) return r;
-  k_query_tiles<<<1, 512, 0, s>>>(f, dec_first, dec_last, dtiles);
+  unsigned int* claim = reinterpret_cast<unsigned int*>(dtiles + (size_t)ndec * DEC_TC_BYTES);
+  k_query_tiles<<<1, 512, 0, s>>>(f, dec_first, dec_last, dtiles, claim);
   NG_CHECK_LAUNCH("k_query_tiles");
   k_query_tc<<<(int)grid, TQ_NW * 32, smem, s>>>(tree, f, a, G, out_mask, dec_first, dec_last, pts, n, out, ncols,
-                                                 counters, dtiles);
+                                                 counters, dtiles, claim);
   NG_CHECK_LAUNCH("k_query_tc");
   return cuda_status(cudaFreeAsync(dtiles, s), "query tiles free");
 }
