@@ -297,6 +297,15 @@ int ng_segments(const ng_hit_pair* hits, const int64_t* d_count, int64_t capacit
 /* ---- rendering (render.py:43-448) --------------------------------------- */
 int ng_camera_rays(const ng_camera* cam, ng_ray* rays, void* stream);
 size_t ng_render_workspace_bytes(int64_t n_rays, int64_t pair_capacity, int64_t hit_capacity);
+/* Byte offsets into a frame workspace of what the last frame's traversal
+ * left there (render path, traversal.py:207-255): out[0] the final hit list
+ * (ng_hit_pair, tile order; .ray holds the voxel's packed cell
+ * x | y << 10 | z << 20 on the tile path, the ray id otherwise), out[1] /
+ * out[2] the per-ray segments [start, end) into it (int64), out[3] the total
+ * size. n_out <= 4 entries are written. Lets callers and tests read the
+ * render path's per-ray voxel lists back without re-running a traversal. */
+int ng_render_workspace_offsets(int64_t n_rays, int64_t pair_capacity, int64_t hit_capacity,
+                                int64_t* out, int32_t n_out);
 /* sphere_trace (render.py:174-274) over an existing final list. */
 int ng_sphere_trace(const ng_octree* tree, const ng_field* fld, const ng_render_cfg* cfg,
                     const ng_ray* rays, int64_t n_rays, const ng_hit_pair* hits,

@@ -300,12 +300,43 @@ class PairList:
         return len(self.rays)
 
 
-def decide(tree, origins, dirs, pairs: PairList, final: bool) -> np.ndarray:
-    """traversal.py:95-110."""
+TIE_REL = 2.0 ** -22  # a slab decision this close to flipping would flip in fp32 (SURVEY.md 8c probe)
+
+
+def count_near_ties(o, d, lo, hi, rel: float = TIE_REL) -> int:
+    """Slab decisions (octree.py:311-333) within `rel` of flipping: the hit
+    test is max(near) <= min(far) and min(far) >= 0; a decision is a near
+    tie when either comparison's two sides differ by at most rel * max(1,
+    |side|). These are the pairs a lower-precision slab test could get
+    wrong; an exact restatement must still agree on every one of them."""
+    o = np.asarray(o, dtype=np.float64)
+    d = np.asarray(d, dtype=np.float64)
+    zero = d == 0.0
+    with np.errstate(divide="ignore", invalid="ignore"):
+        inv = 1.0 / d
+        ta = (lo - o) * inv
+        tb = (hi - o) * inv
+        inside = (o >= lo) & (o <= hi)
+        near = np.where(zero, np.where(inside, -np.inf, np.inf), np.minimum(ta, tb)).max(axis=-1)
+        far = np.where(zero, np.where(inside, np.inf, -np.inf), np.maximum(ta, tb)).min(axis=-1)
+        scale = np.maximum(1.0, np.maximum(np.abs(near), np.abs(far)))
+        t1 = np.isfinite(near) & np.isfinite(far) & (np.abs(far - near) <= rel * scale)
+        t2 = np.isfinite(far) & (np.abs(far) <= rel)
+    return int(np.count_nonzero(t1 | t2))
+
+
+def decide(tree, origins, dirs, pairs: PairList, final: bool, ties: list | None = None) -> np.ndarray:
+    """traversal.py:95-110. With `ties`, appends the level's (near-tie
+    decisions (count_near_ties), decisions) -- diagnostics only, the
+    decisions are unchanged."""
     if len(pairs) == 0:
+        if ties is not None:
+            ties.append((0, 0))
         return np.zeros(0, dtype=np.int64)
     lo, hi = voxel_boxes(tree, pairs.level, pairs.voxels)
     _, _, hit = slab(origins[pairs.rays], dirs[pairs.rays], lo, hi)
+    if ties is not None:
+        ties.append((count_near_ties(origins[pairs.rays], dirs[pairs.rays], lo, hi), len(pairs)))
     if final:
         return hit.astype(np.int64)
     s, e = child_range(tree.level_codes(pairs.level)[pairs.voxels],
@@ -341,10 +372,11 @@ def compact(pairs: PairList, D, S) -> PairList:
     return PairList(pairs.level, pairs.rays[keep].astype(np.int64), pairs.voxels[keep].astype(np.int64))
 
 
-def traverse(tree: OracleOctree, origins, dirs, level: int | None = None) -> list:
+def traverse(tree: OracleOctree, origins, dirs, level: int | None = None, ties: list | None = None) -> list:
     """ray_trace_octree (traversal.py:207-247): lists from the virtual root
     to `level`; intermediate lists are unfiltered candidates, the last holds
-    hits with t_enter/t_exit."""
+    hits with t_enter/t_exit. With `ties` (a list), every level's (near-tie
+    decisions, decisions) is appended to it (count_near_ties)."""
     target = tree.max_level if level is None else level
     if not 0 <= target <= tree.max_level:
         raise OracleError(f"target level {target} outside 0..{tree.max_level}")
@@ -354,10 +386,10 @@ def traverse(tree: OracleOctree, origins, dirs, level: int | None = None) -> lis
     cur = PairList(-len(tree.virtual_codes), np.arange(n, dtype=np.int64), np.zeros(n, dtype=np.int64))
     lists = [cur]
     while cur.level < target:
-        D = decide(tree, origins, dirs, cur, False)
+        D = decide(tree, origins, dirs, cur, False, ties)
         cur = expand(tree, dirs, cur, D, exclusive_scan(D))
         lists.append(cur)
-    D = decide(tree, origins, dirs, cur, True)
+    D = decide(tree, origins, dirs, cur, True, ties)
     fin = compact(cur, D, exclusive_scan(D))
     if len(fin):
         lo, hi = voxel_boxes(tree, fin.level, fin.voxels)
@@ -366,6 +398,54 @@ def traverse(tree: OracleOctree, origins, dirs, level: int | None = None) -> lis
         fin.t_enter, fin.t_exit = np.zeros(0), np.zeros(0)
     lists[-1] = fin
     return lists
+
+
+def compare_final_lists(tree: OracleOctree, origins, dirs, got_rays, got_voxels, got_t_enter, got_t_exit,
+                        ray_ids, level: int) -> dict:
+    """Check a final (ray, voxel, t_enter, t_exit) list produced elsewhere
+    against traverse() on the rays `ray_ids` (indices into origins/dirs),
+    bit for bit and in order (ray_trace_octree's last list,
+    traversal.py:207-247). `got_*` may hold other rays too; only the
+    entries of `ray_ids` are compared. Returns pairs compared, the rays whose
+    sub-lists differ, how many of those have a near-tie slab decision
+    (count_near_ties) and the near-tie decisions of the whole sample."""
+    ray_ids = np.asarray(ray_ids, dtype=np.int64)
+    ties: list = []
+    fin = traverse(tree, origins[ray_ids], dirs[ray_ids], level, ties=ties)[-1]
+    got_rays = np.asarray(got_rays, dtype=np.int64)
+    pos = np.full(len(origins), -1, dtype=np.int64)
+    pos[ray_ids] = np.arange(len(ray_ids))
+    sel = pos[got_rays] >= 0
+    g_r = pos[got_rays[sel]]
+    g_v = np.asarray(got_voxels, dtype=np.int64)[sel]
+    g_a = np.asarray(got_t_enter, dtype=np.float64)[sel]
+    g_b = np.asarray(got_t_exit, dtype=np.float64)[sel]
+    o_r = np.asarray(fin.rays, dtype=np.int64)
+    bad = np.zeros(len(ray_ids), dtype=bool)
+    if len(g_r) != len(o_r) or not np.array_equal(g_r, o_r):
+        gc = np.bincount(g_r, minlength=len(ray_ids))
+        oc = np.bincount(o_r, minlength=len(ray_ids))
+        bad |= gc != oc
+    if not bad.any():
+        same = ((g_v == fin.voxels) & (g_a.view(np.int64) == fin.t_enter.view(np.int64))
+                & (g_b.view(np.int64) == fin.t_exit.view(np.int64)))
+        bad[o_r[~same]] = True
+    else:  # compare the rays whose counts agree entry by entry
+        for r in np.flatnonzero(~bad):
+            gm, om = g_r == r, o_r == r
+            if not (np.array_equal(g_v[gm], fin.voxels[om]) and np.array_equal(g_a[gm], fin.t_enter[om])
+                    and np.array_equal(g_b[gm], fin.t_exit[om])):
+                bad[r] = True
+    bad_ids = ray_ids[bad]
+    tie_bad = 0
+    for r in bad_ids[:1000]:
+        t1: list = []
+        traverse(tree, origins[r:r + 1], dirs[r:r + 1], level, ties=t1)
+        tie_bad += int(sum(a for a, _ in t1) > 0)
+    return {"rays": int(len(ray_ids)), "pairs": int(len(o_r)), "mismatched_rays": int(bad.sum()),
+            "mismatched_near_tie": tie_bad, "near_tie_decisions": int(sum(a for a, _ in ties)),
+            "decisions": int(sum(b for _, b in ties)), "tie_rel": TIE_REL,
+            "first_mismatch": int(bad_ids[0]) if len(bad_ids) else None}
 
 
 def segments(final: PairList, n_rays: int):

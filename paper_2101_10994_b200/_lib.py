@@ -167,6 +167,7 @@ _SIGS = {
     "ng_segments": (C.c_int, [P, P, C.c_int64, C.c_int64, P, P, P]),
     "ng_camera_rays": (C.c_int, [P, P, P]),
     "ng_render_workspace_bytes": (C.c_size_t, [C.c_int64, C.c_int64, C.c_int64]),
+    "ng_render_workspace_offsets": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, P, C.c_int32]),
     "ng_sphere_trace": (C.c_int, [P, P, P, P, C.c_int64, P, P, P, P, P, P, P, P, P, P]),
     "ng_normals": (C.c_int, [P, P, P, P, C.c_int64, P, P, P, P]),
     "ng_shade": (C.c_int, [P, P, C.c_int64, P, P, P]),

@@ -1528,6 +1528,18 @@ size_t ng_render_workspace_bytes(int64_t n_rays, int64_t pair_capacity, int64_t 
   return layout(n_rays, pair_capacity, hit_capacity).total;
 }
 
+int ng_render_workspace_offsets(int64_t n_rays, int64_t pair_capacity, int64_t hit_capacity, int64_t* out,
+                                int32_t n_out) {
+  if (!out || n_out < 0 || n_rays < 0) {
+    set_error("bad workspace-offset arguments");
+    return NG_ERR_STRUCTURAL;
+  }
+  const WsLayout L = layout(n_rays, pair_capacity, hit_capacity);
+  const int64_t v[4] = {(int64_t)L.hits, (int64_t)L.seg_start, (int64_t)L.seg_end, (int64_t)L.total};
+  for (int i = 0; i < n_out && i < 4; ++i) out[i] = v[i];
+  return NG_OK;
+}
+
 int ng_render_frame(const ng_octree* tree, const ng_field* fld, const ng_render_cfg* cfg, const ng_camera* cam,
                     const ng_frame* frame, const ng_workspace* ws, ng_frame_stats* d_stats, void* stream) {
   if (cam->band_rows < 1 || cam->band_stride < 1 || cam->band_offset < 0 || cam->band_offset >= cam->band_stride) {

@@ -585,6 +585,36 @@ class RenderSession:
         raw = self.stats_host.numpy().tobytes()
         return _lib.NgFrameStats.from_buffer_copy(raw[:ctypes.sizeof(_lib.NgFrameStats)])
 
+    def final_list(self, level: int, cells: bool = False):
+        """The last frame's final (ray, voxel, t_enter, t_exit) list as the
+        render path's traversal left it in the workspace, put in the
+        reference's order (ray_trace_octree's last list, traversal.py:207-247:
+        by ray, each ray's voxels front to back). Ray ids are local to this
+        session's rays (a band camera's rows in band order). With `cells`,
+        also the packed cell (x | y << 10 | z << 20) each entry carries on the
+        tile path. Read after a frame without shadow rays (the shadow pass
+        reuses the lists)."""
+        off = (ctypes.c_int64 * 4)()
+        _lib.check(_lib.lib().ng_render_workspace_offsets(self.n, self.pair_cap, self.hit_cap, off, 4),
+                   "ng_render_workspace_offsets")
+        torch.cuda.current_stream().synchronize()
+        b = self.ws_buf
+        s = b[off[1]:off[1] + 8 * self.n].view(torch.int64).cpu().numpy()
+        e = b[off[2]:off[2] + 8 * self.n].view(torch.int64).cpu().numpy()
+        lens = e - s
+        total = int(lens.sum())
+        used = int(e.max(initial=0))
+        raw = b[off[0]:off[0] + _lib.HIT_PAIR_BYTES * used].cpu().numpy()
+        rec = raw.view(np.dtype([("ray", "<i4"), ("voxel", "<i4"), ("t_enter", "<f8"), ("t_exit", "<f8")]))
+        rays = np.repeat(np.arange(self.n, dtype=np.int64), lens)
+        first = np.repeat(s - np.concatenate(([0], np.cumsum(lens)[:-1])), lens)
+        idx = first + np.arange(total, dtype=np.int64)
+        out = RayVoxelPairList(level, rays, rec["voxel"][idx].astype(np.int64), rec["t_enter"][idx].copy(),
+                               rec["t_exit"][idx].copy())
+        if cells:
+            return out, rec["ray"][idx].astype(np.int64)
+        return out
+
     def grow(self, st: _lib.NgFrameStats, n_levels: int) -> bool:
         """Grow capacities after an overflow; True when a rerun is needed."""
         if not st.overflow:
