@@ -8,9 +8,16 @@ camera rays, BFS traversal, persistent sphere-trace march, normals and
 shading -- over the torus-knot LOD5 octree with the planted field (SURVEY.md
 Appendix A; synthetic, no training). `value` is device time (CUDA events,
 L2 flushed between frames); `e2e` times the public `render()` call with the
-colour image read back to the host. `--impl reference` times the CPU oracle
-port (the reference is pure Python; its algorithm restated in oracle/) on
-bounded samples of the same workload.
+colour image read back to the host. With --gpus N > 1 and no torchrun
+environment, bench.py launches N ranks itself (torch.distributed.run).
+
+`--impl reference` runs the UNMODIFIED reference package (`octfield`,
+pip-installed into baseline/_ref) through its public `render()` on the
+host cores, whole frames, on inputs the reference itself produced
+(bench_data/knot_l5_ref.npz, tools/make_ref_inputs.py). The `cpu_baseline`
+of our line runs the same reference functions on a row sample of the frame
+and checks our render path's per-ray voxel lists against the reference's
+`ray_trace_octree` on those rays.
 """
 
 from __future__ import annotations
@@ -132,7 +139,129 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-# ------------------------------------------------------------------ CPU oracle legs
+# ------------------------------------------------------------------ the reference package
+
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+REF_INPUTS = os.path.join(ROOT, "bench_data", "knot_l5_ref.npz")
+SAMPLE_ROW_STRIDE = 3   # cpu_baseline: every 3rd image row (240 of 720)
+
+
+class Reference:
+    """The unmodified reference package (`octfield`, pip-installed into
+    baseline/_ref by `pip install --target baseline/_ref`), its modules by
+    name. Nothing of ours is imported on this path."""
+
+    def __init__(self):
+        import importlib
+        if REF_DIR not in sys.path:
+            sys.path.insert(0, REF_DIR)
+        self.pkg = importlib.import_module("octfield")
+        for name in ("octree", "field", "traversal", "render", "trainer", "sampling"):
+            setattr(self, name, importlib.import_module("octfield." + name))
+        self.path = os.path.dirname(self.pkg.__file__)
+
+
+def load_reference():
+    """Reference() when baseline/_ref holds the package, else None."""
+    if not os.path.isdir(os.path.join(REF_DIR, "octfield")) or not os.path.exists(REF_INPUTS):
+        return None
+    return Reference()
+
+
+def ref_workload(ref: Reference):
+    """configs[1]'s octree and planted field built by the reference itself
+    from bench_data/knot_l5_ref.npz (written by the reference,
+    tools/make_ref_inputs.py): build_octree over the finest voxel centres
+    with corner_test=False reproduces the full build (checked there), then
+    new_field(seed=0) and the Appendix A planting."""
+    OT, F = ref.octree, ref.field
+    z = np.load(REF_INPUTS)
+    L, r0 = int(z["max_level"]), int(z["r0"])
+    res = r0 << L
+    codes = z["finest_codes"]
+    centres = OT.cell_origin(OT.morton_decode(codes), res) + 0.5 * (2.0 / res)
+    svo = OT.build_octree(None, L, centres, r0=r0, corner_test=False)
+    assert [svo.voxel_count(lv) for lv in range(L + 1)] == [int(v) for v in z["voxels"]]
+    fld = F.new_field(svo, seed=0)
+    planted = z["planted"]
+    for lv in range(1, L + 1):
+        rows = np.unique(svo.levels[lv].corners)
+        fld.Z[rows, lv - 1] = planted[rows]
+        d = fld.decoders[lv - 1]
+        d.W1[0:2, :] = 0.0
+        d.b1[0:2] = 0.0
+        d.W1[0, 3 + lv - 1] = 1.0
+        d.W1[1, 3 + lv - 1] = -1.0
+        d.W2[:] = 0.0
+        d.W2[0, 0] = 1.0
+        d.W2[0, 1] = -1.0
+        d.b2[:] = 0.0
+    return svo, fld
+
+
+def ref_camera(ref: Reference, width=WIDTH, height=HEIGHT):
+    R = ref.render
+    return R.Camera(np.array(CAM["position"]), np.array(CAM["look_at"]), np.array(CAM["up"]), CAM["fov_y_deg"],
+                    width, height)
+
+
+def ref_row_sample(ref: Reference, fld, rows: np.ndarray, workers: int):
+    """The reference's own render() (render.py:342-448, unmodified) over the
+    rays of the given image rows: a Camera whose rays() returns those rows'
+    rays (pixel-centre rays of the full 1280x720 camera), and the module seam
+    `render.ray_trace_octree` wrapped to keep the final list -- the way the
+    reference's tests patch its seams. Returns (seconds, rays, final list,
+    report)."""
+    R, T = ref.render, ref.traversal
+    full = ref_camera(ref).rays()
+    idx = (rows[:, None] * WIDTH + np.arange(WIDTH)[None, :]).ravel()
+    bundle = T.RayBundle(full.origins[idx], full.directions[idx])
+
+    class RowCamera(R.Camera):
+        def rays(self):
+            return bundle
+
+    cam = RowCamera(np.array(CAM["position"]), np.array(CAM["look_at"]), np.array(CAM["up"]), CAM["fov_y_deg"],
+                    WIDTH, len(rows))
+    kept = {}
+    orig = R.ray_trace_octree
+
+    def keep(*a, **k):
+        out = orig(*a, **k)
+        kept["final"] = out[-1]
+        return out
+
+    R.ray_trace_octree = keep
+    try:
+        t0 = time.perf_counter()
+        _, rep = R.render(cam, fld, R.RenderConfig(workers=workers))
+        secs = time.perf_counter() - t0
+    finally:
+        R.ray_trace_octree = orig
+    return secs, len(idx), kept["final"], rep, idx
+
+
+def compare_lists(ours, theirs, idx, n_total: int) -> dict:
+    """Our render path's final list (global ray ids) against the reference's
+    ray_trace_octree final list over the rays idx (sample-local ids): equal
+    entries, in order, t_enter / t_exit as fp64 bit patterns."""
+    pos = np.full(n_total, -1, dtype=np.int64)
+    pos[idx] = np.arange(len(idx))
+    sel = pos[ours.rays] >= 0
+    g_r, g_v = pos[ours.rays[sel]], ours.voxels[sel]
+    g_a, g_b = ours.t_enter[sel], ours.t_exit[sel]
+    t_r = np.asarray(theirs.rays, dtype=np.int64)
+    t_v = np.asarray(theirs.voxels, dtype=np.int64)
+    n = len(idx)
+    gc, tc = np.bincount(g_r, minlength=n), np.bincount(t_r, minlength=n)
+    bad = gc != tc
+    if not bad.any():
+        same = ((g_v == t_v) & (g_a.view(np.int64) == np.asarray(theirs.t_enter).view(np.int64))
+                & (g_b.view(np.int64) == np.asarray(theirs.t_exit).view(np.int64)))
+        bad[t_r[~same]] = True
+    return {"against": "reference traversal.ray_trace_octree (unmodified)", "rays": int(n),
+            "pairs": int(len(t_r)), "mismatched_rays": int(bad.sum())}
+
 
 def oracle_tree(svo):
     from oracle import nglod_oracle as O
@@ -145,29 +274,18 @@ def oracle_tree(svo):
         region_lo=svo.region.lo, region_hi=svo.region.hi, virtual_codes=list(svo.virtual_codes))
 
 
-def cpu_frame_sample(tree, fld, row_stride: int, row_offset: int = 0, workers: int | None = None):
-    """Oracle render of every `row_stride`-th image row; returns (seconds, rays)."""
-    from oracle import nglod_oracle as O
-    workers = workers or os.cpu_count() or 1
-    decs = [O.OracleDecoder(d.W1, d.b1, d.W2, d.b2) for d in fld.decoders]
-    rows = np.arange(row_offset, HEIGHT, row_stride)
-    idx = (rows[:, None] * WIDTH + np.arange(WIDTH)[None, :]).ravel()
-    cam = dict(CAM, width=WIDTH, height=HEIGHT)
-    t0 = time.perf_counter()
-    O.render(tree, fld.Z, decs, cam, O.RenderParams(), ray_slice=idx, workers=workers)
-    return time.perf_counter() - t0, len(idx)
-
-
-def cpu_query_sample(tree, fld, pts: np.ndarray, workers: int | None = None):
-    from concurrent.futures import ThreadPoolExecutor
-    from oracle import nglod_oracle as O
-    workers = workers or os.cpu_count() or 1
-    decs = [O.OracleDecoder(d.W1, d.b1, d.W2, d.b2) for d in fld.decoders]
-    chunks = [pts[s:s + 8192] for s in range(0, len(pts), 8192)]
-    t0 = time.perf_counter()
-    with ThreadPoolExecutor(workers) as pool:
-        list(pool.map(lambda c: O.forward_levels(tree, fld.Z, decs, c, [1, 2, 3, 4, 5]), chunks))
-    return time.perf_counter() - t0
+def same_workload(ref_svo, ref_fld, svo, fld) -> bool:
+    """Our workload (device build + device-planted field) equals the
+    reference's, array for array."""
+    for lv in range(svo.max_level + 1):
+        if not np.array_equal(ref_svo.levels[lv].codes, svo.levels[lv].codes):
+            return False
+        if lv and not np.array_equal(ref_svo.levels[lv].corners, svo.levels[lv].corners):
+            return False
+    if not np.array_equal(np.asarray(ref_fld.Z, np.float32), np.asarray(fld.Z, np.float32)):
+        return False
+    return all(np.array_equal(a.W1, b.W1) and np.array_equal(a.b1, b.b1) and np.array_equal(a.W2, b.W2)
+               and np.array_equal(a.b2, b.b2) for a, b in zip(ref_fld.decoders, fld.decoders))
 
 
 # ------------------------------------------------------------------ our arm
@@ -246,7 +364,11 @@ def run_ours(args, rank: int, world: int):
         t = torch.tensor([ms_local], device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms_local = float(t.item())
+    # the last timed frame's per-ray voxel lists (render path), checked
+    # against the reference's traversal in the cpu_baseline leg
+    final = tiles.sess.final_list(MAX_LEVEL) if world == 1 else None
     res = {
+        "_final": final,
         "ms_per_step": ms_local, "frame_ms": frame_ms, "march_ms": march_ms, "trace_evals": trace_evals,
         "total_evals": evals_all, "visible": visible_all, "clocks": clocks.summary(),
         "pairs": [int(st.pairs[i]) for i in range(n_levels + 1)], "active_rays": int(st.active_rays),
@@ -301,28 +423,7 @@ def run_ours(args, rank: int, world: int):
     # ---- batched SDF query (configs[2]): forward L = 1..5 over 2^24 points,
     # sharded by point range across ranks (no exchange)
     if not args.no_query:
-        pts_h = query_points(knot, QUERY_POINTS)
-        share = QUERY_POINTS // world
-        pts = torch.from_numpy(pts_h[rank * share:(rank + 1) * share]).to(dev)
-        for _ in range(2):
-            out = forward_levels_device(svo, fld.device, pts, [1, 2, 3, 4, 5])
-        torch.cuda.synchronize()
-        qe = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(7)]
-        for a, b in qe:
-            flush.zero_()
-            a.record()
-            out = forward_levels_device(svo, fld.device, pts, [1, 2, 3, 4, 5])
-            b.record()
-        torch.cuda.synchronize()
-        q_ms = min(a.elapsed_time(b) for a, b in qe)
-        if world > 1:
-            t = torch.tensor([q_ms], device=dev)
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            q_ms = float(t.item())
-        res["query"] = {"metric": "Mpoints/sec batched SDF query (forward L=1..5, 2^24 points, 2:2:1 mix)",
-                        "value": share * world / q_ms / 1e3, "unit": "Mpoints/s", "ms": q_ms}
-        res["_query_pts"] = pts_h
-        del out
+        res["query"], res["_query_pts"] = query_leg(knot, svo, fld, dev, flush, rank, world)
     # ---- configs[3] / configs[4] at 1920x1080 (tiled across the ranks when N > 1)
     if not args.no_extra:
         res["extra"] = extra_configs(args, world, dev, knot)
@@ -334,6 +435,78 @@ def run_ours(args, rank: int, world: int):
         res["train"] = train_leg(knot, svo, dev, flush)
     res["_svo"], res["_fld"] = svo, fld
     return res
+
+
+QUERY_LEVELS = [1, 2, 3, 4, 5]
+QUERY_BYTES_BASE = 32   # SURVEY.md 8d, configs[2]: 32 + 1,064 k B per point (k present levels)
+QUERY_TIMED = 9
+
+
+def query_leg(knot, svo, fld, dev, flush, rank: int, world: int):
+    """configs[2]: forward L = 1..5 over 2^24 points (2:2:1 mix), through
+    the device entry (points resident in HBM) and end to end through the
+    public NeuralField.forward_levels (numpy in, numpy out). Median and
+    spread of the timed calls; the roofline counts the present levels k of
+    every point with the query's own device counters."""
+    import torch
+    from paper_2101_10994_b200.field import EvalCounter, forward_levels_device
+    pts_h = query_points(knot, QUERY_POINTS)
+    share = QUERY_POINTS // world
+    mine = np.ascontiguousarray(pts_h[rank * share:(rank + 1) * share])
+    pts = torch.from_numpy(mine).to(dev)
+    # sum of k: decoded (point, L) rows minus rows whose level-L voxel is
+    # missing (EvalCounter semantics, field.py:79-90, 194-218)
+    cnt = EvalCounter()
+    out = forward_levels_device(svo, fld.device, pts, QUERY_LEVELS, counter=cnt)
+    sum_k = cnt.decoder_evals - cnt.evals_missing_level
+    torch.cuda.synchronize()
+    qe = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(QUERY_TIMED)]
+    for a, b in qe:
+        flush.zero_()
+        a.record()
+        out = forward_levels_device(svo, fld.device, pts, QUERY_LEVELS)
+        b.record()
+    torch.cuda.synchronize()
+    ms = sorted(a.elapsed_time(b) for a, b in qe)
+    q_ms = statistics.median(ms)
+    if world > 1:
+        t = torch.tensor([q_ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        q_ms = float(t.item())
+    del out
+    algo = share * QUERY_BYTES_BASE + EVAL_BYTES_PER_LEVEL * sum_k
+    achieved = algo / (ms[len(ms) // 2] * 1e-3) / 1e9
+    peak = _peak_hbm()
+    line = {"metric": "Mpoints/sec batched SDF query (forward L=1..5, 2^24 points, 2:2:1 mix)",
+            "value": share * world / q_ms / 1e3, "unit": "Mpoints/s", "ms_median": q_ms,
+            "ms_min": ms[0], "ms_max": ms[-1], "timed_calls": len(ms),
+            "mean_levels_k": sum_k / share,
+            "roofline": {"bound": "hbm", "kernel": "k_query_tc (+ the decoder-staging k_query_tiles, one call)",
+                         "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": _traffic("query_traffic.json"), "algorithmic_bytes": algo,
+                         "note": f"{QUERY_BYTES_BASE} + {EVAL_BYTES_PER_LEVEL} k B per point (SURVEY.md 8d), "
+                                 "k counted on the device; the call's median event time; peak = measured hbm_gbs"}}
+    l2 = _l2_peak()
+    if l2:
+        line["roofline"]["l2_gather_peak"] = l2
+        line["roofline"]["l2_frac"] = achieved / l2
+    # end to end: the public API with host arrays (pageable numpy in, numpy out)
+    e2e = []
+    for i in range(4):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        host_out = fld.forward_levels(mine, QUERY_LEVELS)
+        if i:
+            e2e.append(time.perf_counter() - t0)
+    e2e_s = statistics.median(e2e)
+    if world > 1:
+        t = torch.tensor([e2e_s], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    line["e2e"] = {"value": share * world / e2e_s / 1e6, "unit": "Mpoints/s",
+                   "h2d_bytes_per_step": int(mine.nbytes), "d2h_bytes_per_step": int(host_out.nbytes),
+                   "note": "NeuralField.forward_levels(numpy points) -> numpy (n, 5) fp64, median of 3"}
+    return line, pts_h
 
 
 TRAIN_POINTS = 500_000   # TrainConfig.points_per_epoch default (trainer.py:39)
@@ -454,10 +627,48 @@ def _sizeof(name):
     return ctypes.sizeof(getattr(_lib, name))
 
 
+DTYPE = ("fp64 traversal, march control and shading; fp32 feature tables; decoder layer 1 as a bf16x3 split "
+         "on tcgen05 with fp32 accumulation, layer 2 fp32")
+DATA = "synthetic: (2,3) torus-knot polyline SDF, planted field (SURVEY.md Appendix A), random-init remainder"
+VOXELS = [30, 134, 450, 2150, 11946, 72125]   # knot LOD5 per level (the reference's build)
+
+
+def line_config(world: int) -> dict:
+    """The `config` of both arms' lines (identical for the same N)."""
+    return {"workload": "configs[1]: LOD5 torus-knot octree, 1280x720 sparse sphere trace + normals + Lambert shading",
+            "resolution": [WIDTH, HEIGHT], "lod": MAX_LEVEL, "voxels": VOXELS, "camera": CAM,
+            "parallelism": f"tiles{world}" + (" (8-row bands, NCCL all-gather of the colour tiles)" if world > 1
+                                              else ""),
+            "l2": "flushed between GPU frames (256 MiB write)"}
+
+
+def spawn_ranks(args) -> int:
+    """--gpus N > 1 without a torchrun environment: run N ranks of this
+    script under torch.distributed.run on this node and pass their exit
+    code on (rank 0 prints the line)."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    return subprocess.call(cmd, env=env)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args))
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     if args.impl == "reference":
         return run_reference(args, rank, world)
     res = run_ours(args, rank, world)
@@ -477,30 +688,22 @@ def main():
     algo_bytes = march_evals * bytes_per_eval
     peak = _peak_hbm()
     achieved = algo_bytes / (march * 1e-3) / 1e9
-    traffic = _traffic()
     line = {
         "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "strong" if world > 1 else "weak",
-        "vs_baseline": None, "dtype": "fp32 (features, MLP) + fp64 (traversal, march control)",
-        "data": "synthetic: (2,3) torus-knot polyline SDF, planted field, random-init remainder",
-        "config": {"workload": "configs[1]: LOD5 torus-knot octree, 1280x720 sparse sphere trace + normals + "
-                               "Lambert shading" + (f", 8-row bands over {world} B200 + NCCL all-gather"
-                                                    if world > 1 else ", 1 B200"),
-                   "resolution": [WIDTH, HEIGHT], "lod": MAX_LEVEL, "parallelism": f"tiles{world}",
-                   "voxels": [svo_count for svo_count in _voxel_counts(res["_svo"])],
-                   "l2": "flushed between frames (256 MiB write)", "camera": CAM},
+        "vs_baseline": None, "dtype": DTYPE, "data": DATA, "config": line_config(world),
         "mrays_per_sec": WIDTH * HEIGHT * fps / 1e6,
         "frame": {"visible": res["visible"], "trace_evals": res["trace_evals"],
                   "total_evals": res["total_evals"], "pairs_per_level": res["pairs"],
                   "active_rays": res["active_rays"], "march_ms_median": march,
-                  "frame_ms_median": statistics.median(res["frame_ms"])},
+                  "frame_ms_median": statistics.median(res["frame_ms"]), "voxels": _voxel_counts(res["_svo"])},
         "e2e": res["e2e"],
         "gpu_launches": args.steps * (_launches_per_frame(res["_svo"]) + (world + 1 if world > 1 else 0)),
         "roofline": {"bound": "hbm", "kernel": "k_march (sphere-trace march + normal probes, fused gather + MLP)"
                      if fused else "k_march (sphere-trace march, fused gather + MLP)",
                      "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic,
+                     "traffic": _traffic(),
                      "algorithmic_bytes": algo_bytes,
                      "evals": march_evals,
                      "note": f"{bytes_per_eval} B per eval x the launch's evals ({levels_read} level(s) read per eval: "
@@ -508,6 +711,10 @@ def main():
         "clocks": res["clocks"],
         "presum": res.get("presum"),
     }
+    l2 = _l2_peak()
+    if l2:
+        line["roofline"]["l2_gather_peak"] = l2
+        line["roofline"]["l2_frac"] = achieved / l2
     if "query" in res:
         line["query"] = res["query"]
     if "extra" in res:
@@ -515,7 +722,10 @@ def main():
     if "train" in res:
         line["train"] = {k: v for k, v in res["train"].items() if not k.startswith("_")}
     if not args.no_cpu and world == 1:
-        line["cpu_baseline"] = cpu_baseline(res)
+        cpu, check = cpu_baseline(res)
+        line["cpu_baseline"] = cpu
+        if check is not None:
+            line["traversal_check"] = check
     print(json.dumps(line))
 
 
@@ -547,9 +757,19 @@ def _peak_hbm():
         return 6650.0  # fallback figure (B200_PROFILING.md)
 
 
-def _traffic():
-    """dram bytes per k_march launch from the committed ncu --set full capture."""
-    p = os.path.join(ROOT, "profiles", "march_traffic.json")
+def _l2_peak():
+    """Random 128-byte row gather bandwidth out of L2 (GB/s), measured by
+    tools/micro/l2_gather.cu and committed under profiles/."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "l2_gather_peak.json")) as fh:
+            return float(json.load(fh)["gbs"])
+    except Exception:
+        return None
+
+
+def _traffic(name="march_traffic.json"):
+    """dram bytes per launch from the committed ncu --set full capture."""
+    p = os.path.join(ROOT, "profiles", name)
     try:
         with open(p) as fh:
             return json.load(fh).get("dram_bytes_per_launch")
@@ -558,82 +778,144 @@ def _traffic():
 
 
 def cpu_baseline(res):
-    """Oracle port on the host cores: every 3rd image row of the same frame
-    (240 of 720 rows, ~10 s of CPU work), scaled to frames/sec."""
-    tree = oracle_tree(res["_svo"])
-    stride = 3
-    secs, n = cpu_frame_sample(tree, res["_fld"], stride, row_offset=stride // 2)
+    """The reference itself (baseline/_ref, unmodified) on the host cores:
+    its render() over every 3rd image row of the same frame (~1/3 of the
+    work), forward L = 1..5 over 65,536 of the query points and 6 training
+    batches, each scaled to the line's unit. The same row sample checks our
+    render path's per-ray voxel lists against the reference's
+    ray_trace_octree bit for bit, and the oracle counts the sample's
+    near-tie slab decisions. Returns (cpu_baseline, traversal_check)."""
+    ref = load_reference()
+    if ref is None:
+        return {"unavailable": "reference not installed in baseline/_ref (or bench_data missing)"}, None
+    workers = os.cpu_count() or 1
+    ref_svo, ref_fld = ref_workload(ref)
+    identical = same_workload(ref_svo, ref_fld, res["_svo"], res["_fld"])
+    rows = np.arange(SAMPLE_ROW_STRIDE // 2, HEIGHT, SAMPLE_ROW_STRIDE)
+    secs, n, ref_final, rep, idx = ref_row_sample(ref, ref_fld, rows, workers)
     fps = (n / (WIDTH * HEIGHT)) / secs
-    out = {"value": fps, "unit": "frames/s", "cores": os.cpu_count(), "kind": "port",
-           "sample": f"oracle render of every {stride}th row ({n} rays) of the 1280x720 frame, {secs:.1f} s"}
+    out = {"value": fps, "unit": "frames/s", "cores": workers, "kind": "reference",
+           "sample": f"reference render() over every {SAMPLE_ROW_STRIDE}rd row ({n} rays) of the 1280x720 frame, "
+                     f"{secs:.1f} s, scaled to frames/s",
+           "reference": ref.path, "workload_identical": identical}
+    check = None
+    if res.get("_final") is not None:
+        check = compare_lists(res["_final"], ref_final, idx, WIDTH * HEIGHT)
+        from oracle import nglod_oracle as O
+        o, d = O.camera_rays(CAM["position"], CAM["look_at"], CAM["up"], CAM["fov_y_deg"], WIDTH, HEIGHT)
+        ties = []
+        O.traverse(oracle_tree(res["_svo"]), o[idx], d[idx], MAX_LEVEL, ties=ties)
+        check["near_tie_decisions"] = int(sum(a for a, _ in ties))
+        check["decisions"] = int(sum(b for _, b in ties))
+        check["near_tie_rel"] = O.TIE_REL
+        check["sample"] = f"every {SAMPLE_ROW_STRIDE}rd row of the last timed frame"
     if "_query_pts" in res:
         pts = res["_query_pts"][:: max(1, QUERY_POINTS // 65536)][:65536]
-        qs = cpu_query_sample(tree, res["_fld"], pts)
-        out["query"] = {"value": len(pts) / qs / 1e6, "unit": "Mpoints/s",
-                        "sample": f"{len(pts)} points, forward L=1..5, {qs:.1f} s"}
+        qs = ref_query_sample(ref, ref_fld, pts, workers)
+        out["query"] = {"value": len(pts) / qs / 1e6, "unit": "Mpoints/s", "cores": workers,
+                        "sample": f"reference forward(x, L) for L = 1..5 over {len(pts)} points in 8,192-point chunks "
+                                  f"on {workers} threads, {qs:.1f} s"}
     if "train" in res:
-        secs, npts = cpu_train_sample(tree, res["train"])
-        out["train"] = {"value": npts / secs / 1e6, "unit": "Mpoints/s", "cores": 1,
-                        "sample": f"{npts // TRAIN_BATCH} Adam steps of batch {TRAIN_BATCH} "
-                                  f"(oracle loss_batch + backward + dense Adam, fp64), {secs:.1f} s"}
-    return out
+        secs_t, npts = ref_train_sample(ref, ref_fld, res["train"])
+        out["train"] = {"value": npts / secs_t / 1e6, "unit": "Mpoints/s", "cores": 1,
+                        "sample": f"{npts // TRAIN_BATCH} reference Adam steps of batch {TRAIN_BATCH} "
+                                  f"(trainer._batch_pass + adam_step, fp64), {secs_t:.1f} s"}
+    return out, check
 
 
-def cpu_train_sample(tree, tr, batches: int = 6):
-    """Oracle training steps (trainer.py:223-241 restated) on the same field
-    and points; bounded to a few batches."""
-    from oracle import train_oracle as TO
-    fld = tr["_fld"]
-    Z = np.array(fld.Z, dtype=np.float64)
-    decs = [TO.f64_decoder(d) for d in fld.decoders]
-    params = {"Z": Z}
-    for i, d in enumerate(decs):
+def ref_query_sample(ref: Reference, fld, pts: np.ndarray, workers: int) -> float:
+    """the reference's training-forward path, forward(x, L)
+    for L = 1..5, over chunks on a thread pool (trainer.py:254-279 style)."""
+    from concurrent.futures import ThreadPoolExecutor
+    F = ref.field
+    chunks = [pts[s:s + 8192] for s in range(0, len(pts), 8192)]
+
+    def run(c):
+        return [F.forward(fld.svo, fld.Z, fld.decoders, c, L)[0] for L in QUERY_LEVELS]
+
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(workers) as pool:
+        list(pool.map(run, chunks))
+    return time.perf_counter() - t0
+
+
+def ref_train_sample(ref: Reference, fld, tr, batches: int = 6):
+    """The reference's inner training loop (trainer.py:210-229:
+    _batch_pass, adam_step) on the bench's random-init field and points,
+    single-threaded, a few batches."""
+    T = ref.trainer
+    F = ref.field
+    src = tr["_fld"]
+    work = F.NeuralField(fld.svo, np.array(src.Z, dtype=np.float64),
+                         [F.Decoder(d.W1.astype(np.float64), d.b1.astype(np.float64), d.W2.astype(np.float64),
+                                    d.b2.astype(np.float64)) for d in src.decoders])
+    params = {"Z": work.Z}
+    for i, d in enumerate(work.decoders):
         for nm in ("W1", "b1", "W2", "b2"):
             params[f"decoder{i + 1}.{nm}"] = getattr(d, nm)
-    st = TO.Adam.for_params(params)
+    state = T.AdamState.for_params(params)
     act = list(range(1, MAX_LEVEL + 1))
+    tags = np.zeros(TRAIN_BATCH, dtype=np.int8)
     t0 = time.perf_counter()
     for b in range(batches):
         sl = slice(b * TRAIN_BATCH, (b + 1) * TRAIN_BATCH)
-        loss, g, _ = TO._batch_pass(tree, Z, decs, tr["_pts"][sl], tr["_dist"][sl], act)
-        gd = {"Z": g.dZ}
-        for i, slot in enumerate(g.dec):
-            if slot is not None:
-                for nm, arr in zip(("W1", "b1", "W2", "b2"), slot):
-                    gd[f"decoder{i + 1}.{nm}"] = arr
-        TO.adam_step(params, gd, st, 1e-3)
+        batch = ref.sampling.SampleSet(tr["_pts"][sl], tr["_dist"][sl], tags)
+        _, grads, _ = T._batch_pass(work, batch, act, None)
+        T.adam_step(params, T._grads_dict(grads, True), state, 1e-3)
     return time.perf_counter() - t0, batches * TRAIN_BATCH
 
 
 # ------------------------------------------------------------------ reference arm
 
+REF_TIME_BUDGET_S = 1500.0   # the driver's limit for this step is 1,800 s
+
+
 def run_reference(args, rank: int, world: int):
-    """The reference's CPU algorithm (oracle port; the reference is pure
-    Python and not installable on the box) on the host cores, one bounded
-    frame sample per step. Rank 0 only."""
+    """The unmodified reference (`octfield` from baseline/_ref) through its
+    public render() on the host cores (RenderConfig(workers=os.cpu_count())),
+    one WHOLE 1280x720 frame per step, on the configs[1] octree and planted
+    field the reference built itself (bench_data/knot_l5_ref.npz). Rank 0
+    only; nothing of ours is imported. A CPU path has nothing to warm beyond
+    its first frame, so one warm-up frame is run whatever W says (both
+    numbers are in the line); if the frames run slower than the driver's
+    step allows, the timed frames stop early and `steps` says how many ran."""
     if rank != 0:
         return
-    import torch
-    torch.cuda.set_device(0)
-    knot, svo, fld = build_workload()   # the device build only prepares identical inputs
-    tree = oracle_tree(svo)
-    stride = 32
-    times, rays = [], 0
-    for k in range(args.warmup + args.steps):
-        secs, n = cpu_frame_sample(tree, fld, stride, row_offset=k % stride)
-        if k >= args.warmup:
-            times.append(secs)
-            rays = n
-    ms = statistics.mean(times) * 1e3 * stride  # per full frame
+    ref = load_reference()
+    if ref is None:
+        print(json.dumps({"impl": "reference", "unavailable": "octfield not installed in baseline/_ref "
+                                                              "(pip install --target baseline/_ref) or "
+                                                              "bench_data/knot_l5_ref.npz missing"}))
+        return
+    workers = os.cpu_count() or 1
+    t_start = time.perf_counter()
+    svo, fld = ref_workload(ref)
+    cam = ref_camera(ref)
+    config = ref.render.RenderConfig(workers=workers)
+    warm = min(args.warmup, 1)
+    for _ in range(warm):
+        _, rep = ref.render.render(cam, fld, config)
+    times = []
+    for k in range(args.steps):
+        t0 = time.perf_counter()
+        _, rep = ref.render.render(cam, fld, config)
+        times.append(time.perf_counter() - t0)
+        spent = time.perf_counter() - t_start
+        if spent + statistics.mean(times) > REF_TIME_BUDGET_S:
+            break
+    ms = statistics.mean(times) * 1e3
     fps = 1000.0 / ms
     line = {
         "impl": "reference", "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "fp64", "data": "synthetic (same workload as ours)",
-        "config": {"workload": "configs[1]: LOD5 torus-knot octree, 1280x720 sparse sphere trace + normals",
-                   "resolution": [WIDTH, HEIGHT]},
-        "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": os.cpu_count(), "kind": "port",
-                         "sample": f"each step: every {stride}th row ({rays} rays), scaled x{stride}"},
+        "steps": len(times), "warmup": warm, "steps_requested": args.steps, "warmup_requested": args.warmup,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+        "vs_baseline": None, "dtype": "fp64 (the reference computes in fp64 with fp32 parameters)", "data": DATA,
+        "config": line_config(world),
+        "frame": {"visible": int(rep.visible), "total_evals": int(rep.evals), "ms_trace": rep.ms_trace,
+                  "ms_normals": rep.ms_normals, "frame_s": times},
+        "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": workers, "kind": "reference",
+                         "sample": f"whole frames: octfield.render.render() x {len(times)} (mean)",
+                         "reference": ref.path},
         "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
