@@ -290,6 +290,18 @@ def same_workload(ref_svo, ref_fld, svo, fld) -> bool:
 
 # ------------------------------------------------------------------ our arm
 
+def max_over_ranks(x: float, dev) -> float:
+    """The largest per-rank value (device-timed durations: max over ranks).
+    gloo (NG_DIST_BACKEND=gloo, several ranks on one GPU) reduces CPU tensors."""
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(x)], dtype=torch.float64, device=dev)
+    if dist.get_backend() == "gloo":
+        t = t.cpu()
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def run_ours(args, rank: int, world: int):
     import torch
     import paper_2101_10994_b200 as ng
@@ -320,7 +332,7 @@ def run_ours(args, rank: int, world: int):
     def step():
         tiles.enqueue(cam, cfg)
         if world > 1:
-            return tiles.gather_color()
+            return tiles.gather_color(dst=0)
         return None
 
     # settle capacities (two-phase sizing) before timing
@@ -361,9 +373,7 @@ def run_ours(args, rank: int, world: int):
     trace_evals = int(tiles.frame["evals"].sum().item())
     ms_local = sum(frame_ms) / len(frame_ms)
     if world > 1:
-        t = torch.tensor([ms_local], device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms_local = float(t.item())
+        ms_local = max_over_ranks(ms_local, dev)
     # the last timed frame's per-ray voxel lists (render path), checked
     # against the reference's traversal in the cpu_baseline leg
     final = tiles.sess.final_list(MAX_LEVEL) if world == 1 else None
@@ -405,17 +415,19 @@ def run_ours(args, rank: int, world: int):
         d2h = int(img.nbytes)
     else:
         for _ in range(2):
-            tiles.render(cam, config)[0].cpu()
+            img_d = tiles.render(cam, config, dst=0)[0]
+            if img_d is not None:
+                img_d.cpu()
         torch.distributed.barrier()
         t0 = time.perf_counter()
+        img = np.zeros((HEIGHT, WIDTH, 3), np.uint8)
         for _ in range(e2e_steps):
-            img_d, _v, _e = tiles.render(cam, config)
-            img = img_d.cpu()
+            img_d, _v, _e = tiles.render(cam, config, dst=0)
+            if img_d is not None:
+                img = img_d.cpu().numpy()
         e2e_s = (time.perf_counter() - t0) / e2e_steps
-        t = torch.tensor([e2e_s], device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        e2e_s = float(t.item())
-        d2h = int(img.numel())
+        e2e_s = max_over_ranks(e2e_s, dev)
+        d2h = int(img.nbytes)
     res["e2e"] = {"value": 1.0 / e2e_s, "unit": "frames/s",
                   "h2d_bytes_per_step": _sizeof("NgCamera") + _sizeof("NgRenderCfg"),
                   "d2h_bytes_per_step": d2h + _sizeof("NgFrameStats")}
@@ -470,9 +482,7 @@ def query_leg(knot, svo, fld, dev, flush, rank: int, world: int):
     ms = sorted(a.elapsed_time(b) for a, b in qe)
     q_ms = statistics.median(ms)
     if world > 1:
-        t = torch.tensor([q_ms], device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        q_ms = float(t.item())
+        q_ms = max_over_ranks(q_ms, dev)
     del out
     algo = share * QUERY_BYTES_BASE + EVAL_BYTES_PER_LEVEL * sum_k
     achieved = algo / (ms[len(ms) // 2] * 1e-3) / 1e9
@@ -500,9 +510,7 @@ def query_leg(knot, svo, fld, dev, flush, rank: int, world: int):
             e2e.append(time.perf_counter() - t0)
     e2e_s = statistics.median(e2e)
     if world > 1:
-        t = torch.tensor([e2e_s], device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        e2e_s = float(t.item())
+        e2e_s = max_over_ranks(e2e_s, dev)
     line["e2e"] = {"value": share * world / e2e_s / 1e6, "unit": "Mpoints/s",
                    "h2d_bytes_per_step": int(mine.nbytes), "d2h_bytes_per_step": int(host_out.nbytes),
                    "note": "NeuralField.forward_levels(numpy points) -> numpy (n, 5) fp64, median of 3"}
@@ -577,14 +585,12 @@ def _time_tiled(tiles, cam, cfg, steps, flush, world):
         a.record()
         tiles.enqueue(cam, cfg)
         if world > 1:
-            tiles.gather_color()
+            tiles.gather_color(dst=0)
         b.record()
     torch.cuda.synchronize()
     ms = statistics.median(a.elapsed_time(b) for a, b in ev)
     if world > 1:
-        t = torch.tensor([ms], device=flush.device)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = max_over_ranks(ms, flush.device)
     return ms
 
 

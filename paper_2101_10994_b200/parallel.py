@@ -4,9 +4,11 @@ over NCCL (BASELINE.json configs[3] / [4]).
 One process per GPU. Rays are independent (render.py:389-394 already
 shards them), so each rank renders the bands b with b % world == rank
 (interleaved 8-row bands balance the costlier silhouette rows) with its own
-replica of the octree and field, then the colour (and optionally depth /
-hit) tiles are all-gathered with one NCCL collective and assembled. There
-is no other data-path exchange.
+replica of the octree and field, then the colour (and on request depth,
+hit and the other per-pixel outputs) tiles are gathered with one NCCL
+collective per output -- to one rank (`dst`) or to all -- and assembled.
+A frame's ranks also agree on reruns after a capacity overflow (a one-int
+all-reduce). There is no other data-path exchange.
 """
 
 from __future__ import annotations
@@ -45,15 +47,34 @@ def assemble(gathered: torch.Tensor, layout: list, height: int) -> torch.Tensor:
     return out
 
 
-def gather_tiles(local: torch.Tensor, layout: list, height: int, group=None) -> torch.Tensor:
-    """All-gather row-padded local tiles (rows, ...) and assemble the image."""
+def _staged(t: torch.Tensor, group) -> bool:
+    """gloo moves CPU tensors only: CUDA tiles are staged through the host."""
+    return t.is_cuda and dist.get_backend(group) == "gloo"
+
+
+def gather_tiles(local: torch.Tensor, layout: list, height: int, group=None, dst: int | None = None):
+    """Gather row-padded local tiles (rows, ...) and assemble the image.
+
+    dst=None all-gathers (every rank gets the image); dst=r gathers to rank
+    r only (the other ranks return None). One collective either way."""
     world = dist.get_world_size(group)
     max_rows = max(len(rows) for rows in layout)
     padded = local.new_zeros((max_rows,) + tuple(local.shape[1:]))
     padded[:local.shape[0]] = local
-    flat = local.new_empty((world * max_rows,) + tuple(local.shape[1:]))
-    dist.all_gather_into_tensor(flat, padded, group=group)
-    return assemble(flat.view((world, max_rows) + tuple(local.shape[1:])), layout, height)
+    dev = local.device
+    if _staged(local, group):
+        padded = padded.cpu()
+    tail = tuple(local.shape[1:])
+    if dst is None:
+        flat = padded.new_empty((world * max_rows,) + tail)
+        dist.all_gather_into_tensor(flat, padded, group=group)
+        return assemble(flat.view((world, max_rows) + tail), layout, height).to(dev)
+    rank = dist.get_rank(group)
+    parts = [padded.new_empty(padded.shape) for _ in range(world)] if rank == dst else None
+    dist.gather(padded, parts, dst=dst, group=group)
+    if rank != dst:
+        return None
+    return assemble(torch.stack(parts), layout, height).to(dev)
 
 
 class TiledRenderer:
@@ -82,32 +103,72 @@ class TiledRenderer:
                  ctypes.byref(cs), ctypes.byref(fs), ctypes.byref(self.sess.ws), ptr(self.sess.stats),
                  stream_ptr())
 
-    def gather_color(self) -> torch.Tensor:
-        """(height, width, 3) uint8 image on every rank."""
-        local = self.frame["color"][:self.local_rows * self.width].view(self.local_rows, self.width, 3)
-        if self.world == 1:
-            return local
-        return gather_tiles(local, self.layout, self.height, self.group)
+    # per-pixel outputs a frame can gather: name -> trailing shape
+    _FIELDS = {"color": (3,), "t": (), "hit": (), "normal": (3,), "normal_ok": (), "iterations": (), "evals": ()}
 
-    def render(self, camera: Camera, config: RenderConfig):
-        """One frame: returns (image (H, W, 3) uint8 device tensor, visible, evals)."""
+    def _local(self, name: str) -> torch.Tensor:
+        tail = self._FIELDS[name]
+        v = self.frame[name][:self.local_rows * self.width]
+        return v.reshape((self.local_rows, self.width) + tail)
+
+    def gather(self, fields=("color",), dst: int | None = None) -> dict:
+        """The frame's per-pixel outputs assembled to (height, width, ...)
+        device tensors: on every rank (dst=None, all-gather) or on rank dst
+        only (gather; the other ranks get an empty dict). One collective per
+        field (colour, plus depth / hit on request)."""
+        out = {}
+        for name in fields:
+            local = self._local(name)
+            if self.world == 1:
+                out[name] = local
+                continue
+            img = gather_tiles(local, self.layout, self.height, self.group, dst)
+            if img is not None:
+                out[name] = img
+        return out
+
+    def gather_color(self, dst: int | None = None):
+        """(height, width, 3) uint8 image (None on ranks other than dst)."""
+        return self.gather(("color",), dst).get("color")
+
+    def render(self, camera: Camera, config: RenderConfig, fields=None, dst: int | None = None):
+        """One frame across the ranks. Returns (image (H, W, 3) uint8 device
+        tensor, visible, evals), or with `fields` (names of per-pixel
+        outputs: color, t, hit, normal, ...) a dict of them in place of the
+        image; with dst, only rank dst receives the images."""
         lod = resolve_lod(camera, self.fld, config)
         cfg = resolve_config(self.fld, config, lod)
         n_levels = cfg.trace_level + self.fld.svo.device.n_virtual
+        self.reruns = 0
         while True:
             self.enqueue(camera, cfg)
             st = self.sess.read_stats()
+            # every rank reruns when any rank overflowed (the frame's ranks
+            # must agree on the number of collectives)
             again = torch.tensor([1 if st.overflow else 0], device=_lib.device())
             if self.world > 1:
-                dist.all_reduce(again, group=self.group)
+                if _staged(again, self.group):
+                    a = again.cpu()
+                    dist.all_reduce(a, group=self.group)
+                    again = a
+                else:
+                    dist.all_reduce(again, group=self.group)
             if st.overflow:
                 self.sess.grow(st, n_levels)
             if int(again.item()) == 0:
                 break
+            self.reruns += 1
         if st.counters.evals_missing_level or st.counters.nonfinite_inputs:
             raise OctfieldError("decoder ran outside the queried level's voxels or on non-finite input")
-        img = self.gather_color()
+        imgs = self.gather(fields or ("color",), dst)
         counts = torch.tensor([st.visible, st.counters.decoder_evals], dtype=torch.int64, device=_lib.device())
         if self.world > 1:
-            dist.all_reduce(counts, group=self.group)
-        return img, int(counts[0].item()), int(counts[1].item())
+            if _staged(counts, self.group):
+                c = counts.cpu()
+                dist.all_reduce(c, group=self.group)
+                counts = c
+            else:
+                dist.all_reduce(counts, group=self.group)
+        if fields is None:
+            imgs = imgs.get("color")
+        return imgs, int(counts[0].item()), int(counts[1].item())

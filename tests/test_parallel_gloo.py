@@ -43,6 +43,11 @@ def _body(rank, world, height, width, band_rows, q):
         local[:, :, 1] = torch.arange(width, dtype=torch.int32)[None, :]
         local[:, :, 2] = rank
         img = parallel.gather_tiles(local, layout, height)
+        # gathered to one rank only: the others get None
+        to1 = parallel.gather_tiles(local, layout, height, dst=1)
+        assert (to1 is None) == (rank != 1)
+        if to1 is not None:
+            assert torch.equal(to1, img)
         q.put((rank, img.numpy()))
 
 
