@@ -294,6 +294,21 @@ int ng_traverse_level(const ng_octree* tree, const ng_ray* rays, int32_t t, int3
 int ng_segments(const ng_hit_pair* hits, const int64_t* d_count, int64_t capacity,
                 int64_t n_rays, int64_t* seg_start, int64_t* seg_end, void* stream);
 
+/* ---- the field API in float64 (field.py:104-239, 337-357; render.py:155-171)
+ * Reference semantics computed in fp64 from the caller's parameters: Z is
+ * (C, m) fp64 row-major; decoders are fp64 blocks of dec_stride doubles in
+ * the training layout W1b[h][36] (x weights, m feature weights, b1 in
+ * column 35), W2[h], b2. Serves predict / blend / forward / query_field /
+ * trilinear / sum_features / decode (the hot paths use ng_query and
+ * ng_render_frame). */
+int ng_interp64(const ng_octree* tree, const double* Z, int32_t m, const double* pts, int64_t n,
+                int32_t level_lo, int32_t level_hi, double* z, uint8_t* mask, void* stream);
+int ng_decode64(const double* decoder, int32_t h, int32_t m, const double* x, const double* z, int64_t n,
+                double* out, int64_t* d_nonfinite, void* stream);
+int ng_query64(const ng_octree* tree, const double* Z, int32_t m, const double* decoders, int32_t h,
+               int32_t n_decoders, int32_t dec_stride, const ng_query_args* args, const double* pts, int64_t n,
+               double* out, ng_counters* d_counters, void* stream);
+
 /* ---- rendering (render.py:43-448) --------------------------------------- */
 int ng_camera_rays(const ng_camera* cam, ng_ray* rays, void* stream);
 size_t ng_render_workspace_bytes(int64_t n_rays, int64_t pair_capacity, int64_t hit_capacity);

@@ -156,6 +156,9 @@ _SIGS = {
     "ng_query": (C.c_int, [P, P, P, P, C.c_int64, P, P, P]),
     "ng_interp": (C.c_int, [P, P, P, C.c_int64, C.c_int32, C.c_int32, P, P, P]),
     "ng_empty_value": (C.c_int, [P, P, C.c_int64, P, P]),
+    "ng_interp64": (C.c_int, [P, P, C.c_int32, P, C.c_int64, C.c_int32, C.c_int32, P, P, P]),
+    "ng_decode64": (C.c_int, [P, C.c_int32, C.c_int32, P, P, C.c_int64, P, P, P]),
+    "ng_query64": (C.c_int, [P, P, C.c_int32, P, C.c_int32, C.c_int32, C.c_int32, P, P, C.c_int64, P, P, P]),
     "ng_decode": (C.c_int, [P, C.c_int32, C.c_int32, P, P, C.c_int64, P, P, P]),
     "ng_rays_from_arrays": (C.c_int, [P, P, C.c_int64, P, P]),
     "ng_level_scratch_bytes": (C.c_size_t, [C.c_int64]),

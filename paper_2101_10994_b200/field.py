@@ -112,6 +112,22 @@ def pack_decoders(decoders: list, m: int) -> np.ndarray:
     return buf
 
 
+def pack_decoders64(decoders: list, m: int, h: int) -> np.ndarray:
+    """fp64 decoder blocks, W1b[h][36] | W2[h] | b2 (the training layout)."""
+    stride = decoder_stride(h)
+    buf = np.zeros((len(decoders), stride), dtype=np.float64)
+    for i, d in enumerate(decoders):
+        W1 = np.asarray(d.W1, dtype=np.float64)
+        if W1.shape != (h, 3 + m):
+            raise StructuralError("decoders must share (h, 3 + m) shapes")
+        blk = buf[i, :h * _lib.W1_STRIDE].reshape(h, _lib.W1_STRIDE)
+        blk[:, :3 + m] = W1
+        blk[:, _lib.W1_STRIDE - 1] = np.asarray(d.b1, dtype=np.float64).ravel()
+        buf[i, h * _lib.W1_STRIDE:h * (_lib.W1_STRIDE + 1)] = np.asarray(d.W2, dtype=np.float64).ravel()
+        buf[i, h * (_lib.W1_STRIDE + 1)] = float(np.asarray(d.b2, dtype=np.float64).ravel()[0])
+    return buf
+
+
 class DeviceField:
     """Device copies of Z (padded to 32 channels) and the packed decoders."""
 
@@ -144,9 +160,25 @@ class DeviceField:
         self.struct = s
         self.presum = None
         self._presum_key = None
+        self._src = (Z, decoders)
+        self._exact = None
 
     def ref(self):
         return ctypes.byref(self.struct)
+
+    def exact(self):
+        """fp64 copies of the parameters as given, for the reference-semantics
+        API (csrc/exact.cu): Z (C, m) and the decoders in the training
+        layout. Made on first use."""
+        if self._exact is None:
+            Z, decoders = self._src
+            dev = self.Z.device
+            if isinstance(Z, torch.Tensor):
+                z64 = Z.to(device=dev, dtype=torch.float64).contiguous()
+            else:
+                z64 = torch.from_numpy(np.ascontiguousarray(np.asarray(Z), dtype=np.float64)).to(dev)
+            self._exact = (z64, torch.from_numpy(pack_decoders64(decoders, self.m, self.h)).to(dev))
+        return self._exact
 
     def ensure_presum(self, svo, level: int, out_mask: int) -> None:
         """Build (once per level / output set) the presummed feature tables
@@ -213,6 +245,25 @@ def _run_query(svo, dfield: DeviceField, pts_dev: torch.Tensor, out_levels=0, in
     return out
 
 
+def _run_exact(svo, dfield: DeviceField, pts_dev: torch.Tensor, out_levels=0, inside_level=-1, blend_base=0,
+               blend_alpha=0.0, ncols=1, counter: EvalCounter | None = None) -> torch.Tensor:
+    """predict / blend / query_field with the reference's fp64 semantics
+    (csrc/exact.cu, ng_query64)."""
+    n = pts_dev.shape[0]
+    out = torch.empty((n, ncols), dtype=torch.float64, device=pts_dev.device)
+    z64, d64 = dfield.exact()
+    args = _lib.NgQueryArgs(out_levels, inside_level, blend_base, 0, blend_alpha)
+    cnt = _Counters()
+    call("ng_query64", svo.device.ref(), ptr(z64), dfield.m, ptr(d64), dfield.h, dfield.n_decoders,
+         decoder_stride(dfield.h), ctypes.byref(args), ptr(pts_dev), n, ptr(out), cnt.ptr(), stream_ptr())
+    c = cnt.host()
+    if c[3]:
+        raise OctfieldError("non-finite decoder input")
+    if counter is not None:
+        counter.add(c)
+    return out
+
+
 def _dev_points(pts: np.ndarray) -> torch.Tensor:
     if len(pts) and (np.any(pts < DOMAIN_MIN) or np.any(pts > DOMAIN_MAX)):
         raise StructuralError("point outside the domain box")
@@ -233,15 +284,21 @@ def trilinear_weights(u: np.ndarray) -> np.ndarray:
 
 
 def _interp(svo, Z, pts, lo, hi, dfield=None):
-    df = dfield if dfield is not None else DeviceField(Z, [Decoder(np.zeros((1, 3 + np.shape(Z)[1]), np.float32),
-                                                                   np.zeros(1, np.float32), np.zeros((1, 1), np.float32),
-                                                                   np.zeros(1, np.float32))])
+    """Per-level interpolation summed over levels lo..hi, in fp64 from the
+    parameters as given (ng_interp64)."""
+    if dfield is not None:
+        z64 = dfield.exact()[0]
+    else:
+        z64 = torch.from_numpy(np.ascontiguousarray(np.asarray(Z), dtype=np.float64)).to(_lib.device())
+    m = int(z64.shape[1])
+    if m > _lib.FEAT_PAD:
+        raise StructuralError(f"feature dim {m} above the device limit {_lib.FEAT_PAD}")
     n = len(pts)
-    z = torch.zeros((n, df.m), dtype=torch.float64, device=_lib.device())
+    z = torch.zeros((n, m), dtype=torch.float64, device=_lib.device())
     mask = torch.zeros((n, hi - lo + 1), dtype=torch.uint8, device=_lib.device())
     if n:
         d = _dev_points(pts)
-        call("ng_interp", svo.device.ref(), df.ref(), ptr(d), n, lo, hi, ptr(z), ptr(mask), stream_ptr())
+        call("ng_interp64", svo.device.ref(), ptr(z64), m, ptr(d), n, lo, hi, ptr(z), ptr(mask), stream_ptr())
     return z.cpu().numpy(), mask.cpu().numpy().astype(bool)
 
 
@@ -263,7 +320,7 @@ def sum_features(svo, Z, x, L: int):
 
 
 def decode(decoder: Decoder, x, z):
-    """d = W2 relu(W1 [x, z] + b1) + b2 (field.py:172-182), fp32 on device."""
+    """d = W2 relu(W1 [x, z] + b1) + b2 (field.py:172-182), fp64 on device."""
     pts = np.atleast_2d(np.asarray(x, dtype=np.float64))
     z = np.atleast_2d(np.asarray(z, dtype=np.float64))
     inp = np.concatenate([pts, z], axis=1)
@@ -272,14 +329,16 @@ def decode(decoder: Decoder, x, z):
     m = z.shape[1]
     h = decoder.W1.shape[0]
     dev = _lib.device()
-    blk = torch.from_numpy(pack_decoders([decoder], m)[0]).to(dev)
+    if m > _lib.FEAT_PAD:
+        raise StructuralError(f"feature dim {m} above the device limit {_lib.FEAT_PAD}")
+    blk = torch.from_numpy(pack_decoders64([decoder], m, h)[0]).to(dev)
     n = len(pts)
     out = torch.empty(n, dtype=torch.float64, device=dev)
     bad = torch.zeros(1, dtype=torch.int64, device=dev)
     if n:
         dx = torch.from_numpy(np.ascontiguousarray(pts)).to(dev)
         dz = torch.from_numpy(np.ascontiguousarray(z)).to(dev)
-        call("ng_decode", ptr(blk), h, m, ptr(dx), ptr(dz), n, ptr(out), ptr(bad), stream_ptr())
+        call("ng_decode64", ptr(blk), h, m, ptr(dx), ptr(dz), n, ptr(out), ptr(bad), stream_ptr())
     if int(bad.item()):
         raise OctfieldError("non-finite decoder input")
     return out.cpu().numpy()
@@ -303,7 +362,7 @@ def predict(svo, Z, decoders, x, L: int, counter: EvalCounter | None = None, _df
     pts, single = _as_points(x)
     _check_level(L, len(decoders))
     df = _dfield if _dfield is not None else DeviceField(Z, decoders)
-    out = _run_query(svo, df, _dev_points(pts), out_levels=1 << (L - 1), counter=counter)[:, 0].cpu().numpy()
+    out = _run_exact(svo, df, _dev_points(pts), out_levels=1 << (L - 1), counter=counter)[:, 0].cpu().numpy()
     return float(out[0]) if single else out
 
 
@@ -318,7 +377,7 @@ def blend(svo, Z, decoders, x, L_tilde: float, counter: EvalCounter | None = Non
         return predict(svo, Z, decoders, x, base, counter, _dfield)
     pts, single = _as_points(x)
     df = _dfield if _dfield is not None else DeviceField(Z, decoders)
-    out = _run_query(svo, df, _dev_points(pts), blend_base=base, blend_alpha=alpha, counter=counter)
+    out = _run_exact(svo, df, _dev_points(pts), blend_base=base, blend_alpha=alpha, counter=counter)
     out = out[:, 0].cpu().numpy()
     return float(out[0]) if single else out
 
@@ -381,7 +440,7 @@ def forward(svo, Z, decoders, x, L: int, _dfield=None) -> tuple:
     pts = np.atleast_2d(np.asarray(x, dtype=np.float64))
     _check_level(L, len(decoders))
     df = _dfield if _dfield is not None else DeviceField(Z, decoders)
-    out = _run_query(svo, df, _dev_points(pts), out_levels=1 << (L - 1))[:, 0].cpu().numpy()
+    out = _run_exact(svo, df, _dev_points(pts), out_levels=1 << (L - 1))[:, 0].cpu().numpy()
     return out, ForwardCache(svo, Z, decoders, L, pts, out)
 
 

@@ -178,12 +178,15 @@ class SparseVoxelOctree:
     corner_count: int
     corner_offsets: np.ndarray
     region: Aabb
-    virtual_levels: list = field(default_factory=list)   # OctreeLevel-like (codes only)
+    virtual_codes: list = field(default_factory=list)
     device: DeviceOctree | None = None
+    virtual_levels: list = field(default_factory=list, repr=False)   # device-backed virtual levels
 
-    @property
-    def virtual_codes(self) -> list:
-        return [lv.codes for lv in self.virtual_levels]
+    def __post_init__(self):
+        # the device build passes device-backed virtual levels; a caller may
+        # pass plain code arrays (the reference's constructor, octree.py:107-118)
+        if self.virtual_levels and not self.virtual_codes:
+            self.virtual_codes = [lv.codes for lv in self.virtual_levels]  # <= 64 codes each
 
     def resolution(self, level: int) -> int:
         return self.r0 << level
@@ -195,7 +198,9 @@ class SparseVoxelOctree:
         return 0.5 * np.sqrt(3.0) * self.voxel_edge(level)
 
     def voxel_count(self, level: int) -> int:
-        return int(self.levels[level].d_codes.numel())
+        lv = self.levels[level]
+        d = getattr(lv, "d_codes", None)
+        return int(d.numel()) if d is not None else len(lv.codes)
 
     def traversal_codes(self) -> list:
         return self.virtual_codes + [lv.codes for lv in self.levels]

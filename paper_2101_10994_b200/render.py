@@ -22,7 +22,7 @@ import torch
 from . import _lib
 from ._lib import call, ptr, stream_ptr
 from .errors import ConfigError, OctfieldError, StructuralError
-from .field import EvalCounter, NeuralField, _Counters, _dev_points, _run_query
+from .field import EvalCounter, NeuralField, _Counters, _dev_points, _run_exact
 from .octree import DOMAIN_MAX, DOMAIN_MIN
 from .traversal import RayBundle, RayVoxelPairList, device_rays, ray_segments
 
@@ -303,10 +303,10 @@ def query_field(fld: NeuralField, pts: np.ndarray, lod: float, counter: EvalCoun
         raise StructuralError(f"blend level {lod} above max {len(fld.decoders)}")
     base, alpha = _lod_split(lod)
     if alpha == 0.0:
-        out = _run_query(fld.svo, fld.device, _dev_points(p), out_levels=1 << (base - 1), inside_level=lvl,
+        out = _run_exact(fld.svo, fld.device, _dev_points(p), out_levels=1 << (base - 1), inside_level=lvl,
                          counter=counter)
     else:
-        out = _run_query(fld.svo, fld.device, _dev_points(p), inside_level=lvl, blend_base=base, blend_alpha=alpha,
+        out = _run_exact(fld.svo, fld.device, _dev_points(p), inside_level=lvl, blend_base=base, blend_alpha=alpha,
                          counter=counter)
     return out[:, 0].cpu().numpy()
 

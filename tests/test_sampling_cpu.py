@@ -23,3 +23,17 @@ def test_split_counts_and_dump_roundtrip(tmp_path):
     back = S.load_samples(tmp_path / "s.bin")
     np.testing.assert_allclose(back.points, ss.points.astype(np.float32))
     assert back.scheme_tags[0] == S.SCHEME_UNIFORM
+
+
+def test_mesh_surface_sampler_matches_reference(reference):
+    """sample_surface_mesh (sampling.py:50-63) on a reference TriangleMesh:
+    the same points, bit for bit (same generator call order)."""
+    from paper_2101_10994_b200.sampling import sample_surface_mesh
+    sampling = __import__("octfield.sampling", fromlist=["x"])
+    geometry = __import__("octfield.geometry", fromlist=["x"])
+    v = np.array([[0, 0, 0], [0.5, 0, 0], [0, 0.5, 0], [0, 0, 0.5]], dtype=np.float64)
+    f = np.array([[0, 2, 1], [0, 1, 3], [0, 3, 2], [1, 2, 3]])
+    mesh = geometry.TriangleMesh(v, f)
+    a = sampling.sample_surface_mesh(mesh, 4096, 11)
+    b = sample_surface_mesh(mesh, 4096, 11)
+    assert np.array_equal(a, b)
