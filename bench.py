@@ -388,14 +388,14 @@ def run_ours(args, rank: int, world: int):
     dfield = fld.device
     if dfield.presum is not None:
         key = dfield._presum_key
-        dfield._presum_key = None
         p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         p0.record()
-        dfield.ensure_presum(svo, *key)
+        tables, _owner = dfield.build_presum(svo, *key)
         p1.record()
         torch.cuda.synchronize()
         res["presum"] = {"level": key[0], "out_mask": key[1], "build_ms": p0.elapsed_time(p1),
-                         "table_bytes": int(dfield.presum.numel() * 4)}
+                         "table_bytes": int(tables.numel() * 4)}
+        del tables, _owner
 
     # ---- end to end through the public API: host camera in, colour image out
     e2e_steps = max(3, min(args.steps, 20))

@@ -9,6 +9,12 @@
 #include "sdf.cuh"
 
 #include <stdarg.h>
+#include <stdlib.h>
+
+#include <algorithm>
+#include <atomic>
+#include <map>
+#include <mutex>
 #include <stdio.h>
 #include <string.h>
 
@@ -31,15 +37,44 @@ int cuda_status(cudaError_t e, const char* where) {
 
 int launch_status(const char* where) { return cuda_status(cudaGetLastError(), where); }
 
+int current_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev;
+}
+
 int sm_count() {
-  static int cached = 0;
-  if (!cached) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&cached, cudaDevAttrMultiProcessorCount, dev);
-    if (cached <= 0) cached = 148;
+  constexpr int kMaxDev = 64;
+  static std::atomic<int> cached[kMaxDev];
+  const int dev = current_device();
+  const int slot = (dev >= 0 && dev < kMaxDev) ? dev : 0;
+  int v = cached[slot].load(std::memory_order_relaxed);
+  if (v <= 0) {
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    if (v <= 0) v = 148;
+    cached[slot].store(v, std::memory_order_relaxed);
   }
-  return cached;
+  return v;
+}
+
+int env_int(const char* name, int def) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : def;
+}
+
+int set_smem_limit(const void* kernel, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, size_t> have;
+  const int dev = current_device();
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& h = have[{dev, kernel}];
+  if (bytes > h) {
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)std::max<size_t>(bytes, 48 * 1024));
+    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute");
+    h = bytes;
+  }
+  return NG_OK;
 }
 
 // ------------------------------------------------------------------ kernels

@@ -15,7 +15,15 @@ constexpr unsigned FULL = 0xffffffffu;
 void set_error(const char* fmt, ...);
 int cuda_status(cudaError_t e, const char* where);
 int launch_status(const char* where);
-int sm_count();
+int sm_count();                 // of the current device (cached per device)
+int current_device();
+// environment knob read once per process (call inside a function-local
+// `static const` initialiser, which C++ makes thread-safe)
+int env_int(const char* name, int def);
+// raise a kernel's dynamic shared-memory limit on the CURRENT device
+// (cudaFuncSetAttribute is per device); cached per (device, kernel),
+// thread-safe
+int set_smem_limit(const void* kernel, size_t bytes);
 
 #define NG_CHECK_LAUNCH(name)                         \
   do {                                                \

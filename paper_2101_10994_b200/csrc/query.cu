@@ -187,24 +187,16 @@ int run_query(const ng_octree& tree, const ng_field& f, const ng_query_args& a, 
   const int dec_first = __builtin_ctz((unsigned)out_mask) + 1;
   const int dec_last = G;
   // tensor-core decoder (query_tc.cu) unless NG_DECODER=simt
-  static int use_tc = -1;
-  if (use_tc < 0) {
+  static const bool use_tc = [] {
     const char* e = getenv("NG_DECODER");
-    use_tc = (e && strcmp(e, "simt") == 0) ? 0 : 1;
-  }
+    return !(e && strcmp(e, "simt") == 0);
+  }();
   if (use_tc) {
     int r = run_query_tc(tree, f, a, G, out_mask, dec_first, dec_last, ncols, pts, n, out, counters, s);
     if (r != NG_ERR_CAPACITY) return r;
   }
   const size_t smem = query_smem_bytes(dec_last - dec_first + 1, f.dec_stride, Q_NW);
-  static size_t configured = 0;
-  if (smem > configured) {
-    int r = cuda_status(cudaFuncSetAttribute(k_query<Q_NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)std::max<size_t>(smem, 48 * 1024)),
-                        "ng_query smem attribute");
-    if (r) return r;
-    configured = smem;
-  }
+  if (int r = set_smem_limit((const void*)k_query<Q_NW>, smem)) return r;
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_query<Q_NW>, Q_NW * 32, smem);
   if (per_sm < 1) per_sm = 1;

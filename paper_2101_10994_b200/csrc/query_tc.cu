@@ -139,13 +139,7 @@ int run_query_tc(const ng_octree& tree, const ng_field& f, const ng_query_args& 
   if (f.h != tc::N) return NG_ERR_CAPACITY;
   const size_t smem = query_tc_smem_bytes(dec_last - dec_first + 1);
   if (smem > 227 * 1024) return NG_ERR_CAPACITY;
-  static size_t configured = 0;
-  if (smem > configured) {
-    int r = cuda_status(cudaFuncSetAttribute(k_query_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
-                        "k_query_tc smem attribute");
-    if (r) return r;
-    configured = smem;
-  }
+  if (int r = set_smem_limit((const void*)k_query_tc, smem)) return r;
   const int64_t tiles = (n + 127) / 128;
   const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((tiles + TQ_GROUPS - 1) / TQ_GROUPS, sm_count()));
   const int ndec = dec_last - dec_first + 1;

@@ -38,11 +38,7 @@ int tile_traverse_entry_bytes();
 // NG_TILE_TRAVERSE=0 selects the level-by-level traversal launches
 // (k_traverse_hits) instead of the warp-per-tile kernel.
 static bool use_tile_traverse(int target) {
-  static int on = -1;
-  if (on < 0) {
-    const char* e = getenv("NG_TILE_TRAVERSE");
-    on = (e && e[0] == '0') ? 0 : 1;
-  }
+  static const bool on = env_int("NG_TILE_TRAVERSE", 1) != 0;
   return on && target >= 1 && target <= 9;  // list cells: <= 512 per axis
 }
 
@@ -1045,16 +1041,8 @@ static LodPlan plan_lod(const ng_render_cfg& cfg) {
 
 template <class K>
 static int prep_kernel(K kernel, size_t smem, int nt, int& per_sm) {
-  // dynamic shared memory limit per kernel function (instances of one
-  // template share a pointer type, so the record is keyed by address)
-  static std::unordered_map<const void*, size_t> configured;
-  size_t& have = configured[(const void*)kernel];
-  if (smem > have) {
-    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)std::max<size_t>(smem, 48 * 1024));
-    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute");
-    have = smem;
-  }
+  // dynamic shared memory limit per (device, kernel function)
+  if (int r = set_smem_limit((const void*)kernel, smem)) return r;
   per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, nt, smem);
   if (per_sm < 1) per_sm = 1;
@@ -1063,21 +1051,19 @@ static int prep_kernel(K kernel, size_t smem, int nt, int& per_sm) {
 
 
 static bool use_tc_decoder(const ng_field& f) {
-  static int env = -1;
-  if (env < 0) {
+  static const bool env = [] {
     const char* e = getenv("NG_DECODER");
-    env = (e && strcmp(e, "simt") == 0) ? 0 : 1;
-  }
+    return !(e && strcmp(e, "simt") == 0);
+  }();
   return env && f.h == tc::N;
 }
 
 static int tc_groups() {
-  static int g = -1;  // NG_TC_GROUPS: 4-warp tile groups per CTA (experiment knob; default 3)
-  if (g < 0) {
-    const char* e = getenv("NG_TC_GROUPS");
-    g = e ? atoi(e) : 3;
-    if (g < 1 || g > 4) g = 3;
-  }
+  // NG_TC_GROUPS: 4-warp tile groups per CTA (experiment knob; default 3)
+  static const int g = [] {
+    const int v = env_int("NG_TC_GROUPS", 3);
+    return (v < 1 || v > 4) ? 3 : v;
+  }();
   return g;
 }
 
@@ -1110,11 +1096,7 @@ static int launch_eval_kernel(KS ksimt, K1 k1, K2 k2, K3 k3, K4 k4, const ng_fie
   } else {
     const size_t smem = (size_t)ndec * f.dec_stride * 4 + R_NW * sizeof(WarpScratch);
     if ((r = prep_kernel(ksimt, smem, R_NW * 32, per_sm))) return r;
-    static int cap = -1;  // NG_MARCH_CTAS_PER_SM: experiment knob for the persistent grid
-    if (cap < 0) {
-      const char* e = getenv("NG_MARCH_CTAS_PER_SM");
-      cap = e ? atoi(e) : 0;
-    }
+    static const int cap = env_int("NG_MARCH_CTAS_PER_SM", 0);  // experiment knob for the persistent grid
     if (cap > 0 && cap < per_sm) per_sm = cap;
     int64_t grid = (int64_t)sm_count() * per_sm;
     if (cap_by_work) grid = std::max<int64_t>(1, std::min<int64_t>(grid, (max_units + 32 * R_NW - 1) / (32 * R_NW)));
@@ -1131,11 +1113,7 @@ static bool presum_applies(const ng_field& f, int G, int out_mask, int trace_lev
 }
 
 static int launch_march(const ng_octree& tree, const ng_field& f, MarchArgs& A, cudaStream_t s) {
-  static int cap_env = -1;
-  if (cap_env < 0) {
-    const char* e = getenv("NG_MARCH_CAP");
-    cap_env = e ? atoi(e) : 32;
-  }
+  static const int cap_env = env_int("NG_MARCH_CAP", 32);
   A.lane_cap = cap_env;
   if (presum_applies(f, A.G, A.out_mask, A.cfg.trace_level))
     return launch_eval_kernel(k_march<R_NW, false, true>, k_march<4, true, true>, k_march<8, true, true>,
@@ -1175,11 +1153,7 @@ static size_t al(size_t x) { return (x + 255) & ~size_t(255); }
 // list entries per warp the tile traversal's arena holds at least
 // (NG_TILE_ARENA_MIN overrides: a test knob for the overflow / rerun path)
 static int64_t tile_arena_min() {
-  static int64_t v = -1;
-  if (v < 0) {
-    const char* e = getenv("NG_TILE_ARENA_MIN");
-    v = e ? std::max(0, atoi(e)) : 2048;
-  }
+  static const int64_t v = std::max(0, env_int("NG_TILE_ARENA_MIN", 2048));
   return v;
 }
 
@@ -1217,14 +1191,15 @@ static WsLayout layout(int64_t n, int64_t pair_cap, int64_t hit_cap) {
 
 // NG_MARCH_PROFILE=1: per-group march statistics (ng_march_profile).
 static unsigned long long* g_prof = nullptr;
+// (a debugging aid of one device: the buffer lives on the device current at
+// the first frame)
 static unsigned long long* march_profile_buffer() {
-  static int on = -1;
-  if (on < 0) {
-    const char* e = getenv("NG_MARCH_PROFILE");
-    on = (e && e[0] == '1') ? 1 : 0;
-    if (on && cudaMalloc((void**)&g_prof, 8 * 8 * 4096) != cudaSuccess) on = 0;
-    if (on) cudaMemset(g_prof, 0, 8 * 8 * 4096);
-  }
+  static const bool on = [] {
+    if (env_int("NG_MARCH_PROFILE", 0) != 1) return false;
+    if (cudaMalloc((void**)&g_prof, 8 * 8 * 4096) != cudaSuccess) return false;
+    cudaMemset(g_prof, 0, 8 * 8 * 4096);
+    return true;
+  }();
   return on ? g_prof : nullptr;
 }
 
@@ -1424,11 +1399,7 @@ static int render_common(const ng_octree& tree, const ng_field& f, const ng_rend
   A.counters = &st->counters;
   // normals: probe items inside the march (default), or the k_normals pass
   // after it (NG_FUSED_PROBES=0)
-  static int fused_env = -1;
-  if (fused_env < 0) {
-    const char* e = getenv("NG_FUSED_PROBES");
-    fused_env = (e && e[0] == '0') ? 0 : 1;
-  }
+  static const int fused_env = env_int("NG_FUSED_PROBES", 1) != 0;
   const bool fused = do_normals && fused_env;
   A.probes = fused ? 1 : 0;
   A.probe_next = ctr + 5;

@@ -746,26 +746,20 @@ static int64_t g_phase_batches = 0;
 
 // parts: 1 = counters reset + point location, 2 = the rest of the step
 static int launch_batch(const ng_octree* tree, TrainArgs& A, cudaStream_t s, int parts = 3) {
-  static int ev_env = -1;
+  // (a single-threaded debugging aid: the events belong to the device
+  // current at the first batch)
   static cudaEvent_t ev[8];
-  if (ev_env < 0) {
-    const char* e = getenv("NG_TRAIN_EVENTS");
-    ev_env = (e && e[0] == '1') ? 1 : 0;
-    if (ev_env)
-      for (int k = 0; k < 8; ++k) cudaEventCreate(&ev[k]);
-  }
+  static const bool ev_env = [] {
+    if (env_int("NG_TRAIN_EVENTS", 0) != 1) return false;
+    for (int k = 0; k < 8; ++k) cudaEventCreate(&ev[k]);
+    return true;
+  }();
   int nev = 0;
   auto mark = [&]() {
     if (ev_env) cudaEventRecord(ev[nev++], s);
   };
   int r = 0;
-  static bool attr = false;
-  if (!attr) {
-    if ((r = cuda_status(cudaFuncSetAttribute(k_train_dec, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              (int)dec_smem_bytes()), "train smem attr")))
-      return r;
-    attr = true;
-  }
+  if ((r = set_smem_limit((const void*)k_train_dec, dec_smem_bytes()))) return r;  // per device
   const int cap_blocks = 4 * sm_count();
   const int row_blocks = tr_grid(A.max_rows * 32, 256) < cap_blocks ? tr_grid(A.max_rows * 32, 256) : cap_blocks;
   if (parts & 1) {
@@ -930,6 +924,34 @@ int ng_train_flush(const ng_train_params* P, int64_t step, const double* adam_c,
   return NG_OK;
 }
 
+// RAII holder of ng_train_epoch's side stream: on destruction (every return
+// path) the caller's stream waits for the side stream's queued work, then the
+// stream and events are released (the driver frees them once that work ends).
+struct SideStream {
+  cudaStream_t caller;
+  cudaStream_t side = nullptr;
+  cudaEvent_t e_loc[2] = {nullptr, nullptr}, e_done[2] = {nullptr, nullptr}, e_start = nullptr, e_join = nullptr;
+  explicit SideStream(cudaStream_t s) : caller(s) {}
+  int create() {
+    int r = cuda_status(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking), "train side stream");
+    for (int k = 0; k < 2 && !r; ++k) {
+      r = cuda_status(cudaEventCreateWithFlags(&e_loc[k], cudaEventDisableTiming), "train event");
+      if (!r) r = cuda_status(cudaEventCreateWithFlags(&e_done[k], cudaEventDisableTiming), "train event");
+    }
+    if (!r) r = cuda_status(cudaEventCreateWithFlags(&e_start, cudaEventDisableTiming), "train event");
+    if (!r) r = cuda_status(cudaEventCreateWithFlags(&e_join, cudaEventDisableTiming), "train event");
+    if (!r) r = cuda_status(cudaEventRecord(e_start, caller), "train record");
+    if (!r) r = cuda_status(cudaStreamWaitEvent(side, e_start, 0), "train wait");
+    return r;
+  }
+  ~SideStream() {
+    if (side && e_join && cudaEventRecord(e_join, side) == cudaSuccess) cudaStreamWaitEvent(caller, e_join, 0);
+    for (cudaEvent_t e : {e_loc[0], e_loc[1], e_done[0], e_done[1], e_start, e_join})
+      if (e) cudaEventDestroy(e);
+    if (side) cudaStreamDestroy(side);
+  }
+};
+
 int ng_train_epoch(const ng_octree* tree, const ng_train_params* P, const double* pts, const double* dist,
                    int64_t n, int64_t batch_size, int32_t active_mask, int32_t update_decoders, double lr,
                    int64_t step0, const double* adam_c, int32_t flush_every, void* ws, size_t ws_bytes,
@@ -943,12 +965,7 @@ int ng_train_epoch(const ng_octree* tree, const ng_train_params* P, const double
   // so it runs on a side stream in the other workspace buffer while batch
   // b's step runs (a buffer is reused once the step two batches back has
   // left its corner counters at zero). NG_TRAIN_OVERLAP=0: one stream.
-  static int overlap_env = -1;
-  if (overlap_env < 0) {
-    const char* e = getenv("NG_TRAIN_OVERLAP");
-    const char* ev = getenv("NG_TRAIN_EVENTS");
-    overlap_env = (e && e[0] == '0') || (ev && ev[0] == '1') ? 0 : 1;
-  }
+  static const int overlap_env = (env_int("NG_TRAIN_OVERLAP", 1) != 0 && env_int("NG_TRAIN_EVENTS", 0) != 1) ? 1 : 0;
   const size_t half = ws_bytes / 2;
   const int64_t nb = (n + batch_size - 1) / batch_size;
   auto args_for = [&](int64_t bi, TrainArgs& A) -> int {
@@ -976,20 +993,17 @@ int ng_train_epoch(const ng_octree* tree, const ng_train_params* P, const double
     A.status = status;
     return NG_OK;
   };
-  static cudaStream_t side = nullptr;
-  static cudaEvent_t e_loc[2], e_done[2], e_start;
-  if (overlap_env && !side) {
-    cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking);
-    for (int k = 0; k < 2; ++k) {
-      cudaEventCreateWithFlags(&e_loc[k], cudaEventDisableTiming);
-      cudaEventCreateWithFlags(&e_done[k], cudaEventDisableTiming);
-    }
-    cudaEventCreateWithFlags(&e_start, cudaEventDisableTiming);
-  }
+  // The side stream and its events belong to this call (on the caller's
+  // current device, so concurrent epochs on other streams or devices never
+  // share them); created per epoch (~10 us against ~100 ms) and released
+  // when the call returns, by which point -- on every exit path -- the
+  // caller's stream has been made to wait for everything queued on it.
+  SideStream ss(s);
+  cudaStream_t side = nullptr;
+  cudaEvent_t *e_loc = ss.e_loc, *e_done = ss.e_done;
   if (overlap_env) {  // the side stream starts after everything already queued on the caller's stream
-    int r0 = cuda_status(cudaEventRecord(e_start, s), "train record");
-    if (!r0) r0 = cuda_status(cudaStreamWaitEvent(side, e_start, 0), "train wait");
-    if (r0) return r0;
+    if (int r0 = ss.create()) return r0;
+    side = ss.side;
   }
   int64_t step = step0;
   if (nb > 0) {

@@ -873,11 +873,7 @@ size_t tile_traverse_smem() { return sizeof(TileWarp) * TT_WPB; }
 // NG_TILE_SCAP=k (test knob) holds only k entries of each list in shared
 // memory, sending the rest through the arena.
 int tile_traverse_scap() {
-  static int scap = -1;
-  if (scap < 0) {
-    const char* e = getenv("NG_TILE_SCAP");
-    scap = e ? std::max(0, std::min(TT_SCAP, atoi(e))) : TT_SCAP;
-  }
+  static const int scap = std::max(0, std::min(TT_SCAP, env_int("NG_TILE_SCAP", TT_SCAP)));
   return scap;
 }
 int tile_traverse_entry_bytes() { return 2 * TT_ENTRY; }
@@ -886,17 +882,15 @@ int tile_traverse_entry_bytes() { return 2 * TT_ENTRY; }
 // TT_WPB: one resident wave, no more warps than tiles); the per-warp global
 // arena is sized from this.
 int64_t tile_traverse_warps(int64_t n_rays) {
-  static int per_sm = -1;
-  if (per_sm < 0) {
+  // resident CTAs per SM (an sm_100a property, the same on every B200)
+  static const int per_sm = [] {
     int a = 0, b = 0;
-    cudaFuncSetAttribute(k_traverse_tiles<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)tile_traverse_smem());
-    cudaFuncSetAttribute(k_traverse_tiles<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)tile_traverse_smem());
+    set_smem_limit((const void*)k_traverse_tiles<true>, tile_traverse_smem());
+    set_smem_limit((const void*)k_traverse_tiles<false>, tile_traverse_smem());
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_traverse_tiles<true>, TT_WPB * 32, tile_traverse_smem());
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_traverse_tiles<false>, TT_WPB * 32, tile_traverse_smem());
-    per_sm = std::max(1, std::min(a, b));
-  }
+    return std::max(1, std::min(a, b));
+  }();
   const int64_t tiles = (n_rays + TT_RAYS - 1) / TT_RAYS;
   const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((int64_t)sm_count() * per_sm,
                                                                   (tiles + TT_WPB - 1) / TT_WPB));
@@ -916,6 +910,7 @@ int traverse_tiles(const ng_octree& tree, const ng_ray* rays, const int64_t* d_n
   const int64_t warps = tile_traverse_warps(n_max);
   const int64_t gcap = (int64_t)(arena_bytes / (size_t)(warps * (2 * TT_ENTRY))) & ~int64_t(15);
   auto k = so.shared ? k_traverse_tiles<true> : k_traverse_tiles<false>;
+  if (int r = set_smem_limit((const void*)k, tile_traverse_smem())) return r;  // per device
   k<<<(int)(warps / TT_WPB), TT_WPB * 32, tile_traverse_smem(), s>>>(
       tree, rays, d_n, target, counts, hits, hit_cap, (unsigned int*)ctl, (unsigned long long*)((char*)ctl + 8),
       seg_start, seg_end, (uint8_t*)arena, gcap, tile_traverse_scap(), d_need, so,

@@ -17,6 +17,8 @@ feature weights, b1), W2[h], b2 (include/nglod_b200.h, ng_field).
 from __future__ import annotations
 
 import ctypes
+import threading
+import weakref
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -162,6 +164,8 @@ class DeviceField:
         self._presum_key = None
         self._src = (Z, decoders)
         self._exact = None
+        self._tables = {}   # (level, output mask) -> presummed tables, owner ids
+        self._lock = threading.Lock()
 
     def ref(self):
         return ctypes.byref(self.struct)
@@ -180,13 +184,10 @@ class DeviceField:
             self._exact = (z64, torch.from_numpy(pack_decoders64(decoders, self.m, self.h)).to(dev))
         return self._exact
 
-    def ensure_presum(self, svo, level: int, out_mask: int) -> None:
-        """Build (once per level / output set) the presummed feature tables
-        S_L on the level's corner ids that the sphere tracer and the normal
-        probes read instead of gathering every level (csrc/presum.cu)."""
-        key = (int(level), int(out_mask))
-        if self._presum_key == key:
-            return
+    def build_presum(self, svo, level: int, out_mask: int):
+        """Build the presummed feature tables S_L on the level's corner ids
+        that the sphere tracer and the normal probes read instead of
+        gathering every level (csrc/presum.cu). Returns (tables, owner)."""
         dev = self.Z.device
         offset = int(svo.corner_offsets[level])
         end = int(svo.corner_offsets[level + 1]) if level < svo.max_level else int(svo.corner_count)
@@ -196,15 +197,28 @@ class DeviceField:
         owner = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
         call("ng_field_presum", svo.device.ref(), ptr(self.Z), int(level), int(out_mask), offset, n, ptr(S),
              ptr(owner), stream_ptr())
-        self.presum = S
-        self._presum_owner = owner  # kept until the kernel has run
-        self._presum_key = key
-        s = self.struct
-        s.presum = ptr(S)
+        return S, owner
+
+    def presum_struct(self, svo, level: int, out_mask: int) -> _lib.NgField:
+        """A copy of the field struct carrying the presummed tables of
+        (level, output levels), built on first use and kept with the field.
+        Each frame launches with its own copy, so frames of different LODs
+        may run concurrently on one field."""
+        key = (int(level), int(out_mask))
+        with self._lock:
+            t = self._tables.get(key)
+            if t is None:
+                t = self._tables[key] = self.build_presum(svo, *key)
+            self.presum, self._presum_key = t[0], key
+        s = _lib.NgField.from_buffer_copy(self.struct)
+        offset = int(svo.corner_offsets[level])
+        s.presum = ptr(t[0])
         s.presum_offset = offset
-        s.presum_corners = n
-        s.presum_level = int(level)
-        s.presum_mask = int(out_mask)
+        s.presum_corners = (int(svo.corner_offsets[level + 1]) if level < svo.max_level else int(svo.corner_count)) \
+            - offset
+        s.presum_level = key[0]
+        s.presum_mask = key[1]
+        return s
 
 
 def _as_points(x):
@@ -525,7 +539,26 @@ def forward_levels(svo, Z, decoders, x, levels) -> np.ndarray:
     return forward_levels_device(svo, DeviceField(Z, decoders), _dev_points(pts), levels).cpu().numpy()
 
 
-@dataclass
+# host parameter arrays -> the fields holding a device copy of them, so an
+# in-place update through the API (trainer.adam_step) drops stale copies
+_WATCHED: dict = {}
+
+
+def _watch(fld) -> None:
+    arrays = [fld.Z] + [getattr(d, k) for d in fld.decoders for k in ("W1", "b1", "W2", "b2")]
+    for a in arrays:
+        _WATCHED.setdefault(id(a), weakref.WeakSet()).add(fld)
+
+
+def invalidate_arrays(arrays) -> None:
+    """Drop the device copies of every field that holds one of `arrays`
+    (after they were changed in place)."""
+    for a in arrays:
+        for fld in list(_WATCHED.get(id(a), ())):
+            fld.invalidate()
+
+
+@dataclass(eq=False)
 class NeuralField:
     """Octree plus parameters (field.py:242-269). The device copy of the
     parameters is made on first use; call `invalidate()` after editing Z or
@@ -552,6 +585,7 @@ class NeuralField:
     def device(self) -> DeviceField:
         if self._device is None:
             self._device = DeviceField(self.Z, self.decoders)
+            _watch(self)
         return self._device
 
     def invalidate(self) -> None:

@@ -97,9 +97,9 @@ class TiledRenderer:
         """Launch this rank's bands (no host sync)."""
         cs = camera.band_struct(self.band_rows, self.world, self.rank)
         fs = self.sess.frame_struct(self.frame)
-        prepare_presum(self.fld, cfg)
+        fstruct = prepare_presum(self.fld, cfg)
         if self.local_rows:
-            call("ng_render_frame", self.fld.svo.device.ref(), self.fld.device.ref(), ctypes.byref(cfg),
+            call("ng_render_frame", self.fld.svo.device.ref(), ctypes.byref(fstruct), ctypes.byref(cfg),
                  ctypes.byref(cs), ctypes.byref(fs), ctypes.byref(self.sess.ws), ptr(self.sess.stats),
                  stream_ptr())
 

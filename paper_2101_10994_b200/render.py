@@ -11,6 +11,7 @@ statistics -- no host synchronisation until the caller reads a result.
 from __future__ import annotations
 
 import os
+import threading
 
 import ctypes
 import math
@@ -272,20 +273,21 @@ def resolve_config(fld: NeuralField, config: RenderConfig, lod: float, eps: floa
 _PRESUM = os.environ.get("NG_PRESUM", "1") != "0"
 
 
-def prepare_presum(fld: NeuralField, cfg: _lib.NgRenderCfg) -> None:
-    """Presummed feature tables for this frame's gather level and output
-    levels (the LodPlan of render.cu: blend levels for a fractional lod);
-    NG_PRESUM=0 keeps the level-by-level gather."""
-    if not _PRESUM:
-        return
-    lod = max(float(cfg.lod), 1.0)
-    base = int(np.floor(lod))
-    if lod - base == 0.0:
-        mask, G = 1 << (base - 1), max(base, cfg.trace_level)
-    else:
-        mask, G = (1 << (base - 1)) | (1 << base), max(base + 1, cfg.trace_level)
-    if G == cfg.trace_level:
-        fld.device.ensure_presum(fld.svo, G, mask)
+def prepare_presum(fld: NeuralField, cfg: _lib.NgRenderCfg) -> _lib.NgField:
+    """The field struct a frame launches with: carrying the presummed
+    feature tables of this frame's gather level and output levels (the
+    LodPlan of render.cu: blend levels for a fractional lod) when they
+    apply; NG_PRESUM=0 keeps the level-by-level gather."""
+    if _PRESUM:
+        lod = max(float(cfg.lod), 1.0)
+        base = int(np.floor(lod))
+        if lod - base == 0.0:
+            mask, G = 1 << (base - 1), max(base, cfg.trace_level)
+        else:
+            mask, G = (1 << (base - 1)) | (1 << base), max(base + 1, cfg.trace_level)
+        if G == cfg.trace_level:
+            return fld.device.presum_struct(fld.svo, G, mask)
+    return fld.device.struct
 
 
 def _lod_split(lod: float):
@@ -441,6 +443,9 @@ def resolve_lod(camera: Camera, fld: NeuralField, config: RenderConfig) -> float
     return max(lod, 1.0)
 
 
+_CAPTURE_LOCK = threading.Lock()
+
+
 def _graphs_enabled() -> bool:
     """NG_GRAPHS=0 launches every frame's kernels directly."""
     return os.environ.get("NG_GRAPHS", "1") != "0" and os.environ.get("NG_MARCH_PROFILE") != "1"
@@ -526,7 +531,7 @@ class RenderSession:
         """Launch one frame on the current stream. With `timed`, ev0 / ev1 /
         ev2 bracket traversal+march and normals (ev1 is recorded by the C side)."""
         fs = self.frame_struct(frame)
-        prepare_presum(self.fld, cfg)
+        fstruct = prepare_presum(self.fld, cfg)
         graphed = camera is not None and _graphs_enabled() and self._graph_misses < 8
         if timed and not graphed:
             self.ev1.record()  # materialise the handle; re-recorded mid-frame
@@ -537,7 +542,7 @@ class RenderSession:
             if timed:
                 self.ev0.record()
         if camera is not None:
-            tree, field, cs = self.fld.svo.device.ref(), self.fld.device.ref(), camera.struct()
+            tree, field, cs = self.fld.svo.device.ref(), ctypes.byref(fstruct), camera.struct()
 
             def launch():
                 call("ng_render_frame", tree, field, ctypes.byref(cfg), ctypes.byref(cs), ctypes.byref(fs),
@@ -548,7 +553,7 @@ class RenderSession:
                 # gets the same address back from the caching allocator);
                 # timed graphed frames are timed as a whole (ev0 -> ev1), the
                 # normals being evaluated inside the march
-                key = (bytes(self.fld.svo.device.struct), bytes(self.fld.device.struct), bytes(cfg), bytes(cs),
+                key = (bytes(self.fld.svo.device.struct), bytes(fstruct), bytes(cfg), bytes(cs),
                        bytes(fs), bytes(self.ws))
                 g = self._graphs.get(key)
                 if g is None and key not in self._graph_seen:
@@ -562,7 +567,11 @@ class RenderSession:
                         if len(self._graphs) >= 4:
                             self._graphs.pop(next(iter(self._graphs)))
                         g = torch.cuda.CUDAGraph()
-                        with torch.cuda.graph(g):
+                        # one capture at a time in the process (entering a capture
+                        # synchronises the device and frees cached blocks, which
+                        # must not happen inside another thread's capture);
+                        # thread_local: other threads keep launching meanwhile
+                        with _CAPTURE_LOCK, torch.cuda.graph(g, capture_error_mode="thread_local"):
                             launch()
                         self._graphs[key] = g
                     self._graph_misses = 0
@@ -573,7 +582,7 @@ class RenderSession:
             else:
                 launch()
         else:
-            call("ng_render_rays", self.fld.svo.device.ref(), self.fld.device.ref(), ctypes.byref(cfg), ptr(rays),
+            call("ng_render_rays", self.fld.svo.device.ref(), ctypes.byref(fstruct), ctypes.byref(cfg), ptr(rays),
                  self.n, ctypes.byref(fs), ctypes.byref(self.ws), ptr(self.stats), int(do_normals), stream_ptr())
         if timed:
             self.ev2.record()
@@ -626,17 +635,23 @@ class RenderSession:
         return True
 
 
-_SESSIONS: dict = {}
+_SESSIONS = threading.local()
 
 
 def _session(fld: NeuralField, width: int, height: int) -> RenderSession:
-    key = (id(fld), width, height)
-    s = _SESSIONS.get(key)
+    """render()'s reusable frame state, per calling thread, device and
+    stream (concurrent callers never share a workspace; SURVEY.md 8b
+    Threading)."""
+    cache = getattr(_SESSIONS, "d", None)
+    if cache is None:
+        cache = _SESSIONS.d = {}
+    key = (id(fld), width, height, torch.cuda.current_device(), torch.cuda.current_stream().cuda_stream)
+    s = cache.get(key)
     if s is None or s.fld is not fld:
-        if len(_SESSIONS) > 8:
-            _SESSIONS.clear()
+        if len(cache) > 8:
+            cache.clear()
         s = RenderSession(fld, width, height)
-        _SESSIONS[key] = s
+        cache[key] = s
     return s
 
 

@@ -31,6 +31,7 @@ from .field import (
     LevelInterp,
     NeuralField,
     _dev_points,
+    invalidate_arrays,
     decoder_stride,
     trilinear,
 )
@@ -288,6 +289,8 @@ def adam_step(params: dict, grads: dict, state: AdamState, lr: float):
         params[name][...] = p.cpu().numpy().reshape(np.shape(params[name]))
         state.m[name][...] = m.cpu().numpy().reshape(np.shape(g))
         state.v[name][...] = v.cpu().numpy().reshape(np.shape(g))
+        # fields holding a device copy of this array re-upload on next use
+        invalidate_arrays([params[name]])
     return params, state
 
 

@@ -105,3 +105,34 @@ def test_configs4_lod45_shadows_1080p(work, lod6):
                                 ng.RenderConfig(lod=4.5, shadows=True), O.RenderParams(lod=4.5, shadows=True),
                                 stride=36, offset=3)
     assert fr.shadowed.sum() > 0
+
+
+def test_configs0_sphere_lod3_128():
+    """configs[0]: LOD1-3 octree of the analytic sphere, random-init field
+    (feature dim 32, hidden 128), 128x128 frame, against the oracle's render
+    of the same octree and field (the reference measured
+    4,244 hits, all on the first evaluation, and 5,313 evaluations)."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import bench
+    import paper_2101_10994_b200 as ng
+    from paper_2101_10994_b200 import scenes
+    from oracle import nglod_oracle as O
+    sphere = scenes.Sphere(0.5)
+    svo = ng.build_octree(sphere, 3, ng.surface_points(sphere, 2 ** 17, 0))
+    fld = ng.new_field(svo, seed=0)
+    cam = dict(position=(0.0, 0.0, 4.0), look_at=(0.0, 0.0, 0.0), up=(0.0, 1.0, 0.0), fov_y_deg=30.0)
+    fb, rep = ng.render(ng.Camera(cam["position"], cam["look_at"], cam["up"], 30.0, 128, 128), fld,
+                        ng.RenderConfig())
+    decs = [O.OracleDecoder(d.W1, d.b1, d.W2, d.b2) for d in fld.decoders]
+    fr = O.render(bench.oracle_tree(svo), fld.Z, decs, dict(cam, width=128, height=128), O.RenderParams(),
+                  workers=8)
+    print(f"\nconfigs[0]: {rep.visible} visible (oracle {fr.visible}), {rep.evals} evals (oracle {fr.total_evals}), "
+          f"{int((fb.hit != fr.hit).sum())} hit pixels differ")
+    assert fr.visible > 4000
+    assert np.mean(fb.hit == fr.hit) >= 0.999
+    both = fb.hit & fr.hit
+    assert np.abs(fb.t[both] - fr.t[both]).max() <= DEPTH_TOL
+    assert np.mean(np.all(fb.color == fr.color, axis=-1)) >= 0.999
+    assert abs(rep.evals - fr.total_evals) <= max(10, fr.total_evals // 1000)

@@ -7,7 +7,9 @@ cli stay the reference's. tools/stage_reference_tests.sh copies the
 reference's tests/ and installs its package under baseline/ (git-ignored;
 it travels to the GPU box with the repository snapshot). This test runs
 that suite unchanged on the GPU and requires every test to pass except the
-ones listed in DESELECTED, each for the reason given there.
+ones listed in DESELECTED, each for the reason given there. Acceptance
+criterion 9 is also printed by the run (it must reproduce the reference's
+own numbers).
 """
 
 import os
@@ -36,6 +38,12 @@ DESELECTED = {
     "test_acceptance.py::test_criterion_7_empty_space": "patches render.query_field (host seam) to detect "
                                                          "empty-space decodes; the device frame counts them "
                                                          "(evals_missing_level, asserted zero in every render)",
+    # The unmodified reference fails this criterion itself, with the same
+    # numbers (LOD3 0.582/0.408, LOD4 0.729/0.356; run on CPU in the build
+    # container, profiles/r02_parity/reference_cpu_criteria_5_9.log): the
+    # frozen-decoder torus is 2.05x the joint one at LOD4 against a 2.0x bar.
+    # Reproducing it to three digits is the parity result.
+    "test_acceptance.py::test_criterion_9_frozen_decoder": "fails identically in the unmodified reference",
 }
 
 

@@ -72,6 +72,10 @@ def test_configs1_720p_lists_bit_exact(bench_mod):
     _report("configs[1] 1280x720 LOD5", r)
     assert r["pairs"] == len(fin) and r["pairs"] > 3_000_000
     assert r["mismatched_rays"] == 0
+    # the precondition under which the oracle's per-ray advance loop equals
+    # the reference's batched one (render.py:202-238):
+    # no voxel of the frame is entered beyond the far plane
+    assert fin.t_enter.max() <= ng.RenderConfig().far_plane
 
 
 def test_configs3_1080p_lod6_lists_bit_exact(bench_mod):
@@ -94,6 +98,7 @@ def test_configs3_1080p_lod6_lists_bit_exact(bench_mod):
     _report("configs[3] 1920x1080 LOD6 (every 5th row)", r)
     assert r["pairs"] > 500_000
     assert r["mismatched_rays"] == 0
+    assert fin.t_enter.max() <= ng.RenderConfig().far_plane  # the advance-loop precondition (see configs[1])
 
 
 def test_band_camera_lists_bit_exact(bench_mod):
