@@ -20,6 +20,9 @@
 #ifndef NG_GATHER_BATCH
 #define NG_GATHER_BATCH 8  // points whose 8 corner rows are in flight together per warp (2 quad loads)
 #endif
+#ifndef NG_PROF_SLOTS
+#define NG_PROF_SLOTS 32   // NG_PROFILE builds: uint64 counters per march group (tools/march_profile.py)
+#endif
 #ifndef NG_QUAD_GATHER
 #define NG_QUAD_GATHER 1   // warp_eval: 16-byte row loads, 4 points per load instruction
 #endif
@@ -49,10 +52,8 @@ struct EvalCtx {
   int64_t presum_corners = 0;
 };
 
-__device__ __forceinline__ unsigned long long dbg_now() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
+__device__ __forceinline__ unsigned long long dbg_now() {  // NG_PROFILE laps: SM clock cycles
+  return (unsigned long long)clock64();
 }
 
 // empty_space_value (field.py:185-191) in float64, numpy operation order.

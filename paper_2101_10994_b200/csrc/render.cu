@@ -394,12 +394,26 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_cons
   if constexpr (TC) {
     tcm = tc_policy(D.t, D.tmem_base, A.dec_first, &phase);
 #ifdef NG_PROFILE
-    if (A.prof) tcm.prof = A.prof + 8 * (blockIdx.x * GROUPS + g);
+    if (A.prof && (w & 3) == 0) tcm.prof = A.prof + NG_PROF_SLOTS * (blockIdx.x * GROUPS + g);
 #endif
   }
   EvalCtx c;
 #ifdef NG_PROFILE
-  if (A.prof && w == 0) c.dbg = A.prof + 8 * 4096 - 8 * 1024 + 8 * (blockIdx.x % 1024);
+  // the group leader's eval phases: slots 11 prologue, 12 staging, 13 gather, 14 decoder
+  if (A.prof && (w & 3) == 0) c.dbg = A.prof + NG_PROF_SLOTS * (blockIdx.x * GROUPS + g) + 11;
+  unsigned long long* const gprof = (A.prof && (w & 3) == 0 && lane_id() == 0)
+                                        ? A.prof + NG_PROF_SLOTS * (blockIdx.x * GROUPS + g) : nullptr;
+  long long ck = 0, ck_top = 0;
+  bool light_step = false;
+  auto mark = [&](int slot) {  // clock64 laps of the group leader (slots 8..)
+    if (gprof) {
+      const long long now = clock64();
+      gprof[slot] += (unsigned long long)(now - ck);
+      ck = now;
+    }
+  };
+#else
+  auto mark = [](int) {};
 #endif
   c.Z = f.Z;
   c.dec = D.dec;
@@ -464,6 +478,8 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_cons
   while (true) {
 #ifdef NG_PROFILE
     if (A.prof && (w & 3) == 0 && lane == 0) t_top = globaltimer_ns();
+    ck = clock64();
+    ck_top = ck;
 #endif
     // ---- acquire rays and advance each to its next query point (render.py:200-238)
     while (true) {
@@ -540,6 +556,7 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_cons
       }
       if (!__any_sync(FULL, ray < 0 && !drained && lane < cap)) break;
     }
+    mark(8);  // ray claims + segment walk
     if (__any_sync(FULL, !probes_done)) {  // warp-uniform: the claim below is a warp collective
       // lanes out of rays claim probe items (warp-aggregated) ...
       const bool pw = !probes_done && ray < 0 && pk < 0 && (drained || lane >= cap) &&
@@ -585,6 +602,7 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_cons
         }
       }
     }
+    mark(9);  // probe claims
     const bool act = ray >= 0;
     const bool pact = pk >= 0 && pready;
     // a lane stays in the loop while it marches, holds a probe item or may
@@ -602,9 +620,17 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_cons
       const int gs = gf[4 * g] + gf[4 * g + 1] + gf[4 * g + 2] + gf[4 * g + 3];
       const int active = gs & 0xff, any_alive = (gs >> 8) & 0xff;
       group_marching = gs >> 16;
+      mark(10);  // group barrier
+#ifdef NG_PROFILE
+      if (gprof && active) {
+        gprof[16] += 1;
+        if (active <= 8) gprof[17] += 1;  // light steps: the tail's per-step latency
+      }
+      light_step = active <= 8;
+#endif
 #ifdef NG_PROFILE
       if (A.prof && (w & 3) == 0 && lane == 0) {  // debug profile: per-group steps and busy lanes
-        unsigned long long* pr = A.prof + 8 * (blockIdx.x * GROUPS + g);
+        unsigned long long* pr = A.prof + NG_PROF_SLOTS * (blockIdx.x * GROUPS + g);
         const unsigned long long now = globaltimer_ns();
         if (pr[0] == 0) pr[2] = t_top;
         if (active) {
@@ -689,9 +715,10 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_cons
 #ifdef NG_PROFILE
     if (A.prof && (w & 3) == 0 && lane == 0) {
       t_eval = globaltimer_ns();
-      A.prof[8 * (blockIdx.x * GROUPS + g) + 5] += t_eval - t_acq;  // gather + decoder
+      A.prof[NG_PROF_SLOTS * (blockIdx.x * GROUPS + g) + 5] += t_eval - t_acq;  // gather + decoder
     }
 #endif
+    mark(18);  // query point + evaluation
     // ---- stop rules (render.py:247-272)
     if (eact && !er.inside) lc.empty += 1;  // query_field's own empty-space fallback
     if (pact) {
@@ -752,6 +779,10 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_cons
         ready = false;
       }
     }
+    mark(15);  // stop rules, hit publication
+#ifdef NG_PROFILE
+    if (gprof && light_step) gprof[19] += (unsigned long long)(clock64() - ck_top);
+#endif
   }
   lc.flush(A.counters);
   if (A.fin.st) {  // last CTA out writes the frame statistics
@@ -1196,8 +1227,8 @@ static unsigned long long* g_prof = nullptr;
 static unsigned long long* march_profile_buffer() {
   static const bool on = [] {
     if (env_int("NG_MARCH_PROFILE", 0) != 1) return false;
-    if (cudaMalloc((void**)&g_prof, 8 * 8 * 4096) != cudaSuccess) return false;
-    cudaMemset(g_prof, 0, 8 * 8 * 4096);
+    if (cudaMalloc((void**)&g_prof, 8 * NG_PROF_SLOTS * 4096) != cudaSuccess) return false;
+    cudaMemset(g_prof, 0, 8 * NG_PROF_SLOTS * 4096);
     return true;
   }();
   return on ? g_prof : nullptr;
@@ -1609,14 +1640,15 @@ int ng_shade(const uint8_t* hit, const double* normal, int64_t n, const ng_rende
   return NG_OK;
 }
 
-// Debug: copy the march profile (4 x uint64 per group: steps, busy lanes,
-// first/last globaltimer ns) and reset it; 0 groups when profiling is off.
+// Debug: copy the march profile (NG_PROF_SLOTS x uint64 per group: steps,
+// busy lanes, first/last globaltimer ns, then the phase clocks listed in
+// tools/march_profile.py) and reset it; 0 groups when profiling is off.
 int ng_march_profile(unsigned long long* host_out, int max_groups) {
   if (!g_prof) return 0;
   cudaDeviceSynchronize();
   const int n = max_groups < 4096 ? max_groups : 4096;
-  cudaMemcpy(host_out, g_prof, (size_t)n * 64, cudaMemcpyDeviceToHost);
-  cudaMemset(g_prof, 0, 8 * 8 * 4096);
+  cudaMemcpy(host_out, g_prof, (size_t)n * 8 * NG_PROF_SLOTS, cudaMemcpyDeviceToHost);
+  cudaMemset(g_prof, 0, 8 * NG_PROF_SLOTS * 4096);
   return n;
 }
 

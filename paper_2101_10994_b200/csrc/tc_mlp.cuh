@@ -18,7 +18,7 @@ struct TcMlp {
   uint32_t* phase;
   int wg;
   int bar_id;
-  unsigned long long* prof = nullptr;  // debug: [6] += ns gather->decoder entry, [7] += ns in decoder
+  unsigned long long* prof = nullptr;  // NG_PROFILE: [6] += cycles at the group barrier, [7] += cycles GEMM + epilogue
   // one-level staging (k_query_tc): the CTA holds a single decoder's tiles
   // and re-stages level l from these fp32 decoders before its GEMMs
   const float* restage_src = nullptr;
@@ -43,8 +43,7 @@ struct TcMlp {
   __device__ __forceinline__ float operator()(int l, const float xf[3], const float* zrow, bool /*any*/,
                                               bool& bad) const {
 #ifdef NG_PROFILE
-    unsigned long long t_in = 0;
-    if (prof && wg == 0 && lane_id() == 0) asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_in));
+    const long long t_in = clock64();
 #endif
     const int lane = (int)lane_id();
     const int row = 32 * wg + lane;
@@ -82,11 +81,7 @@ struct TcMlp {
     }
     tc::fence_before_sync();
 #ifdef NG_PROFILE
-    if (prof && wg == 0 && lane_id() == 0) {
-      unsigned long long t_out;
-      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_out));
-      prof[7] += t_out - t_in;
-    }
+    if (prof && lane_id() == 0) prof[7] += (unsigned long long)(clock64() - t_in);
 #endif
     return acc;
   }
@@ -110,7 +105,13 @@ __device__ __forceinline__ float TcMlp::decode_direct(int l, const float xf[3], 
   }
   tc::fence_proxy_async();
   tc::fence_before_sync();
+#ifdef NG_PROFILE
+  const long long t0 = clock64();
+#endif
   tc::named_sync(bar_id, 128);
+#ifdef NG_PROFILE
+  const long long t1 = clock64();
+#endif
   const uint8_t* dt = dec_tiles + (restage_src ? (size_t)0 : (size_t)(l - dec_first) * DEC_TC_BYTES);
   if (wg == 0 && lane == 0)
     tc::issue_gemm(tmem, tc::smem_u32(a_hi), tc::smem_u32(a_lo), tc::smem_u32(dt), tc::smem_u32(dt + tc::TILE_BYTES),
@@ -129,6 +130,12 @@ __device__ __forceinline__ float TcMlp::decode_direct(int l, const float xf[3], 
     for (int i = 0; i < 32; ++i) acc = fmaf(W2[32 * c + i], fmaxf(hh[i], 0.f), acc);
   }
   tc::fence_before_sync();
+#ifdef NG_PROFILE
+  if (prof && lane == 0) {
+    prof[6] += (unsigned long long)(t1 - t0);
+    prof[7] += (unsigned long long)(clock64() - t1);
+  }
+#endif
   return acc;
 }
 
