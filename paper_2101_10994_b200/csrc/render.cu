@@ -306,6 +306,18 @@ struct MarchArgs {
 };
 
 constexpr unsigned PROBE_READY = 0x80000000u;
+
+// Release-ordered atomics for the probe slots: MEMBAR.ALL.GPU before the
+// atomic, no L1 invalidation (a gpu-scope __threadfence or acquire emits
+// CCTL.IVALL, which drops every warp's L1-cached table rows on the SM).
+__device__ __forceinline__ unsigned atom_add_release(unsigned* p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.release.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ void red_or_release(unsigned* p, unsigned v) {
+  asm volatile("red.release.gpu.global.or.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 #ifndef NG_PROBE_GROUP_MAX_HEAVY
 #define NG_PROBE_GROUP_MAX_HEAVY 64
 #endif
@@ -581,8 +593,11 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_cons
       if (pk >= 0 && !pready) {
         const int64_t sl = pk / 6;
         unsigned st;
-        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(st) : "l"(A.probe_cnt + sl) : "memory");
-        if (st & PROBE_READY) {  // acquire: the publisher's t and hit_list stores are visible
+        // relaxed (no L1 invalidation, unlike ld.acquire / __threadfence): the
+        // slot's data is read below with L2 (.cg) loads issued after the flag
+        // is seen, and the publisher wrote it before its release
+        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(st) : "l"(A.probe_cnt + sl) : "memory");
+        if (st & PROBE_READY) {
           const int32_t pix = __ldcg(A.hit_list + sl);
           const double th = __ldcg(A.t + pix);
           ng_ray rr;
@@ -724,11 +739,9 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_cons
     if (pact) {
       // normals (render.py:294-299): g = (v+ - v-) / (2 eps) once all 6 are in
       const int64_t sl = pk / 6;
-      A.probe_val[pk] = dval_of(er, fv, x);
-      __threadfence();
-      const unsigned old = atomicAdd(A.probe_cnt + sl, 1u);
-      if ((old & 0xffffu) == 5u) {
-        __threadfence();
+      __stcg(A.probe_val + pk, dval_of(er, fv, x));
+      const unsigned old = atom_add_release(A.probe_cnt + sl, 1u);  // the value before the count
+      if ((old & 0xffffu) == 5u) {  // the other five values are in L2: read them there
         double vals[6];
 #pragma unroll
         for (int j = 0; j < 6; ++j) vals[j] = __ldcg(A.probe_val + 6 * sl + j);
@@ -764,10 +777,7 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_cons
         if (A.hit_list) {
           const unsigned long long slot = atomicAdd(A.d_hit_count, 1ull);
           A.hit_list[slot] = r_id;
-          if (A.probes) {  // publish the slot's probes (t written above)
-            __threadfence();
-            atomicOr(A.probe_cnt + slot, PROBE_READY);
-          }
+          if (A.probes) red_or_release(A.probe_cnt + slot, PROBE_READY);  // publish (t, hit_list written above)
         }
         if (A.probes) atomicAdd(A.rays_done, 1ull);
       } else if (stalled || it >= A.cfg.max_iters) {

@@ -465,6 +465,13 @@ __device__ __forceinline__ unsigned octants_front_to_back(unsigned x, int dm) {
 }
 
 
+#ifdef NG_PROFILE
+// NG_PROFILE builds: per tile (globaltimer start, end, final pairs, warp) for
+// tools/tile_profile.py (ng_tile_profile_enable / ng_tile_profile_read)
+__device__ unsigned long long* g_tile_prof = nullptr;
+__device__ long long g_tile_prof_cap = 0;
+#endif
+
 template <bool SO>
 __global__ void __launch_bounds__(TT_WPB * 32, NG_TT_MINB) k_traverse_tiles(
     const __grid_constant__ ng_octree tree, const ng_ray* __restrict__ rays, const int64_t* __restrict__ d_n,
@@ -492,6 +499,10 @@ __global__ void __launch_bounds__(TT_WPB * 32, NG_TT_MINB) k_traverse_tiles(
     if (lane == 0) tile = atomicAdd(tile_counter, 1u);
     tile = __shfl_sync(FULL, tile, 0);
     if ((int64_t)tile >= n_tiles) break;
+#ifdef NG_PROFILE
+    unsigned long long tp0 = 0;
+    if (lane == 0) asm volatile("mov.u64 %0, %globaltimer;" : "=l"(tp0));
+#endif
     const int64_t r0 = (int64_t)tile * TT_RAYS;
     const int nr = (int)((n - r0) < TT_RAYS ? (n - r0) : TT_RAYS);
     // ---- the tile's rays, and the root list: rays whose box test hits B
@@ -705,6 +716,17 @@ __global__ void __launch_bounds__(TT_WPB * 32, NG_TT_MINB) k_traverse_tiles(
             make_int4((int)(r0 + j), (int)(e0 - s0), (int)(uint32_t)s0, (int)(s0 >> 32));
     }
     __syncwarp();
+#ifdef NG_PROFILE
+    if (lane == 0 && g_tile_prof && (long long)tile < g_tile_prof_cap) {
+      unsigned long long tp1;
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(tp1));
+      unsigned long long* pr = g_tile_prof + 4 * (int64_t)tile;
+      pr[0] = tp0;
+      pr[1] = tp1;
+      pr[2] = (unsigned long long)nc;
+      pr[3] = (unsigned long long)gw;
+    }
+#endif
   }
   if (lane >= 1 && lane <= target && level_cnt) atomicAdd((unsigned long long*)(counts + lane),
                                                           (unsigned long long)level_cnt);
@@ -1007,3 +1029,23 @@ int ng_ray_aabb(const double* o, const double* d, const double* lo, const double
 }
 
 }  // extern "C"
+
+#ifdef NG_PROFILE
+extern "C" int ng_tile_profile_enable(long long max_tiles) {
+  unsigned long long* p = nullptr;
+  if (cudaMalloc((void**)&p, (size_t)max_tiles * 32) != cudaSuccess) return NG_ERR_CUDA;
+  cudaMemset(p, 0, (size_t)max_tiles * 32);
+  cudaMemcpyToSymbol(g_tile_prof, &p, sizeof(p));
+  cudaMemcpyToSymbol(g_tile_prof_cap, &max_tiles, sizeof(max_tiles));
+  return NG_OK;
+}
+extern "C" int ng_tile_profile_read(unsigned long long* host_out, long long max_tiles) {
+  unsigned long long* p = nullptr;
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(&p, g_tile_prof, sizeof(p));
+  if (!p) return 0;
+  cudaMemcpy(host_out, p, (size_t)max_tiles * 32, cudaMemcpyDeviceToHost);
+  cudaMemset(p, 0, (size_t)max_tiles * 32);
+  return 1;
+}
+#endif
