@@ -384,4 +384,16 @@ __device__ __forceinline__ int64_t block_excl_scan(int64_t v, int64_t& excl, int
   return total;
 }
 
+// Flag words between warps of one grid: a relaxed load (no L1 invalidation)
+// polled until set, and a release store after the data it publishes; the
+// data is read with L2 (.cg) loads once the flag is seen.
+__device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_add_release_u32(unsigned* p, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 }  // namespace ng

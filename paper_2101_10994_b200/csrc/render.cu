@@ -29,7 +29,9 @@ int traverse_tiles(const ng_octree& tree, const ng_ray* rays, const int64_t* d_n
                    ng_hit_pair* hits, int64_t hit_cap, void* ctl, int64_t* seg_start, int64_t* seg_end,
                    void* arena, size_t arena_bytes, unsigned long long* d_need, const double* shared_origin,
                    const ng_camera* cam_rays, const ng_frame* defaults, uint32_t bg, int64_t n_host,
-                   cudaStream_t s);
+                   void* cont, cudaStream_t s);
+size_t tile_cont_bytes();
+size_t tile_cont_ready_bytes();
 int64_t tile_traverse_limit(size_t arena_bytes, int64_t n_max);
 int64_t tile_traverse_warps(int64_t n_max);
 int tile_traverse_scap();
@@ -1185,6 +1187,7 @@ struct WsLayout {
   size_t rays, pairs_a, pairs_b, hits, seg_start, seg_end, active, hit_list, scratch, ctr, total;
   size_t s_rays, s_hit, s_t, s_it, s_ev;  // shadow-ray pass
   size_t sorted, buckets;                 // longest-first march order
+  size_t cont;                            // tile traversal continuations (split silhouette tiles)
   size_t probe_val, probe_cnt;            // normals evaluated in the march
   size_t scratch_bytes;
 };
@@ -1226,6 +1229,7 @@ static WsLayout layout(int64_t n, int64_t pair_cap, int64_t hit_cap) {
   L.probe_val = o; o = al(o + (size_t)n * 6 * 8);
   L.probe_cnt = o; o = al(o + (size_t)n * 4);
   L.buckets = o; o = al(o + 2 * LEN_BUCKETS * 4);
+  L.cont = o; o = al(o + tile_cont_bytes());
   L.total = o;
   return L;
 }
@@ -1270,7 +1274,8 @@ static int trace_pass(const ng_octree& tree, const ng_render_cfg& cfg, const Lod
   const bool tiles = use_tile_traverse(target);
   tov.need = nullptr;
   if (!zeroed && tiles) {  // the tile path reads only its control words (the march takes work items)
-    int rz = cuda_status(cudaMemsetAsync(scratch, 0, 64, s), "tile traversal control words");
+    int rz = cuda_status(cudaMemsetAsync(scratch, 0, 512, s), "tile traversal control words");
+    if (!rz) rz = cuda_status(cudaMemsetAsync(b + L.cont, 0, tile_cont_ready_bytes(), s), "tile continuations");
     if (rz) return rz;
   } else if (!zeroed) {  // the primary pass has these zeroed by k_zero_regions and the ray kernel
     ZeroRegions z;
@@ -1294,7 +1299,8 @@ static int trace_pass(const ng_octree& tree, const ng_render_cfg& cfg, const Lod
     const size_t arena_bytes = L.hits - L.pairs_a;
     unsigned long long* need = (unsigned long long*)((char*)scratch + 16);
     r = traverse_tiles(tree, rays, &counts[0], n, target, reinterpret_cast<int4*>(active), d_active, counts, hits, ws.hit_capacity, scratch, seg_start, seg_end,
-                       b + L.pairs_a, arena_bytes, need, shared_origin, cam_rays, defaults, bg, n_host, s);
+                       b + L.pairs_a, arena_bytes, need, shared_origin, cam_rays, defaults, bg, n_host,
+                       b + L.cont, s);
     if (r) return r;
     tov.need = need;
     tov.lim = tile_traverse_limit(arena_bytes, n);
@@ -1387,13 +1393,15 @@ static int render_common(const ng_octree& tree, const ng_field& f, const ng_rend
     z.p[2] = b + L.scratch;
     // (the tile traversal uses only its control words at the start)
     z.bytes[2] = use_tile_traverse(cfg.trace_level + tree.n_virtual)
-                     ? 64
+                     ? 512
                      : L.scratch_bytes * (size_t)(cfg.trace_level + tree.n_virtual);
     z.p[3] = b + L.buckets;
     z.bytes[3] = 2 * LEN_BUCKETS * 4;
     z.p[4] = b + L.probe_cnt;
     z.bytes[4] = (size_t)n * 4;
-    z.n = 5;
+    z.p[5] = b + L.cont;  // tile traversal continuations' ready counts
+    z.bytes[5] = tile_cont_ready_bytes();
+    z.n = 6;
     k_zero_regions<<<64, 256, 0, s>>>(z);
     NG_CHECK_LAUNCH("k_zero_regions");
   }

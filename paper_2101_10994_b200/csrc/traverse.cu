@@ -465,11 +465,49 @@ __device__ __forceinline__ unsigned octants_front_to_back(unsigned x, int dm) {
 }
 
 
+// Splitting silhouette tiles. A tile's time is proportional to its pairs
+// (one warp runs every round), so a few grazing tiles (~3,000 final pairs,
+// ~190 us) outlast all the others when a frame has few tiles per warp (a
+// band of an N-GPU frame). After a level pass, a list longer than
+// NG_TT_SPLIT entries that covers several rays is cut at a ray boundary near
+// its middle: the warp keeps the first rays and publishes the rest (their
+// entries copied to a pool) as a continuation that any warp takes before a
+// fresh tile. A ray's pairs stay in one part, and each part claims its own
+// block of the hit list, so every ray's segment is still the reference's
+// sub-list in order (traversal.py:207-247); only block placement changes.
+#ifndef NG_TT_SPLIT
+#define NG_TT_SPLIT 256
+#endif
+constexpr int TT_SPLIT = NG_TT_SPLIT;
+constexpr int TT_CONT_RECS = 16384;         // continuation records per pass
+#ifndef NG_TT_HELPERS
+#define NG_TT_HELPERS 2
+#endif
+constexpr int TT_HELPERS = NG_TT_HELPERS;   // warps per CTA that wait for continuations when idle
+constexpr int64_t TT_CONT_POOL = 2 << 20;   // pooled list entries per pass
+struct TileCont {
+  int64_t r0;        // the tile's first ray
+  int64_t pool_off;  // its entries in the pool
+  int32_t nr, ja, jb;  // tile rays; the continuation's ray slots [ja, jb)
+  int32_t pass;      // the next level pass
+  int32_t count;     // entries
+  int32_t pad;
+};
+// `cont` layout: per-record ready counts (u32, zeroed before every pass:
+// each of the pushing warp's 32 lanes adds 1 with release after its pool
+// stores), the records, the entry pool
+size_t tile_cont_ready_bytes() { return (size_t)TT_CONT_RECS * 4; }
+size_t tile_cont_bytes() {
+  return tile_cont_ready_bytes() + (size_t)TT_CONT_RECS * sizeof(TileCont) + (size_t)TT_CONT_POOL * 8;
+}
+
 #ifdef NG_PROFILE
 // NG_PROFILE builds: per tile (globaltimer start, end, final pairs, warp) for
 // tools/tile_profile.py (ng_tile_profile_enable / ng_tile_profile_read)
 __device__ unsigned long long* g_tile_prof = nullptr;
 __device__ long long g_tile_prof_cap = 0;
+__device__ unsigned long long* g_part_prof = nullptr;  // 8 words per part
+__device__ unsigned int g_part_next = 0;
 #endif
 
 template <bool SO>
@@ -479,7 +517,7 @@ __global__ void __launch_bounds__(TT_WPB * 32, NG_TT_MINB) k_traverse_tiles(
     unsigned long long* hit_cursor, int64_t* __restrict__ seg_start, int64_t* __restrict__ seg_end,
     uint8_t* arena, int64_t gcap, int scap, unsigned long long* d_need, const SharedOrigin so,
     const ng_camera cam, int cam_rays, int4* __restrict__ items, unsigned long long* d_active,
-    const ng_frame fr, uint32_t bg, int64_t n_host, int cull) {
+    const ng_frame fr, uint32_t bg, int64_t n_host, int cull, uint8_t* __restrict__ cont) {
   extern __shared__ __align__(16) uint8_t tt_smem[];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -494,19 +532,123 @@ __global__ void __launch_bounds__(TT_WPB * 32, NG_TT_MINB) k_traverse_tiles(
   const int lim = scap + (int)gcap;
   int64_t level_cnt = 0;  // lane t: pairs emitted at traversal level t
   int need = 0;
+  // continuation queue (control words after the tile counter, hit cursor
+  // and longest list, zeroed with them): records pushed / claimed, parts in
+  // progress (tiles + continuations), pool entries used
+  // (each on its own 128-byte line: idle warps poll the queue words, and
+  // the tile counter and `pending` take an atomic per tile)
+  unsigned int* q_tail = tile_counter + 32;
+  unsigned int* q_head = tile_counter + 64;
+  unsigned int* pending = tile_counter + 96;
+  unsigned int* pool_top = tile_counter + 48;  // (pushers only)
+  unsigned int* ready = reinterpret_cast<unsigned int*>(cont);
+  TileCont* recs = reinterpret_cast<TileCont*>(cont + (size_t)TT_CONT_RECS * 4);
+  int2* pool = reinterpret_cast<int2*>(cont + (size_t)TT_CONT_RECS * (4 + sizeof(TileCont)));
+  bool tiles_left = true;
   while (true) {
-    unsigned int tile = 0;
-    if (lane == 0) tile = atomicAdd(tile_counter, 1u);
+    // ---- work: a published continuation first, else a fresh tile; with
+    // neither, wait while any part is in progress (it may still split)
+    int rec = -1;
+    unsigned int tile = 0xffffffffu;
+    if (lane == 0) {
+      unsigned backoff = 256;
+      int ticket = -1;  // a claimed queue position, served once published
+      while (true) {
+        const unsigned tl = *(volatile unsigned*)q_tail;
+        if (ticket < 0 && *(volatile unsigned*)q_head < tl) {
+          ticket = (int)atomicAdd(q_head, 1u);  // (fetch-add: a CAS loop serialised the claims)
+          if (ticket >= TT_CONT_RECS) ticket = INT_MAX;  // past the last record: no more work for it
+        }
+        if (ticket >= 0) {
+          if ((unsigned)ticket < tl) {
+            rec = ticket;
+            break;
+          }
+          // the ticket passed the published records: it is served by the
+          // next push, or dropped when nothing is in progress any more
+          if (*(volatile unsigned*)pending == 0 && (unsigned)ticket >= *(volatile unsigned*)q_tail) break;
+          __nanosleep(backoff);
+          backoff = backoff < 8192 ? 2 * backoff : backoff;
+          continue;
+        }
+        if (tiles_left) {
+          atomicAdd(pending, 1u);
+          tile = atomicAdd(tile_counter, 1u);
+          if ((int64_t)tile < n_tiles) break;
+          atomicSub(pending, 1u);
+          tiles_left = false;
+          tile = 0xffffffffu;
+          continue;
+        }
+        // idle: all but TT_HELPERS warps per CTA leave; the helpers wait for
+        // continuations while any part is in progress (few pollers keep the
+        // queue words' L2 lines free for the pushers' atomics)
+        if (warp >= TT_HELPERS ||
+            (*(volatile unsigned*)pending == 0 && *(volatile unsigned*)q_head >= *(volatile unsigned*)q_tail))
+          break;
+        __nanosleep(backoff);
+        backoff = backoff < 8192 ? 2 * backoff : backoff;
+      }
+    }
+    rec = __shfl_sync(FULL, rec, 0);
     tile = __shfl_sync(FULL, tile, 0);
-    if ((int64_t)tile >= n_tiles) break;
+    tiles_left = __shfl_sync(FULL, tiles_left, 0);
+    if (rec < 0 && tile == 0xffffffffu) break;
 #ifdef NG_PROFILE
     unsigned long long tp0 = 0;
     if (lane == 0) asm volatile("mov.u64 %0, %globaltimer;" : "=l"(tp0));
 #endif
-    const int64_t r0 = (int64_t)tile * TT_RAYS;
-    const int nr = (int)((n - r0) < TT_RAYS ? (n - r0) : TT_RAYS);
-    // ---- the tile's rays, and the root list: rays whose box test hits B
+    int64_t r0;
+    int nr, ja = 0, jb, t0 = 0;
     int nc = 0;
+#ifdef NG_PROFILE
+    int n_splits = 0;
+    unsigned long long split_ns = 0;
+#endif
+    if (rec >= 0) {
+      // ---- a continuation: its rays' slab data, its list at pass t0
+      const TileCont* cr = recs + rec;
+      if (lane == 0)
+        while (ld_relaxed_u32(ready + rec) < 32u) __nanosleep(64);
+      __syncwarp();
+      r0 = __ldcg(&cr->r0);
+      nr = __ldcg(&cr->nr);
+      ja = __ldcg(&cr->ja);
+      jb = __ldcg(&cr->jb);
+      t0 = __ldcg(&cr->pass);
+      nc = __ldcg(&cr->count);
+      const int64_t off = __ldcg(&cr->pool_off);
+#pragma unroll
+      for (int j0 = 0; j0 < TT_RAYS; j0 += 32) {
+        const int j = j0 + lane;
+        if (j >= ja && j < jb) {
+          ng_ray r;
+          if (SO && cam_rays) camera_ray(cam, r0 + j, r);
+          else load_ray_slab(rays, r0 + j, so, r);
+          bool general = true;
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            if (!SO) W->o[j][a] = r.o[a];
+            W->inv[j][a] = r.inv[a];
+            general = general && isfinite(r.o[a]) && isfinite(r.inv[a]) && !((r.flags >> (3 + a)) & 1);
+          }
+          W->flags[j] = r.flags | (general ? TT_GENERAL : 0);
+        }
+        W->seg_s[j] = 0;
+        W->seg_e[j] = 0;
+      }
+      const TileList L0 = tile_list(W, ga, gcap, t0 & 1, scap);
+      for (int i = lane; i < nc; i += 32) {
+        const int2 e = __ldcg(pool + off + i);
+        if (i < L0.scap) L0.s[i] = e;
+        else if (i - L0.scap < gcap) L0.g[i - L0.scap] = e;
+      }
+      __syncwarp();
+    } else {
+    r0 = (int64_t)tile * TT_RAYS;
+    nr = (int)((n - r0) < TT_RAYS ? (n - r0) : TT_RAYS);
+    jb = nr;
+    // ---- the tile's rays, and the root list: rays whose box test hits B
     {
       const TileList L0 = tile_list(W, ga, gcap, 0, scap);
 #pragma unroll
@@ -560,9 +702,14 @@ __global__ void __launch_bounds__(TT_WPB * 32, NG_TT_MINB) k_traverse_tiles(
         nc += __popc(rb);
       }
     }
+    // (an arena too small for even the root list: truncate like any list,
+    // and the overflow asks for a rerun)
+    need = nc > need ? nc : need;
+    nc = nc < lim ? nc : lim;
+    }
     __syncwarp();
     // ---- level passes: hits at level t -> hit children at level t+1
-    for (int t = 0; t < target; ++t) {
+    for (int t = t0; t < target; ++t) {
       const TileList src = tile_list(W, ga, gcap, t & 1, scap);
       const TileList dst = tile_list(W, ga, gcap, (t & 1) ^ 1, scap);
       const int cres = level_res(tree, t - tree.n_virtual + 1);
@@ -647,6 +794,76 @@ __global__ void __launch_bounds__(TT_WPB * 32, NG_TT_MINB) k_traverse_tiles(
       if (lane == t + 1) level_cnt += out;
       need = out > need ? out : need;
       nc = out < lim ? out : lim;
+      // ---- split a long list at a ray boundary near its middle (above)
+      // (only once every tile is claimed: before that idle warps take fresh
+      // tiles, and a split only adds work)
+      if (t + 1 < target && out > TT_SPLIT && out <= lim && jb - ja > 1 &&
+          *(volatile unsigned int*)tile_counter >= (unsigned)n_tiles) {
+#ifdef NG_PROFILE
+        unsigned long long ts0 = 0;
+        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(ts0));
+        ++n_splits;
+#endif
+        // first entry of the ray holding the middle entry, else of the next ray
+        const int rm = tl_ray(dst, nc / 2);
+        int lo = 0, hi = nc / 2;  // lower bound of rm (entries are grouped by ray, ascending)
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (tl_ray(dst, mid) < rm) lo = mid + 1; else hi = mid;
+        }
+        int m = lo;
+        if (m == 0) {
+          lo = nc / 2;
+          hi = nc;
+          while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (tl_ray(dst, mid) <= rm) lo = mid + 1; else hi = mid;
+          }
+          m = lo;
+        }
+        if (m > 0 && m < nc) {
+          const int cnt = nc - m;
+          int slot = -1;
+          unsigned long long off = 0;
+          if (lane == 0) {
+            off = atomicAdd(pool_top, (unsigned)cnt);
+            if ((int64_t)off + cnt <= TT_CONT_POOL) {
+              atomicAdd(pending, 1u);
+              const unsigned tl = atomicAdd(q_tail, 1u);
+              if (tl < (unsigned)TT_CONT_RECS) slot = (int)tl;
+              else atomicSub(pending, 1u);  // (consumers drop tickets past the last record)
+            }
+          }
+          slot = __shfl_sync(FULL, slot, 0);
+          off = __shfl_sync(FULL, off, 0);
+          if (slot >= 0) {
+            for (int i = lane; i < cnt; i += 32) {
+              const int k = m + i;
+              __stcg(pool + off + i, k < dst.scap ? dst.s[k] : dst.g[k - dst.scap]);
+            }
+            const int jm = tl_ray(dst, m);
+            if (lane == 0) {
+              TileCont* cr = recs + slot;
+              cr->r0 = r0;
+              cr->pool_off = (int64_t)off;
+              cr->nr = nr;
+              cr->ja = jm;
+              cr->jb = jb;
+              cr->pass = t + 1;
+              cr->count = cnt;
+            }
+            __syncwarp();
+            red_add_release_u32(ready + slot, 1u);  // every lane: its pool stores (lane 0: the fields) first
+            nc = m;
+            jb = jm;
+          }
+        }
+#ifdef NG_PROFILE
+        unsigned long long ts1 = 0;
+        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(ts1));
+        split_ns += ts1 - ts0;
+#endif
+      }
     }
     // ---- final pairs: claim the tile's block of the hit list, write
     // (cell, voxel, t_enter, t_exit) and the per-ray segments (set above)
@@ -697,7 +914,7 @@ __global__ void __launch_bounds__(TT_WPB * 32, NG_TT_MINB) k_traverse_tiles(
       const int j = j0 + lane;
       bool has = false;
       int64_t s0 = 0, e0 = 0;
-      if (j < nr) {
+      if (j >= ja && j < jb) {
         s0 = hbase + W->seg_s[j];
         e0 = hbase + W->seg_e[j];
         s0 = s0 < hit_cap ? s0 : hit_cap;
@@ -716,8 +933,22 @@ __global__ void __launch_bounds__(TT_WPB * 32, NG_TT_MINB) k_traverse_tiles(
             make_int4((int)(r0 + j), (int)(e0 - s0), (int)(uint32_t)s0, (int)(s0 >> 32));
     }
     __syncwarp();
+    if (lane == 0) atomicSub(pending, 1u);  // (after this part's outputs)
 #ifdef NG_PROFILE
-    if (lane == 0 && g_tile_prof && (long long)tile < g_tile_prof_cap) {
+    if (lane == 0 && g_part_prof) {
+      unsigned long long tp1;
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(tp1));
+      const unsigned k = atomicAdd(&g_part_next, 1u);
+      if (k < (1u << 20)) {
+        unsigned long long* pp = g_part_prof + 8 * (size_t)k;
+        pp[0] = tp0; pp[1] = tp1; pp[2] = (unsigned long long)(long long)rec; pp[3] = tile;
+        pp[4] = (unsigned long long)t0; pp[5] = (unsigned long long)gw; pp[6] = (unsigned long long)n_splits;
+        pp[7] = split_ns;
+      }
+    }
+#endif
+#ifdef NG_PROFILE
+    if (lane == 0 && rec < 0 && g_tile_prof && (long long)tile < g_tile_prof_cap) {
       unsigned long long tp1;
       asm volatile("mov.u64 %0, %globaltimer;" : "=l"(tp1));
       unsigned long long* pr = g_tile_prof + 4 * (int64_t)tile;
@@ -924,8 +1155,11 @@ int traverse_tiles(const ng_octree& tree, const ng_ray* rays, const int64_t* d_n
                    ng_hit_pair* hits, int64_t hit_cap, void* ctl, int64_t* seg_start, int64_t* seg_end,
                    void* arena, size_t arena_bytes, unsigned long long* d_need, const double* shared_origin,
                    const ng_camera* cam_rays, const ng_frame* defaults, uint32_t bg, int64_t n_host,
-                   cudaStream_t s) {
-  // `ctl` (zeroed by the caller): u32 tile counter at 0, u64 hit cursor at 8
+                   void* cont, cudaStream_t s) {
+  // `ctl` (512 bytes zeroed by the caller): u32 tile counter at 0, u64 hit
+  // cursor at 8, longest list at 16, continuation queue words at 128, 132,
+  // 256 and 384; `cont`:
+  // tile_cont_bytes() of continuation records and pooled entries
   SharedOrigin so;
   so.shared = shared_origin != nullptr;
   for (int a = 0; a < 3; ++a) so.o[a] = shared_origin ? shared_origin[a] : 0.0;
@@ -937,7 +1171,7 @@ int traverse_tiles(const ng_octree& tree, const ng_ray* rays, const int64_t* d_n
       tree, rays, d_n, target, counts, hits, hit_cap, (unsigned int*)ctl, (unsigned long long*)((char*)ctl + 8),
       seg_start, seg_end, (uint8_t*)arena, gcap, tile_traverse_scap(), d_need, so,
       cam_rays ? *cam_rays : ng_camera{}, cam_rays != nullptr, items, d_active, defaults ? *defaults : ng_frame{},
-      bg, n_host, target == tree.n_tlevels - 1);
+      bg, n_host, target == tree.n_tlevels - 1, (uint8_t*)cont);
   NG_CHECK_LAUNCH("k_traverse_tiles");
   return NG_OK;
 }
@@ -1031,6 +1265,24 @@ int ng_ray_aabb(const double* o, const double* d, const double* lo, const double
 }  // extern "C"
 
 #ifdef NG_PROFILE
+extern "C" int ng_part_profile(unsigned long long* host_out, int reset) {
+  unsigned long long* p = nullptr;
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(&p, g_part_prof, sizeof(p));
+  if (!p) {
+    cudaMalloc((void**)&p, (size_t)8 * 8 << 20);
+    cudaMemcpyToSymbol(g_part_prof, &p, sizeof(p));
+  }
+  unsigned n = 0;
+  cudaMemcpyFromSymbol(&n, g_part_next, sizeof(n));
+  if (n > (1u << 20)) n = 1u << 20;
+  if (host_out && n) cudaMemcpy(host_out, p, (size_t)n * 64, cudaMemcpyDeviceToHost);
+  if (reset) {
+    unsigned z = 0;
+    cudaMemcpyToSymbol(g_part_next, &z, sizeof(z));
+  }
+  return (int)n;
+}
 extern "C" int ng_tile_profile_enable(long long max_tiles) {
   unsigned long long* p = nullptr;
   if (cudaMalloc((void**)&p, (size_t)max_tiles * 32) != cudaSuccess) return NG_ERR_CUDA;

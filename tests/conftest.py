@@ -16,6 +16,19 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")
 
 
+@pytest.fixture(autouse=True)
+def _drain_gpu(request):
+    """After every GPU test, wait for the device: work a test left queued
+    (a side stream, an unsynchronised launch) is charged to that test, not
+    to whichever test next shares the GPU."""
+    yield
+    if request.node.get_closest_marker("gpu") is None:
+        return
+    import torch
+    if torch.cuda.is_available() and torch.cuda.is_initialized():
+        torch.cuda.synchronize()
+
+
 @pytest.fixture(scope="session")
 def golden():
     cache = {}

@@ -134,9 +134,15 @@ def test_bench_spawns_its_ranks():
     (here on one GPU over gloo) and prints one line with n_gpus = 2."""
     env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")}
     env["NG_DIST_BACKEND"] = "gloo"
-    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "3",
-                        "--warmup", "3", "--no-query", "--no-cpu", "--no-extra", "--no-train"],
-                       capture_output=True, text=True, timeout=900, env=env, cwd=ROOT)
+    try:
+        r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "3",
+                            "--warmup", "3", "--no-query", "--no-cpu", "--no-extra", "--no-train"],
+                           capture_output=True, text=True, timeout=300, env=env, cwd=ROOT)
+    except subprocess.TimeoutExpired as e:  # show where the ranks were
+        err = e.stderr.decode() if isinstance(e.stderr, bytes) else (e.stderr or "")
+        out = e.stdout.decode() if isinstance(e.stdout, bytes) else (e.stdout or "")
+        raise AssertionError("bench.py --gpus 2 timed out\n" + out[-2000:] + "\n" +
+                             "\n".join(ln for ln in err.splitlines() if "NCCL INFO" not in ln)[-4000:])
     assert r.returncode == 0, r.stderr[-3000:]
     lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
     assert len(lines) == 1, r.stdout[-2000:]

@@ -82,3 +82,26 @@ we = np.array(list(w_end.values()))
 print(f"warp end us: median {np.median(we):.1f} p90 {np.percentile(we, 90):.1f} max {we.max():.1f}")
 print(f"pairs vs time: corr {np.corrcoef(a[:, 2], dur)[0, 1]:.3f}; us per 100 final pairs (heavy tiles) "
       f"{np.median(dur[a[:, 2] > 500] / a[a[:, 2] > 500, 2] * 100) if (a[:, 2] > 500).any() else 0:.2f}")
+# per-part records (continuations included): NG_PROFILE builds with ng_part_profile
+if hasattr(lib, "ng_part_profile"):
+    lib.ng_part_profile(None, 1)
+    step()
+    torch.cuda.synchronize()
+    pb = (ctypes.c_ulonglong * (8 << 20))()
+    k = lib.ng_part_profile(pb, 1)
+    p = np.frombuffer(pb, dtype=np.uint64)[:8 * k].reshape(-1, 8).astype(np.int64)
+    if k:
+        t0p = p[:, 0].min()
+        pdur = (p[:, 1] - p[:, 0]) / 1e3
+        cont = p[:, 2] >= 0
+        print(f"parts {k}: fresh {int((~cont).sum())}, continuations {int(cont.sum())}, splits {int(p[:, 6].sum())}, "
+              f"split time {p[:, 7].sum() / 1e3:.0f} us total")
+        for nm, sel in (("fresh", ~cont), ("cont", cont)):
+            if sel.any():
+                d = pdur[sel]
+                print(f"  {nm}: median {np.median(d):.1f} p99 {np.percentile(d, 99):.1f} max {d.max():.1f} us; "
+                      f"split us in the slowest: {p[sel][np.argmax(d), 7] / 1e3:.1f} ({p[sel][np.argmax(d), 6]} splits)")
+        o = np.argsort(-pdur)[:6]
+        for i in o:
+            print(f"   part rec {p[i, 2]} tile {p[i, 3]} t0 {p[i, 4]} start {(p[i, 0] - t0p) / 1e3:.1f} "
+                  f"dur {pdur[i]:.1f} splits {p[i, 6]} split_us {p[i, 7] / 1e3:.1f}")
