@@ -535,8 +535,120 @@ def forward_levels_device(svo, dfield: DeviceField, pts: torch.Tensor, levels, c
 
 
 def forward_levels(svo, Z, decoders, x, levels) -> np.ndarray:
-    pts = np.atleast_2d(np.asarray(x, dtype=np.float64))
-    return forward_levels_device(svo, DeviceField(Z, decoders), _dev_points(pts), levels).cpu().numpy()
+    return _host_query(svo, DeviceField(Z, decoders), x, levels)
+
+
+# ----------------------------------------------------- host arrays in and out
+
+# Points per pipelined chunk of a host query (24 B in, 8 B per level out).
+HOST_CHUNK = 1 << 21
+_STAGING = threading.local()
+
+
+class _Staging:
+    """Per thread and device: pinned host buffers, device buffers and a copy
+    stream for two chunks in flight (reused across calls)."""
+
+    def __init__(self, dev, ncols):
+        self.dev, self.ncols = dev, ncols
+        self.pin_in = [torch.empty((HOST_CHUNK, 3), dtype=torch.float64, pin_memory=True) for _ in range(2)]
+        self.pin_out = [torch.empty((HOST_CHUNK, ncols), dtype=torch.float64, pin_memory=True) for _ in range(2)]
+        self.d_in = [torch.empty((HOST_CHUNK, 3), dtype=torch.float64, device=dev) for _ in range(2)]
+        self.d_out = [torch.empty((HOST_CHUNK, ncols), dtype=torch.float64, device=dev) for _ in range(2)]
+        self.copy = torch.cuda.Stream(dev)
+
+
+def _staging(dev, ncols) -> _Staging:
+    cache = getattr(_STAGING, "d", None)
+    if cache is None:
+        cache = _STAGING.d = {}
+    st = cache.get((dev, ncols))
+    if st is None:
+        st = cache[(dev, ncols)] = _Staging(dev, ncols)
+    return st
+
+
+def _host_query(svo, dfield: DeviceField, x, levels, counter: EvalCounter | None = None) -> np.ndarray:
+    """forward_levels with host arrays: chunks of HOST_CHUNK points go
+    numpy -> pinned (torch's multithreaded copy) -> HBM on a copy stream,
+    through the query kernel on the caller's stream, and back HBM -> pinned
+    -> the result array, two chunks in flight, so the PCIe copies, the
+    kernel and the host copies overlap. The domain check
+    (StructuralError, octree.py:268-269) runs on the device beside the
+    query (points outside are clipped into the domain by the kernels'
+    binning, so the query is safe to run first) and is raised before any
+    result is returned."""
+    levels = sorted(set(int(v) for v in levels))
+    for L in levels:
+        _check_level(L, dfield.n_decoders)
+    mask = 0
+    for L in levels:
+        mask |= 1 << (L - 1)
+    pts = np.ascontiguousarray(np.atleast_2d(np.asarray(x, dtype=np.float64)))
+    n, ncols = len(pts), len(levels)
+    out = np.empty((n, ncols), dtype=np.float64)
+    if n == 0:
+        return out
+    if pts.shape[1] != 3:
+        raise StructuralError("points must be (n, 3)")
+    dev = _lib.device()
+    st = _staging(dev, ncols)
+    cur = torch.cuda.current_stream(dev)
+    cnt = _Counters()
+    lo = torch.full((1,), np.inf, dtype=torch.float64, device=dev)
+    hi = torch.full((1,), -np.inf, dtype=torch.float64, device=dev)
+    args = _lib.NgQueryArgs(mask, -1, 0, 0, 0.0)
+    ev_h2d = [torch.cuda.Event(), torch.cuda.Event()]
+    ev_k = [torch.cuda.Event(), torch.cuda.Event()]
+    ev_d2h = [torch.cuda.Event(), torch.cuda.Event()]
+    used = [False, False]
+    st.copy.wait_stream(cur)  # the caller's queued work (e.g. a field update) first
+    pending = None
+
+    def drain(p):
+        s, a, b = p
+        ev_d2h[s].synchronize()
+        torch.from_numpy(out[a:b]).copy_(st.pin_out[s][:b - a])
+
+    for i, a in enumerate(range(0, n, HOST_CHUNK)):
+        b = min(a + HOST_CHUNK, n)
+        m, s = b - a, i % 2
+        if used[s]:
+            ev_h2d[s].synchronize()  # pin_in[s] was read by its last H2D
+        st.pin_in[s][:m].copy_(torch.from_numpy(pts[a:b]))
+        with torch.cuda.stream(st.copy):
+            if used[s]:
+                st.copy.wait_event(ev_k[s])  # d_in[s] was read by its last kernel
+            st.d_in[s][:m].copy_(st.pin_in[s][:m], non_blocking=True)
+            ev_h2d[s].record(st.copy)
+        cur.wait_event(ev_h2d[s])
+        if used[s]:
+            cur.wait_event(ev_d2h[s])  # d_out[s] was read by its last D2H
+        d_in, d_out = st.d_in[s][:m], st.d_out[s][:m]
+        mn, mx = torch.aminmax(d_in)
+        torch.minimum(lo, mn, out=lo)
+        torch.maximum(hi, mx, out=hi)
+        call("ng_query", svo.device.ref(), dfield.ref(), ctypes.byref(args), ptr(d_in), m, ptr(d_out), cnt.ptr(),
+             stream_ptr())
+        ev_k[s].record(cur)
+        with torch.cuda.stream(st.copy):
+            st.copy.wait_event(ev_k[s])
+            st.pin_out[s][:m].copy_(d_out, non_blocking=True)
+            ev_d2h[s].record(st.copy)
+        used[s] = True
+        if pending is not None:
+            drain(pending)  # the previous chunk, while this one runs
+        pending = (s, a, b)
+    drain(pending)
+    cur.wait_stream(st.copy)
+    if float(lo.item()) < DOMAIN_MIN or float(hi.item()) > DOMAIN_MAX:
+        raise StructuralError("point outside the domain box")
+    c = cnt.host()
+    if c[3]:
+        raise OctfieldError("non-finite decoder input")
+    if counter is not None:
+        counter.add(c)
+    return out
 
 
 # host parameter arrays -> the fields holding a device copy of them, so an
@@ -601,8 +713,7 @@ class NeuralField:
         return forward(self.svo, self.Z, self.decoders, x, L, self.device)
 
     def forward_levels(self, x, levels):
-        pts = np.atleast_2d(np.asarray(x, dtype=np.float64))
-        return forward_levels_device(self.svo, self.device, _dev_points(pts), levels).cpu().numpy()
+        return _host_query(self.svo, self.device, x, levels)
 
 
 def new_field(svo: SparseVoxelOctree, m: int = FEATURE_DIM, h: int = HIDDEN_DIM, seed: int = 0) -> NeuralField:

@@ -75,6 +75,39 @@ def test_configs2_query_2e24(work):
     decs = [O.OracleDecoder(d.W1, d.b1, d.W2, d.b2) for d in fld.decoders]
     ref = O.forward_levels(tree, fld.Z, decs, pts_h[rows], [1, 2, 3, 4, 5])
     np.testing.assert_allclose(out[rows], ref, atol=SDF_TOL, rtol=0)
+    # the public host-array call (chunked, pipelined through pinned staging)
+    # returns the device call's values bit for bit
+    host = fld.forward_levels(pts_h, [1, 2, 3, 4, 5])
+    np.testing.assert_array_equal(host, out)
+
+
+def test_host_query_chunks_and_errors(work):
+    """NeuralField.forward_levels on host arrays: ragged chunk counts, a
+    column subset, empty input, an out-of-domain point in a later chunk
+    (StructuralError, octree.py:268-269) and a NaN point (the device call's
+    outcome)."""
+    bench, knot, svo, fld = work
+    import torch
+    from paper_2101_10994_b200.errors import OctfieldError, StructuralError
+    from paper_2101_10994_b200.field import HOST_CHUNK, forward_levels_device
+    rng = np.random.default_rng(5)
+    for n in (1, 1000, HOST_CHUNK, 2 * HOST_CHUNK + 12345):
+        pts = rng.uniform(-1.0, 1.0, size=(n, 3))
+        want = forward_levels_device(svo, fld.device, torch.from_numpy(pts).cuda(), [2, 5]).cpu().numpy()
+        np.testing.assert_array_equal(fld.forward_levels(pts, [5, 2]), want)
+    assert fld.forward_levels(np.zeros((0, 3)), [1]).shape == (0, 1)
+    bad = rng.uniform(-1.0, 1.0, size=(HOST_CHUNK + 7, 3))
+    bad[HOST_CHUNK + 3, 1] = 1.0 + 1e-12
+    with pytest.raises(StructuralError):
+        fld.forward_levels(bad, [1, 2])
+    bad[HOST_CHUNK + 3, 1] = np.nan  # passes the domain test (as in the reference); same outcome as the device call
+    try:
+        want = forward_levels_device(svo, fld.device, torch.from_numpy(bad).cuda(), [1, 2]).cpu().numpy()
+    except OctfieldError:
+        with pytest.raises(OctfieldError):
+            fld.forward_levels(bad, [1, 2])
+    else:
+        np.testing.assert_array_equal(fld.forward_levels(bad, [1, 2]), want)
 
 
 @pytest.fixture(scope="module")
