@@ -479,6 +479,9 @@ __device__ __forceinline__ unsigned octants_front_to_back(unsigned x, int dm) {
 #define NG_TT_SPLIT 256
 #endif
 constexpr int TT_SPLIT = NG_TT_SPLIT;
+#ifndef NG_TT_SPLIT_AHEAD
+#define NG_TT_SPLIT_AHEAD 0  // splits start this many tiles per warp before the last tile is claimed
+#endif
 constexpr int TT_CONT_RECS = 16384;         // continuation records per pass
 #ifndef NG_TT_HELPERS
 #define NG_TT_HELPERS 2
@@ -798,7 +801,8 @@ __global__ void __launch_bounds__(TT_WPB * 32, NG_TT_MINB) k_traverse_tiles(
       // (only once every tile is claimed: before that idle warps take fresh
       // tiles, and a split only adds work)
       if (t + 1 < target && out > TT_SPLIT && out <= lim && jb - ja > 1 &&
-          *(volatile unsigned int*)tile_counter >= (unsigned)n_tiles) {
+          (int64_t)*(volatile unsigned int*)tile_counter + NG_TT_SPLIT_AHEAD * (int64_t)gridDim.x * TT_WPB >=
+              n_tiles) {
 #ifdef NG_PROFILE
         unsigned long long ts0 = 0;
         asm volatile("mov.u64 %0, %globaltimer;" : "=l"(ts0));
