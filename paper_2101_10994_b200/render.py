@@ -532,7 +532,7 @@ class RenderSession:
         ev2 bracket traversal+march and normals (ev1 is recorded by the C side)."""
         fs = self.frame_struct(frame)
         fstruct = prepare_presum(self.fld, cfg)
-        graphed = camera is not None and _graphs_enabled() and self._graph_misses < 8
+        graphed = camera is not None and _graphs_enabled() and self._graph_misses < 16
         if timed and not graphed:
             self.ev1.record()  # materialise the handle; re-recorded mid-frame
             self.ws.ev_trace_done = self.ev1.cuda_event
@@ -564,7 +564,9 @@ class RenderSession:
                     launch()
                 else:
                     if g is None:  # a few graphs: consecutive frames alternate buffers
-                        if len(self._graphs) >= 4:
+                        # (render_frames keeps three frames alive: their
+                        # buffers cycle through a handful of address sets)
+                        if len(self._graphs) >= 16:
                             self._graphs.pop(next(iter(self._graphs)))
                         g = torch.cuda.CUDAGraph()
                         # one capture at a time in the process (entering a capture
@@ -680,6 +682,63 @@ def render(camera: Camera, fld: NeuralField, config: RenderConfig):
     ms_normals = sess.ev1.elapsed_time(sess.ev2)
     fb = FrameBuffer(camera.width, camera.height, frame, camera=camera, prefetched={"color": color_h})
     report = FrameReport(ms_trace=float(ms_trace), ms_normals=float(ms_normals),
+                         evals=int(st.counters.decoder_evals), visible=int(st.visible), lod=lod,
+                         shadowed=int(st.shadowed))
+    return fb, report
+
+
+def render_frames(cameras, fld: NeuralField, config: RenderConfig):
+    """Render a sequence of cameras; yields (FrameBuffer, FrameReport) per
+    camera, in order, exactly as `render` returns them. Frame i + 1 is
+    launched before frame i's colour image and statistics are read back
+    (double-buffered readback): each frame's device-to-host copies and host
+    work overlap the next frame's kernels, the way a real-time loop
+    consumes frames. A frame whose lists overflowed is grown and re-rendered
+    with `render` before it is yielded. `report.ms_trace` is the whole
+    frame's device time (the normals run inside the march)."""
+    pending = None
+    stats_host = {}
+    k = 0
+    for camera in cameras:
+        lod = resolve_lod(camera, fld, config)
+        cfg = resolve_config(fld, config, lod)
+        sess = _session(fld, camera.width, camera.height)
+        frame = sess.new_frame()
+        ev_a, ev_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev_a.record()
+        sess.enqueue(cfg, frame, camera=camera)
+        ev_b.record()
+        color_h = torch.empty(frame["color"].shape, dtype=torch.uint8, pin_memory=True)
+        color_h.copy_(frame["color"], non_blocking=True)
+        key = (id(sess), k % 2)
+        st_h = stats_host.get(key)
+        if st_h is None:
+            st_h = stats_host[key] = torch.zeros_like(sess.stats, device="cpu").pin_memory()
+        st_h.copy_(sess.stats, non_blocking=True)
+        done = torch.cuda.Event()
+        done.record()
+        if pending is not None:
+            yield _finish_frame(*pending)
+        pending = (camera, fld, config, lod, cfg, sess, frame, color_h, st_h, done, ev_a, ev_b)
+        k += 1
+    if pending is not None:
+        yield _finish_frame(*pending)
+
+
+def _finish_frame(camera, fld, config, lod, cfg, sess, frame, color_h, st_h, done, ev_a, ev_b):
+    done.synchronize()
+    raw = st_h.numpy().tobytes()
+    st = _lib.NgFrameStats.from_buffer_copy(raw[:ctypes.sizeof(_lib.NgFrameStats)])
+    n_levels = cfg.trace_level + fld.svo.device.n_virtual
+    if st.overflow:  # grow, then this frame again (synchronously)
+        sess.grow(st, n_levels)
+        return render(camera, fld, config)
+    if st.counters.nonfinite_inputs:
+        raise OctfieldError("non-finite decoder input")
+    if st.counters.evals_missing_level != 0:
+        raise OctfieldError("internal: decoder ran outside the queried level's voxels")
+    fb = FrameBuffer(camera.width, camera.height, frame, camera=camera, prefetched={"color": color_h})
+    report = FrameReport(ms_trace=float(ev_a.elapsed_time(ev_b)), ms_normals=0.0,
                          evals=int(st.counters.decoder_evals), visible=int(st.visible), lod=lod,
                          shadowed=int(st.shadowed))
     return fb, report

@@ -82,3 +82,29 @@ def test_threshold_lod_frames_golden(ng, golden, tag):
     np.testing.assert_array_equal(di[..., 0], di[..., 2])
     ddiff = np.abs(di.astype(int) - g[f"{tag}_depth_image_5.0"].astype(int))
     assert ddiff[both].max(initial=0) <= 1 and np.all(di[~fb.hit] == 0)
+
+
+def test_render_frames_equals_render(ng, golden):
+    """render_frames (double-buffered readback) yields, frame by frame,
+    exactly what render() returns; an overflowing first frame is grown and
+    re-rendered before it is yielded."""
+    from paper_2101_10994_b200 import scenes
+    from oracle import nglod_oracle as O
+    R = sys.modules["paper_2101_10994_b200.render"]
+    go = golden("octree")
+    svo = ng.build_octree(O.sdf_torus(0.5, 0.2), 4, go["samples_b"])
+    fld = scenes.planted_field(svo, O.sdf_torus(0.5, 0.2), seed=0, device_sdf=False)
+    cams = [ng.Camera((0.0, 2.0, 3.5), (0.0, 0.0, 0.0), (0.0, 1.0, 0.0), 30.0, 96, 72),
+            ng.Camera((2.5, 2.0, 2.0), (0.0, 0.0, 0.0), (0.0, 1.0, 0.0), 35.0, 96, 72),
+            ng.Camera((0.0, 2.0, 3.5), (0.0, 0.0, 0.0), (0.0, 1.0, 0.0), 30.0, 96, 72)]
+    cfg = ng.RenderConfig()
+    want = [ng.render(c, fld, cfg) for c in cams]
+    sess = R._session(fld, 96, 72)
+    sess.pair_cap = sess.hit_cap = 64  # the first streamed frame overflows
+    sess._alloc_ws()
+    got = list(ng.render_frames(cams, fld, cfg))
+    assert len(got) == len(cams)
+    for (fb, rep), (fw, rw) in zip(got, want):
+        for k in ("hit", "t", "normal", "normal_ok", "iterations", "evals", "color"):
+            np.testing.assert_array_equal(getattr(fb, k), getattr(fw, k), err_msg=k)
+        assert (rep.visible, rep.evals, rep.lod) == (rw.visible, rw.evals, rw.lod)
