@@ -536,61 +536,54 @@ __global__ void __launch_bounds__(TT_WPB * 32, NG_TT_MINB) k_traverse_tiles(
   int64_t level_cnt = 0;  // lane t: pairs emitted at traversal level t
   int need = 0;
   // continuation queue (control words after the tile counter, hit cursor
-  // and longest list, zeroed with them): records pushed / claimed, parts in
-  // progress (tiles + continuations), pool entries used
-  // (each on its own 128-byte line: idle warps poll the queue words, and
-  // the tile counter and `pending` take an atomic per tile)
-  unsigned int* q_tail = tile_counter + 32;
+  // and longest list, zeroed with them, each group on its own 128-byte
+  // line): `qstate` = records pushed << 32 | continuations finished (one
+  // word, so one load is a consistent snapshot), the claim cursor, fresh
+  // tiles finished, pool entries used
+  unsigned long long* qstate = reinterpret_cast<unsigned long long*>(tile_counter + 32);
   unsigned int* q_head = tile_counter + 64;
-  unsigned int* pending = tile_counter + 96;
-  unsigned int* pool_top = tile_counter + 48;  // (pushers only)
+  unsigned int* tiles_done = tile_counter + 96;
+  unsigned int* pool_top = tile_counter + 16;
   unsigned int* ready = reinterpret_cast<unsigned int*>(cont);
   TileCont* recs = reinterpret_cast<TileCont*>(cont + (size_t)TT_CONT_RECS * 4);
   int2* pool = reinterpret_cast<int2*>(cont + (size_t)TT_CONT_RECS * (4 + sizeof(TileCont)));
   bool tiles_left = true;
   while (true) {
-    // ---- work: a published continuation first, else a fresh tile; with
-    // neither, wait while any part is in progress (it may still split)
+    // ---- work: a fresh tile while any is left (continuations only appear
+    // once every tile is claimed), then published continuations; idle
+    // helper warps wait while a part may still split
     int rec = -1;
     unsigned int tile = 0xffffffffu;
     if (lane == 0) {
-      unsigned backoff = 256;
-      int ticket = -1;  // a claimed queue position, served once published
-      while (true) {
-        const unsigned tl = *(volatile unsigned*)q_tail;
-        if (ticket < 0 && *(volatile unsigned*)q_head < tl) {
-          ticket = (int)atomicAdd(q_head, 1u);  // (fetch-add: a CAS loop serialised the claims)
-          if (ticket >= TT_CONT_RECS) ticket = INT_MAX;  // past the last record: no more work for it
+      if (tiles_left) {
+        tile = atomicAdd(tile_counter, 1u);
+        if ((int64_t)tile >= n_tiles) {
+          tiles_left = false;
+          tile = 0xffffffffu;
         }
-        if (ticket >= 0) {
-          if ((unsigned)ticket < tl) {
+      }
+      if (!tiles_left) {
+        unsigned backoff = 256;
+        int ticket = -1;  // a claimed queue position, served once published
+        while (true) {
+          const unsigned long long qs = *(volatile unsigned long long*)qstate;
+          const unsigned tl = (unsigned)(qs >> 32), fin = (unsigned)qs;
+          if (ticket < 0 && *(volatile unsigned*)q_head < tl) {
+            ticket = (int)atomicAdd(q_head, 1u);  // (fetch-add: a CAS loop serialised the claims)
+            if (ticket >= TT_CONT_RECS) ticket = INT_MAX;  // past the last record: never served
+          }
+          if (ticket >= 0 && (unsigned)ticket < tl) {
             rec = ticket;
             break;
           }
-          // the ticket passed the published records: it is served by the
-          // next push, or dropped when nothing is in progress any more
-          if (*(volatile unsigned*)pending == 0 && (unsigned)ticket >= *(volatile unsigned*)q_tail) break;
+          // every part finished (fresh tiles, then every pushed continuation:
+          // a push precedes its pusher's own finish) -> nothing can be pushed
+          const bool all_done = *(volatile unsigned*)tiles_done >= (unsigned)n_tiles && fin == tl;
+          if (ticket < 0 ? (warp >= TT_HELPERS || (all_done && *(volatile unsigned*)q_head >= tl)) : all_done)
+            break;  // (non-helper warps leave when idle; a ticket is kept until served or moot)
           __nanosleep(backoff);
           backoff = backoff < 8192 ? 2 * backoff : backoff;
-          continue;
         }
-        if (tiles_left) {
-          atomicAdd(pending, 1u);
-          tile = atomicAdd(tile_counter, 1u);
-          if ((int64_t)tile < n_tiles) break;
-          atomicSub(pending, 1u);
-          tiles_left = false;
-          tile = 0xffffffffu;
-          continue;
-        }
-        // idle: all but TT_HELPERS warps per CTA leave; the helpers wait for
-        // continuations while any part is in progress (few pollers keep the
-        // queue words' L2 lines free for the pushers' atomics)
-        if (warp >= TT_HELPERS ||
-            (*(volatile unsigned*)pending == 0 && *(volatile unsigned*)q_head >= *(volatile unsigned*)q_tail))
-          break;
-        __nanosleep(backoff);
-        backoff = backoff < 8192 ? 2 * backoff : backoff;
       }
     }
     rec = __shfl_sync(FULL, rec, 0);
@@ -832,10 +825,9 @@ __global__ void __launch_bounds__(TT_WPB * 32, NG_TT_MINB) k_traverse_tiles(
           if (lane == 0) {
             off = atomicAdd(pool_top, (unsigned)cnt);
             if ((int64_t)off + cnt <= TT_CONT_POOL) {
-              atomicAdd(pending, 1u);
-              const unsigned tl = atomicAdd(q_tail, 1u);
+              const unsigned tl = (unsigned)(atomicAdd(qstate, 1ull << 32) >> 32);
               if (tl < (unsigned)TT_CONT_RECS) slot = (int)tl;
-              else atomicSub(pending, 1u);  // (consumers drop tickets past the last record)
+              else atomicAdd(qstate, 1ull);  // never published: counted finished (tickets past it are moot)
             }
           }
           slot = __shfl_sync(FULL, slot, 0);
@@ -937,7 +929,10 @@ __global__ void __launch_bounds__(TT_WPB * 32, NG_TT_MINB) k_traverse_tiles(
             make_int4((int)(r0 + j), (int)(e0 - s0), (int)(uint32_t)s0, (int)(s0 >> 32));
     }
     __syncwarp();
-    if (lane == 0) atomicSub(pending, 1u);  // (after this part's outputs)
+    if (lane == 0) {  // (after this part's outputs)
+      if (rec >= 0) atomicAdd(qstate, 1ull);
+      else atomicAdd(tiles_done, 1u);
+    }
 #ifdef NG_PROFILE
     if (lane == 0 && g_part_prof) {
       unsigned long long tp1;
@@ -1161,8 +1156,8 @@ int traverse_tiles(const ng_octree& tree, const ng_ray* rays, const int64_t* d_n
                    const ng_camera* cam_rays, const ng_frame* defaults, uint32_t bg, int64_t n_host,
                    void* cont, cudaStream_t s) {
   // `ctl` (512 bytes zeroed by the caller): u32 tile counter at 0, u64 hit
-  // cursor at 8, longest list at 16, continuation queue words at 128, 132,
-  // 256 and 384; `cont`:
+  // cursor at 8, longest list at 16, pool cursor at 64, continuation queue
+  // words at 128, 256 and 384; `cont`:
   // tile_cont_bytes() of continuation records and pooled entries
   SharedOrigin so;
   so.shared = shared_origin != nullptr;
