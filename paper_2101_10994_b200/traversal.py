@@ -4,7 +4,8 @@ All rays descend together one level per pass. Each pass is one kernel that
 fuses decide (fp64 slab test + occupied-child count), the exclusive scan
 (decoupled look-back) and subdivide (children front to back) -- or, at the
 target level, compactify with entry/exit distances. Lists are bit-identical
-to the reference's, including order (tests/test_gpu_traversal.py).
+to the reference's, including order (tests/test_gpu_parity.py::test_traversal_golden_bit_exact;
+the render path's lists: tests/test_gpu_render_lists.py).
 """
 
 from __future__ import annotations
