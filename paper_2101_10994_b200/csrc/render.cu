@@ -719,8 +719,10 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_cons
     if constexpr (PS) {
       // x lies in the pair's voxel (clamped above), which is locate's answer
       // (a probe point is located as usual)
-      if constexpr (TC) er = warp_eval_presum(tree, c, ws, eact, x, tcm, emit, act ? (int64_t)h.voxel : -1);
-      else er = warp_eval_presum(tree, c, ws, eact, x, SimtMlp{c}, emit, act ? (int64_t)h.voxel : -1);
+      // (four groups: 128 registers, so 4 points' rows per gather round)
+      constexpr int GBM = NW >= 16 ? 4 : NG_GATHER_BATCH;
+      if constexpr (TC) er = warp_eval_presum<GBM>(tree, c, ws, eact, x, tcm, emit, act ? (int64_t)h.voxel : -1);
+      else er = warp_eval_presum<GBM>(tree, c, ws, eact, x, SimtMlp{c}, emit, act ? (int64_t)h.voxel : -1);
     } else {
       if constexpr (TC) er = warp_eval(tree, c, ws, eact, x, tcm, emit);
       else er = warp_eval(tree, c, ws, eact, x, SimtMlp{c}, emit);
@@ -1101,13 +1103,13 @@ static bool use_tc_decoder(const ng_field& f) {
   return env && f.h == tc::N;
 }
 
-static int tc_groups() {
-  // NG_TC_GROUPS: 4-warp tile groups per CTA (experiment knob; default 3)
-  static const int g = [] {
-    const int v = env_int("NG_TC_GROUPS", 3);
-    return (v < 1 || v > 4) ? 3 : v;
-  }();
-  return g;
+// 4-warp tile groups per CTA: the march runs four (the whole TMEM, 128
+// registers, 4-point gather rounds; 720p 0.651 -> 0.627 ms against three
+// groups with 8-point rounds), the normals pass three; NG_TC_GROUPS
+// overrides both (experiment knob)
+static int tc_groups(int dflt) {
+  static const int g = env_int("NG_TC_GROUPS", 0);
+  return (g >= 1 && g <= 4) ? g : dflt;
 }
 
 template <class KT, class Args>
@@ -1125,10 +1127,11 @@ static int launch_tc(KT ktc, int groups, const ng_field& f, const ng_octree& tre
 
 template <class KS, class K1, class K2, class K3, class K4, class Args>
 static int launch_eval_kernel(KS ksimt, K1 k1, K2 k2, K3 k3, K4 k4, const ng_field& f, const ng_octree& tree,
-                              const Args& A, int64_t max_units, bool cap_by_work, const char* name, cudaStream_t s) {
+                              const Args& A, int64_t max_units, bool cap_by_work, const char* name, cudaStream_t s,
+                              int default_groups = 3) {
   const int ndec = A.dec_last - A.dec_first + 1;
   int per_sm, r;
-  int groups = tc_groups();
+  int groups = tc_groups(default_groups);
   while (groups > 1 && tc_smem_bytes(ndec, groups) > 227 * 1024) --groups;
   if (use_tc_decoder(f) && tc_smem_bytes(ndec, groups) <= 227 * 1024) {
     if (groups == 1) r = launch_tc(k1, 1, f, tree, A, max_units, cap_by_work, s);
@@ -1160,7 +1163,8 @@ static int launch_march(const ng_octree& tree, const ng_field& f, MarchArgs& A, 
   A.lane_cap = cap_env;
   if (presum_applies(f, A.G, A.out_mask, A.cfg.trace_level))
     return launch_eval_kernel(k_march<R_NW, false, true>, k_march<4, true, true>, k_march<8, true, true>,
-                              k_march<12, true, true>, k_march<16, true, true>, f, tree, A, 0, false, "k_march", s);
+                              k_march<12, true, true>, k_march<16, true, true>, f, tree, A, 0, false, "k_march", s,
+                              4);
   return launch_eval_kernel(k_march<R_NW, false, false>, k_march<4, true, false>, k_march<8, true, false>,
                             k_march<12, true, false>, k_march<16, true, false>, f, tree, A, 0, false, "k_march", s);
 }
