@@ -23,6 +23,12 @@
 #ifndef NG_PROF_SLOTS
 #define NG_PROF_SLOTS 32   // NG_PROFILE builds: uint64 counters per march group (tools/march_profile.py)
 #endif
+#ifndef NG_STAGE_GATHER
+// presummed direct-z gather: 4 more points per round staged in shared
+// memory with cp.async (experiment knob; measured slower on the 720p frame:
+// 0.650 vs 0.630 ms with .ca, 0.646 with .cg)
+#define NG_STAGE_GATHER 0
+#endif
 #ifndef NG_QUAD_GATHER
 #define NG_QUAD_GATHER 1   // warp_eval: 16-byte row loads, 4 points per load instruction
 #endif
@@ -32,8 +38,18 @@ namespace ng {
 struct WarpScratch {
   int4 ids[32][2];      // corner ids of each lane's point at the current level
   float4 w[32][2];      // trilinear weights
-  float zt[32][33];     // running feature sum, row = point, col = channel (+1 pad)
+  float zt[32][33];     // running feature sum, row = point, col = channel (+1 pad);
+                        // the presummed direct-z gather stages 4 points' rows here instead
 };
+
+// Asynchronous 16-byte global -> shared copies (LDGSTS): rows land in
+// shared memory without occupying registers while in flight.
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 struct EvalCtx {
   const float* __restrict__ Z;       // (C, 32)
@@ -451,12 +467,35 @@ __device__ __forceinline__ EvalLane warp_eval_presum(const ng_octree& tree, cons
       // 16-byte row loads: lane = (point slot lane / 8, channel quad lane % 8)
       const int grp = lane >> 3, sub = lane & 7;
       const float4* __restrict__ S4 = reinterpret_cast<const float4*>(Sc - lane) + sub;
+      // With the direct-z decoder the zt scratch is free: 4 more points per
+      // round stage their rows there with cp.async (no registers in flight)
+      // while the register path loads and sums its GB points; they are summed
+      // after, from shared memory, with the same FMA order.
+      constexpr bool kStage = Mlp::kDirectZ && NG_STAGE_GATHER;
+      float4* const stage = reinterpret_cast<float4*>(&ws.zt[0][0]);  // [grp][row][sub]
       while (pm) {
         int pp[GB];
 #pragma unroll
         for (int q = 0; q < GB; ++q) {
           pp[q] = pm ? __ffs(pm) - 1 : -1;
           pm &= pm ? pm - 1 : 0u;
+        }
+        int smine = -1;
+        if constexpr (kStage) {
+          int ps[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            ps[q] = pm ? __ffs(pm) - 1 : -1;
+            pm &= pm ? pm - 1 : 0u;
+          }
+          smine = grp == 0 ? ps[0] : (grp == 1 ? ps[1] : (grp == 2 ? ps[2] : ps[3]));
+          if (smine >= 0) {
+            const int4 a = ws.ids[smine][0], b = ws.ids[smine][1];
+            const int id[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+            for (int j = 0; j < 8; ++j) cp_async16(stage + (grp * 8 + j) * 8 + sub, S4 + 8 * (int64_t)id[j]);
+          }
+          cp_async_commit();
         }
         int mine[GB / 4];
         float4 v[GB / 4][8];
@@ -501,6 +540,32 @@ __device__ __forceinline__ EvalLane warp_eval_presum(const ng_octree& tree, cons
 #pragma unroll
             for (int e = 0; e < 4; ++e) zr[e] = acc[e];
           }
+        }
+        if constexpr (kStage) {  // the staged point: each lane reads back the rows it copied
+          cp_async_wait_all();
+          if (smine >= 0) {
+            const float4 u0 = ws.w[smine][0], u1 = ws.w[smine][1];
+            const float wj[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
+            float4 r[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) r[j] = stage[(grp * 8 + j) * 8 + sub];
+            float acc[4];
+            acc[0] = wj[0] * r[0].x;
+            acc[1] = wj[0] * r[0].y;
+            acc[2] = wj[0] * r[0].z;
+            acc[3] = wj[0] * r[0].w;
+#pragma unroll
+            for (int jj = 1; jj < 8; ++jj) {
+              acc[0] = fmaf(wj[jj], r[jj].x, acc[0]);
+              acc[1] = fmaf(wj[jj], r[jj].y, acc[1]);
+              acc[2] = fmaf(wj[jj], r[jj].z, acc[2]);
+              acc[3] = fmaf(wj[jj], r[jj].w, acc[3]);
+            }
+            mlp.put_z4(smine, sub, acc);
+            zbad |= (isfinite(acc[0]) && isfinite(acc[1]) && isfinite(acc[2]) && isfinite(acc[3]) ? 0u : 1u)
+                    << smine;
+          }
+          __syncwarp();  // the stage is rewritten next round
         }
       }
     } else
