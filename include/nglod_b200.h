@@ -317,8 +317,10 @@ size_t ng_render_workspace_bytes(int64_t n_rays, int64_t pair_capacity, int64_t 
  * (ng_hit_pair, tile order; .ray holds the voxel's packed cell
  * x | y << 10 | z << 20 on the tile path, the ray id otherwise), out[1] /
  * out[2] the per-ray segments [start, end) into it (int64), out[3] the total
- * size. n_out <= 4 entries are written. Lets callers and tests read the
- * render path's per-ray voxel lists back without re-running a traversal. */
+ * size, out[4] the tile traversal's control words (u64 at +128: the
+ * continuation records pushed << 32 | finished). n_out <= 5 entries are
+ * written. Lets callers and tests read the render path's per-ray voxel
+ * lists back without re-running a traversal. */
 int ng_render_workspace_offsets(int64_t n_rays, int64_t pair_capacity, int64_t hit_capacity,
                                 int64_t* out, int32_t n_out);
 /* sphere_trace (render.py:174-274) over an existing final list. */

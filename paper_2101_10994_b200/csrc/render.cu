@@ -1559,8 +1559,9 @@ int ng_render_workspace_offsets(int64_t n_rays, int64_t pair_capacity, int64_t h
     return NG_ERR_STRUCTURAL;
   }
   const WsLayout L = layout(n_rays, pair_capacity, hit_capacity);
-  const int64_t v[4] = {(int64_t)L.hits, (int64_t)L.seg_start, (int64_t)L.seg_end, (int64_t)L.total};
-  for (int i = 0; i < n_out && i < 4; ++i) out[i] = v[i];
+  const int64_t v[5] = {(int64_t)L.hits, (int64_t)L.seg_start, (int64_t)L.seg_end, (int64_t)L.total,
+                        (int64_t)L.scratch};
+  for (int i = 0; i < n_out && i < 5; ++i) out[i] = v[i];
   return NG_OK;
 }
 

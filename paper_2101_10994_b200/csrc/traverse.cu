@@ -469,19 +469,17 @@ __device__ __forceinline__ unsigned octants_front_to_back(unsigned x, int dm) {
 // (one warp runs every round), so a few grazing tiles (~3,000 final pairs,
 // ~190 us) outlast all the others when a frame has few tiles per warp (a
 // band of an N-GPU frame). After a level pass, a list longer than
-// NG_TT_SPLIT entries that covers several rays is cut at a ray boundary near
+// NG_TILE_SPLIT entries that covers several rays is cut at a ray boundary near
 // its middle: the warp keeps the first rays and publishes the rest (their
 // entries copied to a pool) as a continuation that any warp takes before a
 // fresh tile. A ray's pairs stay in one part, and each part claims its own
 // block of the hit list, so every ray's segment is still the reference's
 // sub-list in order (traversal.py:207-247); only block placement changes.
-#ifndef NG_TT_SPLIT
-#define NG_TT_SPLIT 256
-#endif
-constexpr int TT_SPLIT = NG_TT_SPLIT;
-#ifndef NG_TT_SPLIT_AHEAD
-#define NG_TT_SPLIT_AHEAD 0  // splits start this many tiles per warp before the last tile is claimed
-#endif
+// Run-time knobs (read once per process): NG_TILE_SPLIT, the list length
+// above which a list is split (default 256; a huge value disables
+// splitting), and NG_TILE_SPLIT_AHEAD, tiles per warp before the last tile
+// is claimed at which splitting starts (default 0; the tests set both low
+// to split every tile they can).
 constexpr int TT_CONT_RECS = 16384;         // continuation records per pass
 #ifndef NG_TT_HELPERS
 #define NG_TT_HELPERS 2
@@ -520,7 +518,8 @@ __global__ void __launch_bounds__(TT_WPB * 32, NG_TT_MINB) k_traverse_tiles(
     unsigned long long* hit_cursor, int64_t* __restrict__ seg_start, int64_t* __restrict__ seg_end,
     uint8_t* arena, int64_t gcap, int scap, unsigned long long* d_need, const SharedOrigin so,
     const ng_camera cam, int cam_rays, int4* __restrict__ items, unsigned long long* d_active,
-    const ng_frame fr, uint32_t bg, int64_t n_host, int cull, uint8_t* __restrict__ cont) {
+    const ng_frame fr, uint32_t bg, int64_t n_host, int cull, uint8_t* __restrict__ cont, int split_at,
+    int split_ahead) {
   extern __shared__ __align__(16) uint8_t tt_smem[];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -793,9 +792,8 @@ __global__ void __launch_bounds__(TT_WPB * 32, NG_TT_MINB) k_traverse_tiles(
       // ---- split a long list at a ray boundary near its middle (above)
       // (only once every tile is claimed: before that idle warps take fresh
       // tiles, and a split only adds work)
-      if (t + 1 < target && out > TT_SPLIT && out <= lim && jb - ja > 1 &&
-          (int64_t)*(volatile unsigned int*)tile_counter + NG_TT_SPLIT_AHEAD * (int64_t)gridDim.x * TT_WPB >=
-              n_tiles) {
+      if (t + 1 < target && out > split_at && out <= lim && jb - ja > 1 &&
+          (int64_t)*(volatile unsigned int*)tile_counter + split_ahead * (int64_t)gridDim.x * TT_WPB >= n_tiles) {
 #ifdef NG_PROFILE
         unsigned long long ts0 = 0;
         asm volatile("mov.u64 %0, %globaltimer;" : "=l"(ts0));
@@ -1128,6 +1126,14 @@ int tile_traverse_scap() {
   static const int scap = std::max(0, std::min(TT_SCAP, env_int("NG_TILE_SCAP", TT_SCAP)));
   return scap;
 }
+static int tile_split_at() {
+  static const int v = std::max(1, env_int("NG_TILE_SPLIT", 256));
+  return v;
+}
+static int tile_split_ahead() {
+  static const int v = std::max(0, env_int("NG_TILE_SPLIT_AHEAD", 0));
+  return v;
+}
 int tile_traverse_entry_bytes() { return 2 * TT_ENTRY; }
 
 // Warps the tile traversal runs with for up to `n_rays` rays (grid x
@@ -1170,7 +1176,7 @@ int traverse_tiles(const ng_octree& tree, const ng_ray* rays, const int64_t* d_n
       tree, rays, d_n, target, counts, hits, hit_cap, (unsigned int*)ctl, (unsigned long long*)((char*)ctl + 8),
       seg_start, seg_end, (uint8_t*)arena, gcap, tile_traverse_scap(), d_need, so,
       cam_rays ? *cam_rays : ng_camera{}, cam_rays != nullptr, items, d_active, defaults ? *defaults : ng_frame{},
-      bg, n_host, target == tree.n_tlevels - 1, (uint8_t*)cont);
+      bg, n_host, target == tree.n_tlevels - 1, (uint8_t*)cont, tile_split_at(), tile_split_ahead());
   NG_CHECK_LAUNCH("k_traverse_tiles");
   return NG_OK;
 }

@@ -35,6 +35,11 @@ def frames(tmp_path_factory):
         "spill": _probe(tmp, "spill", {"NG_TILE_SCAP": "3"}),
         "overflow": _probe(tmp, "overflow", {"NG_TILE_SCAP": "0", "NG_TILE_ARENA_MIN": "0"}, "tiny_pairs"),
         "normals_pass": _probe(tmp, "normals_pass", {"NG_FUSED_PROBES": "0"}),
+        # split every list longer than 2 entries from the first tile on
+        # (continuations, the entry pool and the ticket queue on every tile)
+        "split": _probe(tmp, "split", {"NG_TILE_SPLIT": "2", "NG_TILE_SPLIT_AHEAD": "1000000"}),
+        "split_spill": _probe(tmp, "split_spill", {"NG_TILE_SPLIT": "2", "NG_TILE_SPLIT_AHEAD": "1000000",
+                                                   "NG_TILE_SCAP": "3"}),
     }
 
 
@@ -65,6 +70,26 @@ def test_overflow_grows_and_reruns(frames):
     f = frames["overflow"]
     assert int(f["grows"]) >= 1
     _same(f, frames["tiles"])
+
+
+def _same_lists(a, b):
+    for k in ("l_rays", "l_voxels", "l_t_enter", "l_t_exit"):
+        np.testing.assert_array_equal(a[k], b[k], err_msg=k)
+
+
+def test_split_tiles_identical(frames):
+    """Tiles split into continuations at ray boundaries (traverse.cu) give
+    the same per-ray lists (order included) and the same frame, with the
+    lists in shared memory or in the spill arena."""
+    assert len(frames["tiles"]["l_rays"]) > 1000
+    for k in ("split", "split_spill"):
+        assert int(frames[k]["splits"]) > 10, f"{k}: no tile was split"
+        _same_lists(frames[k], frames["tiles"])
+        _same(frames[k], frames["tiles"])
+
+
+def test_tile_lists_equal_level_by_level(frames):
+    _same_lists(frames["tiles"], frames["levels"])
 
 
 def test_probes_in_march_equal_normals_pass(frames):
