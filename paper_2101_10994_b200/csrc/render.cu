@@ -380,9 +380,10 @@ struct DecoderSetup {
   WarpScratch* ws = nullptr;
   TcSmem t;
   uint32_t tmem_base = 0;
-  __device__ __forceinline__ DecoderSetup(uint8_t* smem, const ng_field& f, int first, int last, int groups) {
+  __device__ __forceinline__ DecoderSetup(uint8_t* smem, const ng_field& f, int first, int last, int groups,
+                                          size_t ws_bytes = sizeof(WarpScratch)) {
     if constexpr (TC) {
-      t = tc_carve(smem, last - first + 1, groups);
+      t = tc_carve(smem, last - first + 1, groups, ws_bytes);
       tmem_base = tc_setup(t, f.decoders, first, last, f.dec_stride, groups);
       ws = t.ws;
     } else {
@@ -399,10 +400,12 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_cons
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   __shared__ int gflag[2][NW];  // step parity: a warp is never two steps ahead of its group
   constexpr int GROUPS = TC ? NW / 4 : 1;
-  DecoderSetup<TC> D(smem_raw, f, A.dec_first, A.dec_last, GROUPS);
+  // (the presummed tensor-core march never touches WarpScratch::zt)
+  constexpr size_t WSB = (TC && PS) ? WS_COMPACT_BYTES : sizeof(WarpScratch);
+  DecoderSetup<TC> D(smem_raw, f, A.dec_first, A.dec_last, GROUPS, WSB);
   const int w = threadIdx.x >> 5;
   const int g = w / 4;
-  WarpScratch& ws = D.ws[w];
+  WarpScratch& ws = TC ? D.t.scratch(w) : D.ws[w];
   uint32_t phase = 0;
   TcMlp tcm;
   if constexpr (TC) {
@@ -1114,9 +1117,9 @@ static int tc_groups(int dflt) {
 
 template <class KT, class Args>
 static int launch_tc(KT ktc, int groups, const ng_field& f, const ng_octree& tree, const Args& A, int64_t max_units,
-                     bool cap_by_work, cudaStream_t s) {
+                     bool cap_by_work, cudaStream_t s, size_t ws_bytes) {
   const int ndec = A.dec_last - A.dec_first + 1;
-  const size_t smem = tc_smem_bytes(ndec, groups);
+  const size_t smem = tc_smem_bytes(ndec, groups, ws_bytes);
   int per_sm, r;
   if ((r = prep_kernel(ktc, smem, groups * 128, per_sm))) return r;
   int64_t grid = (int64_t)sm_count() * per_sm;
@@ -1128,16 +1131,16 @@ static int launch_tc(KT ktc, int groups, const ng_field& f, const ng_octree& tre
 template <class KS, class K1, class K2, class K3, class K4, class Args>
 static int launch_eval_kernel(KS ksimt, K1 k1, K2 k2, K3 k3, K4 k4, const ng_field& f, const ng_octree& tree,
                               const Args& A, int64_t max_units, bool cap_by_work, const char* name, cudaStream_t s,
-                              int default_groups = 3) {
+                              int default_groups = 3, size_t ws_bytes = sizeof(WarpScratch)) {
   const int ndec = A.dec_last - A.dec_first + 1;
   int per_sm, r;
   int groups = tc_groups(default_groups);
-  while (groups > 1 && tc_smem_bytes(ndec, groups) > 227 * 1024) --groups;
-  if (use_tc_decoder(f) && tc_smem_bytes(ndec, groups) <= 227 * 1024) {
-    if (groups == 1) r = launch_tc(k1, 1, f, tree, A, max_units, cap_by_work, s);
-    else if (groups == 2) r = launch_tc(k2, 2, f, tree, A, max_units, cap_by_work, s);
-    else if (groups == 3) r = launch_tc(k3, 3, f, tree, A, max_units, cap_by_work, s);
-    else r = launch_tc(k4, 4, f, tree, A, max_units, cap_by_work, s);
+  while (groups > 1 && tc_smem_bytes(ndec, groups, ws_bytes) > 227 * 1024) --groups;
+  if (use_tc_decoder(f) && tc_smem_bytes(ndec, groups, ws_bytes) <= 227 * 1024) {
+    if (groups == 1) r = launch_tc(k1, 1, f, tree, A, max_units, cap_by_work, s, ws_bytes);
+    else if (groups == 2) r = launch_tc(k2, 2, f, tree, A, max_units, cap_by_work, s, ws_bytes);
+    else if (groups == 3) r = launch_tc(k3, 3, f, tree, A, max_units, cap_by_work, s, ws_bytes);
+    else r = launch_tc(k4, 4, f, tree, A, max_units, cap_by_work, s, ws_bytes);
     if (r) return r;
   } else {
     const size_t smem = (size_t)ndec * f.dec_stride * 4 + R_NW * sizeof(WarpScratch);
@@ -1164,7 +1167,7 @@ static int launch_march(const ng_octree& tree, const ng_field& f, MarchArgs& A, 
   if (presum_applies(f, A.G, A.out_mask, A.cfg.trace_level))
     return launch_eval_kernel(k_march<R_NW, false, true>, k_march<4, true, true>, k_march<8, true, true>,
                               k_march<12, true, true>, k_march<16, true, true>, f, tree, A, 0, false, "k_march", s,
-                              4);
+                              4, WS_COMPACT_BYTES);
   return launch_eval_kernel(k_march<R_NW, false, false>, k_march<4, true, false>, k_march<8, true, false>,
                             k_march<12, true, false>, k_march<16, true, false>, f, tree, A, 0, false, "k_march", s);
 }

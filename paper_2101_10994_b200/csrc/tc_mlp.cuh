@@ -190,21 +190,33 @@ struct TcSmem {
   uint8_t* dec_tiles;
   uint8_t* a_tiles;
   WarpScratch* ws;
+  size_t ws_stride;  // bytes per warp's scratch
   uint64_t* mbar;
   uint32_t* tmem_slot;
+  __device__ __forceinline__ WarpScratch& scratch(int w) const {
+    return *reinterpret_cast<WarpScratch*>(reinterpret_cast<uint8_t*>(ws) + (size_t)w * ws_stride);
+  }
 };
 
-__host__ __device__ constexpr size_t tc_smem_bytes(int ndec, int groups) {
-  return (size_t)ndec * DEC_TC_BYTES + (size_t)groups * 2 * tc::TILE_BYTES + (size_t)groups * 4 * sizeof(WarpScratch) +
+// A kernel whose decoder takes z straight into the operand rows (the
+// presummed path) never touches WarpScratch::zt: its warps get only the
+// ids and weights, which frees shared memory for a fourth group with two
+// decoders (the LOD blend) and for L1.
+constexpr size_t WS_COMPACT_BYTES = offsetof(WarpScratch, zt);
+static_assert(WS_COMPACT_BYTES % 16 == 0, "compact scratch keeps 16-byte alignment");
+
+__host__ __device__ constexpr size_t tc_smem_bytes(int ndec, int groups, size_t ws_bytes = sizeof(WarpScratch)) {
+  return (size_t)ndec * DEC_TC_BYTES + (size_t)groups * 2 * tc::TILE_BYTES + (size_t)groups * 4 * ws_bytes +
          (size_t)groups * 8 + 16;
 }
 
-__device__ __forceinline__ TcSmem tc_carve(uint8_t* smem, int ndec, int groups) {
+__device__ __forceinline__ TcSmem tc_carve(uint8_t* smem, int ndec, int groups, size_t ws_bytes = sizeof(WarpScratch)) {
   TcSmem t;
   t.dec_tiles = smem;
   t.a_tiles = t.dec_tiles + (size_t)ndec * DEC_TC_BYTES;
   t.ws = reinterpret_cast<WarpScratch*>(t.a_tiles + (size_t)groups * 2 * tc::TILE_BYTES);
-  t.mbar = reinterpret_cast<uint64_t*>(t.ws + groups * 4);
+  t.ws_stride = ws_bytes;
+  t.mbar = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(t.ws) + (size_t)groups * 4 * ws_bytes);
   t.tmem_slot = reinterpret_cast<uint32_t*>(t.mbar + groups);
   return t;
 }
