@@ -406,7 +406,7 @@ def run_ours(args, rank: int, world: int):
         for _ in range(6):
             fb, _r = ng.render(cam, fld, config)
             _ = fb.color
-        for fb, _r in ng.render_frames([cam] * 8, fld, config):  # (its frame graphs: three buffer sets)
+        for fb, _r in ng.render_frames([cam] * 12, fld, config):  # (its frame graphs: a few buffer sets)
             _ = fb.color
         torch.cuda.synchronize()
         # render_frames: each frame's colour image and statistics come back

@@ -699,6 +699,8 @@ def render_frames(cameras, fld: NeuralField, config: RenderConfig):
     pending = None
     stats_host = {}
     k = 0
+    cur = torch.cuda.current_stream()
+    copy = torch.cuda.Stream()  # the colour readback runs beside the next frame's kernels
     for camera in cameras:
         lod = resolve_lod(camera, fld, config)
         cfg = resolve_config(fld, config, lod)
@@ -708,8 +710,9 @@ def render_frames(cameras, fld: NeuralField, config: RenderConfig):
         ev_a.record()
         sess.enqueue(cfg, frame, camera=camera)
         ev_b.record()
-        color_h = torch.empty(frame["color"].shape, dtype=torch.uint8, pin_memory=True)
-        color_h.copy_(frame["color"], non_blocking=True)
+        # the statistics (one small buffer every frame writes) are copied on
+        # the frame's stream; the 2.8 MB colour image on the copy stream, so
+        # its transfer overlaps the next frame instead of queueing before it
         key = (id(sess), k % 2)
         st_h = stats_host.get(key)
         if st_h is None:
@@ -717,6 +720,15 @@ def render_frames(cameras, fld: NeuralField, config: RenderConfig):
         st_h.copy_(sess.stats, non_blocking=True)
         done = torch.cuda.Event()
         done.record()
+        color = frame["color"]
+        color_h = torch.empty(color.shape, dtype=torch.uint8, pin_memory=True)
+        copy.wait_event(ev_b)
+        with torch.cuda.stream(copy):
+            color_h.copy_(color, non_blocking=True)
+        color.record_stream(copy)  # (the caching allocator keeps the buffer until the copy ran)
+        done_copy = torch.cuda.Event()
+        done_copy.record(copy)
+        done = (done, done_copy)
         if pending is not None:
             yield _finish_frame(*pending)
         pending = (camera, fld, config, lod, cfg, sess, frame, color_h, st_h, done, ev_a, ev_b)
@@ -726,7 +738,8 @@ def render_frames(cameras, fld: NeuralField, config: RenderConfig):
 
 
 def _finish_frame(camera, fld, config, lod, cfg, sess, frame, color_h, st_h, done, ev_a, ev_b):
-    done.synchronize()
+    for ev in done:
+        ev.synchronize()
     raw = st_h.numpy().tobytes()
     st = _lib.NgFrameStats.from_buffer_copy(raw[:ctypes.sizeof(_lib.NgFrameStats)])
     n_levels = cfg.trace_level + fld.svo.device.n_virtual
