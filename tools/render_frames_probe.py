@@ -1,5 +1,7 @@
+"""render_frames (double-buffered readback) vs render() frames/s on the 720p
+knot frame, end to end with the colour image on the host."""
 import os, sys, time
-sys.path.insert(0, "/root/repo")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch, bench, paper_2101_10994_b200 as ng, importlib
 R = importlib.import_module("paper_2101_10994_b200.render")
 knot, svo, fld = bench.build_workload()
