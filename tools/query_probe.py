@@ -30,4 +30,5 @@ for _ in range(7):
     ms.append(a.elapsed_time(b))
 z = fld.device.Z
 print(f"flush {mode}  best {bench.QUERY_POINTS / min(ms) / 1e3:.0f} Mpts/s  median {bench.QUERY_POINTS / sorted(ms)[3] / 1e3:.0f}"
-      f"  Z {z.data_ptr():#x} ({z.numel() * 4 >> 20} MiB)  pts {pts.data_ptr():#x}  out {out.data_ptr():#x}")
+      f"  Z {z.data_ptr():#x} ({z.numel() * 4 >> 20} MiB)  pts {pts.data_ptr():#x}  out {out.data_ptr():#x}"
+      f"  calls ms {[round(v, 2) for v in ms]}")
