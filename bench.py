@@ -483,10 +483,13 @@ def query_leg(knot, svo, fld, dev, flush, rank: int, world: int):
     sum_k = cnt.decoder_evals - cnt.evals_missing_level
     torch.cuda.synchronize()
     qe = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(QUERY_TIMED)]
+    # the output stays resident (out=): a fresh 671 MB allocation per call
+    # while the previous result is alive made single calls take up to 4x
+    # longer (profiles/r02/query_kernel_probe.log)
     for a, b in qe:
         flush.zero_()
         a.record()
-        out = forward_levels_device(svo, fld.device, pts, QUERY_LEVELS)
+        forward_levels_device(svo, fld.device, pts, QUERY_LEVELS, out=out)
         b.record()
     torch.cuda.synchronize()
     ms = sorted(a.elapsed_time(b) for a, b in qe)

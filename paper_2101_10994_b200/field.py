@@ -244,9 +244,14 @@ class _Counters:
 
 
 def _run_query(svo, dfield: DeviceField, pts_dev: torch.Tensor, out_levels=0, inside_level=-1,
-               blend_base=0, blend_alpha=0.0, ncols=1, counter: EvalCounter | None = None) -> torch.Tensor:
+               blend_base=0, blend_alpha=0.0, ncols=1, counter: EvalCounter | None = None,
+               out: torch.Tensor | None = None) -> torch.Tensor:
     n = pts_dev.shape[0]
-    out = torch.empty((n, ncols), dtype=torch.float64, device=pts_dev.device)
+    if out is None:
+        out = torch.empty((n, ncols), dtype=torch.float64, device=pts_dev.device)
+    elif (out.dtype != torch.float64 or tuple(out.shape) != (n, ncols) or not out.is_contiguous()
+          or out.device != pts_dev.device):
+        raise StructuralError(f"out must be a contiguous float64 ({n}, {ncols}) tensor on {pts_dev.device}")
     args = _lib.NgQueryArgs(out_levels, inside_level, blend_base, 0, blend_alpha)
     cnt = _Counters()
     call("ng_query", svo.device.ref(), dfield.ref(), ctypes.byref(args), ptr(pts_dev), n, ptr(out), cnt.ptr(),
@@ -520,18 +525,21 @@ def scatter_add_rows(dst: np.ndarray, idx: np.ndarray, rows: np.ndarray) -> None
     dst[idx_s[starts]] += np.add.reduceat(rows[order], starts, axis=0)
 
 
-def forward_levels_device(svo, dfield: DeviceField, pts: torch.Tensor, levels, counter=None) -> torch.Tensor:
+def forward_levels_device(svo, dfield: DeviceField, pts: torch.Tensor, levels, counter=None,
+                          out: torch.Tensor | None = None) -> torch.Tensor:
     """Batched SDF query on device points: one fp64 column per level in
     `levels` (ascending), each equal to forward(x, L)[0]. All levels share one
     gather pass: z_L is the running prefix sum (the training-forward caller
-    trainer.loss_batch, trainer.py:132-142, recomputes 1..L per L)."""
+    trainer.loss_batch, trainer.py:132-142, recomputes 1..L per L). `out`, a
+    preallocated (n, len(levels)) float64 device tensor, is written in place
+    (a serving loop keeps its output resident instead of allocating per call)."""
     levels = sorted(set(int(v) for v in levels))
     for L in levels:
         _check_level(L, dfield.n_decoders)
     mask = 0
     for L in levels:
         mask |= 1 << (L - 1)
-    return _run_query(svo, dfield, pts, out_levels=mask, ncols=len(levels), counter=counter)
+    return _run_query(svo, dfield, pts, out_levels=mask, ncols=len(levels), counter=counter, out=out)
 
 
 def forward_levels(svo, Z, decoders, x, levels) -> np.ndarray:

@@ -24,7 +24,7 @@ for _ in range(7):
     torch.cuda.synchronize()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
-    out = forward_levels_device(svo, fld.device, pts, [1, 2, 3, 4, 5])
+    forward_levels_device(svo, fld.device, pts, [1, 2, 3, 4, 5], out=out)  # resident output
     b.record()
     torch.cuda.synchronize()
     ms.append(a.elapsed_time(b))
