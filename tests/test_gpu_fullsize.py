@@ -79,6 +79,14 @@ def test_configs2_query_2e24(work):
     # returns the device call's values bit for bit
     host = fld.forward_levels(pts_h, [1, 2, 3, 4, 5])
     np.testing.assert_array_equal(host, out)
+    # a resident output buffer (out=) is written in place with the same values
+    buf = torch.full((bench.QUERY_POINTS, 5), np.nan, dtype=torch.float64, device="cuda")
+    ret = forward_levels_device(svo, fld.device, torch.from_numpy(pts_h).cuda(), [1, 2, 3, 4, 5], out=buf)
+    assert ret is buf
+    np.testing.assert_array_equal(buf.cpu().numpy(), out)
+    from paper_2101_10994_b200.errors import StructuralError
+    with pytest.raises(StructuralError):
+        forward_levels_device(svo, fld.device, torch.from_numpy(pts_h[:10]).cuda(), [1, 2], out=buf)
 
 
 def test_host_query_chunks_and_errors(work):
