@@ -470,6 +470,7 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_cons
   int64_t pk = -1;
   bool pready = false, probes_done = !A.probes;
   int step_parity = 0;
+  unsigned idle_ns = 256;  // back-off of a group waiting for probe items
   // rays the group marched last step: probes are taken only by groups with
   // none left, so they never lengthen the steps of a ray still marching
   int group_marching = 1;
@@ -628,45 +629,19 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_cons
     // a lane stays in the loop while it marches, holds a probe item or may
     // still claim one
     const bool alive = act || pk >= 0 || !probes_done || (!drained && lane < cap);
+    int* gf = gflag[step_parity];
     if constexpr (TC) {
-      // the group's 4 warps step together (one 128-row GEMM per output level)
+      // The group's 4 warps step together (one 128-row GEMM per output
+      // level). Each warp posts its counts here; the decoder's group
+      // barrier inside the evaluation orders them, and every warp reads the
+      // group's totals after it (one barrier per step: a warp's acquire and
+      // gather phases no longer wait for the slowest warp separately).
       const int wf = __popc(__ballot_sync(FULL, act || pact));
       const int wa = __popc(__ballot_sync(FULL, alive));
       const int wm = __popc(__ballot_sync(FULL, act));
-      int* gf = gflag[step_parity];
       step_parity ^= 1;
       if (lane == 0) gf[w] = wf | (wa << 8) | (wm << 16);
-      tc::named_sync(1 + g, 128);
-      const int gs = gf[4 * g] + gf[4 * g + 1] + gf[4 * g + 2] + gf[4 * g + 3];
-      const int active = gs & 0xff, any_alive = (gs >> 8) & 0xff;
-      group_marching = gs >> 16;
-      mark(10);  // group barrier
-#ifdef NG_PROFILE
-      if (gprof && active) {
-        gprof[16] += 1;
-        if (active <= 8) gprof[17] += 1;  // light steps: the tail's per-step latency
-      }
-      light_step = active <= 8;
-#endif
-#ifdef NG_PROFILE
-      if (A.prof && (w & 3) == 0 && lane == 0) {  // debug profile: per-group steps and busy lanes
-        unsigned long long* pr = A.prof + NG_PROF_SLOTS * (blockIdx.x * GROUPS + g);
-        const unsigned long long now = globaltimer_ns();
-        if (pr[0] == 0) pr[2] = t_top;
-        if (active) {
-          pr[0] += 1;
-          pr[1] += active;
-        }
-        pr[3] = now;
-        pr[4] += now - t_top;  // acquire + advance + group barrier
-        t_acq = now;
-      }
-#endif
-      if (!any_alive) break;
-      if (!active) {  // waiting for hits to publish probe items
-        __nanosleep(256);
-        continue;
-      }
+      mark(10);  // (group flags posted)
     } else {
       if (!__any_sync(FULL, alive)) break;
       if (!__any_sync(FULL, act || pact)) {
@@ -741,6 +716,37 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_cons
     }
 #endif
     mark(18);  // query point + evaluation
+    if constexpr (TC) {
+      const int gs = gf[4 * g] + gf[4 * g + 1] + gf[4 * g + 2] + gf[4 * g + 3];
+      const int active = gs & 0xff, any_alive = (gs >> 8) & 0xff;
+      group_marching = gs >> 16;
+#ifdef NG_PROFILE
+      if (gprof && active) {
+        gprof[16] += 1;
+        if (active <= 8) gprof[17] += 1;  // light steps: the tail's per-step latency
+      }
+      light_step = active <= 8;
+      if (A.prof && (w & 3) == 0 && lane == 0) {  // debug profile: per-group steps and busy lanes
+        unsigned long long* pr = A.prof + NG_PROF_SLOTS * (blockIdx.x * GROUPS + g);
+        const unsigned long long now = globaltimer_ns();
+        if (pr[0] == 0) pr[2] = t_top;
+        if (active) {
+          pr[0] += 1;
+          pr[1] += active;
+        }
+        pr[3] = now;
+      }
+#endif
+      if (!any_alive) break;  // (no lane of the group was alive at this step's start)
+      // waiting for hits to publish probe items: an empty step still runs
+      // the group's GEMM, so back off (up to ~4 us) while nothing arrives
+      if (!active) {
+        __nanosleep(idle_ns);
+        idle_ns = idle_ns < 4096 ? 2 * idle_ns : idle_ns;
+      } else {
+        idle_ns = 256;
+      }
+    }
     // ---- stop rules (render.py:247-272)
     if (eact && !er.inside) lc.empty += 1;  // query_field's own empty-space fallback
     if (pact) {
