@@ -308,6 +308,9 @@ struct MarchArgs {
 };
 
 constexpr unsigned PROBE_READY = 0x80000000u;
+#ifdef NG_PROFILE
+__device__ unsigned long long* g_timeline = nullptr;  // ng_march_timeline
+#endif
 
 // Release-ordered atomics for the probe slots: MEMBAR.ALL.GPU before the
 // atomic, no L1 invalidation (a gpu-scope __threadfence or acquire emits
@@ -724,6 +727,15 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_cons
       if (gprof && active) {
         gprof[16] += 1;
         if (active <= 8) gprof[17] += 1;  // light steps: the tail's per-step latency
+      }
+      if (gprof && g_timeline && blockIdx.x < 16) {  // step timeline of 64 groups: (ns, busy lanes)
+        const int gi = blockIdx.x * GROUPS + g;
+        const unsigned k = (unsigned)gprof[20]++;
+        if (gi < 64 && k < 512) {
+          unsigned long long tnow;
+          asm volatile("mov.u64 %0, %globaltimer;" : "=l"(tnow));
+          g_timeline[gi * 512 + k] = (tnow << 8) | (unsigned long long)(active & 0xff);
+        }
       }
       light_step = active <= 8;
       if (A.prof && (w & 3) == 0 && lane == 0) {  // debug profile: per-group steps and busy lanes
@@ -1248,6 +1260,21 @@ static WsLayout layout(int64_t n, int64_t pair_cap, int64_t hit_cap) {
 }
 
 // NG_MARCH_PROFILE=1: per-group march statistics (ng_march_profile).
+#ifdef NG_PROFILE
+extern "C" int ng_march_timeline(unsigned long long* host_out) {  // 64 groups x 512 steps, then reset
+  unsigned long long* p = nullptr;
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(&p, g_timeline, sizeof(p));
+  if (!p) {
+    cudaMalloc((void**)&p, 64 * 512 * 8);
+    cudaMemcpyToSymbol(g_timeline, &p, sizeof(p));
+  } else if (host_out) {
+    cudaMemcpy(host_out, p, 64 * 512 * 8, cudaMemcpyDeviceToHost);
+  }
+  cudaMemset(p, 0, 64 * 512 * 8);
+  return 0;
+}
+#endif
 static unsigned long long* g_prof = nullptr;
 // (a debugging aid of one device: the buffer lives on the device current at
 // the first frame)

@@ -61,12 +61,20 @@ torch.cuda.synchronize()
 SL = 32  # NG_PROF_SLOTS
 buf = (ctypes.c_ulonglong * (SL * 4096))()
 _lib.lib().ng_march_profile(buf, 4096)  # reset
+has_tl = hasattr(_lib.lib(), "ng_march_timeline")
+if has_tl:
+    _lib.lib().ng_march_timeline(None)  # allocate / reset the step timeline
 a0, b0 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 a0.record()
 step()
 b0.record()
 torch.cuda.synchronize()
 n = _lib.lib().ng_march_profile(buf, 4096)
+tl = None
+if has_tl:
+    tbuf = (ctypes.c_ulonglong * (64 * 512))()
+    _lib.lib().ng_march_timeline(tbuf)
+    tl = np.frombuffer(tbuf, dtype=np.uint64).reshape(64, 512)
 a = np.frombuffer(buf, dtype=np.uint64).reshape(-1, SL)[:n].astype(np.int64)
 a = a[a[:, 0] > 0]
 t0 = a[:, 2].min()
@@ -103,6 +111,20 @@ if light:
     print(f"light steps (<= 8 busy lanes): {light}, us per light step {a[:, 19].sum() / light / MHZ:.2f}")
 i = order[-1]
 print("slowest group phases (us/step):", {names[k]: round(a[i, k] / a[i, 16] / MHZ, 3) for k in names})
+# busy lanes per group step over the march's time (64 sampled groups, 10 time bins)
+if tl is not None:
+    ts = (tl >> 8).astype(np.int64)
+    act = (tl & 0xff).astype(np.int64)
+    valid = ts > 0
+    if valid.any():
+        t0l, t1l = ts[valid].min(), ts[valid].max()
+        bins = np.minimum(((ts - t0l) * 10 // max(1, t1l - t0l + 1)), 9)
+        row = []
+        for bi in range(10):
+            sel = valid & (bins == bi)
+            row.append(f"{act[sel].mean():.0f}/{sel.sum()}" if sel.any() else "-")
+        print(f"timeline (64 groups; mean busy lanes per step / steps, per tenth of {(t1l - t0l) / 1e3:.0f} us):",
+              " ".join(row))
 # the frame's ray iteration distribution via the public API (non-profiled timing irrelevant here)
 if world == 1:
     fb, rep = ng.render(cam, fld, config)
