@@ -302,6 +302,7 @@ struct MarchArgs {
   unsigned long long* rays_done;   // rays finished (hits published first)
   unsigned int* probe_cnt;         // per slot: bit 31 published, low bits probes done
   double* probe_val;               // per slot: the 6 probe values
+  double* probe_pt;                // per slot: the hit point, written before the slot is published
   double* normal;
   uint8_t* normal_ok;
   uint8_t* color;                  // null: shading happens later (shadow pass)
@@ -607,14 +608,12 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_cons
         // is seen, and the publisher wrote it before its release
         asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(st) : "l"(A.probe_cnt + sl) : "memory");
         if (st & PROBE_READY) {
-          const int32_t pix = __ldcg(A.hit_list + sl);
-          const double th = __ldcg(A.t + pix);
-          ng_ray rr;
-          ray_at(A.rays, pix, rr);
+          // the hit point the publisher stored with the slot (one L2 round
+          // trip, not hit_list -> t -> the camera ray)
           const int j = (int)(pk % 6), axis = j % 3;
 #pragma unroll
           for (int a = 0; a < 3; ++a) {
-            double v = dadd(rr.o[a], dmul(th, rr.d[a]));  // hit point (render.py:396)
+            double v = __ldcg(A.probe_pt + 3 * sl + a);  // hit point o + t d (render.py:396)
             if (a == axis) v = (j < 3) ? dadd(v, eps) : dsub(v, eps);
             px[a] = np_min(np_max(v, -1.0), 1.0);  // render.py:289-293
           }
@@ -802,7 +801,11 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_cons
         if (A.hit_list) {
           const unsigned long long slot = atomicAdd(A.d_hit_count, 1ull);
           A.hit_list[slot] = r_id;
-          if (A.probes) red_or_release(A.probe_cnt + slot, PROBE_READY);  // publish (t, hit_list written above)
+          if (A.probes) {
+#pragma unroll
+            for (int a = 0; a < 3; ++a) __stcg(A.probe_pt + 3 * slot + a, dadd(o[a], dmul(th, d[a])));
+            red_or_release(A.probe_cnt + slot, PROBE_READY);  // publish (t, hit_list, hit point written above)
+          }
         }
         if (A.probes) atomicAdd(A.rays_done, 1ull);
       } else if (stalled || it >= A.cfg.max_iters) {
@@ -1213,7 +1216,7 @@ struct WsLayout {
   size_t s_rays, s_hit, s_t, s_it, s_ev;  // shadow-ray pass
   size_t sorted, buckets;                 // longest-first march order
   size_t cont;                            // tile traversal continuations (split silhouette tiles)
-  size_t probe_val, probe_cnt;            // normals evaluated in the march
+  size_t probe_val, probe_cnt, probe_pt;  // normals evaluated in the march
   size_t scratch_bytes;
 };
 
@@ -1253,6 +1256,7 @@ static WsLayout layout(int64_t n, int64_t pair_cap, int64_t hit_cap) {
   L.sorted = o; o = al(o + (size_t)n * 4);
   L.probe_val = o; o = al(o + (size_t)n * 6 * 8);
   L.probe_cnt = o; o = al(o + (size_t)n * 4);
+  L.probe_pt = o; o = al(o + (size_t)n * 3 * 8);
   L.buckets = o; o = al(o + 2 * LEN_BUCKETS * 4);
   L.cont = o; o = al(o + tile_cont_bytes());
   L.total = o;
@@ -1495,6 +1499,7 @@ static int render_common(const ng_octree& tree, const ng_field& f, const ng_rend
   A.rays_done = ctr + 6;
   A.probe_cnt = (unsigned int*)(b + L.probe_cnt);
   A.probe_val = (double*)(b + L.probe_val);
+  A.probe_pt = (double*)(b + L.probe_pt);
   A.normal = fr.normal;
   A.normal_ok = fr.normal_ok;
   A.color = cfg.shadows ? nullptr : fr.color;
