@@ -496,7 +496,9 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_cons
     ray = -1;
   };
 
-  unsigned long long t_top = 0, t_acq = 0, t_eval = 0;
+#ifdef NG_PROFILE
+  unsigned long long t_top = 0;
+#endif
   while (true) {
 #ifdef NG_PROFILE
     if (A.prof && (w & 3) == 0 && lane == 0) t_top = globaltimer_ns();
@@ -711,12 +713,6 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_cons
       return field_value(tree, e, v.lo, v.hi, A.blend_alpha, px);
     };
 
-#ifdef NG_PROFILE
-    if (A.prof && (w & 3) == 0 && lane == 0) {
-      t_eval = globaltimer_ns();
-      A.prof[NG_PROF_SLOTS * (blockIdx.x * GROUPS + g) + 5] += t_eval - t_acq;  // gather + decoder
-    }
-#endif
     mark(18);  // query point + evaluation
     if constexpr (TC) {
       const int gs = gf[4 * g] + gf[4 * g + 1] + gf[4 * g + 2] + gf[4 * g + 3];

@@ -628,7 +628,6 @@ __global__ void __launch_bounds__(256) k_train_update(const __grid_constant__ Tr
     return;
   }
   const int64_t n_rows = (int64_t)A.ctr[0];
-  const int LM8 = A.LM * 8;
   for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n_rows;
        i += ((int64_t)row_blocks * blockDim.x) >> 5) {
     const int id = A.touched[i];

@@ -159,7 +159,6 @@ __global__ void __launch_bounds__(TR_NT) k_traverse_hits(
   if (in != nullptr && n > in_cap) n = in_cap;
   const int level = t - tree.n_virtual;
   const int cres = level_res(tree, level + 1);
-  const double cedge = 2.0 / (double)cres;
   const uint64_t* __restrict__ codes = tree.codes[t];
   const int32_t* __restrict__ cstart = tree.child_start[t];
   const uint8_t* __restrict__ cmask = tree.child_mask[t];

@@ -85,14 +85,11 @@ print(f"groups {len(a)}  steps total {steps.sum()}  mean {steps.mean():.1f} max 
 print(f"lane utilisation {busy.sum() / (steps.sum() * 128):.3f}")
 print(f"group end (us): min {dur.min():.0f} median {np.median(dur):.0f} p90 {np.percentile(dur, 90):.0f} "
       f"max {dur.max():.0f}")
-print(f"us per step (median group): {np.median(dur / steps):.2f}  acquire {np.median(a[:, 4] / steps) / 1e3:.2f}  "
-      f"eval {np.median(a[:, 5] / steps) / 1e3:.2f} (decoder {np.median(a[:, 7] / steps) / 1e3:.2f})")
+print(f"us per step (median group): {np.median(dur / steps):.2f}")
 order = np.argsort(dur)
 for q in (0.5, 0.9, 0.99, 1.0):
     i = order[min(len(order) - 1, int(q * len(order)) - (1 if q == 1.0 else 0))]
-    print(f"  q{q}: steps {steps[i]} busy/step {busy[i] / steps[i]:.1f} end {dur[i]:.0f} us  "
-          f"acq/step {a[i, 4] / steps[i] / 1e3:.2f} eval/step {a[i, 5] / steps[i] / 1e3:.2f} "
-          f"dec/step {a[i, 7] / steps[i] / 1e3:.2f}")
+    print(f"  q{q}: steps {steps[i]} busy/step {busy[i] / steps[i]:.1f} end {dur[i]:.0f} us")
 # light-load steps: the slowest 5 groups' last steps are mostly 1-4 lanes
 slow = order[-5:]
 print("slowest groups: steps", steps[slow].tolist(), "busy/step", np.round(busy[slow] / steps[slow], 1).tolist())
