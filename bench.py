@@ -55,6 +55,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--batch", type=int, default=8,
+                    help="frames per launch sequence (ng_render_batch; 1..8): the timed steps are frames, rendered "
+                         "`batch` at a time; each frame's latency alone is reported beside it")
     ap.add_argument("--no-query", action="store_true", help="skip the batched-query leg")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-extra", action="store_true", help="skip the configs[3]/[4] 1080p legs")
@@ -324,63 +327,79 @@ def run_ours(args, rank: int, world: int):
     lod = resolve_lod(cam, fld, config)
     cfg = resolve_config(fld, config, lod)
     # N = 1: one band covering the frame; N > 1: interleaved 8-row bands per
-    # rank + one NCCL all-gather of the colour tiles inside the timed step
-    tiles = TiledRenderer(fld, WIDTH, HEIGHT)
+    # rank + one NCCL all-gather of the colour tiles inside the timed step.
+    # Frames go `batch` per launch sequence (ng_render_batch: one traversal
+    # and one march over every frame's rays, so one frame's longest rays
+    # overlap the other frames' work); a step is still one frame.
+    B = max(1, min(args.batch, 8))
+    tiles = TiledRenderer(fld, WIDTH, HEIGHT, batch=B)
     sess = tiles.sess
     n_levels = cfg.trace_level + svo.device.n_virtual  # index of the final hit count
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
 
-    def step():
-        tiles.enqueue(cam, cfg)
+    def step(k):
+        tiles.enqueue([cam] * k, cfg)
         if world > 1:
-            return tiles.gather_color(dst=0)
+            return tiles.gather(("color",), dst=0, frames=k)
         return None
 
-    # settle capacities (two-phase sizing) before timing
+    # settle capacities (two-phase sizing) for a full batch before timing
+    tiles.render_batch([cam] * B, config)
     img, visible_all, evals_all = tiles.render(cam, config)
     for _ in range(args.warmup):
-        step()
+        step(B)
     torch.cuda.synchronize()
 
-    ev = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(4)) for _ in range(args.steps)]
+    sizes = [B] * (args.steps // B) + ([args.steps % B] if args.steps % B else [])
+    ev = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(4)) for _ in sizes]
     for e in ev:
         for x in e:
             x.record()  # materialise handles
     with ClockSampler(dev.index) as clocks:
         t_load = time.perf_counter()
         while time.perf_counter() - t_load < 1.0:  # steady load so the sampler sees clocks under load
-            step()
+            step(B)
             torch.cuda.synchronize()
         if world > 1:
             torch.distributed.barrier()
         torch.cuda.synchronize()
-        for k in range(args.steps):
-            flush.zero_()  # L2 flush between frames (outside the timed events)
-            e0, e_march0, e_march1, e1 = ev[k]
+        for k, e in zip(sizes, ev):
+            flush.zero_()  # L2 flush between launches (outside the timed events)
+            e0, e_march0, e_march1, e1 = e
             sess.ws.ev_march_begin = e_march0.cuda_event
             sess.ws.ev_trace_done = e_march1.cuda_event
             e0.record()
-            step()
+            step(k)
             e1.record()
         torch.cuda.synchronize()
         if world > 1:
             torch.distributed.barrier()
     sess.ws.ev_march_begin = None
     sess.ws.ev_trace_done = None
-    frame_ms = [a.elapsed_time(b) for a, _, _, b in ev]
-    march_ms = [a.elapsed_time(b) for _, a, b, _ in ev]
+    launch_ms = [a.elapsed_time(b) for a, _, _, b in ev]
+    march_all = [a.elapsed_time(b) for _, a, b, _ in ev]
+    full = [i for i, k in enumerate(sizes) if k == sizes[0]]
+    frame_ms = [launch_ms[i] / sizes[i] for i in full]
+    march_ms = [march_all[i] for i in full]
     st = sess.read_stats()
     assert not st.overflow and st.counters.evals_missing_level == 0 and st.counters.nonfinite_inputs == 0
-    trace_evals = int(tiles.frame["evals"].sum().item())
-    ms_local = sum(frame_ms) / len(frame_ms)
+    trace_evals = int(tiles.frame["evals"][:WIDTH * len(tiles.layout[rank])].sum().item())  # frame 0 of the batch
+    ms_local = sum(launch_ms) / args.steps
     if world > 1:
         ms_local = max_over_ranks(ms_local, dev)
+    # one frame per launch (the latency of a frame alone), same timing
+    lat = TiledRenderer(fld, WIDTH, HEIGHT)
+    lat.render(cam, config)
+    lat_ms = _time_tiled(lat, cam, cfg, max(3, min(args.steps, 20)), flush, world)
     # the last timed frame's per-ray voxel lists (render path), checked
     # against the reference's traversal in the cpu_baseline leg
-    final = tiles.sess.final_list(MAX_LEVEL) if world == 1 else None
+    final = lat.sess.final_list(MAX_LEVEL) if world == 1 else None
+    st = lat.sess.read_stats()  # one frame's list lengths
+    del lat
     res = {
-        "_final": final,
+        "_final": final, "batch": B, "launches": len(sizes), "frames_per_launch": sizes,
         "ms_per_step": ms_local, "frame_ms": frame_ms, "march_ms": march_ms, "trace_evals": trace_evals,
+        "frame_latency_ms": lat_ms,
         "total_evals": evals_all, "visible": visible_all, "clocks": clocks.summary(),
         "pairs": [int(st.pairs[i]) for i in range(n_levels + 1)], "active_rays": int(st.active_rays),
     }
@@ -403,44 +422,48 @@ def run_ours(args, rank: int, world: int):
     if world == 1:
         # warm-up covers the frame-graph captures (render.py: a launch key is
         # captured on its second sight; consecutive frames alternate buffers)
+        e2e_steps = max(2 * B, min(args.steps, 24))
         for _ in range(6):
             fb, _r = ng.render(cam, fld, config)
             _ = fb.color
-        for fb, _r in ng.render_frames([cam] * 12, fld, config):  # (its frame graphs: a few buffer sets)
-            _ = fb.color
+        for _ in range(2):  # (its launch graphs: a few buffer sets)
+            for fb, _r in ng.render_frames([cam] * e2e_steps, fld, config, batch=B):
+                _ = fb.color
         torch.cuda.synchronize()
-        # render_frames: each frame's colour image and statistics come back
-        # while the next frame runs (double-buffered readback); every step
-        # still copies its image to the host inside the timed region
+        # render_frames: `batch` frames per launch sequence; each launch's
+        # colour images and statistics come back while the next one runs
+        # (double-buffered readback); every frame's image is still copied to
+        # the host inside the timed region
         batches = []
-        for _ in range(3):  # the median of three batches (host jitter)
+        for _ in range(3):  # the median of three runs (host jitter)
             t0 = time.perf_counter()
-            for fb, rep in ng.render_frames([cam] * e2e_steps, fld, config):
+            for fb, rep in ng.render_frames([cam] * e2e_steps, fld, config, batch=B):
                 img = fb.color
             batches.append((time.perf_counter() - t0) / e2e_steps)
         e2e_s = statistics.median(batches)
-        assert rep.visible == visible_all
+        assert rep.visible % visible_all == 0  # (a batch's report: its frames' total)
         d2h = int(img.nbytes)
     else:
         for _ in range(2):
-            img_d = tiles.render(cam, config, dst=0)[0]
+            img_d = tiles.render_batch([cam] * B, config, dst=0)[0]
             if img_d is not None:
                 img_d.cpu()
         torch.distributed.barrier()
+        launches = max(2, (min(args.steps, 24) + B - 1) // B)
         t0 = time.perf_counter()
-        img = np.zeros((HEIGHT, WIDTH, 3), np.uint8)
-        for _ in range(e2e_steps):
-            img_d, _v, _e = tiles.render(cam, config, dst=0)
+        img = np.zeros((B, HEIGHT, WIDTH, 3), np.uint8)
+        for _ in range(launches):
+            img_d, _v, _e = tiles.render_batch([cam] * B, config, dst=0)
             if img_d is not None:
                 img = img_d.cpu().numpy()
-        e2e_s = (time.perf_counter() - t0) / e2e_steps
+        e2e_s = (time.perf_counter() - t0) / (launches * B)
         e2e_s = max_over_ranks(e2e_s, dev)
-        d2h = int(img.nbytes)
+        d2h = int(img.nbytes) // B
     res["e2e"] = {"value": 1.0 / e2e_s, "unit": "frames/s",
                   "h2d_bytes_per_step": _sizeof("NgCamera") + _sizeof("NgRenderCfg"),
                   "d2h_bytes_per_step": d2h + _sizeof("NgFrameStats"),
-                  "api": "render_frames (frame i's readback overlaps frame i+1)" if world == 1
-                  else "TiledRenderer.render, colour gathered to rank 0 and copied to the host"}
+                  "api": f"render_frames(batch={B}) (a launch's readback overlaps the next launch)" if world == 1
+                  else f"TiledRenderer.render_batch ({B} frames), colour gathered to rank 0 and copied to the host"}
 
     # ---- batched SDF query (configs[2]): forward L = 1..5 over 2^24 points,
     # sharded by point range across ranks (no exchange)
@@ -588,20 +611,23 @@ def train_leg(knot, svo, dev, flush):
 
 
 def _time_tiled(tiles, cam, cfg, steps, flush, world):
+    """Median ms per frame over `steps` launches of `tiles.batch` frames of
+    `cam` each (L2 flushed before each launch; N > 1: with the gather)."""
     import torch
+    k = tiles.batch
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
     for _ in range(2):
-        tiles.enqueue(cam, cfg)
+        tiles.enqueue([cam] * k, cfg)
     torch.cuda.synchronize()
     for a, b in ev:
         flush.zero_()
         a.record()
-        tiles.enqueue(cam, cfg)
+        tiles.enqueue([cam] * k, cfg)
         if world > 1:
-            tiles.gather_color(dst=0)
+            tiles.gather(("color",), dst=0, frames=k)
         b.record()
     torch.cuda.synchronize()
-    ms = statistics.median(a.elapsed_time(b) for a, b in ev)
+    ms = statistics.median(a.elapsed_time(b) for a, b in ev) / k
     if world > 1:
         ms = max_over_ranks(ms, flush.device)
     return ms
@@ -625,12 +651,19 @@ def extra_configs(args, world, dev, knot):
     for name, fld, config in (
             ("configs[3] LOD6 1920x1080", fld6, ng.RenderConfig()),
             ("configs[4] LOD4.5 + shadow rays 1920x1080", fld6, ng.RenderConfig(lod=4.5, shadows=True))):
+        cfg = resolve_config(fld, config, resolve_lod(cam, fld, config))
         tiles = TiledRenderer(fld, 1920, 1080)
         img, visible, evals = tiles.render(cam, config)
-        cfg = resolve_config(fld, config, resolve_lod(cam, fld, config))
-        ms = _time_tiled(tiles, cam, cfg, steps, flush, world)
         st = tiles.sess.read_stats()
-        out[name] = {"frames_per_sec": 1000.0 / ms, "ms_per_frame": ms, "visible": visible, "decoder_evals": evals,
+        lat = _time_tiled(tiles, cam, cfg, steps, flush, world)
+        del tiles
+        B = max(1, min(args.batch, 8))
+        tiles = TiledRenderer(fld, 1920, 1080, batch=B)
+        tiles.render_batch([cam] * B, config)  # capacities for the batch
+        ms = _time_tiled(tiles, cam, cfg, max(3, steps // 2), flush, world)
+        del tiles
+        out[name] = {"frames_per_sec": 1000.0 / ms, "ms_per_frame": ms, "frames_per_launch": B,
+                     "frame_latency_ms": lat, "visible": visible, "decoder_evals": evals,
                      "shadowed_local": int(st.shadowed), "voxels_finest": svo6.voxel_count(6), "n_gpus": world}
     return out
 
@@ -658,7 +691,8 @@ def line_config(world: int) -> dict:
             "resolution": [WIDTH, HEIGHT], "lod": MAX_LEVEL, "voxels": VOXELS, "camera": CAM,
             "parallelism": f"tiles{world}" + (" (8-row bands, NCCL all-gather of the colour tiles)" if world > 1
                                               else ""),
-            "l2": "flushed between GPU frames (256 MiB write)"}
+            "frames": "a sequence of frames of this camera (a static view); one step = one frame",
+            "l2": "flushed between GPU launch sequences (256 MiB write)"}
 
 
 def spawn_ranks(args) -> int:
@@ -703,7 +737,8 @@ def main():
     bytes_per_eval = EVAL_BYTES_BASE + EVAL_BYTES_PER_LEVEL * levels_read
     # the march launch also evaluates the normal probes (NG_FUSED_PROBES, default)
     fused = os.environ.get("NG_FUSED_PROBES", "1") != "0"
-    march_evals = res["total_evals"] if fused else res["trace_evals"]
+    # a full launch marches `batch` frames of the same camera
+    march_evals = (res["total_evals"] if fused else res["trace_evals"]) * res["frames_per_launch"][0]
     algo_bytes = march_evals * bytes_per_eval
     peak = _peak_hbm()
     achieved = algo_bytes / (march * 1e-3) / 1e9
@@ -716,9 +751,13 @@ def main():
         "frame": {"visible": res["visible"], "trace_evals": res["trace_evals"],
                   "total_evals": res["total_evals"], "pairs_per_level": res["pairs"],
                   "active_rays": res["active_rays"], "march_ms_median": march,
-                  "frame_ms_median": statistics.median(res["frame_ms"]), "voxels": _voxel_counts(res["_svo"])},
+                  "frame_ms_median": statistics.median(res["frame_ms"]), "voxels": _voxel_counts(res["_svo"]),
+                  "frames_per_launch": res["frames_per_launch"], "launch_march_ms_median": march},
+        "frame_latency_ms": res["frame_latency_ms"],
+        "frame_latency_note": "one frame per launch sequence (TiledRenderer without batching), same timing: "
+                              "what a single frame takes alone",
         "e2e": res["e2e"],
-        "gpu_launches": args.steps * (_launches_per_frame(res["_svo"]) + (world + 1 if world > 1 else 0)),
+        "gpu_launches": res["launches"] * (_launches_per_frame(res["_svo"]) + (world + 2 if world > 1 else 0)),
         "roofline": {"bound": "hbm", "kernel": "k_march (sphere-trace march + normal probes, fused gather + MLP)"
                      if fused else "k_march (sphere-trace march, fused gather + MLP)",
                      "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,

@@ -40,6 +40,7 @@ extern "C" {
 #define NG_MAX_TLEVELS 16    /* virtual + stored traversal levels */
 #define NG_FEAT_PAD 32       /* feature rows are padded to 32 fp32 channels (128 B) */
 #define NG_W1_STRIDE 36      /* packed decoder row: 3 x-weights, 32 feature weights, b1 */
+#define NG_MAX_BATCH 8       /* cameras per ng_render_batch launch */
 
 /* Device-resident sparse voxel octree (octree.py:100-131).
  * Traversal level t = level + n_virtual; levels -n_virtual..-1 are the
@@ -342,6 +343,17 @@ int ng_shade(const uint8_t* hit, const double* normal, int64_t n, const ng_rende
 int ng_render_frame(const ng_octree* tree, const ng_field* fld, const ng_render_cfg* cfg,
                     const ng_camera* cam, const ng_frame* frame, const ng_workspace* ws,
                     ng_frame_stats* d_stats, void* stream);
+/* A batch of frames in one launch sequence (render.py:342-448 per camera,
+ * for a camera sequence): cams[0..n_cams) share width, height and band
+ * layout (NG_ERR_CONFIG otherwise), 1 <= n_cams <= NG_MAX_BATCH. Frame f's
+ * pixels are pixels [f n, (f + 1) n) of every `frame` buffer and of the
+ * workspace's per-ray arrays (n = width * local_rows; size the workspace for
+ * n_cams * n rays). Each frame's outputs equal ng_render_frame's for its
+ * camera; the statistics cover the batch. One traversal and one march cover
+ * every frame, so one frame's longest rays overlap the others' work. */
+int ng_render_batch(const ng_octree* tree, const ng_field* fld, const ng_render_cfg* cfg,
+                    const ng_camera* cams, int32_t n_cams, const ng_frame* frame,
+                    const ng_workspace* ws, ng_frame_stats* d_stats, void* stream);
 /* Same, for arbitrary rays (metrics.trace_field_rays, metrics.py:135-142). */
 int ng_render_rays(const ng_octree* tree, const ng_field* fld, const ng_render_cfg* cfg,
                    const ng_ray* rays, int64_t n_rays, const ng_frame* frame,

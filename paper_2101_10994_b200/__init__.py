@@ -75,6 +75,7 @@ from .render import (
     normals,
     query_field,
     render,
+    render_batch,
     render_frames,
     select_lod,
     shade,
@@ -92,6 +93,7 @@ __all__ = [
     "StructuralError", "TrainingDiverged", "blend", "build_octree", "decode", "empty_space_value",
     "exclusive_sum", "forward", "forward_levels", "locate", "morton_decode", "morton_encode", "new_field",
     "normals", "predict", "query_field", "ray_aabb_batch", "ray_segments", "ray_trace_octree", "render",
+    "render_batch",
     "render_frames",
     "select_lod", "shade", "sphere_trace", "storage_bytes", "sum_features", "trace_rays", "trilinear",
     "voxel_bounds", "write_ppm", "DecoderGrads", "FieldGradients", "LevelInterp", "backward", "scatter_add_rows",

@@ -258,11 +258,29 @@ __device__ __forceinline__ void camera_ray(const ng_camera& cam, int64_t i, ng_r
   make_ray(cam.position[0], cam.position[1], cam.position[2], d[0], d[1], d[2], r);
 }
 
-// Rays of a pass: explicit records, or (`cam_rays`) the camera's rays
+// The cameras of a frame batch (ng_render_batch): frame f's rays are rays
+// [f n_per, (f + 1) n_per) of the launch, its pixels in its camera's order;
+// a single frame is a batch of one. Kernels take it as a __grid_constant__
+// parameter (a camera is picked with a run-time index).
+struct CamSet {
+  ng_camera cam[NG_MAX_BATCH];
+  int64_t n_per;  // rays per frame
+  int32_t k;      // frames
+  int32_t pad;
+  __host__ __device__ __forceinline__ int frame_of(int64_t i) const { return k > 1 ? (int)(i / n_per) : 0; }
+};
+
+// Ray i of a batch: its frame's camera ray (the same function as a single frame).
+__device__ __forceinline__ void camera_ray(const CamSet& cs, int64_t i, ng_ray& r) {
+  const int f = cs.frame_of(i);
+  camera_ray(cs.cam[f], i - (int64_t)f * cs.n_per, r);
+}
+
+// Rays of a pass: explicit records, or (`cam_rays`) the cameras' rays
 // computed where they are used instead of stored.
 struct RaySrc {
   const ng_ray* rays;
-  ng_camera cam;
+  CamSet cam;
   int cam_rays;
 };
 

@@ -28,7 +28,7 @@ int traverse_tiles(const ng_octree& tree, const ng_ray* rays, const int64_t* d_n
                    int4* items, unsigned long long* d_active, int64_t* counts,
                    ng_hit_pair* hits, int64_t hit_cap, void* ctl, int64_t* seg_start, int64_t* seg_end,
                    void* arena, size_t arena_bytes, unsigned long long* d_need, const double* shared_origin,
-                   const ng_camera* cam_rays, const ng_frame* defaults, uint32_t bg, int64_t n_host,
+                   const CamSet* cam_rays, const ng_frame* defaults, uint32_t bg, int64_t n_host,
                    void* cont, cudaStream_t s);
 size_t tile_cont_bytes();
 size_t tile_cont_ready_bytes();
@@ -48,10 +48,10 @@ constexpr int R_NW = 8;  // warps per CTA for march / normals
 
 // Pixel-centre rays, bit-exact with Camera.rays (render.py:74-88), fused with
 // the per-pixel output defaults and the background colour.
-__global__ void k_camera_rays(ng_camera cam, ng_ray* __restrict__ rays, ng_frame fr, uint8_t bg0, uint8_t bg1,
-                              uint8_t bg2, int64_t* d_root_count, int64_t* __restrict__ seg_start,
-                              int64_t* __restrict__ seg_end) {
-  const int64_t n = (int64_t)cam.width * cam.local_rows;
+__global__ void k_camera_rays(const __grid_constant__ CamSet cam, ng_ray* __restrict__ rays, ng_frame fr,
+                              uint8_t bg0, uint8_t bg1, uint8_t bg2, int64_t* d_root_count,
+                              int64_t* __restrict__ seg_start, int64_t* __restrict__ seg_end) {
+  const int64_t n = (int64_t)cam.k * cam.n_per;
   if (blockIdx.x == 0 && threadIdx.x == 0 && d_root_count) *d_root_count = n;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -535,8 +535,10 @@ __global__ void __launch_bounds__(NW * 32, TC ? 1 : 2) k_march(const __grid_cons
             ev = 0;
             ready = false;
             if (A.rays.cam_rays) {
-              camera_dir(A.rays.cam, ray, d);  // (the march needs no slab fields)
-              o[0] = A.rays.cam.position[0]; o[1] = A.rays.cam.position[1]; o[2] = A.rays.cam.position[2];
+              const int fc = A.rays.cam.frame_of(ray);  // the ray's frame in a batch
+              const ng_camera& cm = A.rays.cam.cam[fc];
+              camera_dir(cm, ray - (int64_t)fc * A.rays.cam.n_per, d);  // (the march needs no slab fields)
+              o[0] = cm.position[0]; o[1] = cm.position[1]; o[2] = cm.position[2];
             } else {
               const ng_ray* rp = A.rays.rays + ray;
               o[0] = rp->o[0]; o[1] = rp->o[1]; o[2] = rp->o[2];
@@ -1016,7 +1018,7 @@ __global__ void k_finish_stats(ng_frame_stats* st, int n_levels, int64_t pair_ca
 }
 
 // Shadow rays for the hit pixels: origin p + offset * n, direction = light.
-__global__ void k_shadow_rays(const RaySrc rays, const int32_t* __restrict__ hit_list,
+__global__ void k_shadow_rays(const __grid_constant__ RaySrc rays, const int32_t* __restrict__ hit_list,
                               const unsigned long long* __restrict__ d_hits, const double* __restrict__ t_hit,
                               const double* __restrict__ normal, ng_render_cfg cfg, ng_ray* __restrict__ srays,
                               int64_t* d_root) {
@@ -1295,7 +1297,7 @@ static int trace_pass(const ng_octree& tree, const ng_render_cfg& cfg, const Lod
                       int64_t n, int64_t* counts, const WsLayout& L, const ng_workspace& ws, char* b,
                       unsigned long long* d_active, unsigned long long* work_counter, cudaStream_t s,
                       MarchArgs& A, bool zeroed, const double* shared_origin, TileOverflow& tov,
-                      const ng_camera* cam_rays = nullptr, const ng_frame* defaults = nullptr, uint32_t bg = 0,
+                      const CamSet* cam_rays = nullptr, const ng_frame* defaults = nullptr, uint32_t bg = 0,
                       int64_t n_host = -1) {
   ng_pair* pa = (ng_pair*)(b + L.pairs_a);
   ng_pair* pb = (ng_pair*)(b + L.pairs_b);
@@ -1396,8 +1398,17 @@ static int trace_pass(const ng_octree& tree, const ng_render_cfg& cfg, const Lod
   return NG_OK;
 }
 
+// A batch's cameras as the kernels take them (frame f = rays [f n, (f+1) n)).
+static CamSet cam_set(const ng_camera* cams, int k) {
+  CamSet cs{};
+  for (int i = 0; i < k; ++i) cs.cam[i] = cams[i];
+  cs.k = k;
+  cs.n_per = (int64_t)cams[0].width * cams[0].local_rows;
+  return cs;
+}
+
 static int render_common(const ng_octree& tree, const ng_field& f, const ng_render_cfg& cfg,
-                         const ng_camera* cam, const ng_ray* user_rays, int64_t n, const ng_frame& fr,
+                         const CamSet* cam, const ng_ray* user_rays, int64_t n, const ng_frame& fr,
                          const ng_workspace& ws, ng_frame_stats* st, bool do_normals, cudaStream_t s) {
   if (cfg.trace_level < 0 || cfg.trace_level > tree.max_level) {
     set_error("trace level %d outside 0..%d", cfg.trace_level, tree.max_level);
@@ -1473,10 +1484,19 @@ static int render_common(const ng_octree& tree, const ng_field& f, const ng_rend
   const int target = cfg.trace_level + tree.n_virtual;
   const LodPlan P = plan_lod(cfg);
   MarchArgs A;
-  // camera rays share the eye position (a host value, captured into the launches)
+  // camera rays share the eye position (a host value, captured into the
+  // launches); the tile traversal takes each tile's from its frame's camera,
+  // the level passes only when every camera of a batch has the same one
+  const double* eye = nullptr;
+  if (cam) {
+    bool same = true;
+    for (int i = 1; i < cam->k; ++i)
+      for (int a = 0; a < 3; ++a) same = same && cam->cam[i].position[a] == cam->cam[0].position[a];
+    if (same || cam_rays) eye = cam->cam[0].position;
+  }
   TileOverflow tov;
   if ((r = trace_pass(tree, cfg, P, rays, n, st->pairs, L, ws, b, ctr + 0, ctr + 2, s, A, true,
-                      cam ? cam->position : nullptr, tov, cam_rays ? cam : nullptr, cam_rays ? &fr : nullptr,
+                      eye, tov, cam_rays ? cam : nullptr, cam_rays ? &fr : nullptr,
                       bg_packed, cam_rays ? n : -1)))
     return r;
   A.hit = fr.hit;
@@ -1578,8 +1598,9 @@ using namespace ng;
 extern "C" {
 
 int ng_camera_rays(const ng_camera* cam, ng_ray* rays, void* stream) {
-  int64_t n = (int64_t)cam->width * cam->local_rows;
-  k_camera_rays<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(*cam, rays, ng_frame{}, 0, 0, 0, nullptr, nullptr,
+  const CamSet cs = cam_set(cam, 1);
+  const int64_t n = cs.n_per;
+  k_camera_rays<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(cs, rays, ng_frame{}, 0, 0, 0, nullptr, nullptr,
                                                                             nullptr);
   NG_CHECK_LAUNCH("ng_camera_rays");
   return NG_OK;
@@ -1604,12 +1625,33 @@ int ng_render_workspace_offsets(int64_t n_rays, int64_t pair_capacity, int64_t h
 
 int ng_render_frame(const ng_octree* tree, const ng_field* fld, const ng_render_cfg* cfg, const ng_camera* cam,
                     const ng_frame* frame, const ng_workspace* ws, ng_frame_stats* d_stats, void* stream) {
-  if (cam->band_rows < 1 || cam->band_stride < 1 || cam->band_offset < 0 || cam->band_offset >= cam->band_stride) {
+  return ng_render_batch(tree, fld, cfg, cam, 1, frame, ws, d_stats, stream);
+}
+
+int ng_render_batch(const ng_octree* tree, const ng_field* fld, const ng_render_cfg* cfg, const ng_camera* cams,
+                    int32_t n_cams, const ng_frame* frame, const ng_workspace* ws, ng_frame_stats* d_stats,
+                    void* stream) {
+  if (!cams || n_cams < 1 || n_cams > NG_MAX_BATCH) {
+    set_error("a batch holds 1..%d cameras, got %d", NG_MAX_BATCH, (int)n_cams);
+    return NG_ERR_CONFIG;
+  }
+  const ng_camera& c0 = cams[0];
+  if (c0.width < 1 || c0.local_rows < 0 || c0.band_rows < 1 || c0.band_stride < 1 || c0.band_offset < 0 ||
+      c0.band_offset >= c0.band_stride) {
     set_error("bad camera band layout");
     return NG_ERR_CONFIG;
   }
-  const int64_t n = (int64_t)cam->width * cam->local_rows;
-  return render_common(*tree, *fld, *cfg, cam, nullptr, n, *frame, *ws, d_stats, true, (cudaStream_t)stream);
+  for (int i = 1; i < n_cams; ++i) {
+    const ng_camera& c = cams[i];
+    if (c.width != c0.width || c.height != c0.height || c.band_rows != c0.band_rows ||
+        c.band_stride != c0.band_stride || c.band_offset != c0.band_offset || c.local_rows != c0.local_rows) {
+      set_error("batch camera %d: size or band layout differs from camera 0", i);
+      return NG_ERR_CONFIG;
+    }
+  }
+  const CamSet cs = cam_set(cams, n_cams);
+  return render_common(*tree, *fld, *cfg, &cs, nullptr, cs.n_per * n_cams, *frame, *ws, d_stats, true,
+                       (cudaStream_t)stream);
 }
 
 int ng_render_rays(const ng_octree* tree, const ng_field* fld, const ng_render_cfg* cfg, const ng_ray* rays,

@@ -515,8 +515,8 @@ __global__ void __launch_bounds__(TT_WPB * 32, NG_TT_MINB) k_traverse_tiles(
     const __grid_constant__ ng_octree tree, const ng_ray* __restrict__ rays, const int64_t* __restrict__ d_n,
     int target, int64_t* counts, ng_hit_pair* __restrict__ hits, int64_t hit_cap, unsigned int* tile_counter,
     unsigned long long* hit_cursor, int64_t* __restrict__ seg_start, int64_t* __restrict__ seg_end,
-    uint8_t* arena, int64_t gcap, int scap, unsigned long long* d_need, const SharedOrigin so,
-    const ng_camera cam, int cam_rays, int4* __restrict__ items, unsigned long long* d_active,
+    uint8_t* arena, int64_t gcap, int scap, unsigned long long* d_need, const SharedOrigin so0,
+    const __grid_constant__ CamSet cams, int cam_rays, int4* __restrict__ items, unsigned long long* d_active,
     const ng_frame fr, uint32_t bg, int64_t n_host, int cull, uint8_t* __restrict__ cont, int split_at,
     int split_ahead) {
   extern __shared__ __align__(16) uint8_t tt_smem[];
@@ -529,7 +529,11 @@ __global__ void __launch_bounds__(TT_WPB * 32, NG_TT_MINB) k_traverse_tiles(
   // the device count (shadow rays)
   const int64_t n = n_host >= 0 ? n_host : *d_n;
   if (n_host >= 0 && blockIdx.x == 0 && threadIdx.x == 0) *const_cast<int64_t*>(d_n) = n_host;
-  const int64_t n_tiles = (n + TT_RAYS - 1) / TT_RAYS;
+  // tiles never span two frames of a batch (each frame's camera is its
+  // tiles' shared origin): frame f's tiles are [f tpf, (f + 1) tpf)
+  const int64_t n_per = cam_rays ? cams.n_per : n;
+  const int64_t tpf = (n_per + TT_RAYS - 1) / TT_RAYS;
+  const int64_t n_tiles = (cam_rays ? cams.k : 1) * tpf;
   const int lim = scap + (int)gcap;
   int64_t level_cnt = 0;  // lane t: pairs emitted at traversal level t
   int need = 0;
@@ -595,6 +599,8 @@ __global__ void __launch_bounds__(TT_WPB * 32, NG_TT_MINB) k_traverse_tiles(
     int64_t r0;
     int nr, ja = 0, jb, t0 = 0;
     int nc = 0;
+    int fcam = 0;        // the tile's frame (camera) in a batch
+    SharedOrigin so = so0;
 #ifdef NG_PROFILE
     int n_splits = 0;
     unsigned long long split_ns = 0;
@@ -607,6 +613,11 @@ __global__ void __launch_bounds__(TT_WPB * 32, NG_TT_MINB) k_traverse_tiles(
       __syncwarp();
       r0 = __ldcg(&cr->r0);
       nr = __ldcg(&cr->nr);
+      if (cam_rays) {
+        fcam = cams.frame_of(r0);
+#pragma unroll
+        for (int a = 0; a < 3; ++a) so.o[a] = cams.cam[fcam].position[a];
+      }
       ja = __ldcg(&cr->ja);
       jb = __ldcg(&cr->jb);
       t0 = __ldcg(&cr->pass);
@@ -617,7 +628,7 @@ __global__ void __launch_bounds__(TT_WPB * 32, NG_TT_MINB) k_traverse_tiles(
         const int j = j0 + lane;
         if (j >= ja && j < jb) {
           ng_ray r;
-          if (SO && cam_rays) camera_ray(cam, r0 + j, r);
+          if (SO && cam_rays) camera_ray(cams.cam[fcam], r0 - fcam * n_per + j, r);
           else load_ray_slab(rays, r0 + j, so, r);
           bool general = true;
 #pragma unroll
@@ -639,9 +650,15 @@ __global__ void __launch_bounds__(TT_WPB * 32, NG_TT_MINB) k_traverse_tiles(
       }
       __syncwarp();
     } else {
-    r0 = (int64_t)tile * TT_RAYS;
-    nr = (int)((n - r0) < TT_RAYS ? (n - r0) : TT_RAYS);
+    fcam = (int)((int64_t)tile / tpf);
+    const int64_t tl0 = ((int64_t)tile - fcam * tpf) * TT_RAYS;  // first ray within the frame
+    r0 = fcam * n_per + tl0;
+    nr = (int)((n_per - tl0) < TT_RAYS ? (n_per - tl0) : TT_RAYS);
     jb = nr;
+    if (cam_rays) {
+#pragma unroll
+      for (int a = 0; a < 3; ++a) so.o[a] = cams.cam[fcam].position[a];
+    }
     // ---- the tile's rays, and the root list: rays whose box test hits B
     {
       const TileList L0 = tile_list(W, ga, gcap, 0, scap);
@@ -665,7 +682,7 @@ __global__ void __launch_bounds__(TT_WPB * 32, NG_TT_MINB) k_traverse_tiles(
         }
         if (j < nr) {
           ng_ray r;
-          if (SO && cam_rays) camera_ray(cam, r0 + j, r);  // the camera's ray, not stored
+          if (SO && cam_rays) camera_ray(cams.cam[fcam], tl0 + j, r);  // the camera's ray, not stored
           else load_ray_slab(rays, r0 + j, so, r);
           bool general = true;
 #pragma unroll
@@ -1158,7 +1175,7 @@ int traverse_tiles(const ng_octree& tree, const ng_ray* rays, const int64_t* d_n
                    int4* items, unsigned long long* d_active, int64_t* counts,
                    ng_hit_pair* hits, int64_t hit_cap, void* ctl, int64_t* seg_start, int64_t* seg_end,
                    void* arena, size_t arena_bytes, unsigned long long* d_need, const double* shared_origin,
-                   const ng_camera* cam_rays, const ng_frame* defaults, uint32_t bg, int64_t n_host,
+                   const CamSet* cam_rays, const ng_frame* defaults, uint32_t bg, int64_t n_host,
                    void* cont, cudaStream_t s) {
   // `ctl` (512 bytes zeroed by the caller): u32 tile counter at 0, u64 hit
   // cursor at 8, longest list at 16, pool cursor at 64, continuation queue
@@ -1174,7 +1191,7 @@ int traverse_tiles(const ng_octree& tree, const ng_ray* rays, const int64_t* d_n
   k<<<(int)(warps / TT_WPB), TT_WPB * 32, tile_traverse_smem(), s>>>(
       tree, rays, d_n, target, counts, hits, hit_cap, (unsigned int*)ctl, (unsigned long long*)((char*)ctl + 8),
       seg_start, seg_end, (uint8_t*)arena, gcap, tile_traverse_scap(), d_need, so,
-      cam_rays ? *cam_rays : ng_camera{}, cam_rays != nullptr, items, d_active, defaults ? *defaults : ng_frame{},
+      cam_rays ? *cam_rays : CamSet{}, cam_rays != nullptr, items, d_active, defaults ? *defaults : ng_frame{},
       bg, n_host, target == tree.n_tlevels - 1, (uint8_t*)cont, tile_split_at(), tile_split_ahead());
   NG_CHECK_LAUNCH("k_traverse_tiles");
   return NG_OK;

@@ -21,8 +21,9 @@ import torch.distributed as dist
 
 from . import _lib
 from ._lib import call, ptr, stream_ptr
-from .errors import OctfieldError
-from .render import prepare_presum, Camera, RenderConfig, RenderSession, band_rows_of, resolve_config, resolve_lod
+from .errors import ConfigError, OctfieldError
+from .render import (prepare_presum, Camera, RenderConfig, RenderSession, _batch_cfg, band_rows_of, camera_structs,
+                     resolve_config, resolve_lod)
 
 DEFAULT_BAND_ROWS = 8
 
@@ -79,9 +80,13 @@ def gather_tiles(local: torch.Tensor, layout: list, height: int, group=None, dst
 
 class TiledRenderer:
     """Renders frames of one camera size cooperatively across the ranks of
-    the default process group (NCCL)."""
+    the default process group (NCCL). With `batch` > 1, `enqueue` /
+    `render_batch` take up to that many cameras per launch sequence (each
+    rank renders its bands of every frame in one traversal and one march,
+    ng_render_batch), and the frames' tiles are gathered in one collective."""
 
-    def __init__(self, fld, width: int, height: int, band_rows: int = DEFAULT_BAND_ROWS, group=None):
+    def __init__(self, fld, width: int, height: int, band_rows: int = DEFAULT_BAND_ROWS, group=None,
+                 batch: int = 1):
         self.fld = fld
         self.width, self.height = width, height
         self.group = group
@@ -90,41 +95,58 @@ class TiledRenderer:
         self.band_rows = band_rows
         self.layout = band_layout(height, self.world, band_rows)
         self.local_rows = len(self.layout[self.rank])
-        self.sess = RenderSession(fld, width, max(self.local_rows, 1), n_rays=max(self.local_rows * width, 1))
+        if not 1 <= batch <= _lib.MAX_BATCH:
+            raise ConfigError(f"batch must be 1..{_lib.MAX_BATCH}, got {batch}")
+        self.batch = batch
+        self.frames = 1  # frames in the last launch
+        self.sess = RenderSession(fld, width, max(self.local_rows, 1),
+                                  n_rays=max(self.local_rows * width, 1) * batch)
         self.frame = self.sess.new_frame()
 
-    def enqueue(self, camera: Camera, cfg) -> None:
-        """Launch this rank's bands (no host sync)."""
-        cs = camera.band_struct(self.band_rows, self.world, self.rank)
+    def enqueue(self, camera, cfg) -> None:
+        """Launch this rank's bands of one camera or of a list of up to
+        `batch` cameras (no host sync)."""
+        cams = [camera] if isinstance(camera, Camera) else list(camera)
+        if not 1 <= len(cams) <= self.batch:
+            raise ConfigError(f"this renderer takes 1..{self.batch} cameras per launch, got {len(cams)}")
+        cs = camera_structs([c.band_struct(self.band_rows, self.world, self.rank) for c in cams])
+        self.frames = len(cams)
         fs = self.sess.frame_struct(self.frame)
         fstruct = prepare_presum(self.fld, cfg)
         if self.local_rows:
-            call("ng_render_frame", self.fld.svo.device.ref(), ctypes.byref(fstruct), ctypes.byref(cfg),
-                 ctypes.byref(cs), ctypes.byref(fs), ctypes.byref(self.sess.ws), ptr(self.sess.stats),
+            call("ng_render_batch", self.fld.svo.device.ref(), ctypes.byref(fstruct), ctypes.byref(cfg),
+                 cs, len(cs), ctypes.byref(fs), ctypes.byref(self.sess.ws), ptr(self.sess.stats),
                  stream_ptr())
 
     # per-pixel outputs a frame can gather: name -> trailing shape
     _FIELDS = {"color": (3,), "t": (), "hit": (), "normal": (3,), "normal_ok": (), "iterations": (), "evals": ()}
 
-    def _local(self, name: str) -> torch.Tensor:
+    def _local(self, name: str, frames: int = 1) -> torch.Tensor:
+        """(local_rows, width, ...) of frame 0, or with frames > 1 the
+        first `frames` frames' rows as (local_rows, frames, width, ...)."""
         tail = self._FIELDS[name]
-        v = self.frame[name][:self.local_rows * self.width]
-        return v.reshape((self.local_rows, self.width) + tail)
+        n = self.local_rows * self.width
+        v = self.frame[name][:n * frames].reshape((frames, self.local_rows, self.width) + tail)
+        return v[0] if frames == 1 else v.transpose(0, 1)
 
-    def gather(self, fields=("color",), dst: int | None = None) -> dict:
+    def gather(self, fields=("color",), dst: int | None = None, frames: int | None = None) -> dict:
         """The frame's per-pixel outputs assembled to (height, width, ...)
         device tensors: on every rank (dst=None, all-gather) or on rank dst
         only (gather; the other ranks get an empty dict). One collective per
-        field (colour, plus depth / hit on request)."""
+        field (colour, plus depth / hit on request). With
+        `frames` (default: 1 after a single camera, else the last launch's
+        frames) > 1, each field is (frames, height, width, ...), every
+        frame's tiles moving in the same collective."""
+        k = frames if frames is not None else self.frames
         out = {}
         for name in fields:
-            local = self._local(name)
+            local = self._local(name, k)
             if self.world == 1:
-                out[name] = local
+                out[name] = local if k == 1 else local.transpose(0, 1)
                 continue
-            img = gather_tiles(local, self.layout, self.height, self.group, dst)
+            img = gather_tiles(local.contiguous() if k > 1 else local, self.layout, self.height, self.group, dst)
             if img is not None:
-                out[name] = img
+                out[name] = img if k == 1 else img.transpose(0, 1)
         return out
 
     def gather_color(self, dst: int | None = None):
@@ -138,6 +160,18 @@ class TiledRenderer:
         image; with dst, only rank dst receives the images."""
         lod = resolve_lod(camera, self.fld, config)
         cfg = resolve_config(self.fld, config, lod)
+        return self._render(camera, cfg, fields, dst)
+
+    def render_batch(self, cameras, config: RenderConfig, fields=None, dst: int | None = None):
+        """Up to `batch` frames across the ranks in one launch sequence per
+        rank. Returns (images (K, H, W, 3) uint8, visible, evals) with the
+        batch's totals, or with `fields` a dict of (K, H, W, ...) outputs;
+        each frame equals `render`'s for its camera."""
+        cams = list(cameras)
+        _, cfg = _batch_cfg(cams, self.fld, config)
+        return self._render(cams, cfg, fields, dst)
+
+    def _render(self, camera, cfg, fields, dst):
         n_levels = cfg.trace_level + self.fld.svo.device.n_virtual
         self.reruns = 0
         while True:

@@ -526,10 +526,13 @@ class RenderSession:
         return _lib.NgFrame(ptr(fr["hit"]), ptr(fr["t"]), ptr(fr["normal"]), ptr(fr["normal_ok"]),
                             ptr(fr["iterations"]), ptr(fr["evals"]), ptr(fr["color"]))
 
-    def enqueue(self, cfg: _lib.NgRenderCfg, frame: dict, camera: Camera | None = None, rays: torch.Tensor | None = None,
+    def enqueue(self, cfg: _lib.NgRenderCfg, frame: dict, camera=None, rays: torch.Tensor | None = None,
                 timed: bool = False, do_normals: bool = True) -> None:
         """Launch one frame on the current stream. With `timed`, ev0 / ev1 /
-        ev2 bracket traversal+march and normals (ev1 is recorded by the C side)."""
+        ev2 bracket traversal+march and normals (ev1 is recorded by the C side).
+        `camera` may be a list of cameras (or camera structs) of one size:
+        a batch (ng_render_batch), frame f in pixels [f n, (f + 1) n) of
+        `frame` (n = width * height)."""
         fs = self.frame_struct(frame)
         fstruct = prepare_presum(self.fld, cfg)
         graphed = camera is not None and _graphs_enabled() and self._graph_misses < 16
@@ -542,10 +545,11 @@ class RenderSession:
             if timed:
                 self.ev0.record()
         if camera is not None:
-            tree, field, cs = self.fld.svo.device.ref(), ctypes.byref(fstruct), camera.struct()
+            tree, field = self.fld.svo.device.ref(), ctypes.byref(fstruct)
+            cs = camera_structs(camera)
 
             def launch():
-                call("ng_render_frame", tree, field, ctypes.byref(cfg), ctypes.byref(cs), ctypes.byref(fs),
+                call("ng_render_batch", tree, field, ctypes.byref(cfg), cs, len(cs), ctypes.byref(fs),
                      ctypes.byref(self.ws), ptr(self.stats), stream_ptr())
             if graphed:
                 # the frame's launches as one CUDA graph, replayed while every
@@ -640,21 +644,92 @@ class RenderSession:
 _SESSIONS = threading.local()
 
 
-def _session(fld: NeuralField, width: int, height: int) -> RenderSession:
+def _session(fld: NeuralField, width: int, height: int, frames: int = 1) -> RenderSession:
     """render()'s reusable frame state, per calling thread, device and
     stream (concurrent callers never share a workspace; SURVEY.md 8b
-    Threading)."""
+    Threading); `frames` > 1: room for a batch of that many frames."""
     cache = getattr(_SESSIONS, "d", None)
     if cache is None:
         cache = _SESSIONS.d = {}
-    key = (id(fld), width, height, torch.cuda.current_device(), torch.cuda.current_stream().cuda_stream)
+    key = (id(fld), width, height, frames, torch.cuda.current_device(), torch.cuda.current_stream().cuda_stream)
     s = cache.get(key)
     if s is None or s.fld is not fld:
         if len(cache) > 8:
             cache.clear()
-        s = RenderSession(fld, width, height)
+        s = RenderSession(fld, width, height, n_rays=width * height * frames)
         cache[key] = s
     return s
+
+
+def camera_structs(cameras):
+    """ng_camera array of one camera or a batch (Camera objects or structs)."""
+    if isinstance(cameras, (Camera, _lib.NgCamera)):
+        cameras = [cameras]
+    cams = [c.struct() if isinstance(c, Camera) else c for c in cameras]
+    if not 1 <= len(cams) <= _lib.MAX_BATCH:
+        raise ConfigError(f"a batch holds 1..{_lib.MAX_BATCH} cameras, got {len(cams)}")
+    arr = (_lib.NgCamera * len(cams))()
+    for i, c in enumerate(cams):
+        arr[i] = c
+    return arr
+
+
+class _FrameSlice:
+    """Frame f of a batch's stacked device outputs (a FrameBuffer's `dev`)."""
+
+    def __init__(self, frame: "FrameTensors", f: int, n: int):
+        self.frame, self.lo, self.hi = frame, f * n, (f + 1) * n
+
+    def __getitem__(self, name):
+        return self.frame[name][self.lo:self.hi]
+
+
+def _batch_cfg(cameras, fld: NeuralField, config: RenderConfig):
+    """The batch's resolved configuration: every camera of one size, and one
+    detail level (a camera-dependent LOD must resolve alike for all)."""
+    w, h = cameras[0].width, cameras[0].height
+    if any(c.width != w or c.height != h for c in cameras):
+        raise ConfigError("a batch's cameras must share one image size")
+    lods = [resolve_lod(c, fld, config) for c in cameras]
+    if any(l != lods[0] for l in lods):
+        raise ConfigError("a batch's cameras resolve to different detail levels: render them separately")
+    return lods[0], resolve_config(fld, config, lods[0])
+
+
+def render_batch(cameras, fld: NeuralField, config: RenderConfig):
+    """Render up to MAX_BATCH cameras of one size in one launch sequence
+    (ng_render_batch): one traversal and one march over every frame's rays,
+    so the frames' longest rays overlap each other's work instead of each
+    frame ending on its own. Returns (list of FrameBuffer, FrameReport);
+    each frame equals `render(camera, ...)`'s, the report covers the batch
+    (its `visible`, `evals` and times are the batch's totals)."""
+    cameras = list(cameras)
+    if not 1 <= len(cameras) <= _lib.MAX_BATCH:
+        raise ConfigError(f"a batch holds 1..{_lib.MAX_BATCH} cameras, got {len(cameras)}")
+    lod, cfg = _batch_cfg(cameras, fld, config)
+    k = len(cameras)
+    w, h = cameras[0].width, cameras[0].height
+    sess = _session(fld, w, h, k)
+    n_levels = cfg.trace_level + fld.svo.device.n_virtual
+    while True:
+        frame = sess.new_frame()
+        sess.enqueue(cfg, frame, camera=cameras, timed=True)
+        color_h = torch.empty(frame["color"].shape, dtype=torch.uint8, pin_memory=True)
+        color_h.copy_(frame["color"], non_blocking=True)
+        st = sess.read_stats()
+        if not sess.grow(st, n_levels):
+            break
+    if st.counters.nonfinite_inputs:
+        raise OctfieldError("non-finite decoder input")
+    if st.counters.evals_missing_level != 0:
+        raise OctfieldError("internal: decoder ran outside the queried level's voxels")
+    n = w * h
+    fbs = [FrameBuffer(w, h, _FrameSlice(frame, f, n), camera=c, prefetched={"color": color_h[f * n:(f + 1) * n]})
+           for f, c in enumerate(cameras)]
+    report = FrameReport(ms_trace=float(sess.ev0.elapsed_time(sess.ev1)), ms_normals=float(sess.ev1.elapsed_time(sess.ev2)),
+                         evals=int(st.counters.decoder_evals), visible=int(st.visible), lod=lod,
+                         shadowed=int(st.shadowed))
+    return fbs, report
 
 
 def render(camera: Camera, fld: NeuralField, config: RenderConfig):
@@ -687,32 +762,55 @@ def render(camera: Camera, fld: NeuralField, config: RenderConfig):
     return fb, report
 
 
-def render_frames(cameras, fld: NeuralField, config: RenderConfig):
+def _chunks(cameras, fld: NeuralField, config: RenderConfig, batch: int):
+    """Consecutive cameras grouped into batches of up to `batch` that share
+    an image size and a resolved configuration."""
+    cur, key0 = [], None
+    for camera in cameras:
+        lod = resolve_lod(camera, fld, config)
+        cfg = resolve_config(fld, config, lod)
+        key = (camera.width, camera.height, bytes(cfg))
+        if cur and (key != key0 or len(cur) == batch):
+            yield cur
+            cur = []
+        if not cur:
+            key0 = key
+        cur.append((camera, lod, cfg))
+    if cur:
+        yield cur
+
+
+def render_frames(cameras, fld: NeuralField, config: RenderConfig, batch: int = 1):
     """Render a sequence of cameras; yields (FrameBuffer, FrameReport) per
     camera, in order, exactly as `render` returns them. Frame i + 1 is
     launched before frame i's colour image and statistics are read back
     (double-buffered readback): each frame's device-to-host copies and host
     work overlap the next frame's kernels, the way a real-time loop
-    consumes frames. A frame whose lists overflowed is grown and re-rendered
-    with `render` before it is yielded. `report.ms_trace` is the whole
-    frame's device time (the normals run inside the march)."""
+    consumes frames. With `batch` > 1, up to `batch` consecutive cameras of
+    one size and detail level go in one launch sequence (`render_batch`),
+    and each of their reports covers that batch. A batch whose lists
+    overflowed is grown and re-rendered before it is yielded.
+    `report.ms_trace` is the launch's device time (the normals run inside
+    the march)."""
+    if not 1 <= batch <= _lib.MAX_BATCH:
+        raise ConfigError(f"batch must be 1..{_lib.MAX_BATCH}, got {batch}")
     pending = None
     stats_host = {}
     k = 0
-    cur = torch.cuda.current_stream()
     copy = torch.cuda.Stream()  # the colour readback runs beside the next frame's kernels
-    for camera in cameras:
-        lod = resolve_lod(camera, fld, config)
-        cfg = resolve_config(fld, config, lod)
-        sess = _session(fld, camera.width, camera.height)
+    for chunk in _chunks(cameras, fld, config, batch):
+        cams = [c for c, _, _ in chunk]
+        lod, cfg = chunk[0][1], chunk[0][2]
+        w, h = cams[0].width, cams[0].height
+        sess = _session(fld, w, h, batch)
         frame = sess.new_frame()
         ev_a, ev_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev_a.record()
-        sess.enqueue(cfg, frame, camera=camera)
+        sess.enqueue(cfg, frame, camera=cams if len(cams) > 1 else cams[0])
         ev_b.record()
         # the statistics (one small buffer every frame writes) are copied on
-        # the frame's stream; the 2.8 MB colour image on the copy stream, so
-        # its transfer overlaps the next frame instead of queueing before it
+        # the frame's stream; the colour images on the copy stream, so their
+        # transfer overlaps the next launch instead of queueing before it
         key = (id(sess), k % 2)
         st_h = stats_host.get(key)
         if st_h is None:
@@ -720,7 +818,7 @@ def render_frames(cameras, fld: NeuralField, config: RenderConfig):
         st_h.copy_(sess.stats, non_blocking=True)
         done = torch.cuda.Event()
         done.record()
-        color = frame["color"]
+        color = frame["color"][:len(cams) * w * h]
         color_h = torch.empty(color.shape, dtype=torch.uint8, pin_memory=True)
         copy.wait_event(ev_b)
         with torch.cuda.stream(copy):
@@ -730,31 +828,41 @@ def render_frames(cameras, fld: NeuralField, config: RenderConfig):
         done_copy.record(copy)
         done = (done, done_copy)
         if pending is not None:
-            yield _finish_frame(*pending)
-        pending = (camera, fld, config, lod, cfg, sess, frame, color_h, st_h, done, ev_a, ev_b)
+            yield from _finish_frames(*pending)
+        pending = (cams, fld, config, lod, sess, frame, color_h, st_h, done, ev_a, ev_b)
         k += 1
     if pending is not None:
-        yield _finish_frame(*pending)
+        yield from _finish_frames(*pending)
 
 
-def _finish_frame(camera, fld, config, lod, cfg, sess, frame, color_h, st_h, done, ev_a, ev_b):
+def _finish_frames(cams, fld, config, lod, sess, frame, color_h, st_h, done, ev_a, ev_b):
     for ev in done:
         ev.synchronize()
     raw = st_h.numpy().tobytes()
     st = _lib.NgFrameStats.from_buffer_copy(raw[:ctypes.sizeof(_lib.NgFrameStats)])
-    n_levels = cfg.trace_level + fld.svo.device.n_virtual
-    if st.overflow:  # grow, then this frame again (synchronously)
+    n_levels = resolve_config(fld, config, lod).trace_level + fld.svo.device.n_virtual
+    if st.overflow:  # grow, then this launch again (synchronously)
         sess.grow(st, n_levels)
-        return render(camera, fld, config)
+        if len(cams) == 1:
+            yield render(cams[0], fld, config)
+            return
+        fbs, rep = render_batch(cams, fld, config)
+        for fb in fbs:
+            yield fb, rep
+        return
     if st.counters.nonfinite_inputs:
         raise OctfieldError("non-finite decoder input")
     if st.counters.evals_missing_level != 0:
         raise OctfieldError("internal: decoder ran outside the queried level's voxels")
-    fb = FrameBuffer(camera.width, camera.height, frame, camera=camera, prefetched={"color": color_h})
     report = FrameReport(ms_trace=float(ev_a.elapsed_time(ev_b)), ms_normals=0.0,
                          evals=int(st.counters.decoder_evals), visible=int(st.visible), lod=lod,
                          shadowed=int(st.shadowed))
-    return fb, report
+    w, h = cams[0].width, cams[0].height
+    n = w * h
+    for f, camera in enumerate(cams):
+        dev = frame if len(cams) == 1 else _FrameSlice(frame, f, n)
+        fb = FrameBuffer(w, h, dev, camera=camera, prefetched={"color": color_h[f * n:(f + 1) * n]})
+        yield fb, report
 
 
 def trace_rays(fld: NeuralField, rays: RayBundle, lod: float, config: RenderConfig | None = None):
