@@ -78,6 +78,14 @@ def gather_tiles(local: torch.Tensor, layout: list, height: int, group=None, dst
     return assemble(torch.stack(parts), layout, height).to(dev)
 
 
+def gather_frames(local: torch.Tensor, layout: list, height: int, group=None, dst: int | None = None):
+    """K frames' local band rows (K, rows, ...) -> (K, height, ...) images in
+    one collective: the frames ride along as a trailing dimension of each
+    row, so the rank layout and the assembly are `gather_tiles`'s."""
+    img = gather_tiles(local.transpose(0, 1).contiguous(), layout, height, group, dst)
+    return None if img is None else img.transpose(0, 1)
+
+
 class TiledRenderer:
     """Renders frames of one camera size cooperatively across the ranks of
     the default process group (NCCL). With `batch` > 1, `enqueue` /
@@ -123,11 +131,11 @@ class TiledRenderer:
 
     def _local(self, name: str, frames: int = 1) -> torch.Tensor:
         """(local_rows, width, ...) of frame 0, or with frames > 1 the
-        first `frames` frames' rows as (local_rows, frames, width, ...)."""
+        first `frames` frames' rows as (frames, local_rows, width, ...)."""
         tail = self._FIELDS[name]
         n = self.local_rows * self.width
         v = self.frame[name][:n * frames].reshape((frames, self.local_rows, self.width) + tail)
-        return v[0] if frames == 1 else v.transpose(0, 1)
+        return v[0] if frames == 1 else v
 
     def gather(self, fields=("color",), dst: int | None = None, frames: int | None = None) -> dict:
         """The frame's per-pixel outputs assembled to (height, width, ...)
@@ -142,11 +150,14 @@ class TiledRenderer:
         for name in fields:
             local = self._local(name, k)
             if self.world == 1:
-                out[name] = local if k == 1 else local.transpose(0, 1)
+                out[name] = local
                 continue
-            img = gather_tiles(local.contiguous() if k > 1 else local, self.layout, self.height, self.group, dst)
+            if k == 1:
+                img = gather_tiles(local, self.layout, self.height, self.group, dst)
+            else:
+                img = gather_frames(local, self.layout, self.height, self.group, dst)
             if img is not None:
-                out[name] = img if k == 1 else img.transpose(0, 1)
+                out[name] = img
         return out
 
     def gather_color(self, dst: int | None = None):

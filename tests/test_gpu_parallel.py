@@ -43,7 +43,12 @@ def _scene():
     return ng, fld, cam
 
 
-def _worker(rank, world, port, tiny_rank, q):
+def _batch_cams(ng, cam):
+    return [cam, ng.Camera((2.5, 2.0, 2.0), (0.0, 0.0, 0.0), (0.0, 1.0, 0.0), 35.0, cam.width, cam.height),
+            ng.Camera((-1.0, -2.5, 2.5), (0.1, 0.0, 0.0), (0.0, 0.0, 1.0), 40.0, cam.width, cam.height)]
+
+
+def _worker(rank, world, port, tiny_rank, q, batch=False):
     import torch
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -54,6 +59,15 @@ def _worker(rank, world, port, tiny_rank, q):
         dist.init_process_group("gloo", rank=rank, world_size=world)
         ng, fld, cam = _scene()
         from paper_2101_10994_b200.parallel import TiledRenderer
+        if batch:  # three cameras per launch, every frame's tiles in one collective per field
+            tiles = TiledRenderer(fld, cam.width, cam.height, batch=3)
+            to0, vis, ev = tiles.render_batch(_batch_cams(ng, cam), ng.RenderConfig(), fields=FIELDS, dst=0)
+            out = {"rank": rank, "n_visible": vis, "n_evals": ev, "dst_keys": sorted(to0)}
+            if rank == 0:
+                out.update({k: v.cpu().numpy() for k, v in to0.items()})
+            q.put(out)
+            dist.destroy_process_group()
+            return
         tiles = TiledRenderer(fld, cam.width, cam.height)
         if rank == tiny_rank:  # this rank's first attempt overflows its pair buffers
             tiles.sess.pair_cap = 64
@@ -74,12 +88,12 @@ def _worker(rank, world, port, tiny_rank, q):
         q.put({"rank": rank, "error": traceback.format_exc() + repr(e)})
 
 
-def _run(world, tiny_rank=-1):
+def _run(world, tiny_rank=-1, batch=False):
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, tiny_rank, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, tiny_rank, q, batch)) for r in range(world)]
     for p in procs:
         p.start()
     got = {}
@@ -122,6 +136,24 @@ def test_banded_frame_equals_single_rank(single, world):
     for r in range(world):
         assert got[r]["n_visible"] == single["visible"] and got[r]["n_evals"] == single["n_evals"]
         _same({"color": got[r]["all_color"], "t": got[r]["all_t"]}, single, ("color", "t"))
+
+
+def test_banded_batch_equals_render():
+    """Two ranks render three cameras as one batch each (their bands of every frame in one launch
+    sequence), gathered to rank 0 as (3, H, W, ...): every frame equals render() for its camera."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    ng, fld, cam = _scene()
+    cams = _batch_cams(ng, cam)
+    want = [ng.render(c, fld, ng.RenderConfig()) for c in cams]
+    got = _run(2, batch=True)
+    r0 = got[0]
+    assert r0["dst_keys"] == sorted(FIELDS) and got[1]["dst_keys"] == []
+    for f, (fb, rep) in enumerate(want):
+        single = {k: getattr(fb, k) for k in FIELDS}
+        _same({k: r0[k][f] for k in FIELDS}, single, FIELDS)
+    assert got[0]["n_visible"] == got[1]["n_visible"] == sum(r.visible for _, r in want)
 
 
 def test_overflow_on_one_rank_reruns_all(single):

@@ -1,5 +1,6 @@
 """World-size-2 gloo tests of the multi-GPU tile path on CPU: band layout,
-the all-gather of row-padded tiles and the image assembly (the per-rank
+the all-gather of row-padded tiles and the image assembly, for one frame
+and for a batch of frames in one collective (the per-rank
 render is replaced by a synthetic tile whose pixels encode their global
 row, so the check is exact)."""
 
@@ -48,6 +49,16 @@ def _body(rank, world, height, width, band_rows, q):
         assert (to1 is None) == (rank != 1)
         if to1 is not None:
             assert torch.equal(to1, img)
+        # a batch of 3 frames (frame f's pixels also carry f) in one collective
+        frames = torch.stack([local + 1000 * f for f in range(3)])
+        imgs = parallel.gather_frames(frames, layout, height)
+        assert tuple(imgs.shape) == (3, height, width, 3)
+        for f in range(3):
+            assert torch.equal(imgs[f], img + 1000 * f)
+        to0 = parallel.gather_frames(frames, layout, height, dst=0)
+        assert (to0 is None) == (rank != 0)
+        if to0 is not None:
+            assert torch.equal(to0, imgs)
         q.put((rank, img.numpy()))
 
 
