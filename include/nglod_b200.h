@@ -40,7 +40,9 @@ extern "C" {
 #define NG_MAX_TLEVELS 16    /* virtual + stored traversal levels */
 #define NG_FEAT_PAD 32       /* feature rows are padded to 32 fp32 channels (128 B) */
 #define NG_W1_STRIDE 36      /* packed decoder row: 3 x-weights, 32 feature weights, b1 */
+#ifndef NG_MAX_BATCH
 #define NG_MAX_BATCH 8       /* cameras per ng_render_batch launch */
+#endif
 
 /* Device-resident sparse voxel octree (octree.py:100-131).
  * Traversal level t = level + n_virtual; levels -n_virtual..-1 are the

@@ -18,6 +18,8 @@ from paper_2101_10994_b200.parallel import band_layout  # noqa: E402
 from paper_2101_10994_b200.render import (RenderSession, camera_structs, prepare_presum, resolve_config,  # noqa: E402
                                           resolve_lod)
 
+if os.environ.get("MAX_BATCH"):  # a library variant built with -DNG_MAX_BATCH=...
+    _lib.MAX_BATCH = int(os.environ["MAX_BATCH"])
 which = os.environ.get("CONFIG", "1")
 KS = [int(k) for k in os.environ.get("KS", "1,2,4,8").split(",")]
 knot, svo, fld = bench.build_workload()

@@ -2,7 +2,7 @@
 library variant: tools/build_variant.sh prof "-DNG_PROFILE"; run with
 NG_LIB_VARIANT=prof).
 
-    CONFIG=1|3|4 [BAND=world,rank] python tools/march_profile.py
+    CONFIG=1|3|4 [BAND=world,rank] [BATCH=K] python tools/march_profile.py
 
 Prints the groups' step counts, lane utilisation, the spread of group end
 times, the time per step split into acquire / eval / decoder, the ray
@@ -23,7 +23,8 @@ import bench  # noqa: E402
 import paper_2101_10994_b200 as ng  # noqa: E402
 from paper_2101_10994_b200 import _lib, scenes  # noqa: E402
 from paper_2101_10994_b200.parallel import band_layout  # noqa: E402
-from paper_2101_10994_b200.render import RenderSession, prepare_presum, resolve_config, resolve_lod  # noqa: E402
+from paper_2101_10994_b200.render import (RenderSession, camera_structs, prepare_presum, resolve_config,  # noqa: E402
+                                          resolve_lod)
 
 which = os.environ.get("CONFIG", "1")
 band = os.environ.get("BAND")
@@ -41,13 +42,14 @@ cfg = resolve_config(fld, config, resolve_lod(cam, fld, config))
 fstruct = prepare_presum(fld, cfg)
 world, rank = (int(v) for v in band.split(",")) if band else (1, 0)
 rows = len(band_layout(H, world)[rank])
-sess = RenderSession(fld, W, rows, n_rays=rows * W)
+K = int(os.environ.get("BATCH", "1"))
+sess = RenderSession(fld, W, rows, n_rays=rows * W * K)
 fr = sess.new_frame()
-cs = cam.band_struct(8, world, rank)
+cs = camera_structs([cam.band_struct(8, world, rank)] * K)
 
 
 def step():
-    _lib.call("ng_render_frame", svo.device.ref(), ctypes.byref(fstruct), ctypes.byref(cfg), ctypes.byref(cs),
+    _lib.call("ng_render_batch", svo.device.ref(), ctypes.byref(fstruct), ctypes.byref(cfg), cs, K,
               ctypes.byref(sess.frame_struct(fr)), ctypes.byref(sess.ws), _lib.ptr(sess.stats), _lib.stream_ptr())
 
 
@@ -123,7 +125,7 @@ if tl is not None:
         print(f"timeline (64 groups; mean busy lanes per step / steps, per tenth of {(t1l - t0l) / 1e3:.0f} us):",
               " ".join(row))
 # the frame's ray iteration distribution via the public API (non-profiled timing irrelevant here)
-if world == 1:
+if world == 1 and K == 1:
     fb, rep = ng.render(cam, fld, config)
     itr = fb.iterations[fb.iterations > 0]
     print(f"ray iterations: n {itr.size} mean {itr.mean():.2f} p99 {np.percentile(itr, 99):.0f} "
