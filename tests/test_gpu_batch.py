@@ -2,6 +2,8 @@
 TiledRenderer(batch=K)): several cameras in one traversal + one march, each
 frame equal to render()'s for its camera in every per-pixel output."""
 
+import os
+import subprocess
 import sys
 
 import numpy as np
@@ -150,3 +152,18 @@ def test_batch_configs1_frame(ng):
     _same(fbs[0], f0)
     _same(fbs[1], f1)
     assert rep.visible == r0.visible + r1.visible
+
+
+@pytest.mark.parametrize("knobs", [{"NG_TILE_TRAVERSE": "0"}, {"NG_FUSED_PROBES": "0"},
+                                   {"NG_TILE_SPLIT": "2", "NG_TILE_SPLIT_AHEAD": "1000000"},
+                                   {"NG_TILE_SCAP": "3"}],
+                         ids=["level_traversal", "normals_pass", "split_every_tile", "spill"])
+def test_batch_under_knobs(ng, knobs):
+    """The other code paths a batch can take (the level-by-level traversal with explicit per-frame camera
+    rays and no shared eye, the separate normals pass, continuations on every tile, the shared-memory
+    spill) give each frame render()'s outputs too (tests/batch_knob_probe.py in a subprocess: the knobs
+    are read once per process)."""
+    here = os.path.dirname(os.path.abspath(__file__))
+    r = subprocess.run([sys.executable, os.path.join(here, "batch_knob_probe.py")], env={**os.environ, **knobs},
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout[-2000:] + r.stderr[-3000:]
