@@ -35,7 +35,7 @@ cam = ng.Camera(bench.CAM["position"], bench.CAM["look_at"], bench.CAM["up"], be
 cfg = resolve_config(fld, config, resolve_lod(cam, fld, config))
 fstruct = prepare_presum(fld, cfg)
 flush = torch.empty(bench.L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
-for world in (1, 2, 4, 8):
+for world in [int(w) for w in os.environ.get("WORLDS", "1,2,4,8").split(",")]:
     rows = len(band_layout(H, world)[world - 1])
     base = None
     for K in KS:
