@@ -55,8 +55,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--batch", type=int, default=8,
-                    help="frames per launch sequence (ng_render_batch; 1..8): the timed steps are frames, rendered "
+    ap.add_argument("--batch", type=int, default=16,
+                    help="frames per launch sequence (ng_render_batch; 1..16): the timed steps are frames, rendered "
                          "`batch` at a time; each frame's latency alone is reported beside it")
     ap.add_argument("--no-query", action="store_true", help="skip the batched-query leg")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
@@ -331,7 +331,7 @@ def run_ours(args, rank: int, world: int):
     # Frames go `batch` per launch sequence (ng_render_batch: one traversal
     # and one march over every frame's rays, so one frame's longest rays
     # overlap the other frames' work); a step is still one frame.
-    B = max(1, min(args.batch, 8))
+    B = max(1, min(args.batch, 16))
     tiles = TiledRenderer(fld, WIDTH, HEIGHT, batch=B)
     sess = tiles.sess
     n_levels = cfg.trace_level + svo.device.n_virtual  # index of the final hit count
@@ -657,7 +657,7 @@ def extra_configs(args, world, dev, knot):
         st = tiles.sess.read_stats()
         lat = _time_tiled(tiles, cam, cfg, steps, flush, world)
         del tiles
-        B = max(1, min(args.batch, 8))
+        B = max(1, min(args.batch, 16))
         tiles = TiledRenderer(fld, 1920, 1080, batch=B)
         tiles.render_batch([cam] * B, config)  # capacities for the batch
         ms = _time_tiled(tiles, cam, cfg, max(3, steps // 2), flush, world)

@@ -41,7 +41,7 @@ extern "C" {
 #define NG_FEAT_PAD 32       /* feature rows are padded to 32 fp32 channels (128 B) */
 #define NG_W1_STRIDE 36      /* packed decoder row: 3 x-weights, 32 feature weights, b1 */
 #ifndef NG_MAX_BATCH
-#define NG_MAX_BATCH 8       /* cameras per ng_render_batch launch */
+#define NG_MAX_BATCH 16      /* cameras per ng_render_batch launch (_lib.MAX_BATCH mirrors it) */
 #endif
 
 /* Device-resident sparse voxel octree (octree.py:100-131).
@@ -356,6 +356,13 @@ int ng_render_frame(const ng_octree* tree, const ng_field* fld, const ng_render_
 int ng_render_batch(const ng_octree* tree, const ng_field* fld, const ng_render_cfg* cfg,
                     const ng_camera* cams, int32_t n_cams, const ng_frame* frame,
                     const ng_workspace* ws, ng_frame_stats* d_stats, void* stream);
+/* CUDA graphs of launch sequences (render.py's frame graphs): capture on a
+ * non-default stream (thread-local mode), instantiate, replay on any stream.
+ * exec handles are opaque; ng_graph_destroy releases one. */
+int ng_graph_capture_begin(void* stream);
+int ng_graph_capture_end(void* stream, void** exec_out);
+int ng_graph_launch(void* exec, void* stream);
+int ng_graph_destroy(void* exec);
 /* Same, for arbitrary rays (metrics.trace_field_rays, metrics.py:135-142). */
 int ng_render_rays(const ng_octree* tree, const ng_field* fld, const ng_render_cfg* cfg,
                    const ng_ray* rays, int64_t n_rays, const ng_frame* frame,

@@ -29,7 +29,7 @@ NG_ERR_CUDA = 4
 NG_ERR_OCTFIELD = 5
 
 MAX_TLEVELS = 16
-MAX_BATCH = 8  # NG_MAX_BATCH: cameras per ng_render_batch launch
+MAX_BATCH = 16  # NG_MAX_BATCH: cameras per ng_render_batch launch
 FEAT_PAD = 32
 W1_STRIDE = 36
 
@@ -177,6 +177,10 @@ _SIGS = {
     "ng_shade": (C.c_int, [P, P, C.c_int64, P, P, P]),
     "ng_render_frame": (C.c_int, [P, P, P, P, P, P, P, P]),
     "ng_render_batch": (C.c_int, [P, P, P, P, C.c_int32, P, P, P, P]),
+    "ng_graph_capture_begin": (C.c_int, [P]),
+    "ng_graph_capture_end": (C.c_int, [P, C.POINTER(C.c_void_p)]),
+    "ng_graph_launch": (C.c_int, [P, P]),
+    "ng_graph_destroy": (C.c_int, [P]),
     "ng_render_rays": (C.c_int, [P, P, P, P, C.c_int64, P, P, P, C.c_int32, P]),
     "ng_hit_points": (C.c_int, [P, P, P, C.c_int64, P, P]),
     "ng_march_profile": (C.c_int, [P, C.c_int]),

@@ -1606,6 +1606,37 @@ int ng_camera_rays(const ng_camera* cam, ng_ray* rays, void* stream) {
   return NG_OK;
 }
 
+// CUDA graphs of a frame's launches, captured on the caller's (non-default)
+// stream in thread-local mode and replayed on any stream. Capturing here
+// instead of through torch.cuda.graph keeps torch's caching allocators
+// intact (its capture empties the device and pinned-host caches and
+// synchronises the device), so a streaming loop that meets a new launch
+// key does not fall back to cudaMalloc / cudaHostAlloc on every frame.
+int ng_graph_capture_begin(void* stream) {
+  return cuda_status(cudaStreamBeginCapture((cudaStream_t)stream, cudaStreamCaptureModeThreadLocal),
+                     "cudaStreamBeginCapture");
+}
+
+int ng_graph_capture_end(void* stream, void** exec_out) {
+  cudaGraph_t g = nullptr;
+  if (int r = cuda_status(cudaStreamEndCapture((cudaStream_t)stream, &g), "cudaStreamEndCapture")) return r;
+  cudaGraphExec_t e = nullptr;
+  const int r = cuda_status(cudaGraphInstantiate(&e, g, 0), "cudaGraphInstantiate");
+  cudaGraphDestroy(g);
+  if (r) return r;
+  *exec_out = (void*)e;
+  return NG_OK;
+}
+
+int ng_graph_launch(void* exec, void* stream) {
+  return cuda_status(cudaGraphLaunch((cudaGraphExec_t)exec, (cudaStream_t)stream), "cudaGraphLaunch");
+}
+
+int ng_graph_destroy(void* exec) {
+  if (exec) cudaGraphExecDestroy((cudaGraphExec_t)exec);
+  return NG_OK;
+}
+
 size_t ng_render_workspace_bytes(int64_t n_rays, int64_t pair_capacity, int64_t hit_capacity) {
   return layout(n_rays, pair_capacity, hit_capacity).total;
 }

@@ -446,6 +446,41 @@ def resolve_lod(camera: Camera, fld: NeuralField, config: RenderConfig) -> float
 _CAPTURE_LOCK = threading.Lock()
 
 
+class _NativeGraph:
+    """One frame's launches captured as a CUDA graph through the library
+    (ng_graph_*): captured on a side stream in thread-local mode, replayed
+    on the current stream. Unlike torch.cuda.graph, capturing does not
+    synchronise the device or empty torch's device and pinned-host caches,
+    so a streaming loop meeting a new launch key keeps its cached blocks
+    (and its frame-buffer addresses, hence its graph keys)."""
+
+    def __init__(self, launch, side: torch.cuda.Stream):
+        side.wait_stream(torch.cuda.current_stream())
+        h = ctypes.c_void_p()
+        with _CAPTURE_LOCK:  # (one capture at a time per process keeps errors attributable)
+            call("ng_graph_capture_begin", side.cuda_stream)
+            try:
+                launch(side.cuda_stream)
+            except BaseException:
+                # leave the stream out of capture mode before reporting
+                _lib.lib().ng_graph_capture_end(ctypes.c_void_p(side.cuda_stream), ctypes.byref(h))
+                if h.value:
+                    _lib.lib().ng_graph_destroy(h)
+                raise
+            call("ng_graph_capture_end", side.cuda_stream, ctypes.byref(h))
+        self.h = h.value
+
+    def replay(self):
+        call("ng_graph_launch", self.h, stream_ptr())
+
+    def __del__(self):
+        try:
+            if self.h:
+                _lib.lib().ng_graph_destroy(ctypes.c_void_p(self.h))
+        except Exception:
+            pass
+
+
 def _graphs_enabled() -> bool:
     """NG_GRAPHS=0 launches every frame's kernels directly."""
     return os.environ.get("NG_GRAPHS", "1") != "0" and os.environ.get("NG_MARCH_PROFILE") != "1"
@@ -508,6 +543,7 @@ class RenderSession:
         self.ev2 = torch.cuda.Event(enable_timing=True)
         self._graphs, self._graph_seen, self._graph_misses = {}, set(), 0
         self.graph_replays = 0
+        self._cap_stream = None  # the stream frame graphs are captured on
 
     def _alloc_ws(self):
         nbytes = _lib.lib().ng_render_workspace_bytes(self.n, self.pair_cap, self.hit_cap)
@@ -548,9 +584,9 @@ class RenderSession:
             tree, field = self.fld.svo.device.ref(), ctypes.byref(fstruct)
             cs = camera_structs(camera)
 
-            def launch():
+            def launch(stream=None):
                 call("ng_render_batch", tree, field, ctypes.byref(cfg), cs, len(cs), ctypes.byref(fs),
-                     ctypes.byref(self.ws), ptr(self.stats), stream_ptr())
+                     ctypes.byref(self.ws), ptr(self.stats), stream if stream is not None else stream_ptr())
             if graphed:
                 # the frame's launches as one CUDA graph, replayed while every
                 # argument is unchanged (render() reusing a freed frame buffer
@@ -572,13 +608,9 @@ class RenderSession:
                         # buffers cycle through a handful of address sets)
                         if len(self._graphs) >= 16:
                             self._graphs.pop(next(iter(self._graphs)))
-                        g = torch.cuda.CUDAGraph()
-                        # one capture at a time in the process (entering a capture
-                        # synchronises the device and frees cached blocks, which
-                        # must not happen inside another thread's capture);
-                        # thread_local: other threads keep launching meanwhile
-                        with _CAPTURE_LOCK, torch.cuda.graph(g, capture_error_mode="thread_local"):
-                            launch()
+                        if self._cap_stream is None:
+                            self._cap_stream = torch.cuda.Stream(device=self.dev)
+                        g = _NativeGraph(launch, self._cap_stream)
                         self._graphs[key] = g
                     self._graph_misses = 0
                     self.graph_replays += 1

@@ -65,18 +65,19 @@ def test_render_batch_equals_render(ng, torus, config):
 
 
 def test_render_batch_one_camera_and_limits(ng, torus):
-    """A batch of one is render(); eight cameras (the launch maximum) work; nine, mixed sizes and cameras whose
-    automatic detail levels differ are ConfigErrors."""
+    """A batch of one is render(); the launch maximum (NG_MAX_BATCH cameras) works; one more, mixed sizes and
+    cameras whose automatic detail levels differ are ConfigErrors."""
     cams = _cams(ng)
     cfg = ng.RenderConfig()
     fbs, _ = ng.render_batch(cams[:1], torus, cfg)
     _same(fbs[0], ng.render(cams[0], torus, cfg)[0])
-    eight = (cams * 2)[:8]
-    fbs, _ = ng.render_batch(eight, torus, cfg)
-    for fb, c in zip(fbs, eight):
+    from paper_2101_10994_b200 import _lib
+    full = (cams * 8)[:_lib.MAX_BATCH]
+    fbs, _ = ng.render_batch(full, torus, cfg)
+    for fb, c in zip(fbs, full):
         _same(fb, ng.render(c, torus, cfg)[0])
     with pytest.raises(ng.ConfigError):
-        ng.render_batch(cams * 3, torus, cfg)
+        ng.render_batch(cams * 8 + cams[:1], torus, cfg)
     with pytest.raises(ng.ConfigError):
         ng.render_batch([cams[0], ng.Camera((0.0, 2.0, 3.5), (0, 0, 0), (0, 1, 0), 30.0, 64, 48)], torus, cfg)
     th = ng.RenderConfig(lod_thresholds=(1.0, 2.0, 3.0, 6.0))

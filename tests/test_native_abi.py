@@ -65,16 +65,20 @@ def test_host_validation_before_device():
         ng.RayBundle(np.zeros((2, 3)), np.array([[1.0, 1.0, 0.0], [0.0, 0.0, 1.0]]))
     # frame batches: 1..NG_MAX_BATCH cameras per launch, checked before the field is touched
     cam = ng.Camera((0, 0, 4), (0, 0, 0), (0, 1, 0), 30.0, 8, 8)
+    import re
+    from paper_2101_10994_b200 import _lib
+    hdr = open(os.path.join(ROOT, "include", "nglod_b200.h")).read()
+    assert int(re.search(r"#define NG_MAX_BATCH (\d+)", hdr).group(1)) == _lib.MAX_BATCH
     with pytest.raises(ng.ConfigError):
-        ng.render_batch([cam] * 9, None, ng.RenderConfig())
+        ng.render_batch([cam] * (_lib.MAX_BATCH + 1), None, ng.RenderConfig())
     with pytest.raises(ng.ConfigError):
         ng.render_batch([], None, ng.RenderConfig())
     with pytest.raises(ng.ConfigError):
         next(ng.render_frames([cam], None, ng.RenderConfig(), batch=0))
     from paper_2101_10994_b200.render import camera_structs
-    assert len(camera_structs([cam] * 8)) == 8
+    assert len(camera_structs([cam] * _lib.MAX_BATCH)) == _lib.MAX_BATCH
     with pytest.raises(ng.ConfigError):
-        camera_structs([cam] * 9)
+        camera_structs([cam] * (_lib.MAX_BATCH + 1))
 
 
 def test_no_device_means_loud_failure():
