@@ -422,7 +422,7 @@ def run_ours(args, rank: int, world: int):
     if world == 1:
         # warm-up covers the frame-graph captures (render.py: a launch key is
         # captured on its second sight; consecutive frames alternate buffers)
-        e2e_steps = max(2 * B, min(args.steps, 24))
+        e2e_steps = max(3 * B, min(args.steps, 24))  # (three launches: the readback pipeline fills)
         for _ in range(6):
             fb, _r = ng.render(cam, fld, config)
             _ = fb.color
