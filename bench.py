@@ -350,7 +350,10 @@ def run_ours(args, rank: int, world: int):
         step(B)
     torch.cuda.synchronize()
 
-    sizes = [B] * (args.steps // B) + ([args.steps % B] if args.steps % B else [])
+    # the steps split evenly over the fewest launches of at most B frames
+    # (20 steps at B = 16: two launches of 10, not 16 + a short tail of 4)
+    n_launch = max(1, -(-args.steps // B))
+    sizes = [args.steps // n_launch + (1 if i < args.steps % n_launch else 0) for i in range(n_launch)]
     ev = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(4)) for _ in sizes]
     for e in ev:
         for x in e:
@@ -378,7 +381,7 @@ def run_ours(args, rank: int, world: int):
     sess.ws.ev_trace_done = None
     launch_ms = [a.elapsed_time(b) for a, _, _, b in ev]
     march_all = [a.elapsed_time(b) for _, a, b, _ in ev]
-    full = [i for i, k in enumerate(sizes) if k == sizes[0]]
+    full = [i for i, k in enumerate(sizes) if k == sizes[-1]]
     frame_ms = [launch_ms[i] / sizes[i] for i in full]
     march_ms = [march_all[i] for i in full]
     st = sess.read_stats()
@@ -738,7 +741,7 @@ def main():
     # the march launch also evaluates the normal probes (NG_FUSED_PROBES, default)
     fused = os.environ.get("NG_FUSED_PROBES", "1") != "0"
     # a full launch marches `batch` frames of the same camera
-    march_evals = (res["total_evals"] if fused else res["trace_evals"]) * res["frames_per_launch"][0]
+    march_evals = (res["total_evals"] if fused else res["trace_evals"]) * res["frames_per_launch"][-1]
     algo_bytes = march_evals * bytes_per_eval
     peak = _peak_hbm()
     achieved = algo_bytes / (march * 1e-3) / 1e9
