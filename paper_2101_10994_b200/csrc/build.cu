@@ -37,6 +37,21 @@ int cuda_status(cudaError_t e, const char* where) {
 
 int launch_status(const char* where) { return cuda_status(cudaGetLastError(), where); }
 
+int malloc_async(void** p, size_t bytes, cudaStream_t s, const char* where) {
+  static std::atomic<unsigned long long> kept{0};  // devices whose pool threshold is set (bit per device)
+  const int d = current_device();
+  const unsigned long long bit = 1ull << (d & 63);
+  if (!(kept.load(std::memory_order_acquire) & bit)) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, d) == cudaSuccess) {
+      uint64_t keep = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    kept.fetch_or(bit, std::memory_order_acq_rel);
+  }
+  return cuda_status(cudaMallocAsync(p, bytes, s), where);
+}
+
 int current_device() {
   int dev = 0;
   cudaGetDevice(&dev);

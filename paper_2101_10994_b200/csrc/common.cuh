@@ -24,6 +24,11 @@ int env_int(const char* name, int def);
 // (cudaFuncSetAttribute is per device); cached per (device, kernel),
 // thread-safe
 int set_smem_limit(const void* kernel, size_t bytes);
+// cudaMallocAsync with the current device's stream-ordered pool told to keep
+// its memory across synchronisations: with the default release threshold
+// (0) every sync hands the pool's pages back and the next call maps them
+// again, which made single configs[2] queries take 12 to 850 ms
+int malloc_async(void** p, size_t bytes, cudaStream_t s, const char* where);
 
 #define NG_CHECK_LAUNCH(name)                         \
   do {                                                \

@@ -144,7 +144,7 @@ int run_query_tc(const ng_octree& tree, const ng_field& f, const ng_query_args& 
   const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((tiles + TQ_GROUPS - 1) / TQ_GROUPS, sm_count()));
   const int ndec = dec_last - dec_first + 1;
   uint8_t* dtiles = nullptr;
-  int r = cuda_status(cudaMallocAsync((void**)&dtiles, (size_t)ndec * DEC_TC_BYTES + 256, s), "query tiles alloc");
+  int r = malloc_async((void**)&dtiles, (size_t)ndec * DEC_TC_BYTES + 256, s, "query tiles alloc");
   if (r) return r;
   unsigned int* claim = reinterpret_cast<unsigned int*>(dtiles + (size_t)ndec * DEC_TC_BYTES);
   k_query_tiles<<<1, 512, 0, s>>>(f, dec_first, dec_last, dtiles, claim);

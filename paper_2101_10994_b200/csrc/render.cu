@@ -1699,7 +1699,7 @@ int ng_sphere_trace(const ng_octree* tree, const ng_field* fld, const ng_render_
   if (n_rays <= 0) return NG_OK;
   cudaStream_t s = (cudaStream_t)stream;
   unsigned long long* work = nullptr;
-  int r = cuda_status(cudaMallocAsync((void**)&work, 8, s), "ng_sphere_trace alloc");
+  int r = malloc_async((void**)&work, 8, s, "ng_sphere_trace alloc");
   if (r) return r;
   if ((r = cuda_status(cudaMemsetAsync(work, 0, 8, s), "ng_sphere_trace memset"))) return r;
   const LodPlan P = plan_lod(*cfg);
