@@ -764,7 +764,7 @@ def main():
         "roofline": {"bound": "hbm", "kernel": "k_march (sphere-trace march + normal probes, fused gather + MLP)"
                      if fused else "k_march (sphere-trace march, fused gather + MLP)",
                      "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": _traffic(),
+                     "traffic": _march_traffic(res["frames_per_launch"][-1]),
                      "algorithmic_bytes": algo_bytes,
                      "evals": march_evals,
                      "note": f"{bytes_per_eval} B per eval x the launch's evals ({levels_read} level(s) read per eval: "
@@ -824,6 +824,19 @@ def _l2_peak():
     try:
         with open(os.path.join(ROOT, "profiles", "l2_gather_peak.json")) as fh:
             return float(json.load(fh)["gbs"])
+    except Exception:
+        return None
+
+
+def _march_traffic(frames: int):
+    """k_march DRAM bytes per launch of `frames` frames: the committed ncu
+    capture's bytes per frame times the frames (the capture may have been
+    of a different batch size)."""
+    p = os.path.join(ROOT, "profiles", "march_traffic.json")
+    try:
+        with open(p) as fh:
+            d = json.load(fh)
+        return d["dram_bytes_per_launch"] / d.get("frames_per_launch", 1) * frames
     except Exception:
         return None
 
