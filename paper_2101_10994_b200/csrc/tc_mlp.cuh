@@ -6,6 +6,11 @@
 
 namespace ng {
 
+// NG_RESTAGE_ASYNC=0: the per-level decoder restage as a load-store loop (A/B builds)
+#ifndef NG_RESTAGE_ASYNC
+#define NG_RESTAGE_ASYNC 1
+#endif
+
 constexpr int DEC_TC_BYTES = 2 * tc::TILE_BYTES + 128 * 4 + 128;  // B_hi, B_lo, W2[128], b2 (+pad)
 
 struct TcMlp {
@@ -173,9 +178,18 @@ __device__ __forceinline__ void TcMlp::prepare(int l) const {
   tc::fence_before_sync();
   __syncthreads();
   if (restage_tiles) {  // a plain copy of the pre-converted tiles
+    // as asynchronous 16-byte copies, all of a thread's in flight at once
+    // (a load-store loop kept one load in flight per thread: ~4 dependent
+    // L2 round trips per level with the whole CTA waiting), no registers held
     const uint4* src4 = reinterpret_cast<const uint4*>(restage_tiles + (size_t)(l - dec_first) * DEC_TC_BYTES);
     uint4* dst4 = reinterpret_cast<uint4*>(const_cast<uint8_t*>(dec_tiles));
+#if NG_RESTAGE_ASYNC
+    for (int i = threadIdx.x; i < DEC_TC_BYTES / 16; i += blockDim.x) cp_async16(dst4 + i, src4 + i);
+    cp_async_commit();
+    cp_async_wait_all();
+#else
     for (int i = threadIdx.x; i < DEC_TC_BYTES / 16; i += blockDim.x) dst4[i] = __ldg(src4 + i);
+#endif
   } else {
     stage_decoder_tiles(const_cast<uint8_t*>(dec_tiles), restage_src, l, l, restage_stride);
   }
