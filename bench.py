@@ -540,7 +540,9 @@ def query_leg(knot, svo, fld, dev, flush, rank: int, world: int):
                          "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": _traffic("query_traffic.json"), "algorithmic_bytes": algo,
                          "note": f"{QUERY_BYTES_BASE} + {EVAL_BYTES_PER_LEVEL} k B per point (SURVEY.md 8d), "
-                                 "k counted on the device; the call's median event time; peak = measured hbm_gbs"}}
+                                 "k counted on the device; the call's median event time; peak = measured hbm_gbs. "
+                                 "The rows are served from L2 (traffic = the call's DRAM bytes), so frac can pass 1; "
+                                 "the binding roof is the L2 random-row gather peak (l2_frac)"}}
     l2 = _l2_peak()
     if l2:
         line["roofline"]["l2_gather_peak"] = l2
