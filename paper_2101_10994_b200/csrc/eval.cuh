@@ -35,12 +35,56 @@
 
 namespace ng {
 
+// zt row stride in floats: 36 keeps rows 16-byte aligned, so the quad
+// gather's per-point update and the decoder's row read are 128-bit accesses
+// (conflict-free per quarter warp); 33 (A/B builds) is the scalar layout
+#ifndef NG_ZT_STRIDE
+#define NG_ZT_STRIDE 36
+#endif
 struct WarpScratch {
   int4 ids[32][2];      // corner ids of each lane's point at the current level
   float4 w[32][2];      // trilinear weights
-  float zt[32][33];     // running feature sum, row = point, col = channel (+1 pad);
+  float zt[32][NG_ZT_STRIDE];  // running feature sum, row = point, col = channel (+ pad);
                         // the presummed direct-z gather stages 4 points' rows here instead
 };
+
+// A point's 32 channels from its zt row.
+__device__ __forceinline__ void load_zrow(const float* zrow, float z[32]) {
+  if constexpr (NG_ZT_STRIDE % 4 == 0) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const float4 q = reinterpret_cast<const float4*>(zrow)[k];
+      z[4 * k] = q.x;
+      z[4 * k + 1] = q.y;
+      z[4 * k + 2] = q.z;
+      z[4 * k + 3] = q.w;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < 32; ++k) z[k] = zrow[k];
+  }
+}
+
+// zt[p][4 sub .. 4 sub + 3] (+)= acc
+template <bool kAdd>
+__device__ __forceinline__ void zt_quad(float* zr, const float acc[4]) {
+  if constexpr (NG_ZT_STRIDE % 4 == 0) {
+    float4* z4 = reinterpret_cast<float4*>(zr);
+    if constexpr (kAdd) {
+      float4 q = *z4;
+      q.x += acc[0];
+      q.y += acc[1];
+      q.z += acc[2];
+      q.w += acc[3];
+      *z4 = q;
+    } else {
+      *z4 = make_float4(acc[0], acc[1], acc[2], acc[3]);
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) zr[e] = kAdd ? zr[e] + acc[e] : acc[e];
+  }
+}
 
 // Asynchronous 16-byte global -> shared copies (LDGSTS): rows land in
 // shared memory without occupying registers while in flight.
@@ -146,8 +190,7 @@ __device__ __forceinline__ float mlp_eval(const float* __restrict__ dec, int h, 
   in[0] = xin[0];
   in[1] = xin[1];
   in[2] = xin[2];
-#pragma unroll
-  for (int k = 0; k < 32; ++k) in[3 + k] = zrow[k];
+  load_zrow(zrow, in + 3);
   float chk = 0.f;
 #pragma unroll
   for (int k = 0; k < 35; ++k) chk += in[k] - in[k];
@@ -353,9 +396,7 @@ __device__ __forceinline__ EvalLane warp_eval(const ng_octree& tree, const EvalC
           const float wj[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
           float acc[4];
           corner_sum4<NG_FFMA2 != 0>(wj, v[k], acc);
-          float* zr = &ws.zt[mine[k]][4 * sub];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) zr[e] += acc[e];
+          zt_quad<true>(&ws.zt[mine[k]][4 * sub], acc);
         }
       }
     } else
@@ -563,9 +604,7 @@ __device__ __forceinline__ EvalLane warp_eval_presum(const ng_octree& tree, cons
             zbad |= (isfinite(acc[0]) && isfinite(acc[1]) && isfinite(acc[2]) && isfinite(acc[3]) ? 0u : 1u)
                     << mine[k];
           } else {
-            float* zr = &ws.zt[mine[k]][4 * sub];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) zr[e] = acc[e];
+            zt_quad<false>(&ws.zt[mine[k]][4 * sub], acc);
           }
         }
         if constexpr (kStage) {  // the staged point: each lane reads back the rows it copied

@@ -149,7 +149,7 @@ __global__ void k_decode(const float* __restrict__ dec, int h, int m, const doub
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     float xin[3] = {(float)x[3 * i], (float)x[3 * i + 1], (float)x[3 * i + 2]};
-    float zr[32];
+    __align__(16) float zr[32];
     for (int k = 0; k < 32; ++k) zr[k] = k < m ? (float)z[i * m + k] : 0.f;
     bool bad = false;
     float v = mlp_eval(dec, h, xin, zr, bad);

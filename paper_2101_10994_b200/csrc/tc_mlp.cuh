@@ -56,8 +56,7 @@ struct TcMlp {
     v[0] = xf[0];
     v[1] = xf[1];
     v[2] = xf[2];
-#pragma unroll
-    for (int k = 0; k < 32; ++k) v[3 + k] = zrow[k];
+    load_zrow(zrow, v + 3);
     v[35] = 1.0f;  // bias input: B row 35 holds b1
     float chk = 0.f;
 #pragma unroll
