@@ -7,11 +7,12 @@
 // one thread issues the bf16x3 GEMM, and every thread reads its point's
 // hidden row from TMEM for the relu . W2 epilogue. All requested decoders'
 // B tiles stay resident in shared memory for the CTA's lifetime.
-// The batched query has no march control between evaluations, so it keeps
-// more corner rows in flight per warp than the render kernels (measured:
-// 1264 vs 1206 Mpoints/s at 8 vs 4 points per gather batch).
+// Points per gather batch: 8 measured faster than 4 when the decoder
+// restage and the corner sums cost more (1264 vs 1206 Mpoints/s); after
+// those changes 4 is as fast or slightly faster (10.74 vs 10.77 ms,
+// profiles/r02_final/gather_batch_ab.log) with fewer registers in flight.
 #ifndef NG_GATHER_BATCH
-#define NG_GATHER_BATCH 8
+#define NG_GATHER_BATCH 4
 #endif
 #include "tc_mlp.cuh"
 
